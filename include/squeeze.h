@@ -1,0 +1,196 @@
+/*
+ * squeeze.h — C ABI of the B200-native Squeeze hot path (arXiv 2201.00613).
+ *
+ * One automaton step on the COMPACT form of an NBB fractal (§3, §4):
+ * for every compact cell Ω, λ(Ω) gives its expanded (x, y), the 8
+ * Moore neighbours are tested for membership ("the holes were skipped"),
+ * ν maps each member neighbour back to a compact index, the states
+ * are gathered, the rule applied and the result written to a second buffer
+ * ("at most one execution of λ(ω) map and ℓ executions of ν(ω)").
+ *
+ * Conventions (DESIGN.md §3 lists every reading of the paper used here):
+ *  - Ω is the storage index Σ_{μ=1..r} β_μ k^{μ-1} (reading D2): digit μ-1 of Ω in
+ *    base k is the replica id at level μ.  A state buffer holds one uint8 per
+ *    cell (0 dead / 1 alive, reading D10) in Ω order.
+ *  - (x, y) is the expanded coordinate, origin upper-left, y downward.
+ *  - Level μ of x/y has weight s^{μ-1}; axis parity per reading D1.
+ *
+ * Ownership: every device pointer passed in is CALLER-owned (torch allocations in
+ * the Python binding), contiguous and 16-byte aligned; state buffers must be at
+ * least `state_bytes` long (squeeze_geometry).  A sharded context's local buffer
+ * holds Ω in [omega_lo, omega_hi) at offset Ω - omega_lo.  The context owns its
+ * lookup tables, tile tables and halo index arrays, freed by squeeze_destroy.
+ * All device calls are asynchronous and stream-ordered on the given stream; a
+ * context is not thread-safe.  No C++ exception crosses this boundary: every
+ * entry point returns a squeeze_status (negative on error).
+ */
+#ifndef SQUEEZE_H_
+#define SQUEEZE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* squeeze_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  SQZ_OK = 0,
+  SQZ_E_INVALID_SPEC = -1,   /* fractal violates S:29-33 (s>=2, 1<=k<=s^2, τ injective, τ in [0,s-1]^2) */
+  SQZ_E_OVERFLOW = -2,       /* s^r > 2^32 (coordinates) or k^r >= 2^62 (Ω) */
+  SQZ_E_OUT_OF_BOUNDS = -3,  /* scalar map argument outside the compact range / n x n embedding */
+  SQZ_E_HOLE = -4,           /* scalar ν of a non-member (D5) */
+  SQZ_E_INVALID_LEVEL = -5,  /* level or tile level out of range */
+  SQZ_E_CONFIG = -6,         /* NULL/misaligned pointer, bad shard, missing halo binding, buffer too small */
+  SQZ_E_CUDA = -7,           /* a CUDA runtime call failed (asynchronous faults surface on a later call) */
+  SQZ_E_NO_DEVICE = -8,      /* device entry point called on a host-only context (device = -1) */
+  SQZ_E_NOMEM = -9,          /* host or device allocation failed */
+  SQZ_E_HALO = -10           /* a kernel needed a neighbour outside the shard that the halo plan lacks */
+} squeeze_status;
+
+/* An NBB fractal F(n, k, s): k replicas per level, scale s per level, and the
+ * replica offset table τ = H_λ: tau[2b] = τ_x(b), tau[2b+1] = τ_y(b). */
+typedef struct {
+  uint32_t k;
+  uint32_t s;
+  const uint8_t* tau; /* 2k bytes, host memory, copied by squeeze_init */
+} squeeze_fractal;
+
+/* Life-like rule (reading D6): a dead cell with c member neighbours is born iff bit c
+ * of birth_mask is set; a live one survives iff bit c of survive_mask is set (c <= 8).
+ * Conway's B3/S23 is {1<<3, (1<<2)|(1<<3)}. */
+typedef struct {
+  uint16_t birth_mask;
+  uint16_t survive_mask;
+} squeeze_rule;
+
+/* Data-parallel sharding of Ω by contiguous, chunk-aligned ranges.
+ * nranks = 1 is the unsharded case.  Shard ranges are computed identically by every
+ * rank from (fractal, r, nranks). */
+typedef struct {
+  uint32_t rank;
+  uint32_t nranks;
+} squeeze_shard;
+
+/* Tuning knobs; zero-initialise for defaults. */
+typedef struct {
+  uint32_t tile_level;    /* g: level of the compact tile (K = k^g cells); 0 = auto (largest K <= 1024) */
+  uint32_t block_threads; /* threads per CTA of the tile kernel; 0 = auto */
+  uint32_t ctas_per_sm;   /* persistent CTAs per SM; 0 = auto (occupancy) */
+} squeeze_options;
+
+typedef struct {
+  uint64_t cells_total;  /* V = k^r */
+  uint64_t omega_lo;     /* first Ω owned by this shard */
+  uint64_t omega_hi;     /* one past the last Ω owned */
+  uint64_t state_bytes;  /* required bytes of a state buffer: (omega_hi - omega_lo) rounded up to 16 */
+  uint64_t n;            /* expanded side s^r */
+  uint64_t compact_w;    /* k^⌊r/2⌋ (D1) */
+  uint64_t compact_h;    /* k^⌈r/2⌉ */
+  uint32_t r;            /* level */
+  uint32_t tile_level;   /* g actually used */
+  uint64_t tile_cells;   /* K = k^g */
+  uint64_t num_tiles;    /* k^(r-g) in the whole fractal */
+  uint32_t chunk_tiles;  /* tiles per CTA work unit (32: one bit-slice lane per tile) */
+  uint32_t remote_links; /* tile-boundary neighbour links per tile (table size) */
+  uint32_t max_degree;   /* largest member-neighbour count of any cell (<= 8) */
+  uint32_t reserved;
+} squeeze_geometry_t;
+
+const char* squeeze_strerror(squeeze_status st);
+const char* squeeze_version(void);
+
+/* Look up a built-in fractal by name ("sierpinski-triangle", "sierpinski-carpet",
+ * "vicsek", "empty-bottles", "full-square").  `tau_out` receives 2k bytes (cap >= 2k).
+ * Returns SQZ_E_INVALID_SPEC for an unknown name. */
+squeeze_status squeeze_builtin_fractal(const char* name, uint32_t* k, uint32_t* s, uint8_t* tau_out,
+                                       uint32_t cap);
+
+/* Create a context for fractal `f` at level `r` (r = log_s n).  `rule` NULL means
+ * B3/S23; `shard` NULL means unsharded; `opts` NULL means defaults.  device >= 0 binds
+ * the context to that CUDA device and uploads its tables (sets that device current);
+ * device = -1 creates a HOST-ONLY context: geometry, scalar maps and halo planning work,
+ * device entry points return SQZ_E_NO_DEVICE.  Validates the spec and that
+ * s^r <= 2^32 and k^r < 2^62.  For nranks > 1 the halo plan (squeeze_halo_needs) is
+ * built here on the host. */
+squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r, const squeeze_rule* rule,
+                            const squeeze_shard* shard, const squeeze_options* opts, int device);
+void squeeze_destroy(void* ctx);
+
+squeeze_status squeeze_geometry(const void* ctx, squeeze_geometry_t* out);
+
+/* Shard range of any rank under this context's (fractal, r, nranks). */
+squeeze_status squeeze_shard_range(const void* ctx, uint32_t rank, uint64_t* lo, uint64_t* hi);
+
+/* ---- scalar host twins of the maps (tests and tooling; no device needed) ---- */
+/* λ(Ω): Ω in [0, k^r) -> expanded (x, y); SQZ_E_OUT_OF_BOUNDS otherwise. */
+squeeze_status squeeze_lambda_host(const void* ctx, uint64_t omega, uint32_t* x, uint32_t* y);
+/* ν(x, y): member -> Ω; SQZ_E_HOLE on a hole, SQZ_E_OUT_OF_BOUNDS outside n x n. */
+squeeze_status squeeze_nu_host(const void* ctx, uint64_t x, uint64_t y, uint64_t* omega);
+
+/* ---- batched device maps; `count` elements; device pointers; async on `stream` ---- */
+/* d_x[i], d_y[i] = λ(d_omega[i]); Ω >= k^r yields x = y = UINT32_MAX. */
+squeeze_status squeeze_map_lambda(const void* ctx, const uint64_t* d_omega, uint32_t* d_x, uint32_t* d_y,
+                                  uint64_t count, squeeze_stream_t stream);
+/* d_omega[i] = ν(d_x[i], d_y[i]); holes and out-of-range coordinates yield UINT64_MAX. */
+squeeze_status squeeze_map_nu(const void* ctx, const uint32_t* d_x, const uint32_t* d_y, uint64_t* d_omega,
+                              uint64_t count, squeeze_stream_t stream);
+
+/* ---- automaton ---- */
+/* Initial state (reading D9): cell Ω alive iff (mix(((X<<32)|Y) ^ mix(seed)) >> 32) < q at
+ * (X, Y) = λ(Ω), mix = splitmix64 finaliser; q = round(density * 2^32) in [0, 2^32].
+ * Writes state_bytes bytes (padding zeroed). */
+squeeze_status squeeze_seed(const void* ctx, uint8_t* d_state, uint64_t seed, uint64_t q,
+                            squeeze_stream_t stream);
+/* One synchronous step d_next = F(d_cur) with the tile-amortised bit-sliced kernel
+ * (DESIGN.md §5).  d_cur and d_next must not alias.  A sharded context reads
+ * out-of-shard neighbours from the halo receive buffer bound by squeeze_halo_bind,
+ * which the caller must have filled for d_cur's generation. */
+squeeze_status squeeze_step(void* ctx, const uint8_t* d_cur, uint8_t* d_next, squeeze_stream_t stream);
+/* The same step computed literally per cell (one λ and eight membership tests + ν per
+ * cell): the paper's per-thread formulation, kept as a comparison engine. */
+squeeze_status squeeze_step_naive(void* ctx, const uint8_t* d_cur, uint8_t* d_next, squeeze_stream_t stream);
+/* `steps` steps ping-ponging d_a -> d_b -> d_a ...; the final state is in d_b if steps is
+ * odd, else d_a.  Unsharded contexts only (SQZ_E_CONFIG otherwise).  use_graph != 0
+ * captures the two-step ping-pong once into a CUDA graph and replays it. */
+squeeze_status squeeze_run(void* ctx, uint8_t* d_a, uint8_t* d_b, uint64_t steps, int use_graph,
+                           squeeze_stream_t stream);
+/* End to end from HOST memory: copies h_state (cells of this shard, state_bytes long,
+ * ideally pinned) to d_a, runs `steps` steps, copies the final state back into h_state,
+ * and synchronises `stream`.  d_a, d_b are caller-owned device scratch buffers. */
+squeeze_status squeeze_run_host(void* ctx, uint8_t* h_state, uint8_t* d_a, uint8_t* d_b, uint64_t steps,
+                                squeeze_stream_t stream);
+/* *d_out (device uint64) = number of alive cells of this shard. */
+squeeze_status squeeze_count_alive(const void* ctx, const uint8_t* d_state, uint64_t* d_out,
+                                   squeeze_stream_t stream);
+/* Copy of the device-side error flag (synchronises the device): SQZ_OK or SQZ_E_HALO. */
+squeeze_status squeeze_device_error(const void* ctx);
+
+/* ---- halo exchange plan for sharded contexts (data moved by the caller, e.g. NCCL) ---- */
+/* Sorted, unique global Ω outside this shard that some in-shard cell has as a member
+ * neighbour.  Writes min(cap, total) entries, *count = total.  out may be NULL. */
+squeeze_status squeeze_halo_needs(const void* ctx, uint64_t* out, uint64_t cap, uint64_t* count);
+/* Ω (inside this shard) whose states this shard must send each step, in send-buffer order. */
+squeeze_status squeeze_halo_set_sends(void* ctx, const uint64_t* omegas, uint64_t count);
+/* Caller-owned device buffers: d_send receives `send count` bytes from squeeze_halo_pack;
+ * d_recv holds one byte per squeeze_halo_needs entry, in that order. */
+squeeze_status squeeze_halo_bind(void* ctx, uint8_t* d_send, const uint8_t* d_recv);
+/* d_send[i] = d_cur[sends[i] - omega_lo]. */
+squeeze_status squeeze_halo_pack(const void* ctx, const uint8_t* d_cur, squeeze_stream_t stream);
+
+/* ---- expanded bounding-box baseline (the paper's "BB" engine) ---- */
+/* n x n uint8 grid, row-major [y][x]: 0 dead, 1 alive, 2 hole (never changes).  Unsharded only. */
+squeeze_status squeeze_bb_bytes(const void* ctx, uint64_t* bytes);
+squeeze_status squeeze_bb_seed(const void* ctx, uint8_t* d_grid, uint64_t seed, uint64_t q, squeeze_stream_t stream);
+squeeze_status squeeze_bb_step(const void* ctx, const uint8_t* d_cur, uint8_t* d_next, squeeze_stream_t stream);
+/* d_state[Ω] = d_grid[λ(Ω)] — transports a BB grid to compact order for comparison. */
+squeeze_status squeeze_bb_to_compact(const void* ctx, const uint8_t* d_grid, uint8_t* d_state,
+                                     squeeze_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SQUEEZE_H_ */

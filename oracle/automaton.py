@@ -192,3 +192,42 @@ def expanded_run(state: np.ndarray, mask: np.ndarray, steps: int, rule: tuple = 
     for _ in range(steps):
         state = expanded_step(state, mask, rule)
     return state
+
+
+# ---------------------------------------------------------------- sampled forms (large r)
+def lambda_omega_np(f: Fractal, r: int, omega: np.ndarray) -> tuple:
+    """λ on storage indices, vectorised: λ(deinterleave(Ω)) (D2)."""
+    omega = np.asarray(omega, dtype=np.int64)
+    wx, wy = _deinterleave_np(f, r, omega)
+    return _lambda_np(f, r, wx, wy)
+
+
+def nu_omega_np(f: Fractal, r: int, x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """ν to storage indices, vectorised; -1 for holes and out-of-range coordinates."""
+    x = np.asarray(x, dtype=np.int64)
+    y = np.asarray(y, dtype=np.int64)
+    vx, vy, m = _nu_np(f, r, x, y)
+    return np.where(m, _interleave_np(f, r, vx, vy), -1)
+
+
+def seed_at(f: Fractal, r: int, omega: np.ndarray, seed: int, density: float) -> np.ndarray:
+    """O4 at chosen Ω only: the D9 draw at λ(Ω)."""
+    x, y = lambda_omega_np(f, r, omega)
+    return sqz_inputs.alive_bits(x, y, seed, sqz_inputs.density_threshold(density))
+
+
+def compact_step_sampled(f: Fractal, r: int, omegas: np.ndarray, fetch, rule: tuple = B3S23) -> np.ndarray:
+    """O6 restricted to the cells ``omegas``: ``fetch(Ω array) -> uint8 states`` supplies the
+    current state of any cell it needs (the cell itself and its member neighbours)."""
+    omegas = np.asarray(omegas, dtype=np.int64)
+    nbr, mem = compact_neighbours(f, r, omegas)
+    need = np.unique(np.concatenate([omegas, nbr[mem]]))
+    vals = np.asarray(fetch(need), dtype=np.uint8)
+
+    def look(q):
+        return vals[np.searchsorted(need, q)]
+
+    count = np.zeros(omegas.size, dtype=np.uint8)
+    for i in range(8):
+        count += np.where(mem[i], look(np.where(mem[i], nbr[i], omegas)), 0).astype(np.uint8)
+    return apply_rule(look(omegas), count, rule)

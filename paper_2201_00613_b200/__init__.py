@@ -1,0 +1,222 @@
+"""B200-native Squeeze hot path (arXiv 2201.00613): a Game-of-Life step on the compact
+form of an NBB fractal, through the C-ABI library ``libsqueeze.so`` (include/squeeze.h).
+
+PyTorch supplies device memory, streams and process groups only; every step of the path
+runs in the library's sm_100a kernels.
+
+    from paper_2201_00613_b200 import Squeeze, builtin_fractal
+    sq = Squeeze(builtin_fractal("sierpinski-triangle"), r=22, device=0)
+    a, b = sq.new_state(), sq.new_state()
+    sq.seed(a, seed=42, density=0.5)
+    sq.run(a, b, steps=100)
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import Geometry, SqueezeError
+
+__all__ = ["Fractal", "Squeeze", "SqueezeError", "Geometry", "builtin_fractal", "B3S23", "density_q"]
+
+B3S23 = (1 << 3, (1 << 2) | (1 << 3))
+
+
+@dataclass(frozen=True)
+class Fractal:
+    """NBB fractal F(n, k, s) with replica offsets τ = H_λ."""
+    name: str
+    k: int
+    s: int
+    tau: tuple  # ((tx, ty), ...)
+
+
+def builtin_fractal(name: str) -> Fractal:
+    lib = _lib.load()
+    k = ctypes.c_uint32()
+    s = ctypes.c_uint32()
+    buf = (ctypes.c_uint8 * 512)()
+    _lib.check(lib.squeeze_builtin_fractal(name.encode(), ctypes.byref(k), ctypes.byref(s), buf, 512), name)
+    tau = tuple((buf[2 * b], buf[2 * b + 1]) for b in range(k.value))
+    return Fractal(name, k.value, s.value, tau)
+
+
+def density_q(density: float) -> int:
+    """q = round(density * 2^32) (reading D9)."""
+    if not 0.0 <= density <= 1.0:
+        raise ValueError("density must be in [0, 1]")
+    return int(round(density * (1 << 32)))
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def _stream(stream, device):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(int(stream.cuda_stream))
+
+
+class Squeeze:
+    """One context of the library: fractal + level + rule (+ shard) (squeeze_init)."""
+
+    def __init__(self, fractal: Fractal, r: int, rule=B3S23, rank: int = 0, nranks: int = 1,
+                 device: int | None = 0, tile_level: int = 0, block_threads: int = 0, ctas_per_sm: int = 0):
+        self.lib = _lib.load()
+        self.fractal = fractal
+        self.r = r
+        self.rule = rule
+        self.device = device
+        tau = (ctypes.c_uint8 * (2 * fractal.k))(*[v for t in fractal.tau for v in t])
+        self._tau = tau
+        fc = _lib.FractalC(fractal.k, fractal.s, ctypes.cast(tau, _lib.u8p))
+        rc = _lib.RuleC(rule[0], rule[1])
+        sc = _lib.ShardC(rank, nranks)
+        oc = _lib.OptionsC(tile_level, block_threads, ctas_per_sm)
+        ctx = ctypes.c_void_p()
+        dev = -1 if device is None else int(device)
+        _lib.check(self.lib.squeeze_init(ctypes.byref(ctx), ctypes.byref(fc), r, ctypes.byref(rc),
+                                         ctypes.byref(sc), ctypes.byref(oc), dev), "squeeze_init")
+        self.ctx = ctx
+        g = _lib.GeometryC()
+        _lib.check(self.lib.squeeze_geometry(self.ctx, ctypes.byref(g)))
+        self.geometry = Geometry(*[getattr(g, f[0]) for f in _lib.GeometryC._fields_ if f[0] != "reserved"])
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.squeeze_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ host helpers
+    def lambda_host(self, omega: int) -> tuple:
+        x = ctypes.c_uint32()
+        y = ctypes.c_uint32()
+        _lib.check(self.lib.squeeze_lambda_host(self.ctx, omega, ctypes.byref(x), ctypes.byref(y)), "lambda")
+        return (x.value, y.value)
+
+    def nu_host(self, x: int, y: int):
+        """Ω or None for a hole; raises SqueezeError outside the n x n embedding."""
+        om = ctypes.c_uint64()
+        st = self.lib.squeeze_nu_host(self.ctx, x, y, ctypes.byref(om))
+        if st == -4:
+            return None
+        _lib.check(st, "nu")
+        return om.value
+
+    def shard_range(self, rank: int) -> tuple:
+        lo = ctypes.c_uint64()
+        hi = ctypes.c_uint64()
+        _lib.check(self.lib.squeeze_shard_range(self.ctx, rank, ctypes.byref(lo), ctypes.byref(hi)))
+        return lo.value, hi.value
+
+    def halo_needs(self) -> np.ndarray:
+        n = ctypes.c_uint64()
+        _lib.check(self.lib.squeeze_halo_needs(self.ctx, None, 0, ctypes.byref(n)))
+        out = np.zeros(n.value, dtype=np.uint64)
+        if n.value:
+            _lib.check(self.lib.squeeze_halo_needs(self.ctx, out.ctypes.data_as(_lib.u64p), n.value,
+                                                   ctypes.byref(n)))
+        return out
+
+    def halo_set_sends(self, omegas: np.ndarray) -> None:
+        omegas = np.ascontiguousarray(omegas, dtype=np.uint64)
+        _lib.check(self.lib.squeeze_halo_set_sends(self.ctx, omegas.ctypes.data_as(_lib.u64p), omegas.size),
+                   "halo_set_sends")
+
+    # ------------------------------------------------------------------ device
+    def new_state(self, fill: int | None = None):
+        import torch
+        t = torch.empty(self.geometry.state_bytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+        if fill is not None:
+            t.fill_(fill)
+        return t
+
+    def map_lambda(self, omega, stream=None):
+        import torch
+        omega = omega.contiguous()
+        x = torch.empty(omega.numel(), dtype=torch.int32, device=omega.device)
+        y = torch.empty_like(x)
+        _lib.check(self.lib.squeeze_map_lambda(self.ctx, _ptr(omega), _ptr(x), _ptr(y), omega.numel(),
+                                               _stream(stream, omega.device)), "map_lambda")
+        return x, y
+
+    def map_nu(self, x, y, stream=None):
+        import torch
+        x = x.contiguous()
+        y = y.contiguous()
+        om = torch.empty(x.numel(), dtype=torch.int64, device=x.device)
+        _lib.check(self.lib.squeeze_map_nu(self.ctx, _ptr(x), _ptr(y), _ptr(om), x.numel(),
+                                           _stream(stream, x.device)), "map_nu")
+        return om
+
+    def seed(self, state, seed: int = 42, density: float = 0.5, stream=None):
+        _lib.check(self.lib.squeeze_seed(self.ctx, _ptr(state), seed, density_q(density),
+                                         _stream(stream, state.device)), "seed")
+
+    def step(self, cur, nxt, stream=None):
+        _lib.check(self.lib.squeeze_step(self.ctx, _ptr(cur), _ptr(nxt), _stream(stream, cur.device)), "step")
+
+    def step_naive(self, cur, nxt, stream=None):
+        _lib.check(self.lib.squeeze_step_naive(self.ctx, _ptr(cur), _ptr(nxt), _stream(stream, cur.device)),
+                   "step_naive")
+
+    def run(self, a, b, steps: int, use_graph: bool = False, stream=None):
+        """Returns the tensor holding the final state (b if steps is odd, else a)."""
+        _lib.check(self.lib.squeeze_run(self.ctx, _ptr(a), _ptr(b), steps, int(use_graph),
+                                        _stream(stream, a.device)), "run")
+        return b if steps % 2 else a
+
+    def run_host(self, h_state, a, b, steps: int, stream=None):
+        """End to end from host memory (h_state: CPU uint8 tensor, ideally pinned)."""
+        _lib.check(self.lib.squeeze_run_host(self.ctx, _ptr(h_state), _ptr(a), _ptr(b), steps,
+                                             _stream(stream, a.device)), "run_host")
+
+    def count_alive(self, state, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.zeros(1, dtype=torch.int64, device=state.device)
+        _lib.check(self.lib.squeeze_count_alive(self.ctx, _ptr(state), _ptr(out), _stream(stream, state.device)),
+                   "count_alive")
+        return out
+
+    def device_error(self) -> int:
+        return self.lib.squeeze_device_error(self.ctx)
+
+    def halo_bind(self, send, recv) -> None:
+        _lib.check(self.lib.squeeze_halo_bind(self.ctx, _ptr(send), _ptr(recv)), "halo_bind")
+
+    def halo_pack(self, cur, stream=None) -> None:
+        _lib.check(self.lib.squeeze_halo_pack(self.ctx, _ptr(cur), _stream(stream, cur.device)), "halo_pack")
+
+    # ------------------------------------------------------------------ BB baseline
+    def bb_bytes(self) -> int:
+        b = ctypes.c_uint64()
+        _lib.check(self.lib.squeeze_bb_bytes(self.ctx, ctypes.byref(b)), "bb_bytes")
+        return b.value
+
+    def new_bb(self):
+        import torch
+        return torch.empty(self.bb_bytes(), dtype=torch.uint8, device=f"cuda:{self.device}")
+
+    def bb_seed(self, grid, seed: int = 42, density: float = 0.5, stream=None):
+        _lib.check(self.lib.squeeze_bb_seed(self.ctx, _ptr(grid), seed, density_q(density),
+                                            _stream(stream, grid.device)), "bb_seed")
+
+    def bb_step(self, cur, nxt, stream=None):
+        _lib.check(self.lib.squeeze_bb_step(self.ctx, _ptr(cur), _ptr(nxt), _stream(stream, cur.device)),
+                   "bb_step")
+
+    def bb_to_compact(self, grid, state, stream=None):
+        _lib.check(self.lib.squeeze_bb_to_compact(self.ctx, _ptr(grid), _ptr(state),
+                                                  _stream(stream, grid.device)), "bb_to_compact")

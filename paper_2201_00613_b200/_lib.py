@@ -1,0 +1,136 @@
+"""ctypes binding of libsqueeze.so (include/squeeze.h).  Argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels.  There is no CPU or
+PyTorch fallback: if the shared library is missing the import of a device entry point
+fails loudly (SqueezeError), on a GPU box as anywhere else.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsqueeze.so")
+
+u8p = ctypes.POINTER(ctypes.c_uint8)
+u32p = ctypes.POINTER(ctypes.c_uint32)
+u64p = ctypes.POINTER(ctypes.c_uint64)
+
+
+class SqueezeError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        msg = _strerror(status)
+        super().__init__(f"{what}: {msg} (status {status})" if what else f"{msg} (status {status})")
+
+
+class FractalC(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_uint32), ("s", ctypes.c_uint32), ("tau", u8p)]
+
+
+class RuleC(ctypes.Structure):
+    _fields_ = [("birth_mask", ctypes.c_uint16), ("survive_mask", ctypes.c_uint16)]
+
+
+class ShardC(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_uint32), ("nranks", ctypes.c_uint32)]
+
+
+class OptionsC(ctypes.Structure):
+    _fields_ = [("tile_level", ctypes.c_uint32), ("block_threads", ctypes.c_uint32),
+                ("ctas_per_sm", ctypes.c_uint32)]
+
+
+class GeometryC(ctypes.Structure):
+    _fields_ = [("cells_total", ctypes.c_uint64), ("omega_lo", ctypes.c_uint64), ("omega_hi", ctypes.c_uint64),
+                ("state_bytes", ctypes.c_uint64), ("n", ctypes.c_uint64), ("compact_w", ctypes.c_uint64),
+                ("compact_h", ctypes.c_uint64), ("r", ctypes.c_uint32), ("tile_level", ctypes.c_uint32),
+                ("tile_cells", ctypes.c_uint64), ("num_tiles", ctypes.c_uint64), ("chunk_tiles", ctypes.c_uint32),
+                ("remote_links", ctypes.c_uint32), ("max_degree", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+vp = ctypes.c_void_p
+st = ctypes.c_int
+
+# (name, argtypes) for every symbol include/squeeze.h declares
+SIGNATURES = {
+    "squeeze_strerror": ([st], ctypes.c_char_p),
+    "squeeze_version": ([], ctypes.c_char_p),
+    "squeeze_builtin_fractal": ([ctypes.c_char_p, u32p, u32p, u8p, ctypes.c_uint32], st),
+    "squeeze_init": ([ctypes.POINTER(vp), ctypes.POINTER(FractalC), ctypes.c_uint32, ctypes.POINTER(RuleC),
+                      ctypes.POINTER(ShardC), ctypes.POINTER(OptionsC), ctypes.c_int], st),
+    "squeeze_destroy": ([vp], None),
+    "squeeze_geometry": ([vp, ctypes.POINTER(GeometryC)], st),
+    "squeeze_shard_range": ([vp, ctypes.c_uint32, u64p, u64p], st),
+    "squeeze_lambda_host": ([vp, ctypes.c_uint64, u32p, u32p], st),
+    "squeeze_nu_host": ([vp, ctypes.c_uint64, ctypes.c_uint64, u64p], st),
+    "squeeze_map_lambda": ([vp, vp, vp, vp, ctypes.c_uint64, vp], st),
+    "squeeze_map_nu": ([vp, vp, vp, vp, ctypes.c_uint64, vp], st),
+    "squeeze_seed": ([vp, vp, ctypes.c_uint64, ctypes.c_uint64, vp], st),
+    "squeeze_step": ([vp, vp, vp, vp], st),
+    "squeeze_step_naive": ([vp, vp, vp, vp], st),
+    "squeeze_run": ([vp, vp, vp, ctypes.c_uint64, ctypes.c_int, vp], st),
+    "squeeze_run_host": ([vp, vp, vp, vp, ctypes.c_uint64, vp], st),
+    "squeeze_count_alive": ([vp, vp, vp, vp], st),
+    "squeeze_device_error": ([vp], st),
+    "squeeze_halo_needs": ([vp, u64p, ctypes.c_uint64, u64p], st),
+    "squeeze_halo_set_sends": ([vp, u64p, ctypes.c_uint64], st),
+    "squeeze_halo_bind": ([vp, vp, vp], st),
+    "squeeze_halo_pack": ([vp, vp, vp], st),
+    "squeeze_bb_bytes": ([vp, u64p], st),
+    "squeeze_bb_seed": ([vp, vp, ctypes.c_uint64, ctypes.c_uint64, vp], st),
+    "squeeze_bb_step": ([vp, vp, vp, vp], st),
+    "squeeze_bb_to_compact": ([vp, vp, vp, vp], st),
+}
+
+_LIB = None
+
+
+def load() -> ctypes.CDLL:
+    """Loads libsqueeze.so from the package directory (no fallback)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise SqueezeError(-7, f"{LIB_PATH} missing — run __graft_entry__.build()")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _LIB = lib
+    return _LIB
+
+
+def _strerror(status: int) -> str:
+    try:
+        return load().squeeze_strerror(status).decode()
+    except Exception:  # pragma: no cover
+        return "squeeze error"
+
+
+def check(status: int, what: str = "") -> None:
+    if status != 0:
+        raise SqueezeError(status, what)
+
+
+@dataclass(frozen=True)
+class Geometry:
+    cells_total: int
+    omega_lo: int
+    omega_hi: int
+    state_bytes: int
+    n: int
+    compact_w: int
+    compact_h: int
+    r: int
+    tile_level: int
+    tile_cells: int
+    num_tiles: int
+    chunk_tiles: int
+    remote_links: int
+    max_degree: int
+
+    @property
+    def local_cells(self) -> int:
+        return self.omega_hi - self.omega_lo

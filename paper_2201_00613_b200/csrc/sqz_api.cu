@@ -1,0 +1,562 @@
+// sqz_api.cu — the extern "C" boundary declared in include/squeeze.h.
+//
+// Owns the context (host planner state + device copies of the tables) and dispatches to
+// the kernels of sqz_kernels.cu.  No C++ exception crosses the boundary: every entry
+// point is wrapped and returns a squeeze_status.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/squeeze.h"
+#include "sqz_host.h"
+#include "sqz_kernels.cuh"
+
+using namespace sqz;
+
+namespace {
+
+struct DeviceLUTs {
+  uint32_t* d = nullptr;
+  LevelMaps view{};
+};
+
+struct Ctx {
+  Spec f;
+  uint32_t r = 0;
+  squeeze_rule rule{};
+  uint32_t rank = 0, nranks = 1;
+  squeeze_options opts{};
+  uint64_t V = 1, n = 1, cw = 1, ch = 1;
+  HostLevelMaps full, coarse;
+  TileTables tt;
+  uint64_t NT = 1;
+  ShardRange sr{};
+  uint64_t state_bytes = 0;
+  std::vector<uint64_t> needs, sends;
+  // device
+  int device = -1;
+  DeviceLUTs d_full, d_coarse;
+  uint16_t* d_nbr = nullptr;
+  uint32_t* d_link_j2 = nullptr;
+  uint8_t* d_link_dir = nullptr;
+  uint64_t* d_needs = nullptr;
+  uint64_t* d_sends = nullptr;
+  int* d_err = nullptr;
+  uint8_t* d_send = nullptr;
+  const uint8_t* d_recv = nullptr;
+  int tile_threads = 0, tile_grid = 0;
+  size_t tile_smem = 0;
+  // CUDA graph of the two-step ping-pong
+  cudaGraphExec_t graph = nullptr;
+  const uint8_t* graph_a = nullptr;
+  const uint8_t* graph_b = nullptr;
+  cudaStream_t graph_stream = nullptr;
+};
+
+struct DevGuard {
+  int prev = -1;
+  bool active = false;
+  explicit DevGuard(int dev) {
+    if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) {
+      cudaSetDevice(dev);
+      active = true;
+    }
+  }
+  ~DevGuard() {
+    if (active) cudaSetDevice(prev);
+  }
+};
+
+squeeze_status cu(cudaError_t e) { return e == cudaSuccess ? SQZ_OK : SQZ_E_CUDA; }
+
+template <class T>
+squeeze_status upload(T** dst, const T* src, size_t n) {
+  *dst = nullptr;
+  if (n == 0) return SQZ_OK;
+  if (cudaMalloc((void**)dst, n * sizeof(T)) != cudaSuccess) return SQZ_E_NOMEM;
+  return cu(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+squeeze_status upload_maps(const HostLevelMaps& h, DeviceLUTs& d) {
+  size_t n0 = h.lam_full.size(), n1 = h.lam_tail.size(), n2 = h.nu_full.size(), n3 = h.nu_tail.size();
+  std::vector<uint32_t> all;
+  all.reserve(n0 + n1 + n2 + n3);
+  all.insert(all.end(), h.lam_full.begin(), h.lam_full.end());
+  all.insert(all.end(), h.lam_tail.begin(), h.lam_tail.end());
+  all.insert(all.end(), h.nu_full.begin(), h.nu_full.end());
+  all.insert(all.end(), h.nu_tail.begin(), h.nu_tail.end());
+  squeeze_status st = upload(&d.d, all.data(), all.size());
+  if (st != SQZ_OK) return st;
+  d.view = h.view;
+  d.view.lam_full = d.d;
+  d.view.lam_tail = d.d + n0;
+  d.view.nu_full = d.d + n0 + n1;
+  d.view.nu_tail = d.d + n0 + n1 + n2;
+  return SQZ_OK;
+}
+
+void free_device(Ctx* c) {
+  if (c->device < 0) return;
+  DevGuard g(c->device);
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  cudaFree(c->d_full.d);
+  cudaFree(c->d_coarse.d);
+  cudaFree(c->d_nbr);
+  cudaFree(c->d_link_j2);
+  cudaFree(c->d_link_dir);
+  cudaFree(c->d_needs);
+  cudaFree(c->d_sends);
+  cudaFree(c->d_err);
+}
+
+HaloView halo_view(const Ctx* c) {
+  HaloView h;
+  h.omega_lo = c->sr.omega_lo;
+  h.omega_hi = c->sr.omega_hi;
+  h.needs = c->d_needs;
+  h.nneeds = c->needs.size();
+  h.recv = c->d_recv;
+  h.err = c->d_err;
+  return h;
+}
+
+squeeze_status check_state(const Ctx* c, const void* p) {
+  if (c->device < 0) return SQZ_E_NO_DEVICE;
+  if (p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u)) return SQZ_E_CONFIG;
+  return SQZ_OK;
+}
+
+squeeze_status do_step(Ctx* c, const uint8_t* cur, uint8_t* next, cudaStream_t st) {
+  if (c->nranks > 1 && !c->needs.empty() && c->d_recv == nullptr) return SQZ_E_CONFIG;
+  TileParams p{};
+  p.coarse = c->d_coarse.view;
+  p.K = c->tt.K;
+  p.E = c->tt.E;
+  p.zslot = c->tt.zero_slot;
+  p.dmax = c->tt.max_degree;
+  p.ndirs = c->tt.ndirs;
+  for (int i = 0; i < 8; ++i) {
+    p.dir_dx[i] = c->tt.dir_dx[i];
+    p.dir_dy[i] = c->tt.dir_dy[i];
+  }
+  p.nbr = c->d_nbr;
+  p.link_j2 = c->d_link_j2;
+  p.link_dir = c->d_link_dir;
+  p.tile_lo = c->sr.tile_lo;
+  p.tile_hi = c->sr.tile_hi;
+  p.nchunks = (c->sr.tile_hi - c->sr.tile_lo + kChunkTiles - 1) / kChunkTiles;
+  p.birth = c->rule.birth_mask;
+  p.survive = c->rule.survive_mask;
+  p.halo = halo_view(c);
+  int grid = (int)std::min<uint64_t>((uint64_t)c->tile_grid, p.nchunks ? p.nchunks : 1);
+  return cu(launch_step_tile(p, cur, next, grid, c->tile_threads, c->tile_smem, st));
+}
+
+template <class F>
+squeeze_status guarded(F&& f) {
+  try {
+    return f();
+  } catch (const std::bad_alloc&) {
+    return SQZ_E_NOMEM;
+  } catch (...) {
+    return SQZ_E_CONFIG;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* squeeze_version(void) { return "squeeze-b200 0.1 (sm_100a)"; }
+
+const char* squeeze_strerror(squeeze_status st) {
+  switch (st) {
+    case SQZ_OK: return "ok";
+    case SQZ_E_INVALID_SPEC: return "invalid fractal spec (S:29-33 invariants)";
+    case SQZ_E_OVERFLOW: return "level too large: s^r > 2^32 or k^r >= 2^62";
+    case SQZ_E_OUT_OF_BOUNDS: return "coordinate out of bounds";
+    case SQZ_E_HOLE: return "coordinate is a hole of the fractal";
+    case SQZ_E_INVALID_LEVEL: return "invalid level or tile level";
+    case SQZ_E_CONFIG: return "invalid configuration or argument";
+    case SQZ_E_CUDA: return "CUDA runtime error";
+    case SQZ_E_NO_DEVICE: return "host-only context: no device bound";
+    case SQZ_E_NOMEM: return "out of memory";
+    case SQZ_E_HALO: return "halo plan missed a needed out-of-shard neighbour";
+  }
+  return "unknown status";
+}
+
+squeeze_status squeeze_builtin_fractal(const char* name, uint32_t* k, uint32_t* s, uint8_t* tau_out, uint32_t cap) {
+  return guarded([&]() -> squeeze_status {
+    if (!name || !k || !s) return SQZ_E_CONFIG;
+    std::vector<uint8_t> tau;
+    if (!builtin_spec(name, *k, *s, tau)) return SQZ_E_INVALID_SPEC;
+    if (tau_out) {
+      if (cap < tau.size()) return SQZ_E_CONFIG;
+      std::memcpy(tau_out, tau.data(), tau.size());
+    }
+    return SQZ_OK;
+  });
+}
+
+squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r, const squeeze_rule* rule,
+                            const squeeze_shard* shard, const squeeze_options* opts, int device) {
+  return guarded([&]() -> squeeze_status {
+    if (!out_ctx || !f) return SQZ_E_CONFIG;
+    *out_ctx = nullptr;
+    Ctx* c = new Ctx();
+    auto fail = [&](squeeze_status st) {
+      free_device(c);
+      delete c;
+      return st;
+    };
+    int rc = make_spec(f->k, f->s, f->tau, c->f);
+    if (rc != SQZ_OK) return fail((squeeze_status)rc);
+    c->r = r;
+    c->rule = rule ? *rule : squeeze_rule{(uint16_t)(1u << 3), (uint16_t)((1u << 2) | (1u << 3))};
+    if ((c->rule.birth_mask | c->rule.survive_mask) & ~0x1FFu) return fail(SQZ_E_CONFIG);
+    if (shard) {
+      if (shard->nranks == 0 || shard->rank >= shard->nranks) return fail(SQZ_E_CONFIG);
+      c->rank = shard->rank;
+      c->nranks = shard->nranks;
+    }
+    if (opts) c->opts = *opts;
+    // checked geometry: coordinates fit 32 bits, Ω fits 62 bits
+    if (!checked_pow(c->f.s, r, 1ull << 32, c->n) || !checked_pow(c->f.k, r, (1ull << 62) - 1, c->V))
+      return fail(SQZ_E_OVERFLOW);
+    checked_pow(c->f.k, r / 2, ~0ull, c->cw);
+    checked_pow(c->f.k, (r + 1) / 2, ~0ull, c->ch);
+    uint32_t g = c->opts.tile_level ? c->opts.tile_level : auto_tile_level(c->f, r, 1024);
+    if (g > r) return fail(SQZ_E_INVALID_LEVEL);
+    rc = build_tile_tables(c->f, g, c->tt);
+    if (rc != SQZ_OK) return fail((squeeze_status)rc);
+    build_level_maps(c->f, r, c->full);
+    build_level_maps(c->f, r - g, c->coarse);
+    checked_pow(c->f.k, r - g, ~0ull, c->NT);
+    c->sr = shard_range(c->NT, c->tt.K, c->rank, c->nranks);
+    c->state_bytes = ((c->sr.omega_hi - c->sr.omega_lo) + 15) & ~15ull;
+    if (c->nranks > 1) {
+      unsigned th = std::max(1u, std::thread::hardware_concurrency());
+      halo_needs(c->tt, c->coarse.view, c->sr, c->needs, th);
+    }
+    c->device = device;
+    if (device >= 0) {
+      DevGuard dg(device);
+      if (cudaSetDevice(device) != cudaSuccess) return fail(SQZ_E_CUDA);
+      squeeze_status st;
+      if ((st = upload_maps(c->full, c->d_full)) != SQZ_OK) return fail(st);
+      if ((st = upload_maps(c->coarse, c->d_coarse)) != SQZ_OK) return fail(st);
+      if ((st = upload(&c->d_nbr, c->tt.nbr.data(), c->tt.nbr.size())) != SQZ_OK) return fail(st);
+      if ((st = upload(&c->d_link_j2, c->tt.link_j2.data(), c->tt.link_j2.size())) != SQZ_OK) return fail(st);
+      if ((st = upload(&c->d_link_dir, c->tt.link_dir.data(), c->tt.link_dir.size())) != SQZ_OK) return fail(st);
+      if ((st = upload(&c->d_needs, c->needs.data(), c->needs.size())) != SQZ_OK) return fail(st);
+      if (cudaMalloc((void**)&c->d_err, sizeof(int)) != cudaSuccess) return fail(SQZ_E_NOMEM);
+      if (cudaMemset(c->d_err, 0, sizeof(int)) != cudaSuccess) return fail(SQZ_E_CUDA);
+      // tile kernel launch shape: one warp per 32 cells of a tile, persistent CTAs
+      TileParams p{};
+      p.K = c->tt.K;
+      p.E = c->tt.E;
+      p.ndirs = c->tt.ndirs;
+      c->tile_smem = tile_smem_bytes(p);
+      uint32_t threads = c->opts.block_threads;
+      if (threads == 0) threads = (uint32_t)std::min<uint64_t>(1024, std::max<uint64_t>(128, (c->tt.K + 31) / 32 * 32));
+      if (threads % 32 || threads > 1024) return fail(SQZ_E_CONFIG);
+      c->tile_threads = (int)threads;
+      if (tile_kernel_attributes(c->tile_smem) != cudaSuccess) return fail(SQZ_E_CONFIG);
+      int occ = c->opts.ctas_per_sm ? (int)c->opts.ctas_per_sm : tile_occupancy(c->tile_threads, c->tile_smem);
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+      c->tile_grid = sms * std::max(1, occ);
+    }
+    *out_ctx = c;
+    return SQZ_OK;
+  });
+}
+
+void squeeze_destroy(void* ctx) {
+  if (!ctx) return;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  free_device(c);
+  delete c;
+}
+
+squeeze_status squeeze_geometry(const void* ctx, squeeze_geometry_t* out) {
+  if (!ctx || !out) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  std::memset(out, 0, sizeof(*out));
+  out->cells_total = c->V;
+  out->omega_lo = c->sr.omega_lo;
+  out->omega_hi = c->sr.omega_hi;
+  out->state_bytes = c->state_bytes;
+  out->n = c->n;
+  out->compact_w = c->cw;
+  out->compact_h = c->ch;
+  out->r = c->r;
+  out->tile_level = c->tt.g;
+  out->tile_cells = c->tt.K;
+  out->num_tiles = c->NT;
+  out->chunk_tiles = kChunkTiles;
+  out->remote_links = c->tt.E;
+  out->max_degree = c->tt.max_degree;
+  return SQZ_OK;
+}
+
+squeeze_status squeeze_shard_range(const void* ctx, uint32_t rank, uint64_t* lo, uint64_t* hi) {
+  if (!ctx || !lo || !hi) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (rank >= c->nranks) return SQZ_E_CONFIG;
+  ShardRange sr = shard_range(c->NT, c->tt.K, rank, c->nranks);
+  *lo = sr.omega_lo;
+  *hi = sr.omega_hi;
+  return SQZ_OK;
+}
+
+squeeze_status squeeze_lambda_host(const void* ctx, uint64_t omega, uint32_t* x, uint32_t* y) {
+  if (!ctx || !x || !y) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (omega >= c->V) return SQZ_E_OUT_OF_BOUNDS;
+  lambda_level(c->full.view, omega, *x, *y);
+  return SQZ_OK;
+}
+
+squeeze_status squeeze_nu_host(const void* ctx, uint64_t x, uint64_t y, uint64_t* omega) {
+  if (!ctx || !omega) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (x >= c->n || y >= c->n) return SQZ_E_OUT_OF_BOUNDS;
+  uint64_t om = nu_level(c->full.view, (int64_t)x, (int64_t)y);
+  if (om == kNoneU64) return SQZ_E_HOLE;
+  *omega = om;
+  return SQZ_OK;
+}
+
+squeeze_status squeeze_map_lambda(const void* ctx, const uint64_t* d_omega, uint32_t* d_x, uint32_t* d_y,
+                                  uint64_t count, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (c->device < 0) return SQZ_E_NO_DEVICE;
+  if (count && (!d_omega || !d_x || !d_y)) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return cu(launch_map_lambda(c->d_full.view, d_omega, d_x, d_y, count, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_map_nu(const void* ctx, const uint32_t* d_x, const uint32_t* d_y, uint64_t* d_omega,
+                              uint64_t count, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (c->device < 0) return SQZ_E_NO_DEVICE;
+  if (count && (!d_omega || !d_x || !d_y)) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return cu(launch_map_nu(c->d_full.view, d_x, d_y, d_omega, count, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_seed(const void* ctx, uint8_t* d_state, uint64_t seed, uint64_t q, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_state);
+  if (st != SQZ_OK) return st;
+  if (q > (1ull << 32)) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return cu(launch_seed(c->d_full.view, c->sr.omega_lo, c->sr.omega_hi - c->sr.omega_lo, c->state_bytes, d_state,
+                        seed, q, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_step(void* ctx, const uint8_t* d_cur, uint8_t* d_next, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_cur);
+  if (st == SQZ_OK) st = check_state(c, d_next);
+  if (st != SQZ_OK) return st;
+  if (d_cur == d_next) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return do_step(c, d_cur, d_next, (cudaStream_t)stream);
+}
+
+squeeze_status squeeze_step_naive(void* ctx, const uint8_t* d_cur, uint8_t* d_next, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_cur);
+  if (st == SQZ_OK) st = check_state(c, d_next);
+  if (st != SQZ_OK) return st;
+  if (d_cur == d_next) return SQZ_E_CONFIG;
+  if (c->nranks > 1 && !c->needs.empty() && c->d_recv == nullptr) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return cu(launch_step_naive(c->d_full.view, d_cur, d_next, c->sr.omega_hi - c->sr.omega_lo, c->state_bytes,
+                              c->rule.birth_mask, c->rule.survive_mask, halo_view(c), (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_run(void* ctx, uint8_t* d_a, uint8_t* d_b, uint64_t steps, int use_graph,
+                           squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_a);
+  if (st == SQZ_OK) st = check_state(c, d_b);
+  if (st != SQZ_OK) return st;
+  if (c->nranks > 1 || d_a == d_b) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t pairs = steps / 2;
+  if (use_graph && pairs > 0) {
+    if (!(c->graph && c->graph_a == d_a && c->graph_b == d_b && c->graph_stream == s)) {
+      if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+      }
+      cudaStream_t cap;
+      if (cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) return SQZ_E_CUDA;
+      cudaGraph_t graph;
+      if (cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaStreamDestroy(cap);
+        return SQZ_E_CUDA;
+      }
+      squeeze_status s1 = do_step(c, d_a, d_b, cap);
+      squeeze_status s2 = do_step(c, d_b, d_a, cap);
+      cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+      cudaStreamDestroy(cap);
+      if (s1 != SQZ_OK || s2 != SQZ_OK || ce != cudaSuccess) return SQZ_E_CUDA;
+      ce = cudaGraphInstantiate(&c->graph, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ce != cudaSuccess) return SQZ_E_CUDA;
+      c->graph_a = d_a;
+      c->graph_b = d_b;
+      c->graph_stream = s;
+    }
+    for (uint64_t i = 0; i < pairs; ++i)
+      if (cudaGraphLaunch(c->graph, s) != cudaSuccess) return SQZ_E_CUDA;
+  } else {
+    for (uint64_t i = 0; i < pairs; ++i) {
+      if ((st = do_step(c, d_a, d_b, s)) != SQZ_OK) return st;
+      if ((st = do_step(c, d_b, d_a, s)) != SQZ_OK) return st;
+    }
+  }
+  if (steps & 1) return do_step(c, d_a, d_b, s);
+  return SQZ_OK;
+}
+
+squeeze_status squeeze_run_host(void* ctx, uint8_t* h_state, uint8_t* d_a, uint8_t* d_b, uint64_t steps,
+                                squeeze_stream_t stream) {
+  if (!ctx || !h_state) return SQZ_E_CONFIG;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_a);
+  if (st == SQZ_OK) st = check_state(c, d_b);
+  if (st != SQZ_OK) return st;
+  DevGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(d_a, h_state, c->state_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return SQZ_E_CUDA;
+  if ((st = squeeze_run(ctx, d_a, d_b, steps, 0, stream)) != SQZ_OK) return st;
+  const uint8_t* fin = (steps & 1) ? d_b : d_a;
+  if (cudaMemcpyAsync(h_state, fin, c->state_bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) return SQZ_E_CUDA;
+  return cu(cudaStreamSynchronize(s));
+}
+
+squeeze_status squeeze_count_alive(const void* ctx, const uint8_t* d_state, uint64_t* d_out, squeeze_stream_t stream) {
+  if (!ctx || !d_out) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_state);
+  if (st != SQZ_OK) return st;
+  DevGuard g(c->device);
+  return cu(launch_count_alive(d_state, c->state_bytes, d_out, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_device_error(const void* ctx) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (c->device < 0) return SQZ_E_NO_DEVICE;
+  DevGuard g(c->device);
+  int flag = 0;
+  if (cudaDeviceSynchronize() != cudaSuccess) return SQZ_E_CUDA;
+  if (cudaMemcpy(&flag, c->d_err, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return SQZ_E_CUDA;
+  return flag ? SQZ_E_HALO : SQZ_OK;
+}
+
+squeeze_status squeeze_halo_needs(const void* ctx, uint64_t* out, uint64_t cap, uint64_t* count) {
+  if (!ctx || !count) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  *count = c->needs.size();
+  if (out) std::memcpy(out, c->needs.data(), std::min<uint64_t>(cap, c->needs.size()) * sizeof(uint64_t));
+  return SQZ_OK;
+}
+
+squeeze_status squeeze_halo_set_sends(void* ctx, const uint64_t* omegas, uint64_t count) {
+  return guarded([&]() -> squeeze_status {
+    if (!ctx || (count && !omegas)) return SQZ_E_CONFIG;
+    Ctx* c = static_cast<Ctx*>(ctx);
+    for (uint64_t i = 0; i < count; ++i)
+      if (omegas[i] < c->sr.omega_lo || omegas[i] >= c->sr.omega_hi) return SQZ_E_CONFIG;
+    c->sends.assign(omegas, omegas + count);
+    if (c->device >= 0) {
+      DevGuard g(c->device);
+      cudaFree(c->d_sends);
+      c->d_sends = nullptr;
+      return upload(&c->d_sends, c->sends.data(), c->sends.size());
+    }
+    return SQZ_OK;
+  });
+}
+
+squeeze_status squeeze_halo_bind(void* ctx, uint8_t* d_send, const uint8_t* d_recv) {
+  if (!ctx) return SQZ_E_CONFIG;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (c->device < 0) return SQZ_E_NO_DEVICE;
+  if ((!c->sends.empty() && !d_send) || (!c->needs.empty() && !d_recv)) return SQZ_E_CONFIG;
+  c->d_send = d_send;
+  c->d_recv = d_recv;
+  return SQZ_OK;
+}
+
+squeeze_status squeeze_halo_pack(const void* ctx, const uint8_t* d_cur, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_cur);
+  if (st != SQZ_OK) return st;
+  if (!c->sends.empty() && !c->d_send) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return cu(launch_halo_pack(d_cur, c->sr.omega_lo, c->d_sends, c->sends.size(), c->d_send, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_bb_bytes(const void* ctx, uint64_t* bytes) {
+  if (!ctx || !bytes) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (c->n > (1ull << 20)) return SQZ_E_OVERFLOW;
+  *bytes = c->n * c->n;
+  return SQZ_OK;
+}
+
+squeeze_status squeeze_bb_seed(const void* ctx, uint8_t* d_grid, uint64_t seed, uint64_t q, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_grid);
+  if (st != SQZ_OK) return st;
+  if (c->nranks > 1 || q > (1ull << 32) || c->n > (1ull << 20)) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return cu(launch_bb_seed(c->d_full.view, d_grid, seed, q, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_bb_step(const void* ctx, const uint8_t* d_cur, uint8_t* d_next, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_cur);
+  if (st == SQZ_OK) st = check_state(c, d_next);
+  if (st != SQZ_OK) return st;
+  if (c->nranks > 1 || d_cur == d_next || c->n > (1ull << 20)) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return cu(launch_bb_step(d_cur, d_next, c->n, c->rule.birth_mask, c->rule.survive_mask, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_bb_to_compact(const void* ctx, const uint8_t* d_grid, uint8_t* d_state,
+                                     squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_grid);
+  if (st == SQZ_OK) st = check_state(c, d_state);
+  if (st != SQZ_OK) return st;
+  if (c->nranks > 1) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return cu(launch_bb_to_compact(c->d_full.view, d_grid, d_state, c->state_bytes, (cudaStream_t)stream));
+}
+
+}  // extern "C"

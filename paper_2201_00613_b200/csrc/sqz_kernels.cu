@@ -1,0 +1,700 @@
+// sqz_kernels.cu — sm_100a kernels of the Squeeze hot path (arXiv 2201.00613).
+//
+// Kernels:
+//   k_map_lambda / k_map_nu   batched λ / ν with the multi-digit
+//                             lookup tables staged in shared memory
+//   k_seed                    initial state (reading D9) at (X, Y) = λ(Ω)
+//   k_step_naive              the paper's per-thread step: 1 λ + 8 (membership, ν,
+//                             gather) per cell — the literal comparison engine
+//   k_step_tile               the product step: 32 level-g tiles per work
+//                             unit, bit-sliced one tile per bit, one shared intra-tile
+//                             neighbour table, per-tile coarse λ + ν only for the tile
+//                             boundary links, TMA bulk copies in and out of shared memory
+//   k_count_alive, k_halo_pack, BB baseline (k_bb_seed, k_bb_step, k_bb_to_compact)
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sqz_kernels.cuh"
+
+namespace sqz {
+
+// ---------------------------------------------------------------------------------------
+// common device helpers
+
+__device__ __forceinline__ uint64_t seed_mix(uint64_t z) {
+  // splitmix64 finaliser (reading D9; same generator as sqz_inputs.mix)
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+__device__ __forceinline__ uint32_t seed_alive(uint32_t x, uint32_t y, uint64_t mseed, uint64_t q) {
+  uint64_t h = seed_mix((((uint64_t)x) << 32 | y) ^ mseed);
+  return (h >> 32) < q ? 1u : 0u;
+}
+
+// Copies a LevelMaps' four LUTs into shared memory and returns a view on them.
+__device__ __forceinline__ LevelMaps stage_maps(const LevelMaps& g, uint32_t* smem) {
+  LevelMaps m = g;
+  uint32_t* p = smem;
+  uint32_t n0 = g.n_lam_full, n1 = g.n_lam_tail, n2 = g.n_nu_full, n3 = g.n_nu_tail;
+  for (uint32_t i = threadIdx.x; i < n0; i += blockDim.x) p[i] = g.lam_full[i];
+  for (uint32_t i = threadIdx.x; i < n1; i += blockDim.x) p[n0 + i] = g.lam_tail[i];
+  for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) p[n0 + n1 + i] = g.nu_full[i];
+  for (uint32_t i = threadIdx.x; i < n3; i += blockDim.x) p[n0 + n1 + n2 + i] = g.nu_tail[i];
+  m.lam_full = p;
+  m.lam_tail = p + n0;
+  m.nu_full = p + n0 + n1;
+  m.nu_tail = p + n0 + n1 + n2;
+  __syncthreads();
+  return m;
+}
+
+__host__ __device__ inline size_t maps_smem_bytes(const LevelMaps& m) {
+  return (size_t)(m.n_lam_full + m.n_lam_tail + m.n_nu_full + m.n_nu_tail) * sizeof(uint32_t);
+}
+
+// State of a global Ω for a (possibly sharded) buffer: in-shard from `cur`, else from the
+// halo receive buffer (binary search over the sorted needs list).
+__device__ __forceinline__ uint32_t fetch_cell(const uint8_t* __restrict__ cur, uint64_t om, const HaloView& h) {
+  if (om >= h.omega_lo && om < h.omega_hi) return __ldg(cur + (om - h.omega_lo));
+  uint64_t lo = 0, hi = h.nneeds;
+  while (lo < hi) {
+    uint64_t mid = (lo + hi) >> 1;
+    uint64_t v = h.needs[mid];
+    if (v < om) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < h.nneeds && h.needs[lo] == om && h.recv != nullptr) return h.recv[lo];
+  if (h.err) atomicExch(h.err, 1);
+  return 0;
+}
+
+__device__ __forceinline__ uint32_t rule_byte(uint32_t alive, uint32_t count, uint32_t birth, uint32_t survive) {
+  return ((alive ? survive : birth) >> count) & 1u;
+}
+
+// ---------------------------------------------------------------------------------------
+// batched maps
+
+__global__ void k_map_lambda(LevelMaps gm, const uint64_t* __restrict__ om, uint32_t* __restrict__ xo,
+                             uint32_t* __restrict__ yo, uint64_t count) {
+  extern __shared__ uint32_t s_lut[];
+  LevelMaps m = stage_maps(gm, s_lut);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t w = om[i];
+    uint32_t x = 0xFFFFFFFFu, y = 0xFFFFFFFFu;
+    if (w < m.cells) lambda_level(m, w, x, y);
+    xo[i] = x;
+    yo[i] = y;
+  }
+}
+
+__global__ void k_map_nu(LevelMaps gm, const uint32_t* __restrict__ xi, const uint32_t* __restrict__ yi,
+                         uint64_t* __restrict__ om, uint64_t count) {
+  extern __shared__ uint32_t s_lut[];
+  LevelMaps m = stage_maps(gm, s_lut);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
+    om[i] = nu_level(m, (int64_t)xi[i], (int64_t)yi[i]);
+}
+
+// ---------------------------------------------------------------------------------------
+// seed: 4 cells per thread, one 32-bit store; bytes past the shard are zero padding
+
+__global__ void k_seed(LevelMaps gm, uint64_t omega_lo, uint64_t cells, uint64_t words, uint32_t* __restrict__ state,
+                       uint64_t mseed, uint64_t q) {
+  extern __shared__ uint32_t s_lut[];
+  LevelMaps m = stage_maps(gm, s_lut);
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words; w += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      uint64_t loc = w * 4 + b;
+      if (loc < cells) {
+        uint32_t x, y;
+        lambda_level(m, omega_lo + loc, x, y);
+        v |= seed_alive(x, y, mseed, q) << (8 * b);
+      }
+    }
+    state[w] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// literal per-cell step: one λ, eight (membership + ν), gather, rule
+
+__global__ void k_step_naive(LevelMaps gm, const uint8_t* __restrict__ cur, uint32_t* __restrict__ next,
+                             uint64_t cells, uint64_t words, uint32_t birth, uint32_t survive, HaloView halo) {
+  extern __shared__ uint32_t s_lut[];
+  LevelMaps m = stage_maps(gm, s_lut);
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words; w += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t out = 0;
+#pragma unroll 1
+    for (int b = 0; b < 4; ++b) {
+      uint64_t loc = w * 4 + b;
+      if (loc >= cells) break;
+      uint64_t om = halo.omega_lo + loc;
+      uint32_t x, y;
+      lambda_level(m, om, x, y);
+      uint32_t count = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint64_t nb = nu_level(m, (int64_t)x + moore_dx(i), (int64_t)y + moore_dy(i));
+        if (nb != kNoneU64) count += fetch_cell(cur, nb, halo);
+      }
+      out |= rule_byte(__ldg(cur + loc), count, birth, survive) << (8 * b);
+    }
+    next[w] = out;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// tile kernel
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_store_1d(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Bit-sliced rule: each bit position is an independent cell; (c3 c2 c1 c0) its member-
+// neighbour count (<= 8).  f(c) = bit c of `mask`, evaluated as a mux tree on c0..c3.
+__device__ __forceinline__ uint32_t mask_word(uint32_t mask, int v) { return ((mask >> v) & 1u) ? 0xFFFFFFFFu : 0u; }
+
+__device__ __forceinline__ uint32_t rule_bits(uint32_t mask, uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
+  uint32_t m0 = (mask_word(mask, 0) & ~c0) | (mask_word(mask, 1) & c0);
+  uint32_t m1 = (mask_word(mask, 2) & ~c0) | (mask_word(mask, 3) & c0);
+  uint32_t m2 = (mask_word(mask, 4) & ~c0) | (mask_word(mask, 5) & c0);
+  uint32_t m3 = (mask_word(mask, 6) & ~c0) | (mask_word(mask, 7) & c0);
+  uint32_t m4 = mask_word(mask, 8) & ~c0;
+  uint32_t n0 = (m0 & ~c1) | (m1 & c1);
+  uint32_t n1 = (m2 & ~c1) | (m3 & c1);
+  uint32_t n2 = m4 & ~c1;
+  uint32_t o0 = (n0 & ~c2) | (n1 & c2);
+  uint32_t o1 = n2 & ~c2;
+  return (o0 & ~c3) | (o1 & c3);
+}
+
+struct TileSmem {
+  uint8_t* in[2];
+  uint8_t* out;
+  uint32_t* Z;       // K state words, E remote words, zero word
+  uint32_t* W;       // K next words
+  uint16_t* nbr;     // K*8
+  int64_t* ntile[2]; // [ndirs][32] neighbour tile per lane, -1 = none
+  uint64_t* bar;     // 2 mbarriers
+};
+
+__host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
+
+__host__ __device__ inline size_t tile_chunk_bytes(uint64_t K) { return align16((size_t)K * kChunkTiles); }
+
+__host__ __device__ inline size_t tile_layout(const TileParams& p, uint8_t* base, TileSmem* s) {
+  size_t off = 0;
+  size_t cb = tile_chunk_bytes(p.K);
+  if (s) s->in[0] = base + off;
+  off += cb;
+  if (s) s->in[1] = base + off;
+  off += cb;
+  if (s) s->out = base + off;
+  off += cb;
+  if (s) s->Z = (uint32_t*)(base + off);
+  off += align16((size_t)(p.K + p.E + 1) * 4);
+  if (s) s->W = (uint32_t*)(base + off);
+  off += align16((size_t)p.K * 4);
+  if (s) s->nbr = (uint16_t*)(base + off);
+  off += align16((size_t)p.K * 16);
+  size_t nt = (size_t)(p.ndirs ? p.ndirs : 1) * kChunkTiles * 8;
+  if (s) s->ntile[0] = (int64_t*)(base + off);
+  off += nt;
+  if (s) s->ntile[1] = (int64_t*)(base + off);
+  off += nt;
+  if (s) s->bar = (uint64_t*)(base + off);
+  off += 16;
+  return off;
+}
+
+size_t tile_smem_bytes(const TileParams& p) { return tile_layout(p, nullptr, nullptr); }
+
+// Lane i: coarse λ of tile (chunk*32 + i) and ν of its neighbour tiles (one per direction).
+__device__ __forceinline__ void compute_ntile(const TileParams& p, uint64_t chunk, int64_t* dst, int lane) {
+  uint64_t t = p.tile_lo + chunk * kChunkTiles + lane;
+  if (t < p.tile_hi) {
+    uint32_t X, Y;
+    lambda_level(p.coarse, t, X, Y);
+    for (uint32_t d = 0; d < p.ndirs; ++d) {
+      uint64_t nt = nu_level(p.coarse, (int64_t)X + p.dir_dx[d], (int64_t)Y + p.dir_dy[d]);
+      dst[d * kChunkTiles + lane] = (nt == kNoneU64) ? -1 : (int64_t)nt;
+    }
+  } else {
+    for (uint32_t d = 0; d < p.ndirs; ++d) dst[d * kChunkTiles + lane] = -1;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_step_tile(TileParams p, const uint8_t* __restrict__ cur,
+                                                    uint8_t* __restrict__ next) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  TileSmem S;
+  tile_layout(p, smem_raw, &S);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t K = (uint32_t)p.K;
+  const uint32_t nblk = (K + 31) / 32;
+
+  // one-time: neighbour table to shared memory, zero word, barriers
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(p.nbr);
+    uint4* dst = reinterpret_cast<uint4*>(S.nbr);
+    for (uint32_t i = tid; i < K; i += blockDim.x) dst[i] = src[i];
+  }
+  if (tid == 0) {
+    S.Z[p.zslot] = 0;
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  uint64_t chunk = blockIdx.x;
+  if (chunk < p.nchunks) {
+    if (tid == 0) {
+      uint64_t t0 = p.tile_lo + chunk * kChunkTiles;
+      uint64_t nt = min((uint64_t)kChunkTiles, p.tile_hi - t0);
+      tma_load_1d(S.in[0], cur + chunk * kChunkTiles * p.K, (uint32_t)align16(nt * p.K), &S.bar[0]);
+    }
+    if (warp == nwarps - 1) compute_ntile(p, chunk, S.ntile[0], lane);
+  }
+  __syncthreads();
+
+  uint32_t it = 0;
+  for (; chunk < p.nchunks; chunk += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const uint64_t t0 = p.tile_lo + chunk * kChunkTiles;
+    const uint32_t nt = (uint32_t)min((uint64_t)kChunkTiles, p.tile_hi - t0);
+    const uint64_t nxt = chunk + gridDim.x;
+    if (nxt < p.nchunks) {
+      if (tid == 0) {
+        uint64_t n0 = p.tile_lo + nxt * kChunkTiles;
+        uint64_t nn = min((uint64_t)kChunkTiles, p.tile_hi - n0);
+        fence_proxy_async();
+        tma_load_1d(S.in[buf ^ 1], cur + nxt * kChunkTiles * p.K, (uint32_t)align16(nn * p.K), &S.bar[buf ^ 1]);
+      }
+      if (warp == nwarps - 1) compute_ntile(p, nxt, S.ntile[buf ^ 1], lane);
+    }
+    mbar_wait(&S.bar[buf], (it >> 1) & 1);
+    const uint8_t* inb = S.in[buf];
+
+    // Phase A: byte tiles -> bit-sliced words, Z[j] bit i = cell j of tile i
+    for (uint32_t jb = warp; jb < nblk; jb += nwarps) {
+      uint32_t mine = 0;
+      const uint8_t* src = inb + (size_t)lane * K + jb * 32;
+      const bool active = lane < nt;
+#pragma unroll 8
+      for (int jj = 0; jj < 32; ++jj) {
+        if (jb * 32 + jj < K) {
+          uint32_t v = active ? src[jj] : 0u;
+          uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
+          mine = (lane == jj) ? bal : mine;
+        }
+      }
+      if (jb * 32 + lane < K) S.Z[jb * 32 + lane] = mine;
+    }
+    // Phase B: one bit-sliced word per tile-boundary link (neighbour tile's cell j2)
+    {
+      const int64_t* ntl = S.ntile[buf];
+      for (uint32_t e = warp; e < p.E; e += nwarps) {
+        uint32_t d = p.link_dir[e], j2 = p.link_j2[e];
+        int64_t tn = ntl[d * kChunkTiles + lane];
+        uint32_t v = 0;
+        if (tn >= 0) {
+          uint64_t tu = (uint64_t)tn;
+          if (tu >= t0 && tu < t0 + nt) v = inb[(size_t)(tu - t0) * K + j2];
+          else v = fetch_cell(cur, tu * p.K + j2, p.halo);
+        }
+        uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
+        if (lane == 0) S.Z[K + e] = bal;
+      }
+    }
+    __syncthreads();
+
+    // Phase C: bit-sliced neighbour count and rule, 32 tiles per word
+    const uint32_t live_lanes = nt >= 32 ? 0xFFFFFFFFu : ((1u << nt) - 1u);
+    for (uint32_t j = tid; j < K; j += blockDim.x) {
+      uint4 row = reinterpret_cast<const uint4*>(S.nbr)[j];
+      uint32_t idx[8] = {row.x & 0xFFFFu, row.x >> 16, row.y & 0xFFFFu, row.y >> 16,
+                         row.z & 0xFFFFu, row.z >> 16, row.w & 0xFFFFu, row.w >> 16};
+      uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+      for (int d = 0; d < 8; ++d) {
+        if (d < (int)p.dmax) {
+          uint32_t x = S.Z[idx[d]];
+          uint32_t t1 = c0 & x;
+          c0 ^= x;
+          uint32_t t2 = c1 & t1;
+          c1 ^= t1;
+          uint32_t t3 = c2 & t2;
+          c2 ^= t2;
+          c3 |= t3;
+        }
+      }
+      uint32_t a = S.Z[j];
+      uint32_t nw = (a & rule_bits(p.survive, c0, c1, c2, c3)) | (~a & rule_bits(p.birth, c0, c1, c2, c3));
+      S.W[j] = nw & live_lanes;
+    }
+    if (tid == 0) bulk_wait_read_all();  // previous chunk's bulk store has read S.out
+    __syncthreads();
+
+    // Phase D: bit-sliced words -> byte tiles
+    for (uint32_t jb = warp; jb < nblk; jb += nwarps) {
+      uint32_t w = (jb * 32 + lane < K) ? S.W[jb * 32 + lane] : 0u;
+      uint8_t* dst = S.out + (size_t)lane * K + jb * 32;
+      const bool active = lane < nt;
+#pragma unroll 8
+      for (int jj = 0; jj < 32; ++jj) {
+        if (jb * 32 + jj < K) {
+          uint32_t b = __shfl_sync(0xFFFFFFFFu, w, jj);
+          if (active) dst[jj] = (uint8_t)((b >> lane) & 1u);
+        }
+      }
+    }
+    const uint32_t bytes = nt * K;
+    const uint32_t padded = (uint32_t)align16(bytes);
+    for (uint32_t i = bytes + tid; i < padded; i += blockDim.x) S.out[i] = 0;
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) tma_store_1d(next + chunk * kChunkTiles * p.K, S.out, padded);
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------------------
+// alive count, halo pack
+
+__global__ void k_count_alive(const uint4* __restrict__ st, uint64_t n16, const uint8_t* __restrict__ tail,
+                              uint32_t ntail, unsigned long long* __restrict__ out) {
+  uint64_t acc = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 v = st[i];
+    uint32_t s = __dp4a(v.x, 0x01010101u, 0u);
+    s = __dp4a(v.y, 0x01010101u, s);
+    s = __dp4a(v.z, 0x01010101u, s);
+    s = __dp4a(v.w, 0x01010101u, s);
+    acc += s;
+  }
+  if (blockIdx.x == 0)
+    for (uint32_t i = threadIdx.x; i < ntail; i += blockDim.x) acc += tail[i];
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  __shared__ unsigned long long red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    unsigned long long v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0ull;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if (threadIdx.x == 0) atomicAdd(out, v);
+  }
+}
+
+__global__ void k_halo_pack(const uint8_t* __restrict__ cur, uint64_t omega_lo, const uint64_t* __restrict__ sends,
+                            uint64_t n, uint8_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = cur[sends[i] - omega_lo];
+}
+
+// ---------------------------------------------------------------------------------------
+// BB baseline: expanded n x n grid, 0 dead / 1 alive / 2 hole ("BB")
+
+__global__ void k_bb_seed(LevelMaps gm, uint8_t* __restrict__ grid, uint64_t n, uint64_t mseed, uint64_t q) {
+  extern __shared__ uint32_t s_lut[];
+  LevelMaps m = stage_maps(gm, s_lut);
+  uint64_t total = n * n;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t y = i / n, x = i - y * n;
+    uint64_t om = nu_level(m, (int64_t)x, (int64_t)y);
+    grid[i] = (om == kNoneU64) ? 2 : (uint8_t)seed_alive((uint32_t)x, (uint32_t)y, mseed, q);
+  }
+}
+
+__device__ __forceinline__ uint32_t alive_bytes(uint32_t v) { return v & ~(v >> 1) & 0x01010101u; }
+
+// 16 cells of one row per thread; n % 16 == 0.
+__global__ void k_bb_step16(const uint8_t* __restrict__ cur, uint8_t* __restrict__ next, uint64_t n, uint32_t birth,
+                            uint32_t survive) {
+  uint64_t per_row = n / 16;
+  uint64_t total = per_row * n;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t y = i / per_row, x0 = (i - y * per_row) * 16;
+    uint32_t A[3][6];  // rows y-1, y, y+1: [0] = left byte, [1..4] = words, [5] = right byte
+    uint32_t mid_raw[4];
+#pragma unroll
+    for (int rr = 0; rr < 3; ++rr) {
+      int64_t yy = (int64_t)y + rr - 1;
+      if (yy < 0 || yy >= (int64_t)n) {
+#pragma unroll
+        for (int q = 0; q < 6; ++q) A[rr][q] = 0;
+        if (rr == 1) mid_raw[0] = mid_raw[1] = mid_raw[2] = mid_raw[3] = 0;
+        continue;
+      }
+      const uint8_t* row = cur + (uint64_t)yy * n;
+      uint4 v = __ldg(reinterpret_cast<const uint4*>(row + x0));
+      if (rr == 1) {
+        mid_raw[0] = v.x; mid_raw[1] = v.y; mid_raw[2] = v.z; mid_raw[3] = v.w;
+      }
+      A[rr][1] = alive_bytes(v.x);
+      A[rr][2] = alive_bytes(v.y);
+      A[rr][3] = alive_bytes(v.z);
+      A[rr][4] = alive_bytes(v.w);
+      uint32_t l = x0 > 0 ? __ldg(row + x0 - 1) : 0u;
+      uint32_t r = x0 + 16 < n ? __ldg(row + x0 + 16) : 0u;
+      A[rr][0] = (l == 1u) ? 1u : 0u;
+      A[rr][5] = (r == 1u) ? 1u : 0u;
+    }
+    uint32_t out[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int rr = 0; rr < 3; ++rr) {
+        uint32_t c = A[rr][w + 1];
+        uint32_t prev_top = (w == 0) ? A[rr][0] : (A[rr][w] >> 24);
+        uint32_t next_low = (w == 3) ? A[rr][5] : (A[rr][w + 2] & 0xFFu);
+        uint32_t left = (c << 8) | prev_top;
+        uint32_t right = (c >> 8) | (next_low << 24);
+        cnt += left + right + (rr == 1 ? 0u : c);
+      }
+      uint32_t raw = mid_raw[w];
+      uint32_t o = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        uint32_t v = (raw >> (8 * b)) & 0xFFu;
+        uint32_t c = (cnt >> (8 * b)) & 0xFFu;
+        uint32_t nb = (v == 2u) ? 2u : rule_byte(v, c, birth, survive);
+        o |= nb << (8 * b);
+      }
+      out[w] = o;
+    }
+    *reinterpret_cast<uint4*>(next + y * n + x0) = make_uint4(out[0], out[1], out[2], out[3]);
+  }
+}
+
+// generic per-cell BB step (n < 16 or n % 16 != 0)
+__global__ void k_bb_step1(const uint8_t* __restrict__ cur, uint8_t* __restrict__ next, uint64_t n, uint32_t birth,
+                           uint32_t survive) {
+  uint64_t total = n * n;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    int64_t y = (int64_t)(i / n), x = (int64_t)(i - (uint64_t)y * n);
+    uint32_t v = cur[i];
+    if (v == 2u) {
+      next[i] = 2;
+      continue;
+    }
+    uint32_t c = 0;
+    for (int d = 0; d < 8; ++d) {
+      int64_t xx = x + moore_dx(d), yy = y + moore_dy(d);
+      if (xx >= 0 && yy >= 0 && xx < (int64_t)n && yy < (int64_t)n) c += cur[(uint64_t)yy * n + xx] == 1u;
+    }
+    next[i] = (uint8_t)rule_byte(v, c, birth, survive);
+  }
+}
+
+__global__ void k_bb_to_compact(LevelMaps gm, const uint8_t* __restrict__ grid, uint8_t* __restrict__ st,
+                                uint64_t cells, uint64_t state_bytes) {
+  extern __shared__ uint32_t s_lut[];
+  LevelMaps m = stage_maps(gm, s_lut);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < state_bytes;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint8_t v = 0;
+    if (i < cells) {
+      uint32_t x, y;
+      lambda_level(m, i, x, y);
+      v = grid[(uint64_t)y * m.n + x];
+    }
+    st[i] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// launchers
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+static unsigned grid_for(uint64_t work, int threads, int per_sm = 8) {
+  uint64_t blocks = (work + threads - 1) / threads;
+  uint64_t cap = (uint64_t)num_sms() * per_sm;
+  if (blocks > cap) blocks = cap;
+  if (blocks == 0) blocks = 1;
+  return (unsigned)blocks;
+}
+
+static cudaError_t maps_attr(const void* fn, size_t smem) {
+  if (smem > 48 * 1024) return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return cudaSuccess;
+}
+
+cudaError_t launch_map_lambda(const LevelMaps& m, const uint64_t* om, uint32_t* x, uint32_t* y, uint64_t count,
+                              cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  size_t sm = maps_smem_bytes(m);
+  cudaError_t e = maps_attr((const void*)k_map_lambda, sm);
+  if (e != cudaSuccess) return e;
+  k_map_lambda<<<grid_for(count, 256), 256, sm, st>>>(m, om, x, y, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_map_nu(const LevelMaps& m, const uint32_t* x, const uint32_t* y, uint64_t* om, uint64_t count,
+                          cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  size_t sm = maps_smem_bytes(m);
+  cudaError_t e = maps_attr((const void*)k_map_nu, sm);
+  if (e != cudaSuccess) return e;
+  k_map_nu<<<grid_for(count, 256), 256, sm, st>>>(m, x, y, om, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_seed(const LevelMaps& m, uint64_t omega_lo, uint64_t cells, uint64_t state_bytes, uint8_t* state,
+                        uint64_t seed, uint64_t q, cudaStream_t st) {
+  uint64_t words = state_bytes / 4;
+  if (words == 0) return cudaSuccess;
+  size_t sm = maps_smem_bytes(m);
+  cudaError_t e = maps_attr((const void*)k_seed, sm);
+  if (e != cudaSuccess) return e;
+  uint64_t mseed = 0;
+  {  // host splitmix64 finaliser of the seed
+    uint64_t z = seed;
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    mseed = z;
+  }
+  k_seed<<<grid_for(words, 256), 256, sm, st>>>(m, omega_lo, cells, words, reinterpret_cast<uint32_t*>(state), mseed,
+                                                 q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step_naive(const LevelMaps& m, const uint8_t* cur, uint8_t* next, uint64_t cells,
+                              uint64_t state_bytes, uint32_t birth, uint32_t survive, const HaloView& halo,
+                              cudaStream_t st) {
+  uint64_t words = state_bytes / 4;
+  if (words == 0) return cudaSuccess;
+  size_t sm = maps_smem_bytes(m);
+  cudaError_t e = maps_attr((const void*)k_step_naive, sm);
+  if (e != cudaSuccess) return e;
+  k_step_naive<<<grid_for(words, 256), 256, sm, st>>>(m, cur, reinterpret_cast<uint32_t*>(next), cells, words, birth,
+                                                       survive, halo);
+  return cudaGetLastError();
+}
+
+cudaError_t tile_kernel_attributes(size_t smem) {
+  return cudaFuncSetAttribute((const void*)k_step_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+int tile_occupancy(int threads, size_t smem) {
+  int blocks = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_step_tile, threads, smem) != cudaSuccess) return 1;
+  return blocks > 0 ? blocks : 1;
+}
+
+cudaError_t launch_step_tile(const TileParams& p, const uint8_t* cur, uint8_t* next, int grid, int threads,
+                             size_t smem, cudaStream_t st) {
+  if (p.nchunks == 0) return cudaSuccess;
+  k_step_tile<<<grid, threads, smem, st>>>(p, cur, next);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count_alive(const uint8_t* state, uint64_t bytes, uint64_t* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(uint64_t), st);
+  if (e != cudaSuccess) return e;
+  uint64_t n16 = bytes / 16;
+  uint32_t ntail = (uint32_t)(bytes - n16 * 16);
+  k_count_alive<<<grid_for(n16 ? n16 : 1, 256, 4), 256, 0, st>>>(reinterpret_cast<const uint4*>(state), n16,
+                                                                  state + n16 * 16, ntail,
+                                                                  reinterpret_cast<unsigned long long*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_halo_pack(const uint8_t* cur, uint64_t omega_lo, const uint64_t* sends, uint64_t nsends,
+                             uint8_t* out, cudaStream_t st) {
+  if (nsends == 0) return cudaSuccess;
+  k_halo_pack<<<grid_for(nsends, 256), 256, 0, st>>>(cur, omega_lo, sends, nsends, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bb_seed(const LevelMaps& m, uint8_t* grid, uint64_t seed, uint64_t q, cudaStream_t st) {
+  size_t sm = maps_smem_bytes(m);
+  cudaError_t e = maps_attr((const void*)k_bb_seed, sm);
+  if (e != cudaSuccess) return e;
+  uint64_t z = seed;
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  k_bb_seed<<<grid_for(m.n * m.n, 256), 256, sm, st>>>(m, grid, m.n, z, q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bb_step(const uint8_t* cur, uint8_t* next, uint64_t n, uint32_t birth, uint32_t survive,
+                           cudaStream_t st) {
+  if (n % 16 == 0) {
+    k_bb_step16<<<grid_for(n * n / 16, 256), 256, 0, st>>>(cur, next, n, birth, survive);
+  } else {
+    k_bb_step1<<<grid_for(n * n, 256), 256, 0, st>>>(cur, next, n, birth, survive);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bb_to_compact(const LevelMaps& m, const uint8_t* grid, uint8_t* state, uint64_t state_bytes,
+                                 cudaStream_t st) {
+  size_t sm = maps_smem_bytes(m);
+  cudaError_t e = maps_attr((const void*)k_bb_to_compact, sm);
+  if (e != cudaSuccess) return e;
+  k_bb_to_compact<<<grid_for(state_bytes, 256), 256, sm, st>>>(m, grid, state, m.cells, state_bytes);
+  return cudaGetLastError();
+}
+
+}  // namespace sqz

@@ -1,0 +1,60 @@
+// sqz_kernels.cuh — kernel parameter blocks and launcher declarations (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sqz_common.h"
+
+namespace sqz {
+
+struct HaloView {
+  uint64_t omega_lo, omega_hi;  // this shard
+  const uint64_t* needs;        // sorted Ω outside the shard
+  uint64_t nneeds;
+  const uint8_t* recv;          // recv[i] = state of needs[i]
+  int* err;                     // set to 1 on a halo miss
+};
+
+struct TileParams {
+  LevelMaps coarse;  // maps at level r - g (tile coordinates)
+  uint64_t K;        // cells per tile
+  uint32_t E;        // remote links per tile
+  uint32_t zslot;    // index of the zero word in Z
+  uint32_t dmax;     // max neighbour entries per cell
+  uint32_t ndirs;
+  int dir_dx[8], dir_dy[8];
+  const uint16_t* nbr;       // K*8
+  const uint32_t* link_j2;   // E
+  const uint8_t* link_dir;   // E
+  uint64_t tile_lo, tile_hi, nchunks;
+  uint32_t birth, survive;
+  HaloView halo;
+};
+
+// Shared-memory bytes the tile kernel needs for these parameters.
+size_t tile_smem_bytes(const TileParams& p);
+cudaError_t tile_kernel_attributes(size_t smem);
+int tile_occupancy(int threads, size_t smem);
+
+cudaError_t launch_map_lambda(const LevelMaps& m, const uint64_t* om, uint32_t* x, uint32_t* y, uint64_t count,
+                              cudaStream_t st);
+cudaError_t launch_map_nu(const LevelMaps& m, const uint32_t* x, const uint32_t* y, uint64_t* om, uint64_t count,
+                          cudaStream_t st);
+cudaError_t launch_seed(const LevelMaps& m, uint64_t omega_lo, uint64_t cells, uint64_t state_bytes, uint8_t* state,
+                        uint64_t seed, uint64_t q, cudaStream_t st);
+cudaError_t launch_step_naive(const LevelMaps& m, const uint8_t* cur, uint8_t* next, uint64_t cells,
+                              uint64_t state_bytes, uint32_t birth, uint32_t survive, const HaloView& halo,
+                              cudaStream_t st);
+cudaError_t launch_step_tile(const TileParams& p, const uint8_t* cur, uint8_t* next, int grid, int threads,
+                             size_t smem, cudaStream_t st);
+cudaError_t launch_count_alive(const uint8_t* state, uint64_t bytes, uint64_t* out, cudaStream_t st);
+cudaError_t launch_halo_pack(const uint8_t* cur, uint64_t omega_lo, const uint64_t* sends, uint64_t nsends,
+                             uint8_t* out, cudaStream_t st);
+cudaError_t launch_bb_seed(const LevelMaps& m, uint8_t* grid, uint64_t seed, uint64_t q, cudaStream_t st);
+cudaError_t launch_bb_step(const uint8_t* cur, uint8_t* next, uint64_t n, uint32_t birth, uint32_t survive,
+                           cudaStream_t st);
+cudaError_t launch_bb_to_compact(const LevelMaps& m, const uint8_t* grid, uint8_t* state, uint64_t state_bytes,
+                                 cudaStream_t st);
+
+}  // namespace sqz

@@ -1,0 +1,99 @@
+"""Data-parallel sharding of the compact array across ranks.
+
+Ω is split into contiguous, chunk-aligned ranges, one per rank (squeeze_shard_range).
+Sierpinski sub-triangles touch only at corners, so a shard needs only a handful of
+out-of-shard neighbour states per step (the halo plan, squeeze_halo_needs).  Per step:
+
+    squeeze_halo_pack(cur)             library kernel: send[i] = cur[sends[i]]
+    all_to_all_single(recv, send)      torch.distributed (NCCL over NVLink on GPUs)
+    squeeze_step(cur, next)            library kernel: reads out-of-shard cells from recv
+
+``HaloExchange`` is the pure plumbing (who sends which Ω to whom, and the per-step
+collective); it works on CPU tensors with gloo as on CUDA tensors with NCCL, so the
+multi-rank logic is tested without GPUs.  ``ShardedSqueeze`` binds it to the library.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import B3S23, Fractal, Squeeze
+
+
+class HaloExchange:
+    """Request/response plan of the halo, built once with two all_to_all collectives.
+
+    needs:  sorted global Ω this rank reads but does not own (library plan)
+    ranges: [(lo, hi)] of every rank
+    After construction:
+      sends        Ω this rank must send each step, grouped by destination rank
+      send_counts  per destination;  recv_counts per source (recv order == needs order)
+    """
+
+    def __init__(self, needs: np.ndarray, ranges: list, rank: int, nranks: int, device, group=None):
+        self.rank, self.nranks, self.group, self.device = rank, nranks, group, device
+        needs = np.asarray(needs, dtype=np.int64)
+        his = np.array([hi for _, hi in ranges], dtype=np.int64)
+        owner = np.searchsorted(his, needs, side="right")
+        if needs.size and (owner >= nranks).any():
+            raise ValueError("needed cell outside every shard")
+        if needs.size and (owner == rank).any():
+            raise ValueError("halo plan lists an owned cell")
+        # needs are sorted and shards contiguous, so grouping by owner keeps the needs order
+        self.recv_counts = [int((owner == p).sum()) for p in range(nranks)]
+        req_counts = torch.tensor(self.recv_counts, dtype=torch.int64, device=device)
+        got_counts = torch.empty(nranks, dtype=torch.int64, device=device)
+        dist.all_to_all_single(got_counts, req_counts, group=group)
+        self.send_counts = [int(v) for v in got_counts.cpu()]
+        req = torch.from_numpy(needs).to(device)
+        sends = torch.empty(sum(self.send_counts), dtype=torch.int64, device=device)
+        dist.all_to_all_single(sends, req, output_split_sizes=self.send_counts,
+                               input_split_sizes=self.recv_counts, group=group)
+        self.sends = sends.cpu().numpy().astype(np.uint64)
+        lo, hi = ranges[rank]
+        if self.sends.size and ((self.sends < lo).any() or (self.sends >= hi).any()):
+            raise ValueError("peer requested a cell this rank does not own")
+        self.send_buf = torch.zeros(max(1, int(self.sends.size)), dtype=torch.uint8, device=device)
+        self.recv_buf = torch.zeros(max(1, int(needs.size)), dtype=torch.uint8, device=device)
+        self.nneeds = int(needs.size)
+
+    def exchange(self) -> None:
+        """recv_buf[needs order] <- peers' packed send_bufs (one collective per step)."""
+        if self.nranks == 1:
+            return
+        n_send = int(self.sends.size)
+        dist.all_to_all_single(self.recv_buf[:self.nneeds], self.send_buf[:n_send],
+                               output_split_sizes=self.recv_counts, input_split_sizes=self.send_counts,
+                               group=self.group)
+
+
+class ShardedSqueeze:
+    """One rank's shard of a level-r fractal: library context + halo exchange."""
+
+    def __init__(self, fractal: Fractal, r: int, rank: int, nranks: int, device: int, rule=B3S23,
+                 group=None, **opts):
+        self.sq = Squeeze(fractal, r, rule=rule, rank=rank, nranks=nranks, device=device, **opts)
+        self.geometry = self.sq.geometry
+        ranges = [self.sq.shard_range(p) for p in range(nranks)]
+        self.halo = HaloExchange(self.sq.halo_needs(), ranges, rank, nranks, torch.device(f"cuda:{device}"),
+                                 group)
+        self.sq.halo_set_sends(self.halo.sends)
+        self.sq.halo_bind(self.halo.send_buf, self.halo.recv_buf)
+
+    def new_state(self):
+        return self.sq.new_state()
+
+    def seed(self, state, seed=42, density=0.5):
+        self.sq.seed(state, seed, density)
+
+    def step(self, cur, nxt, naive: bool = False):
+        self.sq.halo_pack(cur)
+        self.halo.exchange()
+        (self.sq.step_naive if naive else self.sq.step)(cur, nxt)
+
+    def run(self, a, b, steps: int):
+        for i in range(steps):
+            cur, nxt = (a, b) if i % 2 == 0 else (b, a)
+            self.step(cur, nxt)
+        return b if steps % 2 else a

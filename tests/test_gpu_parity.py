@@ -1,0 +1,360 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+All state and indexing are integers, so the bar is bit-exact everywhere.  Inputs are
+seeded and synthetic (reading D9); every expected value comes from ``oracle/`` (or a
+closed form), never from the CUDA path.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2201_00613_b200 as sq
+import sqz_inputs
+from oracle import automaton as A
+from oracle import construction
+from oracle.fractals import BUILTINS, SIERPINSKI
+
+pytestmark = pytest.mark.gpu
+
+DEV = 0
+
+
+def mk(name, r, **kw):
+    return sq.Squeeze(sq.builtin_fractal(name), r, device=DEV, **kw)
+
+
+def host(t, n):
+    torch.cuda.synchronize()
+    return t[:n].cpu().numpy()
+
+
+def oracle_run(name, r, seed, density, steps, rule=A.B3S23):
+    o = BUILTINS[name]
+    cur = A.seed_compact(o, r, seed, density)
+    out = [cur]
+    for _ in range(steps):
+        cur = A.compact_step(o, r, cur, rule)
+        out.append(cur)
+    return out
+
+
+# ------------------------------------------------------------------ maps
+@pytest.mark.parametrize("name,rmax", [("sierpinski-triangle", 9), ("sierpinski-carpet", 4), ("vicsek", 4),
+                                       ("empty-bottles", 4), ("full-square", 5)])
+def test_maps_exhaustive(name, rmax):
+    o = BUILTINS[name]
+    for r in range(rmax + 1):
+        p = mk(name, r)
+        xs, ys = construction.construction_table(o, r)
+        om = torch.arange(o.k ** r + 3, dtype=torch.int64, device="cuda")
+        x, y = p.map_lambda(om)
+        x, y = x.cpu().numpy().astype(np.int64), y.cpu().numpy().astype(np.int64)
+        assert np.array_equal(x[:o.k ** r], xs) and np.array_equal(y[:o.k ** r], ys)
+        assert (x[o.k ** r:] == -1).all()  # out of range -> UINT32_MAX
+        n = o.s ** r
+        gy, gx = np.meshgrid(np.arange(n + 1), np.arange(n + 1), indexing="ij")
+        tx = torch.from_numpy(gx.ravel().astype(np.int32)).cuda()
+        ty = torch.from_numpy(gy.ravel().astype(np.int32)).cuda()
+        got = p.map_nu(tx, ty).cpu().numpy().reshape(n + 1, n + 1)
+        e = construction.inverse_table(o, r)
+        assert np.array_equal(got[:n, :n], e)  # -1 == UINT64_MAX on holes
+        assert (got[n, :] == -1).all() and (got[:, n] == -1).all()
+
+
+@pytest.mark.parametrize("name,r", [("sierpinski-triangle", 22), ("sierpinski-triangle", 24),
+                                    ("sierpinski-triangle", 32), ("sierpinski-carpet", 10), ("empty-bottles", 11)])
+def test_maps_sampled_large(name, r):
+    o = BUILTINS[name]
+    p = mk(name, r)
+    om = sqz_inputs.random_indices(200_000, o.k ** r, seed=r).astype(np.int64)
+    wx, wy = A.lambda_omega_np(o, r, om)
+    x, y = p.map_lambda(torch.from_numpy(om).cuda())
+    assert np.array_equal(x.cpu().numpy().astype(np.uint32), wx.astype(np.uint32))
+    assert np.array_equal(y.cpu().numpy().astype(np.uint32), wy.astype(np.uint32))
+    back = p.map_nu(x, y).cpu().numpy()
+    assert np.array_equal(back, om)
+    rx, ry = sqz_inputs.random_coords(200_000, min(o.s ** r, 2 ** 31 - 1), seed=r + 1)
+    want = A.nu_omega_np(o, r, rx.astype(np.int64), ry.astype(np.int64))
+    got = p.map_nu(torch.from_numpy(rx.astype(np.int32)).cuda(), torch.from_numpy(ry.astype(np.int32)).cuda())
+    assert np.array_equal(got.cpu().numpy(), want)
+
+
+# ------------------------------------------------------------------ seed
+@pytest.mark.parametrize("name,r", [("sierpinski-triangle", 10), ("sierpinski-carpet", 4), ("empty-bottles", 4)])
+def test_seed_full(name, r):
+    p = mk(name, r)
+    st = p.new_state()
+    p.seed(st, 42, 0.3)
+    g = p.geometry
+    got = host(st, g.state_bytes)
+    assert np.array_equal(got[:g.cells_total], A.seed_compact(BUILTINS[name], r, 42, 0.3))
+    assert not got[g.cells_total:].any()
+
+
+# ------------------------------------------------------------------ the step, small levels, every step
+@pytest.mark.parametrize("engine", ["tile", "naive"])
+def test_config_c1_r8_10_steps(engine):
+    """BASELINE config[0]: Sierpinski r=8, 10 steps, full compare every step."""
+    p = mk("sierpinski-triangle", 8)
+    want = oracle_run("sierpinski-triangle", 8, 42, 0.3, 10)
+    a, b = p.new_state(), p.new_state()
+    p.seed(a, 42, 0.3)
+    for t in range(10):
+        (p.step if engine == "tile" else p.step_naive)(a, b)
+        assert np.array_equal(host(b, 3 ** 8), want[t + 1]), f"step {t + 1}"
+        a, b = b, a
+
+
+@pytest.mark.parametrize("name,r,g", [
+    ("sierpinski-triangle", 0, 0), ("sierpinski-triangle", 1, 1), ("sierpinski-triangle", 2, 1),
+    ("sierpinski-triangle", 3, 3), ("sierpinski-triangle", 5, 2), ("sierpinski-triangle", 7, 1),
+    ("sierpinski-triangle", 9, 4), ("sierpinski-triangle", 10, 6), ("sierpinski-triangle", 11, 7),
+    ("sierpinski-triangle", 12, 5), ("sierpinski-carpet", 3, 2), ("sierpinski-carpet", 4, 3),
+    ("vicsek", 4, 2), ("vicsek", 5, 4), ("empty-bottles", 4, 3), ("empty-bottles", 5, 2),
+    ("full-square", 6, 5), ("full-square", 7, 3)])
+def test_tile_step_levels_and_tilings(name, r, g):
+    """Tile levels from 0 (every neighbour remote) to 7; chunk counts with ragged tails."""
+    p = mk(name, r, tile_level=g)
+    steps = 4
+    want = oracle_run(name, r, 7, 0.4, steps)
+    a, b = p.new_state(), p.new_state()
+    p.seed(a, 7, 0.4)
+    n = BUILTINS[name].k ** r
+    for t in range(steps):
+        p.step(a, b)
+        got = host(b, p.geometry.state_bytes)
+        assert np.array_equal(got[:n], want[t + 1]), f"step {t + 1}"
+        assert not got[n:].any()
+        a, b = b, a
+
+
+RULES = [A.B3S23, (1 << 3 | 1 << 6, 1 << 2 | 1 << 3), (1 << 1, 0x1FF), (0x1FF, 0), (1 << 0 | 1 << 4, 1 << 5 | 1 << 8)]
+
+
+@pytest.mark.parametrize("rule", RULES)
+@pytest.mark.parametrize("engine", ["tile", "naive"])
+def test_rules(rule, engine):
+    r = 9
+    p = mk("sierpinski-triangle", r, rule=rule)
+    want = oracle_run("sierpinski-triangle", r, 3, 0.5, 3, rule)
+    a, b = p.new_state(), p.new_state()
+    p.seed(a, 3, 0.5)
+    for t in range(3):
+        (p.step if engine == "tile" else p.step_naive)(a, b)
+        assert np.array_equal(host(b, 3 ** r), want[t + 1])
+        a, b = b, a
+
+
+def test_block_threads_and_ctas_variants():
+    want = oracle_run("sierpinski-triangle", 10, 5, 0.5, 2)
+    for bt, cps in [(128, 1), (256, 3), (1024, 1), (736, 2)]:
+        p = mk("sierpinski-triangle", 10, block_threads=bt, ctas_per_sm=cps)
+        a, b = p.new_state(), p.new_state()
+        p.seed(a, 5, 0.5)
+        p.step(a, b)
+        p.step(b, a)
+        assert np.array_equal(host(a, 3 ** 10), want[2]), (bt, cps)
+
+
+def test_run_graph_and_host():
+    r = 10
+    p = mk("sierpinski-triangle", r)
+    want = oracle_run("sierpinski-triangle", r, 11, 0.5, 7)
+    for use_graph in (False, True):
+        a, b = p.new_state(), p.new_state()
+        p.seed(a, 11, 0.5)
+        fin = p.run(a, b, 7, use_graph=use_graph)
+        assert fin is b
+        assert np.array_equal(host(fin, 3 ** r), want[7])
+        p.seed(a, 11, 0.5)
+        fin = p.run(a, b, 6, use_graph=use_graph)
+        assert np.array_equal(host(fin, 3 ** r), want[6])
+    h = torch.from_numpy(np.concatenate([want[0], np.zeros(p.geometry.state_bytes - 3 ** r, np.uint8)])).pin_memory()
+    a, b = p.new_state(), p.new_state()
+    p.run_host(h, a, b, 5)
+    assert np.array_equal(h.numpy()[:3 ** r], want[5])
+
+
+def test_count_alive():
+    for r in (0, 3, 8, 11):
+        p = mk("sierpinski-triangle", r)
+        a = p.new_state()
+        p.seed(a, 9, 0.37)
+        assert int(p.count_alive(a).item()) == int(A.seed_compact(SIERPINSKI, r, 9, 0.37).sum())
+
+
+# ------------------------------------------------------------------ full-size sampled parity (bench config)
+@pytest.mark.parametrize("r", [16, 22])
+def test_full_size_sampled_first_step(r):
+    """At BASELINE.json's sizes: seed and one tile step vs the oracle at 2e5 sampled cells,
+    the oracle computing every input it needs itself (seed_at), in the bench's launch shape."""
+    p = mk("sierpinski-triangle", r)
+    a, b = p.new_state(), p.new_state()
+    p.seed(a, 42, 0.5)
+    p.step(a, b)
+    torch.cuda.synchronize()
+    om = np.unique(sqz_inputs.random_indices(200_000, 3 ** r, seed=1234).astype(np.int64))
+    om = np.concatenate([om, [0, 1, 2, 3 ** r - 1, 3 ** r - 2]]).astype(np.int64)
+    idx = torch.from_numpy(om).cuda()
+    assert np.array_equal(a[idx].cpu().numpy(), A.seed_at(SIERPINSKI, r, om, 42, 0.5))
+    want = A.compact_step_sampled(SIERPINSKI, r, om, lambda q: A.seed_at(SIERPINSKI, r, q, 42, 0.5))
+    assert np.array_equal(b[idx].cpu().numpy(), want)
+    del a, b
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("r", [12, 22])
+def test_histogram_pin_full_size(r):
+    """Closed form: all alive, birth = ∅, survive = {c} -> alive count is the
+    number of cells with exactly c member neighbours: {2: 3, 3: 4·3^(r-2)-2, 4: 4·3^(r-2), 5: 3^(r-2)-1}."""
+    t = 3 ** (r - 2)
+    hist = {2: 3, 3: 4 * t - 2, 4: 4 * t, 5: t - 1}
+    a = None
+    for c in range(9):
+        p = mk("sierpinski-triangle", r, rule=(0, 1 << c))
+        if a is None:
+            a, b = p.new_state(), p.new_state()
+            a.zero_()
+            a[:3 ** r] = 1
+        p.step(a, b)
+        assert int(p.count_alive(b).item()) == hist.get(c, 0), c
+    # B3/S23 from all alive: survivors are cells with 2 or 3 neighbours
+    p = mk("sierpinski-triangle", r)
+    p.step(a, b)
+    assert int(p.count_alive(b).item()) == 3 + 4 * t - 2
+    del a, b
+    torch.cuda.empty_cache()
+
+
+def test_tile_equals_naive_multistep_r16():
+    """Two independent CUDA formulations agree over 20 steps at r=16 (plus oracle at step 1)."""
+    p = mk("sierpinski-triangle", 16)
+    a, b = p.new_state(), p.new_state()
+    c, d = p.new_state(), p.new_state()
+    p.seed(a, 42, 0.5)
+    c.copy_(a)
+    for _ in range(20):
+        p.step(a, b)
+        p.step_naive(c, d)
+        a, b, c, d = b, a, d, c
+    torch.cuda.synchronize()
+    assert torch.equal(a, c)
+
+
+# ------------------------------------------------------------------ BB baseline
+@pytest.mark.parametrize("name,r", [("sierpinski-triangle", 6), ("sierpinski-triangle", 9), ("sierpinski-carpet", 3),
+                                    ("empty-bottles", 3), ("full-square", 2)])
+def test_bb_engine_vs_oracle(name, r):
+    """The expanded bounding-box engine equals the oracle's O5 definition on the embedding."""
+    o = BUILTINS[name]
+    p = mk(name, r)
+    st, mask = A.seed_expanded(o, r, 42, 0.3)
+    g0, g1 = p.new_bb(), p.new_bb()
+    p.bb_seed(g0, 42, 0.3)
+    n = o.s ** r
+    grid = host(g0, n * n).reshape(n, n)
+    assert np.array_equal(grid == 2, ~mask)
+    assert np.array_equal(np.where(mask, grid, 0), st)
+    comp = p.new_state()
+    for t in range(4):
+        p.bb_step(g0, g1)
+        st = A.expanded_step(st, mask, A.B3S23)
+        grid = host(g1, n * n).reshape(n, n)
+        assert np.array_equal(np.where(mask, grid, 0), st) and (grid[~mask] == 2).all()
+        p.bb_to_compact(g1, comp)
+        assert np.array_equal(host(comp, o.k ** r), A.transport(o, r, st))
+        g0, g1 = g1, g0
+
+
+def test_bb_equals_compact_r16():
+    """BASELINE config[1]: at r=16 the BB engine and the compact engine agree for 5 steps."""
+    p = mk("sierpinski-triangle", 16)
+    g0, g1 = p.new_bb(), p.new_bb()
+    a, b = p.new_state(), p.new_state()
+    p.bb_seed(g0, 42, 0.5)
+    p.seed(a, 42, 0.5)
+    comp = p.new_state()
+    for _ in range(5):
+        p.bb_step(g0, g1)
+        p.step(a, b)
+        g0, g1, a, b = g1, g0, b, a
+    p.bb_to_compact(g0, comp)
+    torch.cuda.synchronize()
+    assert torch.equal(comp, a)
+    del g0, g1
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ sharded (P shards on one GPU)
+def run_sharded_local(name, r, nranks, steps, naive=False, g=0):
+    """Shards on one device; the halo exchange done with device copies (what NCCL moves)."""
+    f = sq.builtin_fractal(name)
+    parts = [sq.Squeeze(f, r, rank=i, nranks=nranks, device=DEV, tile_level=g) for i in range(nranks)]
+    ranges = [p.shard_range(i) for i, p in enumerate(parts)]
+    bufs = []
+    for p in parts:
+        a, b = p.new_state(), p.new_state()
+        p.seed(a, 42, 0.5)
+        bufs.append([a, b])
+    needs = [p.halo_needs() for p in parts]
+    recv = [torch.zeros(max(1, len(nd)), dtype=torch.uint8, device="cuda") for nd in needs]
+    for p, rv in zip(parts, recv):
+        p.halo_set_sends(np.zeros(0, np.uint64))
+        p.halo_bind(None, rv)
+    for _ in range(steps):
+        for i, nd in enumerate(needs):  # gather needed cells from their owners' current state
+            for j, (lo, hi) in enumerate(ranges):
+                sel = np.nonzero((nd >= lo) & (nd < hi))[0]
+                if sel.size:
+                    src = torch.from_numpy((nd[sel] - lo).astype(np.int64)).cuda()
+                    recv[i][torch.from_numpy(sel).cuda()] = bufs[j][0][src]
+        for p, bf in zip(parts, bufs):
+            (p.step_naive if naive else p.step)(bf[0], bf[1])
+        for bf in bufs:
+            bf.reverse()
+    torch.cuda.synchronize()
+    for p in parts:
+        assert p.device_error() == 0
+    return np.concatenate([bf[0][:hi - lo].cpu().numpy() for bf, (lo, hi) in zip(bufs, ranges)])
+
+
+@pytest.mark.parametrize("name,r,nranks,g", [("sierpinski-triangle", 10, 2, 3), ("sierpinski-triangle", 12, 3, 4),
+                                             ("sierpinski-triangle", 12, 8, 3), ("sierpinski-carpet", 5, 4, 2),
+                                             ("empty-bottles", 6, 5, 2), ("sierpinski-triangle", 4, 4, 1)])
+@pytest.mark.parametrize("naive", [False, True])
+def test_sharded_equals_oracle(name, r, nranks, g, naive):
+    got = run_sharded_local(name, r, nranks, 5, naive, g)
+    assert np.array_equal(got, oracle_run(name, r, 42, 0.5, 5)[5])
+
+
+def test_sharded_r16_equals_unsharded():
+    got = run_sharded_local("sierpinski-triangle", 16, 4, 6)
+    p = mk("sierpinski-triangle", 16)
+    a, b = p.new_state(), p.new_state()
+    p.seed(a, 42, 0.5)
+    fin = p.run(a, b, 6)
+    assert np.array_equal(got, host(fin, 3 ** 16))
+
+
+def test_halo_pack_kernel():
+    p = sq.Squeeze(sq.builtin_fractal("sierpinski-triangle"), 10, rank=1, nranks=3, device=DEV, tile_level=3)
+    lo, hi = p.shard_range(1)
+    sends = np.array([lo, lo + 5, hi - 1, lo + 77], dtype=np.uint64)
+    p.halo_set_sends(sends)
+    cur = p.new_state()
+    p.seed(cur, 42, 0.5)
+    send = torch.zeros(4, dtype=torch.uint8, device="cuda")
+    recv = torch.zeros(max(1, len(p.halo_needs())), dtype=torch.uint8, device="cuda")
+    p.halo_bind(send, recv)
+    p.halo_pack(cur)
+    want = A.seed_at(SIERPINSKI, 10, sends.astype(np.int64), 42, 0.5)
+    assert np.array_equal(host(send, 4), want)
+
+
+def test_halo_miss_sets_device_error():
+    p = sq.Squeeze(sq.builtin_fractal("sierpinski-triangle"), 10, rank=1, nranks=3, device=DEV, tile_level=3)
+    assert len(p.halo_needs()) > 0
+    a, b = p.new_state(), p.new_state()
+    p.seed(a, 1, 0.5)
+    with pytest.raises(sq.SqueezeError):
+        p.step(a, b)  # no halo bound
