@@ -140,10 +140,9 @@ squeeze_status do_step(Ctx* c, const uint8_t* cur, uint8_t* next, cudaStream_t s
   p.zslot = c->tt.zero_slot;
   p.dmax = c->tt.max_degree;
   p.ndirs = c->tt.ndirs;
-  for (int i = 0; i < 8; ++i) {
-    p.dir_dx[i] = c->tt.dir_dx[i];
-    p.dir_dy[i] = c->tt.dir_dy[i];
-  }
+  p.dir_code = 0;
+  for (uint32_t i = 0; i < c->tt.ndirs; ++i)
+    p.dir_code |= (uint32_t)((c->tt.dir_dx[i] + 1) | ((c->tt.dir_dy[i] + 1) << 2)) << (4 * i);
   p.nbr = c->d_nbr;
   p.link_j2 = c->d_link_j2;
   p.link_dir = c->d_link_dir;
@@ -257,18 +256,22 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       if ((st = upload(&c->d_needs, c->needs.data(), c->needs.size())) != SQZ_OK) return fail(st);
       if (cudaMalloc((void**)&c->d_err, sizeof(int)) != cudaSuccess) return fail(SQZ_E_NOMEM);
       if (cudaMemset(c->d_err, 0, sizeof(int)) != cudaSuccess) return fail(SQZ_E_CUDA);
-      // tile kernel launch shape: one warp per 32 cells of a tile, persistent CTAs
+      // tile kernel launch shape: persistent CTAs, threads ~ one per tile cell
       TileParams p{};
       p.K = c->tt.K;
       p.E = c->tt.E;
       p.ndirs = c->tt.ndirs;
+      p.dmax = c->tt.max_degree;
+      p.birth = c->rule.birth_mask;
+      p.survive = c->rule.survive_mask;
       c->tile_smem = tile_smem_bytes(p);
       uint32_t threads = c->opts.block_threads;
-      if (threads == 0) threads = (uint32_t)std::min<uint64_t>(1024, std::max<uint64_t>(128, (c->tt.K + 31) / 32 * 32));
+      if (threads == 0) threads = (uint32_t)std::min<uint64_t>(512, std::max<uint64_t>(128, (c->tt.K + 31) / 32 * 32));
       if (threads % 32 || threads > 1024) return fail(SQZ_E_CONFIG);
       c->tile_threads = (int)threads;
-      if (tile_kernel_attributes(c->tile_smem) != cudaSuccess) return fail(SQZ_E_CONFIG);
-      int occ = c->opts.ctas_per_sm ? (int)c->opts.ctas_per_sm : tile_occupancy(c->tile_threads, c->tile_smem);
+      int occ = 0;
+      if (tile_prepare(p, c->tile_smem, c->tile_threads, &occ) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
+      if (c->opts.ctas_per_sm) occ = std::min<int>(occ, (int)c->opts.ctas_per_sm);
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
       c->tile_grid = sms * std::max(1, occ);

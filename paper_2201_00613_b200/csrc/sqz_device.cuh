@@ -1,0 +1,27 @@
+// sqz_device.cuh — device helpers shared by the kernel translation units (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sqz_kernels.cuh"
+
+namespace sqz {
+
+// State of a global Ω for a (possibly sharded) buffer: in-shard from `cur`, else from the
+// halo receive buffer (binary search over the sorted needs list).
+__device__ __forceinline__ uint32_t fetch_cell(const uint8_t* __restrict__ cur, uint64_t om, const HaloView& h) {
+  if (om >= h.omega_lo && om < h.omega_hi) return __ldg(cur + (om - h.omega_lo));
+  uint64_t lo = 0, hi = h.nneeds;
+  while (lo < hi) {
+    uint64_t mid = (lo + hi) >> 1;
+    uint64_t v = h.needs[mid];
+    if (v < om) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < h.nneeds && h.needs[lo] == om && h.recv != nullptr) return h.recv[lo];
+  if (h.err) atomicExch(h.err, 1);
+  return 0;
+}
+
+}  // namespace sqz

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "sqz_device.cuh"
 #include "sqz_kernels.cuh"
 
 namespace sqz {
@@ -55,22 +56,6 @@ __device__ __forceinline__ LevelMaps stage_maps(const LevelMaps& g, uint32_t* sm
 
 __host__ __device__ inline size_t maps_smem_bytes(const LevelMaps& m) {
   return (size_t)(m.n_lam_full + m.n_lam_tail + m.n_nu_full + m.n_nu_tail) * sizeof(uint32_t);
-}
-
-// State of a global Ω for a (possibly sharded) buffer: in-shard from `cur`, else from the
-// halo receive buffer (binary search over the sorted needs list).
-__device__ __forceinline__ uint32_t fetch_cell(const uint8_t* __restrict__ cur, uint64_t om, const HaloView& h) {
-  if (om >= h.omega_lo && om < h.omega_hi) return __ldg(cur + (om - h.omega_lo));
-  uint64_t lo = 0, hi = h.nneeds;
-  while (lo < hi) {
-    uint64_t mid = (lo + hi) >> 1;
-    uint64_t v = h.needs[mid];
-    if (v < om) lo = mid + 1;
-    else hi = mid;
-  }
-  if (lo < h.nneeds && h.needs[lo] == om && h.recv != nullptr) return h.recv[lo];
-  if (h.err) atomicExch(h.err, 1);
-  return 0;
 }
 
 __device__ __forceinline__ uint32_t rule_byte(uint32_t alive, uint32_t count, uint32_t birth, uint32_t survive) {
@@ -149,257 +134,6 @@ __global__ void k_step_naive(LevelMaps gm, const uint8_t* __restrict__ cur, uint
     }
     next[w] = out;
   }
-}
-
-// ---------------------------------------------------------------------------------------
-// tile kernel
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-
-__device__ __forceinline__ void tma_store_1d(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
-               "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-
-__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-// Bit-sliced rule: each bit position is an independent cell; (c3 c2 c1 c0) its member-
-// neighbour count (<= 8).  f(c) = bit c of `mask`, evaluated as a mux tree on c0..c3.
-__device__ __forceinline__ uint32_t mask_word(uint32_t mask, int v) { return ((mask >> v) & 1u) ? 0xFFFFFFFFu : 0u; }
-
-__device__ __forceinline__ uint32_t rule_bits(uint32_t mask, uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
-  uint32_t m0 = (mask_word(mask, 0) & ~c0) | (mask_word(mask, 1) & c0);
-  uint32_t m1 = (mask_word(mask, 2) & ~c0) | (mask_word(mask, 3) & c0);
-  uint32_t m2 = (mask_word(mask, 4) & ~c0) | (mask_word(mask, 5) & c0);
-  uint32_t m3 = (mask_word(mask, 6) & ~c0) | (mask_word(mask, 7) & c0);
-  uint32_t m4 = mask_word(mask, 8) & ~c0;
-  uint32_t n0 = (m0 & ~c1) | (m1 & c1);
-  uint32_t n1 = (m2 & ~c1) | (m3 & c1);
-  uint32_t n2 = m4 & ~c1;
-  uint32_t o0 = (n0 & ~c2) | (n1 & c2);
-  uint32_t o1 = n2 & ~c2;
-  return (o0 & ~c3) | (o1 & c3);
-}
-
-struct TileSmem {
-  uint8_t* in[2];
-  uint8_t* out;
-  uint32_t* Z;       // K state words, E remote words, zero word
-  uint32_t* W;       // K next words
-  uint16_t* nbr;     // K*8
-  int64_t* ntile[2]; // [ndirs][32] neighbour tile per lane, -1 = none
-  uint64_t* bar;     // 2 mbarriers
-};
-
-__host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
-
-__host__ __device__ inline size_t tile_chunk_bytes(uint64_t K) { return align16((size_t)K * kChunkTiles); }
-
-__host__ __device__ inline size_t tile_layout(const TileParams& p, uint8_t* base, TileSmem* s) {
-  size_t off = 0;
-  size_t cb = tile_chunk_bytes(p.K);
-  if (s) s->in[0] = base + off;
-  off += cb;
-  if (s) s->in[1] = base + off;
-  off += cb;
-  if (s) s->out = base + off;
-  off += cb;
-  if (s) s->Z = (uint32_t*)(base + off);
-  off += align16((size_t)(p.K + p.E + 1) * 4);
-  if (s) s->W = (uint32_t*)(base + off);
-  off += align16((size_t)p.K * 4);
-  if (s) s->nbr = (uint16_t*)(base + off);
-  off += align16((size_t)p.K * 16);
-  size_t nt = (size_t)(p.ndirs ? p.ndirs : 1) * kChunkTiles * 8;
-  if (s) s->ntile[0] = (int64_t*)(base + off);
-  off += nt;
-  if (s) s->ntile[1] = (int64_t*)(base + off);
-  off += nt;
-  if (s) s->bar = (uint64_t*)(base + off);
-  off += 16;
-  return off;
-}
-
-size_t tile_smem_bytes(const TileParams& p) { return tile_layout(p, nullptr, nullptr); }
-
-// Lane i: coarse λ of tile (chunk*32 + i) and ν of its neighbour tiles (one per direction).
-__device__ __forceinline__ void compute_ntile(const TileParams& p, uint64_t chunk, int64_t* dst, int lane) {
-  uint64_t t = p.tile_lo + chunk * kChunkTiles + lane;
-  if (t < p.tile_hi) {
-    uint32_t X, Y;
-    lambda_level(p.coarse, t, X, Y);
-    for (uint32_t d = 0; d < p.ndirs; ++d) {
-      uint64_t nt = nu_level(p.coarse, (int64_t)X + p.dir_dx[d], (int64_t)Y + p.dir_dy[d]);
-      dst[d * kChunkTiles + lane] = (nt == kNoneU64) ? -1 : (int64_t)nt;
-    }
-  } else {
-    for (uint32_t d = 0; d < p.ndirs; ++d) dst[d * kChunkTiles + lane] = -1;
-  }
-}
-
-__global__ void __launch_bounds__(1024) k_step_tile(TileParams p, const uint8_t* __restrict__ cur,
-                                                    uint8_t* __restrict__ next) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  TileSmem S;
-  tile_layout(p, smem_raw, &S);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const uint32_t K = (uint32_t)p.K;
-  const uint32_t nblk = (K + 31) / 32;
-
-  // one-time: neighbour table to shared memory, zero word, barriers
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(p.nbr);
-    uint4* dst = reinterpret_cast<uint4*>(S.nbr);
-    for (uint32_t i = tid; i < K; i += blockDim.x) dst[i] = src[i];
-  }
-  if (tid == 0) {
-    S.Z[p.zslot] = 0;
-    mbar_init(&S.bar[0], 1);
-    mbar_init(&S.bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  uint64_t chunk = blockIdx.x;
-  if (chunk < p.nchunks) {
-    if (tid == 0) {
-      uint64_t t0 = p.tile_lo + chunk * kChunkTiles;
-      uint64_t nt = min((uint64_t)kChunkTiles, p.tile_hi - t0);
-      tma_load_1d(S.in[0], cur + chunk * kChunkTiles * p.K, (uint32_t)align16(nt * p.K), &S.bar[0]);
-    }
-    if (warp == nwarps - 1) compute_ntile(p, chunk, S.ntile[0], lane);
-  }
-  __syncthreads();
-
-  uint32_t it = 0;
-  for (; chunk < p.nchunks; chunk += gridDim.x, ++it) {
-    const int buf = it & 1;
-    const uint64_t t0 = p.tile_lo + chunk * kChunkTiles;
-    const uint32_t nt = (uint32_t)min((uint64_t)kChunkTiles, p.tile_hi - t0);
-    const uint64_t nxt = chunk + gridDim.x;
-    if (nxt < p.nchunks) {
-      if (tid == 0) {
-        uint64_t n0 = p.tile_lo + nxt * kChunkTiles;
-        uint64_t nn = min((uint64_t)kChunkTiles, p.tile_hi - n0);
-        fence_proxy_async();
-        tma_load_1d(S.in[buf ^ 1], cur + nxt * kChunkTiles * p.K, (uint32_t)align16(nn * p.K), &S.bar[buf ^ 1]);
-      }
-      if (warp == nwarps - 1) compute_ntile(p, nxt, S.ntile[buf ^ 1], lane);
-    }
-    mbar_wait(&S.bar[buf], (it >> 1) & 1);
-    const uint8_t* inb = S.in[buf];
-
-    // Phase A: byte tiles -> bit-sliced words, Z[j] bit i = cell j of tile i
-    for (uint32_t jb = warp; jb < nblk; jb += nwarps) {
-      uint32_t mine = 0;
-      const uint8_t* src = inb + (size_t)lane * K + jb * 32;
-      const bool active = lane < nt;
-#pragma unroll 8
-      for (int jj = 0; jj < 32; ++jj) {
-        if (jb * 32 + jj < K) {
-          uint32_t v = active ? src[jj] : 0u;
-          uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
-          mine = (lane == jj) ? bal : mine;
-        }
-      }
-      if (jb * 32 + lane < K) S.Z[jb * 32 + lane] = mine;
-    }
-    // Phase B: one bit-sliced word per tile-boundary link (neighbour tile's cell j2)
-    {
-      const int64_t* ntl = S.ntile[buf];
-      for (uint32_t e = warp; e < p.E; e += nwarps) {
-        uint32_t d = p.link_dir[e], j2 = p.link_j2[e];
-        int64_t tn = ntl[d * kChunkTiles + lane];
-        uint32_t v = 0;
-        if (tn >= 0) {
-          uint64_t tu = (uint64_t)tn;
-          if (tu >= t0 && tu < t0 + nt) v = inb[(size_t)(tu - t0) * K + j2];
-          else v = fetch_cell(cur, tu * p.K + j2, p.halo);
-        }
-        uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
-        if (lane == 0) S.Z[K + e] = bal;
-      }
-    }
-    __syncthreads();
-
-    // Phase C: bit-sliced neighbour count and rule, 32 tiles per word
-    const uint32_t live_lanes = nt >= 32 ? 0xFFFFFFFFu : ((1u << nt) - 1u);
-    for (uint32_t j = tid; j < K; j += blockDim.x) {
-      uint4 row = reinterpret_cast<const uint4*>(S.nbr)[j];
-      uint32_t idx[8] = {row.x & 0xFFFFu, row.x >> 16, row.y & 0xFFFFu, row.y >> 16,
-                         row.z & 0xFFFFu, row.z >> 16, row.w & 0xFFFFu, row.w >> 16};
-      uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-#pragma unroll
-      for (int d = 0; d < 8; ++d) {
-        if (d < (int)p.dmax) {
-          uint32_t x = S.Z[idx[d]];
-          uint32_t t1 = c0 & x;
-          c0 ^= x;
-          uint32_t t2 = c1 & t1;
-          c1 ^= t1;
-          uint32_t t3 = c2 & t2;
-          c2 ^= t2;
-          c3 |= t3;
-        }
-      }
-      uint32_t a = S.Z[j];
-      uint32_t nw = (a & rule_bits(p.survive, c0, c1, c2, c3)) | (~a & rule_bits(p.birth, c0, c1, c2, c3));
-      S.W[j] = nw & live_lanes;
-    }
-    if (tid == 0) bulk_wait_read_all();  // previous chunk's bulk store has read S.out
-    __syncthreads();
-
-    // Phase D: bit-sliced words -> byte tiles
-    for (uint32_t jb = warp; jb < nblk; jb += nwarps) {
-      uint32_t w = (jb * 32 + lane < K) ? S.W[jb * 32 + lane] : 0u;
-      uint8_t* dst = S.out + (size_t)lane * K + jb * 32;
-      const bool active = lane < nt;
-#pragma unroll 8
-      for (int jj = 0; jj < 32; ++jj) {
-        if (jb * 32 + jj < K) {
-          uint32_t b = __shfl_sync(0xFFFFFFFFu, w, jj);
-          if (active) dst[jj] = (uint8_t)((b >> lane) & 1u);
-        }
-      }
-    }
-    const uint32_t bytes = nt * K;
-    const uint32_t padded = (uint32_t)align16(bytes);
-    for (uint32_t i = bytes + tid; i < padded; i += blockDim.x) S.out[i] = 0;
-    fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) tma_store_1d(next + chunk * kChunkTiles * p.K, S.out, padded);
-  }
-  if (tid == 0) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -626,23 +360,6 @@ cudaError_t launch_step_naive(const LevelMaps& m, const uint8_t* cur, uint8_t* n
   if (e != cudaSuccess) return e;
   k_step_naive<<<grid_for(words, 256), 256, sm, st>>>(m, cur, reinterpret_cast<uint32_t*>(next), cells, words, birth,
                                                        survive, halo);
-  return cudaGetLastError();
-}
-
-cudaError_t tile_kernel_attributes(size_t smem) {
-  return cudaFuncSetAttribute((const void*)k_step_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-}
-
-int tile_occupancy(int threads, size_t smem) {
-  int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_step_tile, threads, smem) != cudaSuccess) return 1;
-  return blocks > 0 ? blocks : 1;
-}
-
-cudaError_t launch_step_tile(const TileParams& p, const uint8_t* cur, uint8_t* next, int grid, int threads,
-                             size_t smem, cudaStream_t st) {
-  if (p.nchunks == 0) return cudaSuccess;
-  k_step_tile<<<grid, threads, smem, st>>>(p, cur, next);
   return cudaGetLastError();
 }
 

@@ -23,7 +23,7 @@ struct TileParams {
   uint32_t zslot;    // index of the zero word in Z
   uint32_t dmax;     // max neighbour entries per cell
   uint32_t ndirs;
-  int dir_dx[8], dir_dy[8];
+  uint32_t dir_code;  // 4 bits per direction d: (dx+1) | (dy+1) << 2
   const uint16_t* nbr;       // K*8
   const uint32_t* link_j2;   // E
   const uint8_t* link_dir;   // E
@@ -34,8 +34,9 @@ struct TileParams {
 
 // Shared-memory bytes the tile kernel needs for these parameters.
 size_t tile_smem_bytes(const TileParams& p);
-cudaError_t tile_kernel_attributes(size_t smem);
-int tile_occupancy(int threads, size_t smem);
+// Sets the shared-memory attribute of the kernel variant `p` selects and returns its
+// occupancy (CTAs per SM) at `threads` threads.
+cudaError_t tile_prepare(const TileParams& p, size_t smem, int threads, int* occupancy);
 
 cudaError_t launch_map_lambda(const LevelMaps& m, const uint64_t* om, uint32_t* x, uint32_t* y, uint64_t count,
                               cudaStream_t st);
