@@ -137,7 +137,7 @@ class Squeeze:
     # ------------------------------------------------------------------ device
     def new_state(self, fill: int | None = None):
         import torch
-        t = torch.empty(self.geometry.state_bytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+        t = torch.empty(max(16, self.geometry.state_bytes), dtype=torch.uint8, device=f"cuda:{self.device}")
         if fill is not None:
             t.fill_(fill)
         return t

@@ -127,6 +127,7 @@ HaloView halo_view(const Ctx* c) {
 
 squeeze_status check_state(const Ctx* c, const void* p) {
   if (c->device < 0) return SQZ_E_NO_DEVICE;
+  if (c->state_bytes == 0 && p == nullptr) return SQZ_OK;  // empty shard: every call is a no-op
   if (p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u)) return SQZ_E_CONFIG;
   return SQZ_OK;
 }
@@ -266,8 +267,8 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       p.survive = c->rule.survive_mask;
       c->tile_smem = tile_smem_bytes(p);
       uint32_t threads = c->opts.block_threads;
-      if (threads == 0) threads = (uint32_t)std::min<uint64_t>(512, std::max<uint64_t>(128, (c->tt.K + 31) / 32 * 32));
-      if (threads % 32 || threads > 1024) return fail(SQZ_E_CONFIG);
+      if (threads == 0) threads = 256;  // tools/sweep.py on B200
+      if (threads % 32 || threads < 64 || threads > 1024) return fail(SQZ_E_CONFIG);
       c->tile_threads = (int)threads;
       int occ = 0;
       if (tile_prepare(p, c->tile_smem, c->tile_threads, &occ) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);

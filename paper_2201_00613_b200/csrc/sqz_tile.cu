@@ -60,16 +60,31 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // 32x32 bit transpose across the warp: afterwards lane L bit i = (lane i bit L) before.
-__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+// Stage s swaps the off-diagonal s x s blocks: each lane sends the block its partner keeps
+// (a rotate of x & sel) and keeps x & ~sel; 4 instructions per stage.
+struct Transposer {
+  uint32_t sel[5], amt[5];
+  __device__ __forceinline__ explicit Transposer(int lane) {
 #pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const uint32_t m = (s == 16) ? 0x0000FFFFu : (s == 8) ? 0x00FF00FFu : (s == 4) ? 0x0F0F0F0Fu
-                       : (s == 2) ? 0x33333333u : 0x55555555u;
-    uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, s);
-    x = (lane & s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y << s) & ~m));
+    for (int k = 0; k < 5; ++k) {
+      const int s = 16 >> k;
+      const uint32_t m = (s == 16) ? 0x0000FFFFu : (s == 8) ? 0x00FF00FFu : (s == 4) ? 0x0F0F0F0Fu
+                         : (s == 2) ? 0x33333333u : 0x55555555u;
+      const bool hi = lane & s;
+      sel[k] = hi ? m : ~m;
+      amt[k] = hi ? (uint32_t)s : (uint32_t)(32 - s);
+    }
   }
-  return x;
-}
+  __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const uint32_t v = x & sel[k];
+      const uint32_t send = __funnelshift_l(v, v, amt[k]);
+      x = (x & ~sel[k]) | __shfl_xor_sync(0xFFFFFFFFu, send, 16 >> k);
+    }
+    return x;
+  }
+};
 
 // Bit-sliced rule f(c) = bit c of `mask` (c <= 8), a mux tree on the count bits.
 __device__ __forceinline__ uint32_t mask_word(uint32_t mask, int v) { return ((mask >> v) & 1u) ? 0xFFFFFFFFu : 0u; }
@@ -90,28 +105,42 @@ __device__ __forceinline__ uint32_t rule_bits(uint32_t mask, uint32_t c0, uint32
 
 __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
 
+__host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
+// chunk bytes + slack for the 36-byte windows read past the last tile
+__host__ __device__ inline size_t chunk_buf_bytes(uint64_t K) { return align16((size_t)K * kChunkTiles) + 64; }
+
+// Boundary links whose neighbour tile is outside the chunk are prefetched one chunk ahead
+// with 4-byte cp.async gathers into R; at most kMaxPrefetchLinks (larger E falls back to a
+// synchronous gather).
+constexpr uint32_t kMaxPrefetchLinks = 32;
+
 struct TileSmem {
-  uint8_t* in0;       // 2 chunk buffers of `cb` bytes (each reused in place for the output)
+  uint8_t* in0;    // 2 chunk buffers (input, then output in place)
   uint32_t cb;
-  uint32_t* Z;        // K state words | E link words | zero word
-  uint32_t* W;        // K next words
-  uint16_t* nbr;      // K x 8 neighbour slots into Z
-  int64_t* nt0;       // 2 x [ndirs][32] neighbour tile of each lane's tile, -1 = none
-  uint32_t ntn;       // int64 entries per ntile buffer
-  uint64_t* bar;      // 2 mbarriers
+  uint32_t* Z;     // K state words | E link words | zero word
+  uint32_t* W;     // K next-state words
+  uint16_t* nbr;   // K x 8 neighbour slots into Z
+  uint32_t* XY0;   // 2 x [32] coarse (X, Y) of the chunk's tiles, packed as 2 x u32
+  int64_t* ntl0;   // 2 x [ndirs][32] neighbour tile of each lane's tile (-1 = none)
+  uint32_t ntn;
+  uint32_t* R0;    // 2 x [E][32] prefetched words holding out-of-chunk neighbour bytes
+  uint32_t rn;
+  uint64_t* bar;   // 2 mbarriers (TMA loads)
   __device__ __forceinline__ uint8_t* in(int b) const { return in0 + (size_t)b * cb; }
-  __device__ __forceinline__ int64_t* ntile(int b) const { return nt0 + (size_t)b * ntn; }
+  __device__ __forceinline__ uint32_t* XY(int b) const { return XY0 + (size_t)b * 64; }
+  __device__ __forceinline__ int64_t* ntl(int b) const { return ntl0 + (size_t)b * ntn; }
+  __device__ __forceinline__ uint32_t* R(int b) const { return R0 + (size_t)b * rn; }
 };
 
-__host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
-// chunk bytes + slack for the 36-byte windows of the last tile
-__host__ __device__ inline size_t chunk_buf_bytes(uint64_t K) { return align16((size_t)K * kChunkTiles) + 64; }
+__host__ __device__ inline uint32_t prefetch_links(const TileParams& p) {
+  return p.E <= kMaxPrefetchLinks ? p.E : 0;
+}
 
 __host__ __device__ inline size_t tile_layout(const TileParams& p, uint8_t* base, TileSmem* s) {
   size_t off = 0;
-  size_t cb = chunk_buf_bytes(p.K);
+  const size_t cb = chunk_buf_bytes(p.K);
   if (s) {
-    s->in0 = base + off;
+    s->in0 = base;
     s->cb = (uint32_t)cb;
   }
   off += 2 * cb;
@@ -121,54 +150,99 @@ __host__ __device__ inline size_t tile_layout(const TileParams& p, uint8_t* base
   off += align16((size_t)p.K * 4);
   if (s) s->nbr = (uint16_t*)(base + off);
   off += align16((size_t)p.K * 16);
-  size_t nt = (size_t)(p.ndirs ? p.ndirs : 1) * kChunkTiles * 8;
+  if (s) s->XY0 = (uint32_t*)(base + off);
+  off += 2 * 64 * 4;
+  const size_t ntn = (size_t)(p.ndirs ? p.ndirs : 1) * kChunkTiles;
   if (s) {
-    s->nt0 = (int64_t*)(base + off);
-    s->ntn = (uint32_t)(nt / 8);
+    s->ntl0 = (int64_t*)(base + off);
+    s->ntn = (uint32_t)ntn;
   }
-  off += 2 * nt;
+  off += 2 * ntn * 8;
+  const size_t rn = (size_t)(prefetch_links(p) ? prefetch_links(p) : 1) * kChunkTiles;
+  if (s) {
+    s->R0 = (uint32_t*)(base + off);
+    s->rn = (uint32_t)rn;
+  }
+  off += 2 * rn * 4;
   if (s) s->bar = (uint64_t*)(base + off);
   off += 16;
-  return off;
+  return align16(off);
 }
 
 size_t tile_smem_bytes(const TileParams& p) { return tile_layout(p, nullptr, nullptr); }
 
-// Warp w < ndirs: for each lane's tile of chunk `chunk`, the neighbour tile in direction w
-// (coarse λ then coarse ν, P:189 at tile granularity), or -1.
-__device__ __forceinline__ void compute_ntile_dir(const TileParams& p, uint64_t chunk, int64_t* dst, int dir,
-                                                  int lane) {
-  uint64_t t = p.tile_lo + chunk * kChunkTiles + lane;
-  int64_t v = -1;
-  if (t < p.tile_hi) {
-    uint32_t X, Y;
-    lambda_level(p.coarse, t, X, Y);
-    const uint32_t code = (p.dir_code >> (4 * dir)) & 0xFu;
-    const int dx = (int)(code & 3u) - 1, dy = (int)(code >> 2) - 1;
-    uint64_t nt = nu_level(p.coarse, (int64_t)X + dx, (int64_t)Y + dy);
-    v = (nt == kNoneU64) ? -1 : (int64_t)nt;
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Coarse λ of each lane's tile of `chunk` (one warp; P:212-230 at tile level).
+__device__ __forceinline__ void chunk_lambda(const TileParams& p, uint64_t chunk, uint32_t* XY, int lane) {
+  const uint64_t t = p.tile_lo + chunk * kChunkTiles + lane;
+  uint32_t X = 0, Y = 0;
+  if (t < p.tile_hi) lambda_level(p.coarse, t, X, Y);
+  XY[2 * lane] = X;
+  XY[2 * lane + 1] = Y;
+}
+
+// Warp w handles directions d = w, w + nwarps, ...: the neighbour tile in direction d of each
+// lane's tile (coarse ν, P:252-278 at tile level) and, for every link of direction d whose
+// neighbour tile is outside the chunk, an asynchronous 4-byte gather of the word holding the
+// neighbour cell's byte.  The same warp later consumes them in Phase B (per-thread cp.async).
+__device__ __forceinline__ void chunk_neighbours(const TileParams& p, const TileSmem& S, uint64_t chunk, int b,
+                                                 const uint8_t* __restrict__ cur, int warp, int nwarps, int lane) {
+  const uint64_t t0 = p.tile_lo + chunk * kChunkTiles;
+  const uint64_t t = t0 + lane;
+  const uint64_t t_end = min(t0 + kChunkTiles, p.tile_hi);
+  const uint32_t X = S.XY(b)[2 * lane], Y = S.XY(b)[2 * lane + 1];
+  const uint32_t Epf = prefetch_links(p);
+  for (int d = warp; d < (int)p.ndirs; d += nwarps) {
+    int64_t tn = -1;
+    if (t < p.tile_hi) {
+      const uint32_t code = (p.dir_code >> (4 * d)) & 0xFu;
+      const int dx = (int)(code & 3u) - 1, dy = (int)(code >> 2) - 1;
+      const uint64_t nt = nu_level(p.coarse, (int64_t)X + dx, (int64_t)Y + dy);
+      tn = nt == kNoneU64 ? -1 : (int64_t)nt;
+    }
+    S.ntl(b)[d * kChunkTiles + lane] = tn;
+    const bool outside = tn >= 0 && ((uint64_t)tn < t0 || (uint64_t)tn >= t_end);
+    for (uint32_t e = 0; e < Epf; ++e) {
+      if (p.link_dir[e] != d) continue;
+      uint32_t* dst = &S.R(b)[e * kChunkTiles + lane];
+      if (outside) {
+        const uint64_t om = (uint64_t)tn * p.K + p.link_j2[e];
+        if (om >= p.halo.omega_lo && om < p.halo.omega_hi) {
+          cp_async4(dst, cur + ((om - p.halo.omega_lo) & ~3ull));
+        } else {
+          *dst = fetch_cell(cur, om, p.halo) << (8 * (uint32_t)(om & 3));  // halo: rare, synchronous
+        }
+      }
+    }
   }
-  dst[dir * kChunkTiles + lane] = v;
+  cp_async_commit();
 }
 
 template <int DMAX, bool CONWAY>
-__global__ void __launch_bounds__(1024) k_step_tile(TileParams p, const uint8_t* __restrict__ cur,
-                                                    uint8_t* __restrict__ next) {
+__global__ void k_step_tile(TileParams p, const uint8_t* __restrict__ cur, uint8_t* __restrict__ next) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   TileSmem S;
   tile_layout(p, smem_raw, &S);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const uint32_t K = (uint32_t)p.K;
   const uint32_t nblk = (K + 31) / 32;
-  // bits of the packed layout (bit 8p+m = cell 4m+p) that are valid in the last j-block
-  uint32_t tail_mask = 0;
+  const uint32_t E = p.E, Epf = prefetch_links(p);
+  uint32_t tail_mask = 0;  // packed bits (bit 8p+m = cell 4m+p) valid in the last j-block
   {
     const uint32_t nv = K - (nblk - 1) * 32;
 #pragma unroll
     for (int b = 0; b < 32; ++b)
       if ((uint32_t)(4 * (b & 7) + (b >> 3)) < nv) tail_mask |= 1u << b;
   }
-  const uint32_t my_jj = 4 * (lane & 7) + (lane >> 3);  // cell offset this lane owns after a transpose
+  const uint32_t my_jj = 4 * (lane & 7) + (lane >> 3);  // cell offset this lane holds after a transpose
+  const Transposer tr(lane);
+  const int lw = nwarps - 1;  // the last warp issues the TMA copies and the coarse λ
+  const bool issuer = (warp == lw) && lane == 0;
 
   {
     const uint4* src = reinterpret_cast<const uint4*>(p.nbr);
@@ -184,15 +258,15 @@ __global__ void __launch_bounds__(1024) k_step_tile(TileParams p, const uint8_t*
   __syncthreads();
 
   uint64_t chunk = blockIdx.x;
-  if (chunk < p.nchunks) {
-    if (tid == 0) {
-      uint64_t t0 = p.tile_lo + chunk * kChunkTiles;
-      uint64_t nt = min((uint64_t)kChunkTiles, p.tile_hi - t0);
-      tma_load_1d(S.in(0), cur + chunk * kChunkTiles * p.K, (uint32_t)align16(nt * p.K), &S.bar[0]);
-    }
-    if (warp < (int)p.ndirs) compute_ntile_dir(p, chunk, S.ntile(0), warp, lane);
+  if (chunk >= p.nchunks) return;
+  if (issuer) {
+    const uint64_t t0 = p.tile_lo + chunk * kChunkTiles;
+    const uint64_t nt = min((uint64_t)kChunkTiles, p.tile_hi - t0);
+    tma_load_1d(S.in(0), cur + chunk * kChunkTiles * p.K, (uint32_t)align16(nt * p.K), &S.bar[0]);
   }
+  if (warp == lw) chunk_lambda(p, chunk, S.XY(0), lane);
   __syncthreads();
+  chunk_neighbours(p, S, chunk, 0, cur, warp, nwarps, lane);
 
   uint32_t it = 0;
   for (; chunk < p.nchunks; chunk += gridDim.x, ++it) {
@@ -200,24 +274,24 @@ __global__ void __launch_bounds__(1024) k_step_tile(TileParams p, const uint8_t*
     const uint64_t t0 = p.tile_lo + chunk * kChunkTiles;
     const uint32_t nt = (uint32_t)min((uint64_t)kChunkTiles, p.tile_hi - t0);
     const uint64_t nxt = chunk + gridDim.x;
-    if (nxt < p.nchunks) {
-      if (tid == 0) {
-        // in[buf^1] held the previous chunk's output: its bulk store must have read it
-        bulk_wait_read_all();
-        uint64_t n0 = p.tile_lo + nxt * kChunkTiles;
-        uint64_t nn = min((uint64_t)kChunkTiles, p.tile_hi - n0);
+    const bool has_next = nxt < p.nchunks;
+    if (has_next && warp == lw) {
+      if (lane == 0) {
+        bulk_wait_read_all();  // in(buf^1) held the previous chunk's output
+        const uint64_t n0 = p.tile_lo + nxt * kChunkTiles;
+        const uint64_t nn = min((uint64_t)kChunkTiles, p.tile_hi - n0);
         fence_proxy_async();
         tma_load_1d(S.in(buf ^ 1), cur + nxt * kChunkTiles * p.K, (uint32_t)align16(nn * p.K), &S.bar[buf ^ 1]);
       }
-      if (warp < (int)p.ndirs) compute_ntile_dir(p, nxt, S.ntile(buf ^ 1), warp, lane);
+      chunk_lambda(p, nxt, S.XY(buf ^ 1), lane);
     }
     mbar_wait(&S.bar[buf], (it >> 1) & 1);
     uint8_t* inb = S.in(buf);
     const uint32_t* in32 = reinterpret_cast<const uint32_t*>(inb);
     const bool active = (uint32_t)lane < nt;
 
-    // Phase A: lane = tile.  32 bytes (cells j0..j0+31) -> 32 bits, bit 8p+m = cell 4m+p,
-    // then a 32x32 transpose leaves lane L with the word of cell j0 + my_jj(L).
+    // Phase A: lane = tile; 32 bytes (cells j0..j0+31) -> bits 8p+m = cell 4m+p -> transpose,
+    // leaving lane L with the bit-sliced word of cell j0 + my_jj(L)
     for (uint32_t jb = warp; jb < nblk; jb += nwarps) {
       const uint32_t j0 = jb * 32;
       const uint32_t a = (uint32_t)lane * K + j0;
@@ -227,26 +301,34 @@ __global__ void __launch_bounds__(1024) k_step_tile(TileParams p, const uint8_t*
       for (int m = 0; m < 9; ++m) w[m] = in32[wi + m];
       uint32_t acc = 0;
 #pragma unroll
-      for (int m = 0; m < 8; ++m) acc |= (__funnelshift_r(w[m], w[m + 1], sh) & 0x01010101u) << m;
+      for (int m = 0; m < 8; ++m) acc += (__funnelshift_r(w[m], w[m + 1], sh) & 0x01010101u) << m;
       if (jb == nblk - 1) acc &= tail_mask;
       if (!active) acc = 0;
-      uint32_t x = transpose32(acc, lane);
+      const uint32_t x = tr(acc);
       if (j0 + my_jj < K) S.Z[j0 + my_jj] = x;
     }
-    // Phase B: tile-boundary links; lane i reads its neighbour tile's cell j2
-    {
-      const int64_t* ntl = S.ntile(buf);
-      for (uint32_t e = warp; e < p.E; e += nwarps) {
-        const uint32_t d = p.link_dir[e], j2 = p.link_j2[e];
-        const int64_t tn = ntl[d * kChunkTiles + lane];
-        uint32_t v = 0;
-        if (tn >= 0) {
-          const uint64_t tu = (uint64_t)tn;
-          if (tu >= t0 && tu < t0 + nt) v = inb[(size_t)(tu - t0) * K + j2];
-          else v = fetch_cell(cur, tu * p.K + j2, p.halo);
+    // Phase B: boundary-link words; warp w owns the links of directions w, w + nwarps, ...
+    if (warp < (int)p.ndirs) {
+      cp_async_wait_all();  // this warp's gathers for this chunk (issued last iteration)
+      const uint32_t* R = S.R(buf);
+      for (int d = warp; d < (int)p.ndirs; d += nwarps) {
+        const int64_t tn = S.ntl(buf)[d * kChunkTiles + lane];
+        const uint64_t rel = (uint64_t)(tn - (int64_t)t0);
+        const bool inside = tn >= 0 && rel < nt;
+        const uint32_t shb = (uint32_t)tn * K;  // low bits of the neighbour tile's base offset
+        for (uint32_t e = 0; e < E; ++e) {
+          if (p.link_dir[e] != d) continue;
+          const uint32_t j2 = p.link_j2[e];
+          uint32_t v = 0;
+          if (inside) {
+            v = inb[(uint32_t)rel * K + j2];
+          } else if (tn >= 0) {
+            if (e < Epf) v = (R[e * kChunkTiles + lane] >> (8 * ((shb + j2) & 3u))) & 0xFFu;
+            else v = fetch_cell(cur, (uint64_t)tn * p.K + j2, p.halo);
+          }
+          const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
+          if (lane == 0) S.Z[K + e] = bal;
         }
-        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
-        if (lane == 0) S.Z[K + e] = bal;
       }
     }
     __syncthreads();
@@ -295,20 +377,21 @@ __global__ void __launch_bounds__(1024) k_step_tile(TileParams p, const uint8_t*
       }
       S.W[j] = nw & live_lanes;
     }
+    // next chunk's neighbour tiles and link prefetch (needs XY from before the barrier)
+    if (has_next) chunk_neighbours(p, S, nxt, buf ^ 1, cur, warp, nwarps, lane);
     __syncthreads();
 
-    // Phase D: transpose back (lane = tile) and write the 32 bytes of each j-block in place
+    // Phase D: transpose back (lane = tile) and write each j-block's 32 bytes in place
     for (uint32_t jb = warp; jb < nblk; jb += nwarps) {
       const uint32_t j0 = jb * 32;
       uint32_t x = (j0 + my_jj < K) ? S.W[j0 + my_jj] : 0u;
-      x = transpose32(x, lane);  // bit 8p+m = cell j0 + 4m + p of this lane's tile
+      x = tr(x);  // bit 8p+m = cell j0 + 4m + p of this lane's tile
       if (!active) continue;
       const uint32_t a = (uint32_t)lane * K + j0;
       const uint32_t nv = min(32u, K - j0);
-      uint32_t bw[9];
+      uint32_t bw[8];
 #pragma unroll
       for (int m = 0; m < 8; ++m) bw[m] = (x >> m) & 0x01010101u;
-      bw[8] = 0;
       if (nv == 32) {
         const uint32_t sh = a & 3;
         uint32_t* out32 = reinterpret_cast<uint32_t*>(inb + (a - sh));
@@ -316,15 +399,12 @@ __global__ void __launch_bounds__(1024) k_step_tile(TileParams p, const uint8_t*
 #pragma unroll
           for (int m = 0; m < 8; ++m) out32[m] = bw[m];
         } else {
-          const uint32_t d = 4 - sh;  // bytes before the first aligned word
-          // head: bytes 0..d-1 go to the tail of word out32[0]
+          const uint32_t d = 4 - sh;  // bytes before the first aligned word (byte stores)
 #pragma unroll
           for (int q = 0; q < 3; ++q)
             if ((uint32_t)q < d) inb[a + q] = (uint8_t)(bw[0] >> (8 * q));
-          // body: aligned words 1..7 hold bytes d + 4(k-1) .. d + 4(k-1) + 3
 #pragma unroll
           for (int k = 1; k < 8; ++k) out32[k] = __funnelshift_r(bw[k - 1], bw[k], 8 * d);
-          // tail: the last sh bytes (q = 32 - sh .. 31) live in bw[7] bytes (4 - sh) .. 3
 #pragma unroll
           for (int q = 1; q < 4; ++q)
             if ((uint32_t)q >= d) inb[a + 28 + q] = (uint8_t)(bw[7] >> (8 * q));
@@ -340,9 +420,10 @@ __global__ void __launch_bounds__(1024) k_step_tile(TileParams p, const uint8_t*
     for (uint32_t i = bytes + tid; i < padded; i += blockDim.x) inb[i] = 0;
     fence_proxy_async();
     __syncthreads();
-    if (tid == 0) tma_store_1d(next + chunk * kChunkTiles * p.K, inb, padded);
+    if (issuer) tma_store_1d(next + chunk * kChunkTiles * p.K, inb, padded);
   }
-  if (tid == 0) bulk_wait_all();
+  cp_async_wait_all();
+  if (issuer) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------------------

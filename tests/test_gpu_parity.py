@@ -147,7 +147,7 @@ def test_rules(rule, engine):
 
 def test_block_threads_and_ctas_variants():
     want = oracle_run("sierpinski-triangle", 10, 5, 0.5, 2)
-    for bt, cps in [(128, 1), (256, 3), (1024, 1), (736, 2)]:
+    for bt, cps in [(64, 4), (96, 2), (128, 1), (288, 3), (544, 1), (800, 1)]:
         p = mk("sierpinski-triangle", 10, block_threads=bt, ctas_per_sm=cps)
         a, b = p.new_state(), p.new_state()
         p.seed(a, 5, 0.5)
@@ -351,7 +351,20 @@ def test_halo_pack_kernel():
     assert np.array_equal(host(send, 4), want)
 
 
-def test_halo_miss_sets_device_error():
+def test_one_warp_ctas_small_tiles():
+    """One consumer warp + the producer warp must still cover every link direction (g = 1 has 8)."""
+    for r, g in [(2, 1), (5, 1), (6, 2)]:
+        p = mk("sierpinski-triangle", r, tile_level=g, block_threads=64)
+        want = oracle_run("sierpinski-triangle", r, 7, 0.4, 4)
+        a, b = p.new_state(), p.new_state()
+        p.seed(a, 7, 0.4)
+        for t in range(4):
+            p.step(a, b)
+            assert np.array_equal(host(b, 3 ** r), want[t + 1]), (r, g, t)
+            a, b = b, a
+
+
+def test_unbound_halo_is_rejected():
     p = sq.Squeeze(sq.builtin_fractal("sierpinski-triangle"), 10, rank=1, nranks=3, device=DEV, tile_level=3)
     assert len(p.halo_needs()) > 0
     a, b = p.new_state(), p.new_state()
