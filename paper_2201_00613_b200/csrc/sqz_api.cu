@@ -44,6 +44,7 @@ struct Ctx {
   uint16_t* d_nbr = nullptr;
   uint32_t* d_link_j2 = nullptr;
   uint8_t* d_link_dir = nullptr;
+  uint16_t* d_dir_start = nullptr;
   uint64_t* d_needs = nullptr;
   uint64_t* d_sends = nullptr;
   int* d_err = nullptr;
@@ -109,6 +110,7 @@ void free_device(Ctx* c) {
   cudaFree(c->d_nbr);
   cudaFree(c->d_link_j2);
   cudaFree(c->d_link_dir);
+  cudaFree(c->d_dir_start);
   cudaFree(c->d_needs);
   cudaFree(c->d_sends);
   cudaFree(c->d_err);
@@ -147,6 +149,7 @@ squeeze_status do_step(Ctx* c, const uint8_t* cur, uint8_t* next, cudaStream_t s
   p.nbr = c->d_nbr;
   p.link_j2 = c->d_link_j2;
   p.link_dir = c->d_link_dir;
+  p.dir_start = c->d_dir_start;
   p.tile_lo = c->sr.tile_lo;
   p.tile_hi = c->sr.tile_hi;
   p.nchunks = (c->sr.tile_hi - c->sr.tile_lo + kChunkTiles - 1) / kChunkTiles;
@@ -254,6 +257,7 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       if ((st = upload(&c->d_nbr, c->tt.nbr.data(), c->tt.nbr.size())) != SQZ_OK) return fail(st);
       if ((st = upload(&c->d_link_j2, c->tt.link_j2.data(), c->tt.link_j2.size())) != SQZ_OK) return fail(st);
       if ((st = upload(&c->d_link_dir, c->tt.link_dir.data(), c->tt.link_dir.size())) != SQZ_OK) return fail(st);
+      if ((st = upload(&c->d_dir_start, c->tt.dir_start.data(), c->tt.dir_start.size())) != SQZ_OK) return fail(st);
       if ((st = upload(&c->d_needs, c->needs.data(), c->needs.size())) != SQZ_OK) return fail(st);
       if (cudaMalloc((void**)&c->d_err, sizeof(int)) != cudaSuccess) return fail(SQZ_E_NOMEM);
       if (cudaMemset(c->d_err, 0, sizeof(int)) != cudaSuccess) return fail(SQZ_E_CUDA);
@@ -267,8 +271,8 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       p.survive = c->rule.survive_mask;
       c->tile_smem = tile_smem_bytes(p);
       uint32_t threads = c->opts.block_threads;
-      if (threads == 0) threads = 256;  // tools/sweep.py on B200
-      if (threads % 32 || threads < 64 || threads > 1024) return fail(SQZ_E_CONFIG);
+      if (threads == 0) threads = 288;  // 8 consumer warps + 1 producer warp (tools/sweep.py)
+      if (threads % 32 || threads < 64 || threads > 1024) return fail(SQZ_E_CONFIG);  // >= 1 consumer + producer
       c->tile_threads = (int)threads;
       int occ = 0;
       if (tile_prepare(p, c->tile_smem, c->tile_threads, &occ) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);

@@ -227,10 +227,32 @@ int build_tile_tables(const Spec& f, uint32_t g, TileTables& t) {
   t.E = (uint32_t)t.link_j.size();
   t.zero_slot = (uint32_t)(K + t.E);
   if (t.zero_slot > 0xFFFFu) return SQZ_E_INVALID_LEVEL;
+  // sort links by direction (stable) so each direction's links are contiguous
+  std::vector<uint32_t> order(t.E), where(t.E);
+  for (uint32_t e = 0; e < t.E; ++e) order[e] = e;
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return t.link_dir[a] < t.link_dir[b]; });
+  std::vector<uint32_t> lj(t.E), lj2(t.E);
+  std::vector<uint8_t> ld(t.E);
+  for (uint32_t e = 0; e < t.E; ++e) {
+    lj[e] = t.link_j[order[e]];
+    lj2[e] = t.link_j2[order[e]];
+    ld[e] = t.link_dir[order[e]];
+    where[order[e]] = e;
+  }
+  t.link_j.swap(lj);
+  t.link_j2.swap(lj2);
+  t.link_dir.swap(ld);
+  t.dir_start.assign(t.ndirs + 1, 0);
+  for (uint32_t e = 0; e < t.E; ++e) t.dir_start[t.link_dir[e] + 1]++;
+  for (uint32_t d = 0; d < t.ndirs; ++d) t.dir_start[d + 1] += t.dir_start[d];
   t.nbr.assign(K * 8, (uint16_t)t.zero_slot);
   for (uint64_t j = 0; j < K; ++j) {
     t.max_degree = std::max<uint32_t>(t.max_degree, (uint32_t)entries[j].size());
-    for (size_t e = 0; e < entries[j].size(); ++e) t.nbr[j * 8 + e] = (uint16_t)entries[j][e];
+    for (size_t e = 0; e < entries[j].size(); ++e) {
+      uint32_t v = entries[j][e];
+      if (v >= K) v = (uint32_t)(K + where[v - K]);
+      t.nbr[j * 8 + e] = (uint16_t)v;
+    }
   }
   return SQZ_OK;
 }

@@ -50,7 +50,8 @@ struct TileTables {
   std::vector<uint16_t> nbr;       // K*8 indices into Z = [state words 0..K) | remote words | zero]
   std::vector<uint32_t> link_j;    // E: own local cell
   std::vector<uint32_t> link_j2;   // E: local cell inside the neighbour tile
-  std::vector<uint8_t> link_dir;   // E: index into dir_dx/dir_dy
+  std::vector<uint8_t> link_dir;   // E: index into dir_dx/dir_dy (links sorted by direction)
+  std::vector<uint16_t> dir_start; // ndirs + 1: links of direction d are [dir_start[d], dir_start[d+1])
   std::vector<uint32_t> local_x, local_y;  // K: λ_g(j)
 };
 // Builds the tables for level-g tiles.  Returns 0 or an error code.

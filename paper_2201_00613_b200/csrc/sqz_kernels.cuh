@@ -26,7 +26,8 @@ struct TileParams {
   uint32_t dir_code;  // 4 bits per direction d: (dx+1) | (dy+1) << 2
   const uint16_t* nbr;       // K*8
   const uint32_t* link_j2;   // E
-  const uint8_t* link_dir;   // E
+  const uint8_t* link_dir;   // E (sorted by direction)
+  const uint16_t* dir_start; // ndirs + 1
   uint64_t tile_lo, tile_hi, nchunks;
   uint32_t birth, survive;
   HaloView halo;
