@@ -271,8 +271,8 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       p.survive = c->rule.survive_mask;
       c->tile_smem = tile_smem_bytes(p);
       uint32_t threads = c->opts.block_threads;
-      if (threads == 0) threads = 288;  // 8 consumer warps + 1 producer warp (tools/sweep.py)
-      if (threads % 32 || threads < 64 || threads > 1024) return fail(SQZ_E_CONFIG);  // >= 1 consumer + producer
+      if (threads == 0) threads = 256;  // 8 warps, 3 CTAs per SM (tools/sweep.py)
+      if (threads % 32 || threads > 1024) return fail(SQZ_E_CONFIG);
       c->tile_threads = (int)threads;
       int occ = 0;
       if (tile_prepare(p, c->tile_smem, c->tile_threads, &occ) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);

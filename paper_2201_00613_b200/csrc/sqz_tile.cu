@@ -115,16 +115,18 @@ __host__ __device__ inline size_t chunk_buf_bytes(uint64_t K) { return align16((
 constexpr uint32_t kMaxPrefetchLinks = 32;
 
 struct TileSmem {
-  uint8_t* st0;    // 2 stages x [chunk bytes (input, then output in place) | Z words]
-  uint32_t stride, zoff;
+  uint8_t* in0;    // 2 chunk buffers (input, then output in place)
+  uint32_t cb;
+  uint32_t* Z;     // K state words | E link words | zero word
   uint16_t* nbr;   // K x 8 neighbour slots into Z
-  int64_t* ntl0;   // 2 x [ndirs][32] neighbour tile of each lane's tile (-1 = none)  (producer)
+  uint32_t* XY0;   // 2 x [32] coarse (X, Y) of a chunk's tiles (by chunk parity)
+  int64_t* ntl0;   // 2 x [ndirs][32] neighbour tile of each lane's tile (-1 = none)
   uint32_t ntn;
-  uint32_t* R0;    // 2 x [E][32] prefetched words holding out-of-chunk neighbour bytes (producer)
+  uint32_t* R0;    // 2 x [E][32] prefetched words holding out-of-chunk neighbour bytes
   uint32_t rn;
-  uint64_t* bar;   // [0,2) full (TMA landed), [2,4) links ready, [4,6) output written
-  __device__ __forceinline__ uint8_t* buf(int b) const { return st0 + (size_t)b * stride; }
-  __device__ __forceinline__ uint32_t* Z(int b) const { return reinterpret_cast<uint32_t*>(st0 + (size_t)b * stride + zoff); }
+  uint64_t* bar;   // 2 mbarriers (TMA loads)
+  __device__ __forceinline__ uint8_t* in(int b) const { return in0 + (size_t)b * cb; }
+  __device__ __forceinline__ uint32_t* XY(int b) const { return XY0 + (size_t)b * 64; }
   __device__ __forceinline__ int64_t* ntl(int b) const { return ntl0 + (size_t)b * ntn; }
   __device__ __forceinline__ uint32_t* R(int b) const { return R0 + (size_t)b * rn; }
 };
@@ -134,16 +136,19 @@ __host__ __device__ inline uint32_t prefetch_links(const TileParams& p) {
 }
 
 __host__ __device__ inline size_t tile_layout(const TileParams& p, uint8_t* base, TileSmem* s) {
-  const size_t cb = chunk_buf_bytes(p.K), zb = align16((size_t)(p.K + p.E + 1) * 4);
   size_t off = 0;
+  const size_t cb = chunk_buf_bytes(p.K);
   if (s) {
-    s->st0 = base;
-    s->stride = (uint32_t)(cb + zb);
-    s->zoff = (uint32_t)cb;
+    s->in0 = base;
+    s->cb = (uint32_t)cb;
   }
-  off += 2 * (cb + zb);
+  off += 2 * cb;
+  if (s) s->Z = (uint32_t*)(base + off);
+  off += align16((size_t)(p.K + p.E + 1) * 4);
   if (s) s->nbr = (uint16_t*)(base + off);
   off += align16((size_t)p.K * 16);
+  if (s) s->XY0 = (uint32_t*)(base + off);
+  off += 2 * 64 * 4;
   const size_t ntn = (size_t)(p.ndirs ? p.ndirs : 1) * kChunkTiles;
   if (s) {
     s->ntl0 = (int64_t*)(base + off);
@@ -157,7 +162,7 @@ __host__ __device__ inline size_t tile_layout(const TileParams& p, uint8_t* base
   }
   off += 2 * rn * 4;
   if (s) s->bar = (uint64_t*)(base + off);
-  off += 6 * 8;
+  off += 16;
   return align16(off);
 }
 
@@ -167,37 +172,42 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void consumer_sync(int nthreads) { asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory"); }
 
 struct ChunkInfo {
   uint64_t chunk, t0;
   uint32_t nt;
 };
 
-__device__ __forceinline__ ChunkInfo chunk_info(const TileParams& p, uint64_t i) {
+__device__ __forceinline__ ChunkInfo chunk_info(const TileParams& p, uint64_t chunk) {
   ChunkInfo c;
-  c.chunk = blockIdx.x + i * gridDim.x;
-  c.t0 = p.tile_lo + c.chunk * kChunkTiles;
+  c.chunk = chunk;
+  c.t0 = p.tile_lo + chunk * kChunkTiles;
   c.nt = (uint32_t)min((uint64_t)kChunkTiles, p.tile_hi - c.t0);
   return c;
 }
 
-// Producer, lane = tile: coarse λ of the tile (P:212-230 at tile level), then per direction
-// the neighbour tile (coarse ν) and, for each link of that direction whose
-// neighbour tile lies outside the chunk, an asynchronous 4-byte gather of the word holding
-// the neighbour cell's byte (consumed by the same lane in finish_links).
-__device__ __forceinline__ void prep_links(const TileParams& p, const TileSmem& S, const ChunkInfo& c, int b,
-                                           const uint8_t* __restrict__ cur, int lane) {
+// Coarse λ of each lane's tile (P:212-230 at tile level), one warp.
+__device__ __forceinline__ void chunk_lambda(const TileParams& p, const ChunkInfo& c, uint32_t* XY, int lane) {
   const uint64_t t = c.t0 + lane;
-  const uint64_t t_end = c.t0 + c.nt;
   uint32_t X = 0, Y = 0;
   if (t < p.tile_hi) lambda_level(p.coarse, t, X, Y);
+  XY[2 * lane] = X;
+  XY[2 * lane + 1] = Y;
+}
+
+// Warp w, directions d = w, w + nwarps, ...: neighbour tile of each lane's tile (coarse ν,
+// P:252-278 at tile level) and, for each link of direction d whose neighbour tile is outside
+// the chunk, a 4-byte cp.async gather of the word holding the neighbour cell's byte.  The same
+// warp consumes them in Phase B of that chunk.  Always commits exactly one group.
+__device__ __forceinline__ void chunk_neighbours(const TileParams& p, const TileSmem& S, const ChunkInfo& c, int b,
+                                                 const uint8_t* __restrict__ cur, int warp, int nwarps, int lane) {
+  const uint64_t t = c.t0 + lane;
+  const uint64_t t_end = c.t0 + c.nt;
+  const uint32_t X = S.XY(b)[2 * lane], Y = S.XY(b)[2 * lane + 1];
   const uint32_t Epf = prefetch_links(p);
-  for (uint32_t d = 0; d < p.ndirs; ++d) {
+  for (int d = warp; d < (int)p.ndirs; d += nwarps) {
     int64_t tn = -1;
     if (t < p.tile_hi) {
       const uint32_t code = (p.dir_code >> (4 * d)) & 0xFu;
@@ -219,109 +229,16 @@ __device__ __forceinline__ void prep_links(const TileParams& p, const TileSmem& 
   cp_async_commit();
 }
 
-// Producer: one bit-sliced word per tile-boundary link (Z[K+e]) once the chunk has landed.
-__device__ __forceinline__ void finish_links(const TileParams& p, const TileSmem& S, const ChunkInfo& c, int b,
-                                             const uint8_t* __restrict__ cur, int lane) {
-  const uint32_t K = (uint32_t)p.K;
-  const uint32_t Epf = prefetch_links(p);
-  const uint8_t* buf = S.buf(b);
-  uint32_t* Z = S.Z(b);
-  cp_async_wait_all();
-  for (uint32_t d = 0; d < p.ndirs; ++d) {
-    const int64_t tn = S.ntl(b)[d * kChunkTiles + lane];
-    const uint64_t rel = (uint64_t)(tn - (int64_t)c.t0);
-    const bool inside = tn >= 0 && rel < c.nt;
-    const uint32_t lowbase = (uint32_t)tn * K;
-    const uint32_t e1 = p.dir_start[d + 1];
-    for (uint32_t e = p.dir_start[d]; e < e1; ++e) {
-      const uint32_t j2 = p.link_j2[e];
-      uint32_t v = 0;
-      if (inside) v = buf[(uint32_t)rel * K + j2];
-      else if (tn >= 0) {
-        if (e < Epf) v = (S.R(b)[e * kChunkTiles + lane] >> (8 * ((lowbase + j2) & 3u))) & 0xFFu;
-        else v = fetch_cell(cur, (uint64_t)tn * p.K + j2, p.halo);
-      }
-      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
-      if (lane == 0) Z[K + e] = bal;
-    }
-  }
-  __syncwarp();
-  if (lane == 0) mbar_arrive(&S.bar[2 + b]);
-}
-
-// Producer warp: TMA ring (load chunk i+2 as soon as chunk i's output has been read out),
-// link prefetch two chunks ahead, link words one chunk ahead.
-__device__ __forceinline__ void producer(const TileParams& p, const TileSmem& S, const uint8_t* __restrict__ cur,
-                                         uint8_t* __restrict__ next, int lane, uint64_t n) {
-  const uint32_t K = (uint32_t)p.K;
-  auto load = [&](uint64_t i) {
-    const ChunkInfo c = chunk_info(p, i);
-    const int b = (int)(i & 1);
-    if (lane == 0) {
-      fence_proxy_async();
-      tma_load_1d(S.buf(b), cur + c.chunk * kChunkTiles * p.K, (uint32_t)align16((size_t)c.nt * K), &S.bar[b]);
-    }
-    prep_links(p, S, c, b, cur, lane);
-  };
-  load(0);
-  if (n > 1) load(1);
-  mbar_wait(&S.bar[0], 0);
-  finish_links(p, S, chunk_info(p, 0), 0, cur, lane);
-  for (uint64_t i = 0; i < n; ++i) {
-    const int b = (int)(i & 1);
-    const uint32_t u = (uint32_t)((i >> 1) & 1);
-    if (i + 1 < n) {  // link words of the next chunk (its data landed a chunk ago)
-      mbar_wait(&S.bar[b ^ 1], (uint32_t)(((i + 1) >> 1) & 1));
-      finish_links(p, S, chunk_info(p, i + 1), b ^ 1, cur, lane);
-    }
-    mbar_wait(&S.bar[4 + b], u);  // consumers wrote chunk i's output
-    const ChunkInfo c = chunk_info(p, i);
-    if (lane == 0) {
-      tma_store_1d(next + c.chunk * kChunkTiles * p.K, S.buf(b), (uint32_t)align16((size_t)c.nt * K));
-      if (i + 2 < n) bulk_wait_read_all();
-    }
-    __syncwarp();
-    if (i + 2 < n) load(i + 2);
-  }
-  cp_async_wait_all();
-  if (lane == 0) bulk_wait_all();
-}
-
-// MAXT/MINB: launch bounds; the default 288-thread shape is compiled for 3 CTAs per SM.
 template <int DMAX, bool CONWAY, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const uint8_t* __restrict__ cur,
                                                          uint8_t* __restrict__ next) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   TileSmem S;
   tile_layout(p, smem_raw, &S);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NC = (int)(blockDim.x >> 5) - 1;  // consumer warps; the last warp produces
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const uint32_t K = (uint32_t)p.K;
   const uint32_t nblk = (K + 31) / 32;
-  const uint64_t n = p.nchunks > blockIdx.x ? (p.nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(p.nbr);
-    uint4* dst = reinterpret_cast<uint4*>(S.nbr);
-    for (uint32_t i = tid; i < K; i += blockDim.x) dst[i] = src[i];
-  }
-  if (tid == 0) {
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&S.bar[b], 1);
-      mbar_init(&S.bar[2 + b], 1);
-      mbar_init(&S.bar[4 + b], (uint32_t)NC);
-      S.Z(b)[p.zslot] = 0;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (n == 0) return;
-  if (warp == NC) {
-    producer(p, S, cur, next, lane, n);
-    return;
-  }
-
-  // ---------------------------------------------------------------- consumer warps
+  const uint32_t Epf = prefetch_links(p);
   uint32_t tail_mask = 0;  // packed bits (bit 8p+m = cell 4m+p) valid in the last j-block
   {
     const uint32_t nv = K - (nblk - 1) * 32;
@@ -331,21 +248,66 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
   }
   const uint32_t my_jj = 4 * (lane & 7) + (lane >> 3);  // cell offset this lane holds after a transpose
   const Transposer tr(lane);
-  const int nct = NC * 32;
+  const int lw = nwarps - 1;  // the last warp (fewest j-blocks) issues TMA and the coarse λ
+  const bool issuer = (warp == lw) && lane == 0;
 
-  for (uint64_t i = 0; i < n; ++i) {
-    const int b = (int)(i & 1);
-    const uint32_t u = (uint32_t)((i >> 1) & 1);
-    const ChunkInfo c = chunk_info(p, i);
-    const bool active = (uint32_t)lane < c.nt;
-    uint8_t* inb = S.buf(b);
-    uint32_t* Z = S.Z(b);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(p.nbr);
+    uint4* dst = reinterpret_cast<uint4*>(S.nbr);
+    for (uint32_t i = tid; i < K; i += blockDim.x) dst[i] = src[i];
+  }
+  if (tid == 0) {
+    S.Z[p.zslot] = 0;
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  uint64_t chunk = blockIdx.x;
+  if (chunk >= p.nchunks) return;
+  const uint64_t G = gridDim.x;
+  {  // prologue: chunk 0 loaded, λ of chunks 0 and 1, neighbours + prefetch of chunk 0
+    const ChunkInfo c0 = chunk_info(p, chunk);
+    if (issuer)
+      tma_load_1d(S.in(0), cur + c0.chunk * kChunkTiles * p.K, (uint32_t)align16((size_t)c0.nt * K), &S.bar[0]);
+    if (warp == lw) {
+      chunk_lambda(p, c0, S.XY(0), lane);
+      if (chunk + G < p.nchunks) chunk_lambda(p, chunk_info(p, chunk + G), S.XY(1), lane);
+    }
+    __syncthreads();
+    chunk_neighbours(p, S, c0, 0, cur, warp, nwarps, lane);
+  }
+
+  uint32_t it = 0;
+  for (; chunk < p.nchunks; chunk += G, ++it) {
+    const int buf = it & 1;
+    const ChunkInfo c = chunk_info(p, chunk);
+    const bool has_next = chunk + G < p.nchunks;
+    if (has_next) {
+      const ChunkInfo cn = chunk_info(p, chunk + G);
+      if (warp == lw) {
+        if (lane == 0) {
+          bulk_wait_read_all();  // in(buf^1) held the previous chunk's output
+          fence_proxy_async();
+          tma_load_1d(S.in(buf ^ 1), cur + cn.chunk * kChunkTiles * p.K, (uint32_t)align16((size_t)cn.nt * K),
+                      &S.bar[buf ^ 1]);
+        }
+        // λ two chunks ahead: XY(buf) is free again (this chunk's ν ran last iteration)
+        if (chunk + 2 * G < p.nchunks) chunk_lambda(p, chunk_info(p, chunk + 2 * G), S.XY(buf), lane);
+      }
+      chunk_neighbours(p, S, cn, buf ^ 1, cur, warp, nwarps, lane);  // reads XY(buf^1), written last iteration
+    } else {
+      cp_async_commit();  // one group per iteration keeps wait_group 1 exact
+    }
+    mbar_wait(&S.bar[buf], (it >> 1) & 1);
+    uint8_t* inb = S.in(buf);
     const uint32_t* in32 = reinterpret_cast<const uint32_t*>(inb);
-    mbar_wait(&S.bar[b], u);
+    const bool active = (uint32_t)lane < c.nt;
 
     // Phase A: lane = tile; 32 bytes (cells j0..j0+31) -> bits 8p+m = cell 4m+p -> transpose,
     // leaving lane L with the bit-sliced word of cell j0 + my_jj(L)
-    for (uint32_t jb = warp; jb < nblk; jb += NC) {
+    for (uint32_t jb = warp; jb < nblk; jb += nwarps) {
       const uint32_t j0 = jb * 32;
       const uint32_t a = (uint32_t)lane * K + j0;
       const uint32_t wi = a >> 2, sh = (a & 3) * 8;
@@ -358,30 +320,51 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
       if (jb == nblk - 1) acc &= tail_mask;
       if (!active) acc = 0;
       const uint32_t x = tr(acc);
-      if (j0 + my_jj < K) Z[j0 + my_jj] = x;
+      if (j0 + my_jj < K) S.Z[j0 + my_jj] = x;
     }
-    consumer_sync(nct);             // all state words of the chunk are in Z
-    mbar_wait(&S.bar[2 + b], u);    // the producer wrote the link words
+    // Phase B: boundary-link words; warp w owns the links of directions w, w + nwarps, ...
+    if (warp < (int)p.ndirs) {
+      cp_async_wait_prev();  // this chunk's gathers (issued last iteration) have landed
+      for (int d = warp; d < (int)p.ndirs; d += nwarps) {
+        const int64_t tn = S.ntl(buf)[d * kChunkTiles + lane];
+        const uint64_t rel = (uint64_t)(tn - (int64_t)c.t0);
+        const bool inside = tn >= 0 && rel < c.nt;
+        const uint32_t lowbase = (uint32_t)tn * K;
+        const uint32_t e1 = p.dir_start[d + 1];
+        for (uint32_t e = p.dir_start[d]; e < e1; ++e) {
+          const uint32_t j2 = p.link_j2[e];
+          uint32_t v = 0;
+          if (inside) v = inb[(uint32_t)rel * K + j2];
+          else if (tn >= 0) {
+            if (e < Epf) v = (S.R(buf)[e * kChunkTiles + lane] >> (8 * ((lowbase + j2) & 3u))) & 0xFFu;
+            else v = fetch_cell(cur, (uint64_t)tn * p.K + j2, p.halo);
+          }
+          const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
+          if (lane == 0) S.Z[K + e] = bal;
+        }
+      }
+    }
+    __syncthreads();
 
     // Phases C + D per j-block: lane L computes cell j0 + my_jj(L) of all 32 tiles (carry-save
     // count, rule), then the block is transposed back (lane = tile) and written in place
     const uint32_t live_lanes = c.nt >= 32 ? 0xFFFFFFFFu : ((1u << c.nt) - 1u);
-    for (uint32_t jb = warp; jb < nblk; jb += NC) {
+    for (uint32_t jb = warp; jb < nblk; jb += nwarps) {
       const uint32_t j0 = jb * 32;
       const uint32_t j = j0 + my_jj;
       uint32_t nw = 0;
       if (j < K) {
         const uint4 row = reinterpret_cast<const uint4*>(S.nbr)[j];
         uint32_t x[8];
-        x[0] = Z[row.x & 0xFFFFu];
-        x[1] = Z[row.x >> 16];
-        x[2] = Z[row.y & 0xFFFFu];
-        x[3] = Z[row.y >> 16];
-        x[4] = Z[row.z & 0xFFFFu];
+        x[0] = S.Z[row.x & 0xFFFFu];
+        x[1] = S.Z[row.x >> 16];
+        x[2] = S.Z[row.y & 0xFFFFu];
+        x[3] = S.Z[row.y >> 16];
+        x[4] = S.Z[row.z & 0xFFFFu];
         if (DMAX > 5) {
-          x[5] = Z[row.z >> 16];
-          x[6] = Z[row.w & 0xFFFFu];
-          x[7] = Z[row.w >> 16];
+          x[5] = S.Z[row.z >> 16];
+          x[6] = S.Z[row.w & 0xFFFFu];
+          x[7] = S.Z[row.w >> 16];
         }
         uint32_t c0, c1, c2, c3;
         if (DMAX <= 5) {
@@ -403,7 +386,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
           c2 = ke ^ kf;
           c3 = ke & kf;
         }
-        const uint32_t alive = Z[j];
+        const uint32_t alive = S.Z[j];
         if (CONWAY) {
           nw = c1 & ~c2 & ~c3 & (c0 | alive);  // B3/S23: count 3, or count 2 and alive
         } else {
@@ -447,9 +430,12 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
       if (bytes + lane < padded) inb[bytes + lane] = 0;
     }
     fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&S.bar[4 + b]);
+    __syncthreads();
+    if (issuer)
+      tma_store_1d(next + c.chunk * kChunkTiles * p.K, inb, (uint32_t)align16((size_t)c.nt * K));
   }
+  cp_async_wait_all();
+  if (issuer) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -458,9 +444,9 @@ using TileFn = void (*)(TileParams, const uint8_t*, uint8_t*);
 
 static TileFn pick(const TileParams& p, int threads) {
   const bool conway = (p.birth == (1u << 3)) && (p.survive == ((1u << 2) | (1u << 3)));
-  if (threads <= 288) {
-    if (p.dmax <= 5) return conway ? k_step_tile<5, true, 288, 3> : k_step_tile<5, false, 288, 3>;
-    return conway ? k_step_tile<8, true, 288, 3> : k_step_tile<8, false, 288, 3>;
+  if (threads <= 256) {
+    if (p.dmax <= 5) return conway ? k_step_tile<5, true, 256, 3> : k_step_tile<5, false, 256, 3>;
+    return conway ? k_step_tile<8, true, 256, 3> : k_step_tile<8, false, 256, 3>;
   }
   if (p.dmax <= 5) return conway ? k_step_tile<5, true, 1024, 1> : k_step_tile<5, false, 1024, 1>;
   return conway ? k_step_tile<8, true, 1024, 1> : k_step_tile<8, false, 1024, 1>;

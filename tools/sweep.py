@@ -19,7 +19,7 @@ ap.add_argument("--fractal", default="sierpinski-triangle")
 ap.add_argument("--level", type=int, default=22)
 ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--tile-levels", default="5,6,7")
-ap.add_argument("--threads", default="160,224,288,544")
+ap.add_argument("--threads", default="128,192,256,384")
 ap.add_argument("--ctas", default="0")
 a = ap.parse_args()
 f = pkg.builtin_fractal(a.fractal)
