@@ -9,16 +9,20 @@
  * ("at most one execution of λ(ω) map and ℓ executions of ν(ω)").
  *
  * Conventions (DESIGN.md §3 lists every reading of the paper used here):
- *  - Ω is the storage index Σ_{μ=1..r} β_μ k^{μ-1} (reading D2): digit μ-1 of Ω in
+ *  - Ω is the compact index Σ_{μ=1..r} β_μ k^{μ-1} (reading D2): digit μ-1 of Ω in
  *    base k is the replica id at level μ.  A state buffer holds one uint8 per
- *    cell (0 dead / 1 alive, reading D10) in Ω order.
+ *    cell (0 dead / 1 alive, reading D10) in Ω order, TILE-PADDED: Ω = t·K + j
+ *    (K = k^g cells per level-g tile) lives at byte offset
+ *    (t - t_lo)·Kp + j, Kp = tile_bytes = K rounded up to 16, so that every tile
+ *    starts on a 16-byte boundary and moves with one TMA bulk copy.  The Kp - K
+ *    padding bytes of each tile are zero (≈1% of the buffer for K = 729).
  *  - (x, y) is the expanded coordinate, origin upper-left, y downward.
  *  - Level μ of x/y has weight s^{μ-1}; axis parity per reading D1.
  *
  * Ownership: every device pointer passed in is CALLER-owned (torch allocations in
  * the Python binding), contiguous and 16-byte aligned; state buffers must be at
  * least `state_bytes` long (squeeze_geometry).  A sharded context's local buffer
- * holds Ω in [omega_lo, omega_hi) at offset Ω - omega_lo.  The context owns its
+ * holds the tiles [t_lo, t_hi) of Ω in [omega_lo, omega_hi).  The context owns its
  * lookup tables, tile tables and halo index arrays, freed by squeeze_destroy.
  * All device calls are asynchronous and stream-ordered on the given stream; a
  * context is not thread-safe.  No C++ exception crosses this boundary: every
@@ -85,7 +89,7 @@ typedef struct {
   uint64_t cells_total;  /* V = k^r */
   uint64_t omega_lo;     /* first Ω owned by this shard */
   uint64_t omega_hi;     /* one past the last Ω owned */
-  uint64_t state_bytes;  /* required bytes of a state buffer: (omega_hi - omega_lo) rounded up to 16 */
+  uint64_t state_bytes;  /* required bytes of a state buffer: local tiles x tile_bytes */
   uint64_t n;            /* expanded side s^r */
   uint64_t compact_w;    /* k^⌊r/2⌋ (D1) */
   uint64_t compact_h;    /* k^⌈r/2⌉ */
@@ -95,8 +99,8 @@ typedef struct {
   uint64_t num_tiles;    /* k^(r-g) in the whole fractal */
   uint32_t chunk_tiles;  /* tiles per CTA work unit (32: one bit-slice lane per tile) */
   uint32_t remote_links; /* tile-boundary neighbour links per tile (table size) */
-  uint32_t max_degree;   /* largest member-neighbour count of any cell (<= 8) */
-  uint32_t reserved;
+  uint32_t max_degree;   /* largest neighbour-slot count of any cell of a tile (<= 8) */
+  uint32_t tile_bytes;   /* Kp: bytes per tile in a state buffer (K rounded up to 16) */
 } squeeze_geometry_t;
 
 const char* squeeze_strerror(squeeze_status st);
@@ -157,7 +161,7 @@ squeeze_status squeeze_step_naive(void* ctx, const uint8_t* d_cur, uint8_t* d_ne
  * captures the two-step ping-pong once into a CUDA graph and replays it. */
 squeeze_status squeeze_run(void* ctx, uint8_t* d_a, uint8_t* d_b, uint64_t steps, int use_graph,
                            squeeze_stream_t stream);
-/* End to end from HOST memory: copies h_state (cells of this shard, state_bytes long,
+/* End to end from HOST memory: copies h_state (this shard's tile-padded state, state_bytes long,
  * ideally pinned) to d_a, runs `steps` steps, copies the final state back into h_state,
  * and synchronises `stream`.  d_a, d_b are caller-owned device scratch buffers. */
 squeeze_status squeeze_run_host(void* ctx, uint8_t* h_state, uint8_t* d_a, uint8_t* d_b, uint64_t steps,
@@ -177,7 +181,7 @@ squeeze_status squeeze_halo_set_sends(void* ctx, const uint64_t* omegas, uint64_
 /* Caller-owned device buffers: d_send receives `send count` bytes from squeeze_halo_pack;
  * d_recv holds one byte per squeeze_halo_needs entry, in that order. */
 squeeze_status squeeze_halo_bind(void* ctx, uint8_t* d_send, const uint8_t* d_recv);
-/* d_send[i] = d_cur[sends[i] - omega_lo]. */
+/* d_send[i] = state of cell sends[i] in d_cur. */
 squeeze_status squeeze_halo_pack(const void* ctx, const uint8_t* d_cur, squeeze_stream_t stream);
 
 /* ---- expanded bounding-box baseline (the paper's "BB" engine) ---- */
@@ -185,7 +189,7 @@ squeeze_status squeeze_halo_pack(const void* ctx, const uint8_t* d_cur, squeeze_
 squeeze_status squeeze_bb_bytes(const void* ctx, uint64_t* bytes);
 squeeze_status squeeze_bb_seed(const void* ctx, uint8_t* d_grid, uint64_t seed, uint64_t q, squeeze_stream_t stream);
 squeeze_status squeeze_bb_step(const void* ctx, const uint8_t* d_cur, uint8_t* d_next, squeeze_stream_t stream);
-/* d_state[Ω] = d_grid[λ(Ω)] — transports a BB grid to compact order for comparison. */
+/* state of cell Ω in d_state = d_grid[λ(Ω)] — transports a BB grid to the compact layout. */
 squeeze_status squeeze_bb_to_compact(const void* ctx, const uint8_t* d_grid, uint8_t* d_state,
                                      squeeze_stream_t stream);
 

@@ -85,7 +85,7 @@ class Squeeze:
         self.ctx = ctx
         g = _lib.GeometryC()
         _lib.check(self.lib.squeeze_geometry(self.ctx, ctypes.byref(g)))
-        self.geometry = Geometry(*[getattr(g, f[0]) for f in _lib.GeometryC._fields_ if f[0] != "reserved"])
+        self.geometry = Geometry(*[getattr(g, f[0]) for f in _lib.GeometryC._fields_])
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -141,6 +141,23 @@ class Squeeze:
         if fill is not None:
             t.fill_(fill)
         return t
+
+    def to_cells(self, state):
+        """Ω-ordered cells of this shard from a tile-padded state buffer (a copy; any device)."""
+        g = self.geometry
+        return state[:g.local_tiles * g.tile_bytes].view(g.local_tiles, g.tile_bytes)[:, :g.tile_cells].reshape(-1)
+
+    def from_cells(self, cells, out=None):
+        """Tile-padded state buffer from Ω-ordered cells (padding zeroed)."""
+        import torch
+        g = self.geometry
+        if out is None:
+            out = torch.zeros(max(16, g.state_bytes), dtype=torch.uint8, device=cells.device)
+        else:
+            out.zero_()
+        out[:g.local_tiles * g.tile_bytes].view(g.local_tiles, g.tile_bytes)[:, :g.tile_cells] = \
+            cells.reshape(g.local_tiles, g.tile_cells)
+        return out
 
     def map_lambda(self, omega, stream=None):
         import torch

@@ -47,7 +47,7 @@ class GeometryC(ctypes.Structure):
                 ("state_bytes", ctypes.c_uint64), ("n", ctypes.c_uint64), ("compact_w", ctypes.c_uint64),
                 ("compact_h", ctypes.c_uint64), ("r", ctypes.c_uint32), ("tile_level", ctypes.c_uint32),
                 ("tile_cells", ctypes.c_uint64), ("num_tiles", ctypes.c_uint64), ("chunk_tiles", ctypes.c_uint32),
-                ("remote_links", ctypes.c_uint32), ("max_degree", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("remote_links", ctypes.c_uint32), ("max_degree", ctypes.c_uint32), ("tile_bytes", ctypes.c_uint32)]
 
 
 vp = ctypes.c_void_p
@@ -130,7 +130,19 @@ class Geometry:
     chunk_tiles: int
     remote_links: int
     max_degree: int
+    tile_bytes: int
 
     @property
     def local_cells(self) -> int:
         return self.omega_hi - self.omega_lo
+
+    @property
+    def local_tiles(self) -> int:
+        return self.local_cells // self.tile_cells
+
+    def offsets(self, omegas):
+        """Byte offsets of (in-shard) cells Ω in a tile-padded state buffer (include/squeeze.h)."""
+        import numpy as np
+        om = np.asarray(omegas, dtype=np.int64)
+        t = om // self.tile_cells
+        return (t - self.omega_lo // self.tile_cells) * self.tile_bytes + (om - t * self.tile_cells)

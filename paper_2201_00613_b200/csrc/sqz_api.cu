@@ -37,7 +37,8 @@ struct Ctx {
   uint64_t NT = 1;
   ShardRange sr{};
   uint64_t state_bytes = 0;
-  std::vector<uint64_t> needs, sends;
+  uint32_t Kp = 16;  // bytes per tile in a state buffer (tile-padded layout)
+  std::vector<uint64_t> needs, sends, send_offsets;
   // device
   int device = -1;
   DeviceLUTs d_full, d_coarse;
@@ -116,8 +117,20 @@ void free_device(Ctx* c) {
   cudaFree(c->d_err);
 }
 
+PadLayout pad_layout(const Ctx* c) {
+  PadLayout L;
+  L.tile_lo = c->sr.tile_lo;
+  L.ntiles = c->sr.tile_hi - c->sr.tile_lo;
+  L.K = (uint32_t)c->tt.K;
+  L.Kp = c->Kp;
+  L.divK = make_fastdiv(c->tt.K);
+  L.divKp = make_fastdiv(c->Kp);
+  return L;
+}
+
 HaloView halo_view(const Ctx* c) {
   HaloView h;
+  h.L = pad_layout(c);
   h.omega_lo = c->sr.omega_lo;
   h.omega_hi = c->sr.omega_hi;
   h.needs = c->d_needs;
@@ -139,6 +152,8 @@ squeeze_status do_step(Ctx* c, const uint8_t* cur, uint8_t* next, cudaStream_t s
   TileParams p{};
   p.coarse = c->d_coarse.view;
   p.K = c->tt.K;
+  p.Kp = c->Kp;
+  p.St = (uint32_t)(((c->tt.K + 31) / 32) * 32 + 16);
   p.E = c->tt.E;
   p.zslot = c->tt.zero_slot;
   p.dmax = c->tt.max_degree;
@@ -242,7 +257,8 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
     build_level_maps(c->f, r - g, c->coarse);
     checked_pow(c->f.k, r - g, ~0ull, c->NT);
     c->sr = shard_range(c->NT, c->tt.K, c->rank, c->nranks);
-    c->state_bytes = ((c->sr.omega_hi - c->sr.omega_lo) + 15) & ~15ull;
+    c->Kp = (uint32_t)((c->tt.K + 15) & ~15ull);
+    c->state_bytes = (c->sr.tile_hi - c->sr.tile_lo) * c->Kp;
     if (c->nranks > 1) {
       unsigned th = std::max(1u, std::thread::hardware_concurrency());
       halo_needs(c->tt, c->coarse.view, c->sr, c->needs, th);
@@ -311,6 +327,7 @@ squeeze_status squeeze_geometry(const void* ctx, squeeze_geometry_t* out) {
   out->chunk_tiles = kChunkTiles;
   out->remote_links = c->tt.E;
   out->max_degree = c->tt.max_degree;
+  out->tile_bytes = c->Kp;
   return SQZ_OK;
 }
 
@@ -369,8 +386,7 @@ squeeze_status squeeze_seed(const void* ctx, uint8_t* d_state, uint64_t seed, ui
   if (st != SQZ_OK) return st;
   if (q > (1ull << 32)) return SQZ_E_CONFIG;
   DevGuard g(c->device);
-  return cu(launch_seed(c->d_full.view, c->sr.omega_lo, c->sr.omega_hi - c->sr.omega_lo, c->state_bytes, d_state,
-                        seed, q, (cudaStream_t)stream));
+  return cu(launch_seed(c->d_full.view, pad_layout(c), d_state, seed, q, (cudaStream_t)stream));
 }
 
 squeeze_status squeeze_step(void* ctx, const uint8_t* d_cur, uint8_t* d_next, squeeze_stream_t stream) {
@@ -393,8 +409,8 @@ squeeze_status squeeze_step_naive(void* ctx, const uint8_t* d_cur, uint8_t* d_ne
   if (d_cur == d_next) return SQZ_E_CONFIG;
   if (c->nranks > 1 && !c->needs.empty() && c->d_recv == nullptr) return SQZ_E_CONFIG;
   DevGuard g(c->device);
-  return cu(launch_step_naive(c->d_full.view, d_cur, d_next, c->sr.omega_hi - c->sr.omega_lo, c->state_bytes,
-                              c->rule.birth_mask, c->rule.survive_mask, halo_view(c), (cudaStream_t)stream));
+  return cu(launch_step_naive(c->d_full.view, d_cur, d_next, c->rule.birth_mask, c->rule.survive_mask, halo_view(c),
+                              (cudaStream_t)stream));
 }
 
 squeeze_status squeeze_run(void* ctx, uint8_t* d_a, uint8_t* d_b, uint64_t steps, int use_graph,
@@ -496,11 +512,16 @@ squeeze_status squeeze_halo_set_sends(void* ctx, const uint64_t* omegas, uint64_
     for (uint64_t i = 0; i < count; ++i)
       if (omegas[i] < c->sr.omega_lo || omegas[i] >= c->sr.omega_hi) return SQZ_E_CONFIG;
     c->sends.assign(omegas, omegas + count);
+    c->send_offsets.resize(count);
+    for (uint64_t i = 0; i < count; ++i) {  // tile-padded byte offsets of the cells to send
+      const uint64_t t = omegas[i] / c->tt.K;
+      c->send_offsets[i] = (t - c->sr.tile_lo) * c->Kp + (omegas[i] - t * c->tt.K);
+    }
     if (c->device >= 0) {
       DevGuard g(c->device);
       cudaFree(c->d_sends);
       c->d_sends = nullptr;
-      return upload(&c->d_sends, c->sends.data(), c->sends.size());
+      return upload(&c->d_sends, c->send_offsets.data(), c->send_offsets.size());
     }
     return SQZ_OK;
   });
@@ -523,7 +544,7 @@ squeeze_status squeeze_halo_pack(const void* ctx, const uint8_t* d_cur, squeeze_
   if (st != SQZ_OK) return st;
   if (!c->sends.empty() && !c->d_send) return SQZ_E_CONFIG;
   DevGuard g(c->device);
-  return cu(launch_halo_pack(d_cur, c->sr.omega_lo, c->d_sends, c->sends.size(), c->d_send, (cudaStream_t)stream));
+  return cu(launch_halo_pack(d_cur, c->d_sends, c->sends.size(), c->d_send, (cudaStream_t)stream));
 }
 
 squeeze_status squeeze_bb_bytes(const void* ctx, uint64_t* bytes) {
@@ -564,7 +585,7 @@ squeeze_status squeeze_bb_to_compact(const void* ctx, const uint8_t* d_grid, uin
   if (st != SQZ_OK) return st;
   if (c->nranks > 1) return SQZ_E_CONFIG;
   DevGuard g(c->device);
-  return cu(launch_bb_to_compact(c->d_full.view, d_grid, d_state, c->state_bytes, (cudaStream_t)stream));
+  return cu(launch_bb_to_compact(c->d_full.view, pad_layout(c), d_grid, d_state, (cudaStream_t)stream));
 }
 
 }  // extern "C"

@@ -10,8 +10,14 @@ namespace sqz {
 
 // State of a global Ω for a (possibly sharded) buffer: in-shard from `cur`, else from the
 // halo receive buffer (binary search over the sorted needs list).
+// Byte offset of an in-shard Ω in a tile-padded state buffer.
+__device__ __forceinline__ uint64_t pad_offset(const PadLayout& L, uint64_t om) {
+  const uint64_t t = fdiv(L.divK, om);
+  return (t - L.tile_lo) * L.Kp + (om - t * L.K);
+}
+
 __device__ __forceinline__ uint32_t fetch_cell(const uint8_t* __restrict__ cur, uint64_t om, const HaloView& h) {
-  if (om >= h.omega_lo && om < h.omega_hi) return __ldg(cur + (om - h.omega_lo));
+  if (om >= h.omega_lo && om < h.omega_hi) return __ldg(cur + pad_offset(h.L, om));
   uint64_t lo = 0, hi = h.nneeds;
   while (lo < hi) {
     uint64_t mid = (lo + hi) >> 1;

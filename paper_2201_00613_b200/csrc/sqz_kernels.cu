@@ -89,18 +89,20 @@ __global__ void k_map_nu(LevelMaps gm, const uint32_t* __restrict__ xi, const ui
 // ---------------------------------------------------------------------------------------
 // seed: 4 cells per thread, one 32-bit store; bytes past the shard are zero padding
 
-__global__ void k_seed(LevelMaps gm, uint64_t omega_lo, uint64_t cells, uint64_t words, uint32_t* __restrict__ state,
-                       uint64_t mseed, uint64_t q) {
+__global__ void k_seed(LevelMaps gm, PadLayout L, uint64_t words, uint32_t* __restrict__ state, uint64_t mseed,
+                       uint64_t q) {
   extern __shared__ uint32_t s_lut[];
   LevelMaps m = stage_maps(gm, s_lut);
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words; w += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t v = 0;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      uint64_t loc = w * 4 + b;
-      if (loc < cells) {
+      const uint64_t off = w * 4 + b;
+      const uint64_t tl = fdiv(L.divKp, off);
+      const uint64_t j = off - tl * L.Kp;
+      if (j < L.K) {
         uint32_t x, y;
-        lambda_level(m, omega_lo + loc, x, y);
+        lambda_level(m, (L.tile_lo + tl) * L.K + j, x, y);
         v |= seed_alive(x, y, mseed, q) << (8 * b);
       }
     }
@@ -111,17 +113,20 @@ __global__ void k_seed(LevelMaps gm, uint64_t omega_lo, uint64_t cells, uint64_t
 // ---------------------------------------------------------------------------------------
 // literal per-cell step: one λ, eight (membership + ν), gather, rule
 
-__global__ void k_step_naive(LevelMaps gm, const uint8_t* __restrict__ cur, uint32_t* __restrict__ next,
-                             uint64_t cells, uint64_t words, uint32_t birth, uint32_t survive, HaloView halo) {
+__global__ void k_step_naive(LevelMaps gm, const uint8_t* __restrict__ cur, uint32_t* __restrict__ next, uint64_t words,
+                             uint32_t birth, uint32_t survive, HaloView halo) {
   extern __shared__ uint32_t s_lut[];
   LevelMaps m = stage_maps(gm, s_lut);
+  const PadLayout& L = halo.L;
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words; w += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t out = 0;
 #pragma unroll 1
     for (int b = 0; b < 4; ++b) {
-      uint64_t loc = w * 4 + b;
-      if (loc >= cells) break;
-      uint64_t om = halo.omega_lo + loc;
+      const uint64_t off = w * 4 + b;
+      const uint64_t tl = fdiv(L.divKp, off);
+      const uint64_t j = off - tl * L.Kp;
+      if (j >= L.K) continue;  // tile padding stays zero
+      const uint64_t om = (L.tile_lo + tl) * L.K + j;
       uint32_t x, y;
       lambda_level(m, om, x, y);
       uint32_t count = 0;
@@ -130,7 +135,7 @@ __global__ void k_step_naive(LevelMaps gm, const uint8_t* __restrict__ cur, uint
         uint64_t nb = nu_level(m, (int64_t)x + moore_dx(i), (int64_t)y + moore_dy(i));
         if (nb != kNoneU64) count += fetch_cell(cur, nb, halo);
       }
-      out |= rule_byte(__ldg(cur + loc), count, birth, survive) << (8 * b);
+      out |= rule_byte(__ldg(cur + off), count, birth, survive) << (8 * b);
     }
     next[w] = out;
   }
@@ -163,10 +168,10 @@ __global__ void k_count_alive(const uint4* __restrict__ st, uint64_t n16, const 
   }
 }
 
-__global__ void k_halo_pack(const uint8_t* __restrict__ cur, uint64_t omega_lo, const uint64_t* __restrict__ sends,
-                            uint64_t n, uint8_t* __restrict__ out) {
+__global__ void k_halo_pack(const uint8_t* __restrict__ cur, const uint64_t* __restrict__ offs, uint64_t n,
+                            uint8_t* __restrict__ out) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    out[i] = cur[sends[i] - omega_lo];
+    out[i] = cur[offs[i]];
 }
 
 // ---------------------------------------------------------------------------------------
@@ -265,16 +270,17 @@ __global__ void k_bb_step1(const uint8_t* __restrict__ cur, uint8_t* __restrict_
   }
 }
 
-__global__ void k_bb_to_compact(LevelMaps gm, const uint8_t* __restrict__ grid, uint8_t* __restrict__ st,
-                                uint64_t cells, uint64_t state_bytes) {
+__global__ void k_bb_to_compact(LevelMaps gm, PadLayout L, const uint8_t* __restrict__ grid, uint8_t* __restrict__ st,
+                                uint64_t bytes) {
   extern __shared__ uint32_t s_lut[];
   LevelMaps m = stage_maps(gm, s_lut);
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < state_bytes;
-       i += (uint64_t)gridDim.x * blockDim.x) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < bytes; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t tl = fdiv(L.divKp, i);
+    const uint64_t j = i - tl * L.Kp;
     uint8_t v = 0;
-    if (i < cells) {
+    if (j < L.K) {
       uint32_t x, y;
-      lambda_level(m, i, x, y);
+      lambda_level(m, (L.tile_lo + tl) * L.K + j, x, y);
       v = grid[(uint64_t)y * m.n + x];
     }
     st[i] = v;
@@ -328,37 +334,35 @@ cudaError_t launch_map_nu(const LevelMaps& m, const uint32_t* x, const uint32_t*
   return cudaGetLastError();
 }
 
-cudaError_t launch_seed(const LevelMaps& m, uint64_t omega_lo, uint64_t cells, uint64_t state_bytes, uint8_t* state,
-                        uint64_t seed, uint64_t q, cudaStream_t st) {
-  uint64_t words = state_bytes / 4;
+static uint64_t splitmix_final(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+cudaError_t launch_seed(const LevelMaps& m, const PadLayout& L, uint8_t* state, uint64_t seed, uint64_t q,
+                        cudaStream_t st) {
+  const uint64_t words = L.ntiles * L.Kp / 4;
   if (words == 0) return cudaSuccess;
   size_t sm = maps_smem_bytes(m);
   cudaError_t e = maps_attr((const void*)k_seed, sm);
   if (e != cudaSuccess) return e;
-  uint64_t mseed = 0;
-  {  // host splitmix64 finaliser of the seed
-    uint64_t z = seed;
-    z ^= z >> 30;
-    z *= 0xBF58476D1CE4E5B9ull;
-    z ^= z >> 27;
-    z *= 0x94D049BB133111EBull;
-    z ^= z >> 31;
-    mseed = z;
-  }
-  k_seed<<<grid_for(words, 256), 256, sm, st>>>(m, omega_lo, cells, words, reinterpret_cast<uint32_t*>(state), mseed,
+  k_seed<<<grid_for(words, 256), 256, sm, st>>>(m, L, words, reinterpret_cast<uint32_t*>(state), splitmix_final(seed),
                                                  q);
   return cudaGetLastError();
 }
 
-cudaError_t launch_step_naive(const LevelMaps& m, const uint8_t* cur, uint8_t* next, uint64_t cells,
-                              uint64_t state_bytes, uint32_t birth, uint32_t survive, const HaloView& halo,
-                              cudaStream_t st) {
-  uint64_t words = state_bytes / 4;
+cudaError_t launch_step_naive(const LevelMaps& m, const uint8_t* cur, uint8_t* next, uint32_t birth, uint32_t survive,
+                              const HaloView& halo, cudaStream_t st) {
+  const uint64_t words = halo.L.ntiles * halo.L.Kp / 4;
   if (words == 0) return cudaSuccess;
   size_t sm = maps_smem_bytes(m);
   cudaError_t e = maps_attr((const void*)k_step_naive, sm);
   if (e != cudaSuccess) return e;
-  k_step_naive<<<grid_for(words, 256), 256, sm, st>>>(m, cur, reinterpret_cast<uint32_t*>(next), cells, words, birth,
+  k_step_naive<<<grid_for(words, 256), 256, sm, st>>>(m, cur, reinterpret_cast<uint32_t*>(next), words, birth,
                                                        survive, halo);
   return cudaGetLastError();
 }
@@ -374,10 +378,10 @@ cudaError_t launch_count_alive(const uint8_t* state, uint64_t bytes, uint64_t* o
   return cudaGetLastError();
 }
 
-cudaError_t launch_halo_pack(const uint8_t* cur, uint64_t omega_lo, const uint64_t* sends, uint64_t nsends,
-                             uint8_t* out, cudaStream_t st) {
+cudaError_t launch_halo_pack(const uint8_t* cur, const uint64_t* send_offsets, uint64_t nsends, uint8_t* out,
+                             cudaStream_t st) {
   if (nsends == 0) return cudaSuccess;
-  k_halo_pack<<<grid_for(nsends, 256), 256, 0, st>>>(cur, omega_lo, sends, nsends, out);
+  k_halo_pack<<<grid_for(nsends, 256), 256, 0, st>>>(cur, send_offsets, nsends, out);
   return cudaGetLastError();
 }
 
@@ -385,13 +389,7 @@ cudaError_t launch_bb_seed(const LevelMaps& m, uint8_t* grid, uint64_t seed, uin
   size_t sm = maps_smem_bytes(m);
   cudaError_t e = maps_attr((const void*)k_bb_seed, sm);
   if (e != cudaSuccess) return e;
-  uint64_t z = seed;
-  z ^= z >> 30;
-  z *= 0xBF58476D1CE4E5B9ull;
-  z ^= z >> 27;
-  z *= 0x94D049BB133111EBull;
-  z ^= z >> 31;
-  k_bb_seed<<<grid_for(m.n * m.n, 256), 256, sm, st>>>(m, grid, m.n, z, q);
+  k_bb_seed<<<grid_for(m.n * m.n, 256), 256, sm, st>>>(m, grid, m.n, splitmix_final(seed), q);
   return cudaGetLastError();
 }
 
@@ -405,12 +403,14 @@ cudaError_t launch_bb_step(const uint8_t* cur, uint8_t* next, uint64_t n, uint32
   return cudaGetLastError();
 }
 
-cudaError_t launch_bb_to_compact(const LevelMaps& m, const uint8_t* grid, uint8_t* state, uint64_t state_bytes,
+cudaError_t launch_bb_to_compact(const LevelMaps& m, const PadLayout& L, const uint8_t* grid, uint8_t* state,
                                  cudaStream_t st) {
+  const uint64_t bytes = L.ntiles * L.Kp;
+  if (bytes == 0) return cudaSuccess;
   size_t sm = maps_smem_bytes(m);
   cudaError_t e = maps_attr((const void*)k_bb_to_compact, sm);
   if (e != cudaSuccess) return e;
-  k_bb_to_compact<<<grid_for(state_bytes, 256), 256, sm, st>>>(m, grid, state, m.cells, state_bytes);
+  k_bb_to_compact<<<grid_for(bytes, 256), 256, sm, st>>>(m, L, grid, state, bytes);
   return cudaGetLastError();
 }
 

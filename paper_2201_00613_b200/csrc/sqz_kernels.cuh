@@ -8,8 +8,19 @@
 
 namespace sqz {
 
+// Tile-padded state layout (include/squeeze.h): cell Ω = t·K + j of this shard lives at byte
+// (t - tile_lo)·Kp + j of a state buffer.
+struct PadLayout {
+  uint64_t tile_lo;
+  uint64_t ntiles;   // local tiles
+  uint32_t K, Kp;
+  FastDiv64 divK;    // division by K
+  FastDiv64 divKp;   // division by Kp
+};
+
 struct HaloView {
   uint64_t omega_lo, omega_hi;  // this shard
+  PadLayout L;
   const uint64_t* needs;        // sorted Ω outside the shard
   uint64_t nneeds;
   const uint8_t* recv;          // recv[i] = state of needs[i]
@@ -19,6 +30,8 @@ struct HaloView {
 struct TileParams {
   LevelMaps coarse;  // maps at level r - g (tile coordinates)
   uint64_t K;        // cells per tile
+  uint32_t Kp;       // bytes per tile in a state buffer (K rounded up to 16)
+  uint32_t St;       // bytes per tile slot in shared memory (odd multiple of 16, >= round_up(K, 32))
   uint32_t E;        // remote links per tile
   uint32_t zslot;    // index of the zero word in Z
   uint32_t dmax;     // max neighbour entries per cell
@@ -43,20 +56,19 @@ cudaError_t launch_map_lambda(const LevelMaps& m, const uint64_t* om, uint32_t* 
                               cudaStream_t st);
 cudaError_t launch_map_nu(const LevelMaps& m, const uint32_t* x, const uint32_t* y, uint64_t* om, uint64_t count,
                           cudaStream_t st);
-cudaError_t launch_seed(const LevelMaps& m, uint64_t omega_lo, uint64_t cells, uint64_t state_bytes, uint8_t* state,
-                        uint64_t seed, uint64_t q, cudaStream_t st);
-cudaError_t launch_step_naive(const LevelMaps& m, const uint8_t* cur, uint8_t* next, uint64_t cells,
-                              uint64_t state_bytes, uint32_t birth, uint32_t survive, const HaloView& halo,
-                              cudaStream_t st);
+cudaError_t launch_seed(const LevelMaps& m, const PadLayout& L, uint8_t* state, uint64_t seed, uint64_t q,
+                        cudaStream_t st);
+cudaError_t launch_step_naive(const LevelMaps& m, const uint8_t* cur, uint8_t* next, uint32_t birth, uint32_t survive,
+                              const HaloView& halo, cudaStream_t st);
 cudaError_t launch_step_tile(const TileParams& p, const uint8_t* cur, uint8_t* next, int grid, int threads,
                              size_t smem, cudaStream_t st);
 cudaError_t launch_count_alive(const uint8_t* state, uint64_t bytes, uint64_t* out, cudaStream_t st);
-cudaError_t launch_halo_pack(const uint8_t* cur, uint64_t omega_lo, const uint64_t* sends, uint64_t nsends,
-                             uint8_t* out, cudaStream_t st);
+cudaError_t launch_halo_pack(const uint8_t* cur, const uint64_t* send_offsets, uint64_t nsends, uint8_t* out,
+                             cudaStream_t st);
 cudaError_t launch_bb_seed(const LevelMaps& m, uint8_t* grid, uint64_t seed, uint64_t q, cudaStream_t st);
 cudaError_t launch_bb_step(const uint8_t* cur, uint8_t* next, uint64_t n, uint32_t birth, uint32_t survive,
                            cudaStream_t st);
-cudaError_t launch_bb_to_compact(const LevelMaps& m, const uint8_t* grid, uint8_t* state, uint64_t state_bytes,
+cudaError_t launch_bb_to_compact(const LevelMaps& m, const PadLayout& L, const uint8_t* grid, uint8_t* state,
                                  cudaStream_t st);
 
 }  // namespace sqz

@@ -106,8 +106,10 @@ __device__ __forceinline__ uint32_t rule_bits(uint32_t mask, uint32_t c0, uint32
 __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
-// chunk bytes + slack for the 36-byte windows read past the last tile
-__host__ __device__ inline size_t chunk_buf_bytes(uint64_t K) { return align16((size_t)K * kChunkTiles) + 64; }
+// 32 tile slots of St bytes each (St = round_up(K, 32) + 16: an odd multiple of 16, so the
+// 16-byte accesses of 8 consecutive lanes hit distinct bank groups)
+__host__ __device__ inline uint32_t slot_bytes(uint64_t K) { return (uint32_t)(((K + 31) / 32) * 32 + 16); }
+__host__ __device__ inline size_t chunk_buf_bytes(uint64_t K) { return (size_t)slot_bytes(K) * kChunkTiles; }
 
 // Boundary links whose neighbour tile is outside the chunk are prefetched one chunk ahead
 // with 4-byte cp.async gathers into R; at most kMaxPrefetchLinks (larger E falls back to a
@@ -220,13 +222,40 @@ __device__ __forceinline__ void chunk_neighbours(const TileParams& p, const Tile
       const uint32_t e1 = min((uint32_t)p.dir_start[d + 1], Epf);
       for (uint32_t e = p.dir_start[d]; e < e1; ++e) {
         uint32_t* dst = &S.R(b)[e * kChunkTiles + lane];
-        const uint64_t om = (uint64_t)tn * p.K + p.link_j2[e];
-        if (om >= p.halo.omega_lo && om < p.halo.omega_hi) cp_async4(dst, cur + ((om - p.halo.omega_lo) & ~3ull));
-        else *dst = fetch_cell(cur, om, p.halo) << (8 * (uint32_t)(om & 3));  // halo: rare, synchronous
+        const uint32_t j2 = p.link_j2[e];
+        if ((uint64_t)tn >= p.tile_lo && (uint64_t)tn < p.tile_hi) {
+          const uint64_t off = ((uint64_t)tn - p.tile_lo) * p.Kp + j2;  // tile-padded layout
+          cp_async4(dst, cur + (off & ~3ull));
+        } else {
+          *dst = fetch_cell(cur, (uint64_t)tn * p.K + j2, p.halo) << (8 * (j2 & 3u));  // halo: rare, synchronous
+        }
       }
     }
   }
   cp_async_commit();
+}
+
+// Lanes of one warp: tile i of the chunk -> slot i (one bulk copy per tile, Kp bytes each).
+__device__ __forceinline__ void chunk_load(const TileParams& p, const ChunkInfo& c, uint8_t* buf, uint64_t* bar,
+                                           const uint8_t* __restrict__ cur, int lane, uint32_t St) {
+  if (lane == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(c.nt * p.Kp)
+                 : "memory");
+  }
+  __syncwarp();
+  if ((uint32_t)lane < c.nt) {
+    const uint8_t* src = cur + (c.t0 + lane - p.tile_lo) * p.Kp;
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(buf + (size_t)lane * St)),
+        "l"(src), "r"(p.Kp), "r"(smem_u32(bar))
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void chunk_store(const TileParams& p, const ChunkInfo& c, const uint8_t* buf,
+                                            uint8_t* __restrict__ next, int lane, uint32_t St) {
+  if ((uint32_t)lane < c.nt) tma_store_1d(next + (c.t0 + lane - p.tile_lo) * p.Kp, buf + (size_t)lane * St, p.Kp);
 }
 
 template <int DMAX, bool CONWAY, int MAXT, int MINB>
@@ -249,7 +278,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
   const uint32_t my_jj = 4 * (lane & 7) + (lane >> 3);  // cell offset this lane holds after a transpose
   const Transposer tr(lane);
   const int lw = nwarps - 1;  // the last warp (fewest j-blocks) issues TMA and the coarse λ
-  const bool issuer = (warp == lw) && lane == 0;
+  const uint32_t St = slot_bytes(K);
 
   {
     const uint4* src = reinterpret_cast<const uint4*>(p.nbr);
@@ -269,9 +298,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
   const uint64_t G = gridDim.x;
   {  // prologue: chunk 0 loaded, λ of chunks 0 and 1, neighbours + prefetch of chunk 0
     const ChunkInfo c0 = chunk_info(p, chunk);
-    if (issuer)
-      tma_load_1d(S.in(0), cur + c0.chunk * kChunkTiles * p.K, (uint32_t)align16((size_t)c0.nt * K), &S.bar[0]);
     if (warp == lw) {
+      chunk_load(p, c0, S.in(0), &S.bar[0], cur, lane, St);
       chunk_lambda(p, c0, S.XY(0), lane);
       if (chunk + G < p.nchunks) chunk_lambda(p, chunk_info(p, chunk + G), S.XY(1), lane);
     }
@@ -287,12 +315,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     if (has_next) {
       const ChunkInfo cn = chunk_info(p, chunk + G);
       if (warp == lw) {
-        if (lane == 0) {
-          bulk_wait_read_all();  // in(buf^1) held the previous chunk's output
-          fence_proxy_async();
-          tma_load_1d(S.in(buf ^ 1), cur + cn.chunk * kChunkTiles * p.K, (uint32_t)align16((size_t)cn.nt * K),
-                      &S.bar[buf ^ 1]);
-        }
+        bulk_wait_read_all();  // in(buf^1) held the previous chunk's output (each lane stored one tile)
+        fence_proxy_async();
+        chunk_load(p, cn, S.in(buf ^ 1), &S.bar[buf ^ 1], cur, lane, St);
         // λ two chunks ahead: XY(buf) is free again (this chunk's ν ran last iteration)
         if (chunk + 2 * G < p.nchunks) chunk_lambda(p, chunk_info(p, chunk + 2 * G), S.XY(buf), lane);
       }
@@ -302,21 +327,17 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     }
     mbar_wait(&S.bar[buf], (it >> 1) & 1);
     uint8_t* inb = S.in(buf);
-    const uint32_t* in32 = reinterpret_cast<const uint32_t*>(inb);
     const bool active = (uint32_t)lane < c.nt;
 
-    // Phase A: lane = tile; 32 bytes (cells j0..j0+31) -> bits 8p+m = cell 4m+p -> transpose,
-    // leaving lane L with the bit-sliced word of cell j0 + my_jj(L)
+    // Phase A: lane = tile; 32 aligned bytes (cells j0..j0+31 of its slot) -> bits 8p+m =
+    // cell 4m+p -> transpose, leaving lane L with the bit-sliced word of cell j0 + my_jj(L)
     for (uint32_t jb = warp; jb < nblk; jb += nwarps) {
       const uint32_t j0 = jb * 32;
-      const uint32_t a = (uint32_t)lane * K + j0;
-      const uint32_t wi = a >> 2, sh = (a & 3) * 8;
-      uint32_t w[9];
-#pragma unroll
-      for (int m = 0; m < 9; ++m) w[m] = in32[wi + m];
-      uint32_t acc = 0;
-#pragma unroll
-      for (int m = 0; m < 8; ++m) acc += (__funnelshift_r(w[m], w[m + 1], sh) & 0x01010101u) << m;
+      const uint4* src = reinterpret_cast<const uint4*>(inb + (size_t)lane * St + j0);
+      const uint4 lo = src[0], hi = src[1];
+      uint32_t acc = (lo.x & 0x01010101u) | ((lo.y & 0x01010101u) << 1) | ((lo.z & 0x01010101u) << 2) |
+                     ((lo.w & 0x01010101u) << 3) | ((hi.x & 0x01010101u) << 4) | ((hi.y & 0x01010101u) << 5) |
+                     ((hi.z & 0x01010101u) << 6) | ((hi.w & 0x01010101u) << 7);
       if (jb == nblk - 1) acc &= tail_mask;
       if (!active) acc = 0;
       const uint32_t x = tr(acc);
@@ -329,14 +350,13 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
         const int64_t tn = S.ntl(buf)[d * kChunkTiles + lane];
         const uint64_t rel = (uint64_t)(tn - (int64_t)c.t0);
         const bool inside = tn >= 0 && rel < c.nt;
-        const uint32_t lowbase = (uint32_t)tn * K;
         const uint32_t e1 = p.dir_start[d + 1];
         for (uint32_t e = p.dir_start[d]; e < e1; ++e) {
           const uint32_t j2 = p.link_j2[e];
           uint32_t v = 0;
-          if (inside) v = inb[(uint32_t)rel * K + j2];
+          if (inside) v = inb[(uint32_t)rel * St + j2];
           else if (tn >= 0) {
-            if (e < Epf) v = (S.R(buf)[e * kChunkTiles + lane] >> (8 * ((lowbase + j2) & 3u))) & 0xFFu;
+            if (e < Epf) v = (S.R(buf)[e * kChunkTiles + lane] >> (8 * (j2 & 3u))) & 0xFFu;
             else v = fetch_cell(cur, (uint64_t)tn * p.K + j2, p.halo);
           }
           const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
@@ -394,48 +414,19 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
         }
         nw &= live_lanes;
       }
-      const uint32_t xb = tr(nw);  // bit 8p+m = cell j0 + 4m + p of this lane's tile
+      const uint32_t xb = tr(nw);  // bit 8p+m = cell j0 + 4m + p of this lane's tile (0 past K)
       if (!active) continue;
-      const uint32_t a = (uint32_t)lane * K + j0;
-      const uint32_t nv = min(32u, K - j0);
-      uint32_t bw[8];
-#pragma unroll
-      for (int m = 0; m < 8; ++m) bw[m] = (xb >> m) & 0x01010101u;
-      if (nv == 32) {
-        const uint32_t sh = a & 3;
-        uint32_t* out32 = reinterpret_cast<uint32_t*>(inb + (a - sh));
-        if (sh == 0) {
-#pragma unroll
-          for (int m = 0; m < 8; ++m) out32[m] = bw[m];
-        } else {
-          const uint32_t d = 4 - sh;  // bytes before the first aligned word (byte stores)
-#pragma unroll
-          for (int q = 0; q < 3; ++q)
-            if ((uint32_t)q < d) inb[a + q] = (uint8_t)(bw[0] >> (8 * q));
-#pragma unroll
-          for (int k = 1; k < 8; ++k) out32[k] = __funnelshift_r(bw[k - 1], bw[k], 8 * d);
-#pragma unroll
-          for (int q = 1; q < 4; ++q)
-            if ((uint32_t)q >= d) inb[a + 28 + q] = (uint8_t)(bw[7] >> (8 * q));
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 32; ++q)
-          if ((uint32_t)q < nv) inb[a + q] = (uint8_t)(bw[q >> 2] >> (8 * (q & 3)));
-      }
-    }
-    if (warp == 0) {  // zero padding up to the 16-byte bulk-copy granule
-      const uint32_t bytes = c.nt * K;
-      const uint32_t padded = (uint32_t)align16(bytes);
-      if (bytes + lane < padded) inb[bytes + lane] = 0;
+      uint4* dst = reinterpret_cast<uint4*>(inb + (size_t)lane * St + j0);
+      dst[0] = make_uint4(xb & 0x01010101u, (xb >> 1) & 0x01010101u, (xb >> 2) & 0x01010101u, (xb >> 3) & 0x01010101u);
+      dst[1] = make_uint4((xb >> 4) & 0x01010101u, (xb >> 5) & 0x01010101u, (xb >> 6) & 0x01010101u,
+                          (xb >> 7) & 0x01010101u);
     }
     fence_proxy_async();
     __syncthreads();
-    if (issuer)
-      tma_store_1d(next + c.chunk * kChunkTiles * p.K, inb, (uint32_t)align16((size_t)c.nt * K));
+    if (warp == lw) chunk_store(p, c, inb, next, lane, St);
   }
   cp_async_wait_all();
-  if (issuer) bulk_wait_all();
+  if (warp == lw) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------------------

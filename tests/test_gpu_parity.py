@@ -23,9 +23,20 @@ def mk(name, r, **kw):
     return sq.Squeeze(sq.builtin_fractal(name), r, device=DEV, **kw)
 
 
-def host(t, n):
+def host(p, t):
+    """Ω-ordered cells of a tile-padded state buffer, as numpy."""
     torch.cuda.synchronize()
-    return t[:n].cpu().numpy()
+    return p.to_cells(t).cpu().numpy()
+
+
+def padding_is_zero(p, t):
+    g = p.geometry
+    v = t[:g.local_tiles * g.tile_bytes].view(g.local_tiles, g.tile_bytes)[:, g.tile_cells:]
+    return not bool(v.any())
+
+
+def offsets_t(p, om):
+    return torch.from_numpy(p.geometry.offsets(om)).cuda()
 
 
 def oracle_run(name, r, seed, density, steps, rule=A.B3S23):
@@ -86,9 +97,8 @@ def test_seed_full(name, r):
     st = p.new_state()
     p.seed(st, 42, 0.3)
     g = p.geometry
-    got = host(st, g.state_bytes)
-    assert np.array_equal(got[:g.cells_total], A.seed_compact(BUILTINS[name], r, 42, 0.3))
-    assert not got[g.cells_total:].any()
+    assert np.array_equal(host(p, st), A.seed_compact(BUILTINS[name], r, 42, 0.3))
+    assert padding_is_zero(p, st)
 
 
 # ------------------------------------------------------------------ the step, small levels, every step
@@ -101,7 +111,7 @@ def test_config_c1_r8_10_steps(engine):
     p.seed(a, 42, 0.3)
     for t in range(10):
         (p.step if engine == "tile" else p.step_naive)(a, b)
-        assert np.array_equal(host(b, 3 ** 8), want[t + 1]), f"step {t + 1}"
+        assert np.array_equal(host(p, b), want[t + 1]), f"step {t + 1}"
         a, b = b, a
 
 
@@ -119,12 +129,10 @@ def test_tile_step_levels_and_tilings(name, r, g):
     want = oracle_run(name, r, 7, 0.4, steps)
     a, b = p.new_state(), p.new_state()
     p.seed(a, 7, 0.4)
-    n = BUILTINS[name].k ** r
     for t in range(steps):
         p.step(a, b)
-        got = host(b, p.geometry.state_bytes)
-        assert np.array_equal(got[:n], want[t + 1]), f"step {t + 1}"
-        assert not got[n:].any()
+        assert np.array_equal(host(p, b), want[t + 1]), f"step {t + 1}"
+        assert padding_is_zero(p, b)
         a, b = b, a
 
 
@@ -141,7 +149,7 @@ def test_rules(rule, engine):
     p.seed(a, 3, 0.5)
     for t in range(3):
         (p.step if engine == "tile" else p.step_naive)(a, b)
-        assert np.array_equal(host(b, 3 ** r), want[t + 1])
+        assert np.array_equal(host(p, b), want[t + 1])
         a, b = b, a
 
 
@@ -153,7 +161,7 @@ def test_block_threads_and_ctas_variants():
         p.seed(a, 5, 0.5)
         p.step(a, b)
         p.step(b, a)
-        assert np.array_equal(host(a, 3 ** 10), want[2]), (bt, cps)
+        assert np.array_equal(host(p, a), want[2]), (bt, cps)
 
 
 def test_run_graph_and_host():
@@ -165,14 +173,14 @@ def test_run_graph_and_host():
         p.seed(a, 11, 0.5)
         fin = p.run(a, b, 7, use_graph=use_graph)
         assert fin is b
-        assert np.array_equal(host(fin, 3 ** r), want[7])
+        assert np.array_equal(host(p, fin), want[7])
         p.seed(a, 11, 0.5)
         fin = p.run(a, b, 6, use_graph=use_graph)
-        assert np.array_equal(host(fin, 3 ** r), want[6])
-    h = torch.from_numpy(np.concatenate([want[0], np.zeros(p.geometry.state_bytes - 3 ** r, np.uint8)])).pin_memory()
+        assert np.array_equal(host(p, fin), want[6])
+    h = p.from_cells(torch.from_numpy(want[0])).pin_memory()
     a, b = p.new_state(), p.new_state()
     p.run_host(h, a, b, 5)
-    assert np.array_equal(h.numpy()[:3 ** r], want[5])
+    assert np.array_equal(p.to_cells(h).numpy(), want[5])
 
 
 def test_count_alive():
@@ -195,7 +203,7 @@ def test_full_size_sampled_first_step(r):
     torch.cuda.synchronize()
     om = np.unique(sqz_inputs.random_indices(200_000, 3 ** r, seed=1234).astype(np.int64))
     om = np.concatenate([om, [0, 1, 2, 3 ** r - 1, 3 ** r - 2]]).astype(np.int64)
-    idx = torch.from_numpy(om).cuda()
+    idx = offsets_t(p, om)
     assert np.array_equal(a[idx].cpu().numpy(), A.seed_at(SIERPINSKI, r, om, 42, 0.5))
     want = A.compact_step_sampled(SIERPINSKI, r, om, lambda q: A.seed_at(SIERPINSKI, r, q, 42, 0.5))
     assert np.array_equal(b[idx].cpu().numpy(), want)
@@ -214,8 +222,9 @@ def test_histogram_pin_full_size(r):
         p = mk("sierpinski-triangle", r, rule=(0, 1 << c))
         if a is None:
             a, b = p.new_state(), p.new_state()
+            g = p.geometry
             a.zero_()
-            a[:3 ** r] = 1
+            a[:g.local_tiles * g.tile_bytes].view(g.local_tiles, g.tile_bytes)[:, :g.tile_cells] = 1
         p.step(a, b)
         assert int(p.count_alive(b).item()) == hist.get(c, 0), c
     # B3/S23 from all alive: survivors are cells with 2 or 3 neighbours
@@ -252,17 +261,18 @@ def test_bb_engine_vs_oracle(name, r):
     g0, g1 = p.new_bb(), p.new_bb()
     p.bb_seed(g0, 42, 0.3)
     n = o.s ** r
-    grid = host(g0, n * n).reshape(n, n)
+    torch.cuda.synchronize()
+    grid = g0[:n * n].cpu().numpy().reshape(n, n)
     assert np.array_equal(grid == 2, ~mask)
     assert np.array_equal(np.where(mask, grid, 0), st)
     comp = p.new_state()
     for t in range(4):
         p.bb_step(g0, g1)
         st = A.expanded_step(st, mask, A.B3S23)
-        grid = host(g1, n * n).reshape(n, n)
+        grid = g1[:n * n].cpu().numpy().reshape(n, n)
         assert np.array_equal(np.where(mask, grid, 0), st) and (grid[~mask] == 2).all()
         p.bb_to_compact(g1, comp)
-        assert np.array_equal(host(comp, o.k ** r), A.transport(o, r, st))
+        assert np.array_equal(host(p, comp), A.transport(o, r, st))
         g0, g1 = g1, g0
 
 
@@ -306,7 +316,7 @@ def run_sharded_local(name, r, nranks, steps, naive=False, g=0):
             for j, (lo, hi) in enumerate(ranges):
                 sel = np.nonzero((nd >= lo) & (nd < hi))[0]
                 if sel.size:
-                    src = torch.from_numpy((nd[sel] - lo).astype(np.int64)).cuda()
+                    src = offsets_t(parts[j], nd[sel].astype(np.int64))
                     recv[i][torch.from_numpy(sel).cuda()] = bufs[j][0][src]
         for p, bf in zip(parts, bufs):
             (p.step_naive if naive else p.step)(bf[0], bf[1])
@@ -315,7 +325,7 @@ def run_sharded_local(name, r, nranks, steps, naive=False, g=0):
     torch.cuda.synchronize()
     for p in parts:
         assert p.device_error() == 0
-    return np.concatenate([bf[0][:hi - lo].cpu().numpy() for bf, (lo, hi) in zip(bufs, ranges)])
+    return np.concatenate([host(pp, bf[0]) for pp, bf in zip(parts, bufs)])
 
 
 @pytest.mark.parametrize("name,r,nranks,g", [("sierpinski-triangle", 10, 2, 3), ("sierpinski-triangle", 12, 3, 4),
@@ -333,7 +343,7 @@ def test_sharded_r16_equals_unsharded():
     a, b = p.new_state(), p.new_state()
     p.seed(a, 42, 0.5)
     fin = p.run(a, b, 6)
-    assert np.array_equal(got, host(fin, 3 ** 16))
+    assert np.array_equal(got, host(p, fin))
 
 
 def test_halo_pack_kernel():
@@ -348,7 +358,8 @@ def test_halo_pack_kernel():
     p.halo_bind(send, recv)
     p.halo_pack(cur)
     want = A.seed_at(SIERPINSKI, 10, sends.astype(np.int64), 42, 0.5)
-    assert np.array_equal(host(send, 4), want)
+    torch.cuda.synchronize()
+    assert np.array_equal(send.cpu().numpy(), want)
 
 
 def test_one_warp_ctas_small_tiles():
@@ -360,7 +371,7 @@ def test_one_warp_ctas_small_tiles():
         p.seed(a, 7, 0.4)
         for t in range(4):
             p.step(a, b)
-            assert np.array_equal(host(b, 3 ** r), want[t + 1]), (r, g, t)
+            assert np.array_equal(host(p, b), want[t + 1]), (r, g, t)
             a, b = b, a
 
 
