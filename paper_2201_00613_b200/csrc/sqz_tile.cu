@@ -127,6 +127,7 @@ struct TileSmem {
   uint32_t* R0;    // 2 x [E][32] prefetched words holding out-of-chunk neighbour bytes
   uint32_t rn;
   uint64_t* bar;   // 2 mbarriers (TMA loads)
+  uint32_t* ctr;   // [2] Phase-A and [2] count/write-back block counters, by chunk parity
   __device__ __forceinline__ uint8_t* in(int b) const { return in0 + (size_t)b * cb; }
   __device__ __forceinline__ uint32_t* XY(int b) const { return XY0 + (size_t)b * 64; }
   __device__ __forceinline__ int64_t* ntl(int b) const { return ntl0 + (size_t)b * ntn; }
@@ -164,6 +165,8 @@ __host__ __device__ inline size_t tile_layout(const TileParams& p, uint8_t* base
   }
   off += 2 * rn * 4;
   if (s) s->bar = (uint64_t*)(base + off);
+  off += 16;
+  if (s) s->ctr = (uint32_t*)(base + off);
   off += 16;
   return align16(off);
 }
@@ -258,6 +261,13 @@ __device__ __forceinline__ void chunk_store(const TileParams& p, const ChunkInfo
   if ((uint32_t)lane < c.nt) tma_store_1d(next + (c.t0 + lane - p.tile_lo) * p.Kp, buf + (size_t)lane * St, p.Kp);
 }
 
+// Dynamic j-block distribution: warps that carry extra work (coarse maps, TMA) take fewer blocks.
+__device__ __forceinline__ uint32_t grab(uint32_t* ctr, int lane) {
+  uint32_t v = 0;
+  if (lane == 0) v = atomicAdd(ctr, 1u);
+  return __shfl_sync(0xFFFFFFFFu, v, 0);
+}
+
 template <int DMAX, bool CONWAY, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const uint8_t* __restrict__ cur,
                                                          uint8_t* __restrict__ next) {
@@ -287,6 +297,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
   }
   if (tid == 0) {
     S.Z[p.zslot] = 0;
+    S.ctr[0] = S.ctr[1] = S.ctr[2] = S.ctr[3] = 0;
     mbar_init(&S.bar[0], 1);
     mbar_init(&S.bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -318,8 +329,6 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
         bulk_wait_read_all();  // in(buf^1) held the previous chunk's output (each lane stored one tile)
         fence_proxy_async();
         chunk_load(p, cn, S.in(buf ^ 1), &S.bar[buf ^ 1], cur, lane, St);
-        // λ two chunks ahead: XY(buf) is free again (this chunk's ν ran last iteration)
-        if (chunk + 2 * G < p.nchunks) chunk_lambda(p, chunk_info(p, chunk + 2 * G), S.XY(buf), lane);
       }
       chunk_neighbours(p, S, cn, buf ^ 1, cur, warp, nwarps, lane);  // reads XY(buf^1), written last iteration
     } else {
@@ -331,7 +340,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
 
     // Phase A: lane = tile; 32 aligned bytes (cells j0..j0+31 of its slot) -> bits 8p+m =
     // cell 4m+p -> transpose, leaving lane L with the bit-sliced word of cell j0 + my_jj(L)
-    for (uint32_t jb = warp; jb < nblk; jb += nwarps) {
+    for (uint32_t jb = grab(&S.ctr[buf], lane); jb < nblk; jb = grab(&S.ctr[buf], lane)) {
       const uint32_t j0 = jb * 32;
       const uint4* src = reinterpret_cast<const uint4*>(inb + (size_t)lane * St + j0);
       const uint4 lo = src[0], hi = src[1];
@@ -365,11 +374,14 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
       }
     }
     __syncthreads();
+    if (tid == 0) S.ctr[buf ^ 1] = 0;  // next chunk's Phase-A counter (its last use ended at the barrier)
+    // λ two chunks ahead (XY(buf) is free: this chunk's ν ran last iteration); overlaps the blocks below
+    if (warp == lw && chunk + 2 * G < p.nchunks) chunk_lambda(p, chunk_info(p, chunk + 2 * G), S.XY(buf), lane);
 
     // Phases C + D per j-block: lane L computes cell j0 + my_jj(L) of all 32 tiles (carry-save
     // count, rule), then the block is transposed back (lane = tile) and written in place
     const uint32_t live_lanes = c.nt >= 32 ? 0xFFFFFFFFu : ((1u << c.nt) - 1u);
-    for (uint32_t jb = warp; jb < nblk; jb += nwarps) {
+    for (uint32_t jb = grab(&S.ctr[2 + buf], lane); jb < nblk; jb = grab(&S.ctr[2 + buf], lane)) {
       const uint32_t j0 = jb * 32;
       const uint32_t j = j0 + my_jj;
       uint32_t nw = 0;
@@ -423,6 +435,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     }
     fence_proxy_async();
     __syncthreads();
+    if (tid == 0) S.ctr[2 + (buf ^ 1)] = 0;  // next chunk's count/write-back counter
     if (warp == lw) chunk_store(p, c, inb, next, lane, St);
   }
   cp_async_wait_all();

@@ -23,10 +23,6 @@ ap.add_argument("--threads", default="128,192,256,384")
 ap.add_argument("--ctas", default="0")
 a = ap.parse_args()
 f = pkg.builtin_fractal(a.fractal)
-base = pkg.Squeeze(f, a.level, device=0)
-x, y = base.new_state(), base.new_state()
-base.seed(x, 42, 0.5)
-ref = None
 for g, th, cps in itertools.product([int(v) for v in a.tile_levels.split(",")],
                                     [int(v) for v in a.threads.split(",")],
                                     [int(v) for v in a.ctas.split(",")]):
@@ -35,6 +31,8 @@ for g, th, cps in itertools.product([int(v) for v in a.tile_levels.split(",")],
     except pkg.SqueezeError as e:
         print(json.dumps({"g": g, "threads": th, "ctas": cps, "error": str(e)}), flush=True)
         continue
+    x, y = p.new_state(), p.new_state()  # the tile-padded layout depends on the tile level
+    p.seed(x, 42, 0.5)
     for _ in range(3):
         p.step(x, y)
     torch.cuda.synchronize()
@@ -48,4 +46,5 @@ for g, th, cps in itertools.product([int(v) for v in a.tile_levels.split(",")],
     cells = p.geometry.cells_total
     print(json.dumps({"g": g, "threads": th, "ctas": cps, "ms": round(ms, 3), "gcells_s": round(cells / ms / 1e6, 1),
                       "GBps": round(2 * cells / ms / 1e6, 1)}), flush=True)
-    del p
+    del p, x, y
+    torch.cuda.empty_cache()
