@@ -256,6 +256,7 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
     build_level_maps(c->f, r, c->full);
     build_level_maps(c->f, r - g, c->coarse);
     checked_pow(c->f.k, r - g, ~0ull, c->NT);
+    if (c->NT >= 0xFFFFFFFFull) return fail(SQZ_E_OVERFLOW);  // tile indices are 32-bit in the tile kernel
     c->sr = shard_range(c->NT, c->tt.K, c->rank, c->nranks);
     c->Kp = (uint32_t)((c->tt.K + 15) & ~15ull);
     c->state_bytes = (c->sr.tile_hi - c->sr.tile_lo) * c->Kp;

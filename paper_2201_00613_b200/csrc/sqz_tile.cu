@@ -120,9 +120,8 @@ struct TileSmem {
   uint8_t* in0;    // 2 chunk buffers (input, then output in place)
   uint32_t cb;
   uint32_t* Z;     // K state words | E link words | zero word
-  uint16_t* nbr;   // K x 8 neighbour slots into Z
   uint32_t* XY0;   // 2 x [32] coarse (X, Y) of a chunk's tiles (by chunk parity)
-  int64_t* ntl0;   // 2 x [ndirs][32] neighbour tile of each lane's tile (-1 = none)
+  uint32_t* ntl0;  // 2 x [ndirs][32] neighbour tile + 1 of each lane's tile (0 = none)
   uint32_t ntn;
   uint32_t* R0;    // 2 x [E][32] prefetched words holding out-of-chunk neighbour bytes
   uint32_t rn;
@@ -130,7 +129,7 @@ struct TileSmem {
   uint32_t* ctr;   // [2] Phase-A and [2] count/write-back block counters, by chunk parity
   __device__ __forceinline__ uint8_t* in(int b) const { return in0 + (size_t)b * cb; }
   __device__ __forceinline__ uint32_t* XY(int b) const { return XY0 + (size_t)b * 64; }
-  __device__ __forceinline__ int64_t* ntl(int b) const { return ntl0 + (size_t)b * ntn; }
+  __device__ __forceinline__ uint32_t* ntl(int b) const { return ntl0 + (size_t)b * ntn; }
   __device__ __forceinline__ uint32_t* R(int b) const { return R0 + (size_t)b * rn; }
 };
 
@@ -148,16 +147,14 @@ __host__ __device__ inline size_t tile_layout(const TileParams& p, uint8_t* base
   off += 2 * cb;
   if (s) s->Z = (uint32_t*)(base + off);
   off += align16((size_t)(p.K + p.E + 1) * 4);
-  if (s) s->nbr = (uint16_t*)(base + off);
-  off += align16((size_t)p.K * 16);
   if (s) s->XY0 = (uint32_t*)(base + off);
   off += 2 * 64 * 4;
   const size_t ntn = (size_t)(p.ndirs ? p.ndirs : 1) * kChunkTiles;
   if (s) {
-    s->ntl0 = (int64_t*)(base + off);
+    s->ntl0 = (uint32_t*)(base + off);
     s->ntn = (uint32_t)ntn;
   }
-  off += 2 * ntn * 8;
+  off += 2 * ntn * 4;
   const size_t rn = (size_t)(prefetch_links(p) ? prefetch_links(p) : 1) * kChunkTiles;
   if (s) {
     s->R0 = (uint32_t*)(base + off);
@@ -220,7 +217,7 @@ __device__ __forceinline__ void chunk_neighbours(const TileParams& p, const Tile
       const uint64_t nt = nu_level(p.coarse, (int64_t)X + dx, (int64_t)Y + dy);
       tn = nt == kNoneU64 ? -1 : (int64_t)nt;
     }
-    S.ntl(b)[d * kChunkTiles + lane] = tn;
+    S.ntl(b)[d * kChunkTiles + lane] = (uint32_t)(tn + 1);  // tiles < 2^32 - 1 (checked on the host)
     if (tn >= 0 && ((uint64_t)tn < c.t0 || (uint64_t)tn >= t_end)) {
       const uint32_t e1 = min((uint32_t)p.dir_start[d + 1], Epf);
       for (uint32_t e = p.dir_start[d]; e < e1; ++e) {
@@ -290,11 +287,6 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
   const int lw = nwarps - 1;  // the last warp (fewest j-blocks) issues TMA and the coarse λ
   const uint32_t St = slot_bytes(K);
 
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(p.nbr);
-    uint4* dst = reinterpret_cast<uint4*>(S.nbr);
-    for (uint32_t i = tid; i < K; i += blockDim.x) dst[i] = src[i];
-  }
   if (tid == 0) {
     S.Z[p.zslot] = 0;
     S.ctr[0] = S.ctr[1] = S.ctr[2] = S.ctr[3] = 0;
@@ -356,7 +348,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     if (warp < (int)p.ndirs) {
       cp_async_wait_prev();  // this chunk's gathers (issued last iteration) have landed
       for (int d = warp; d < (int)p.ndirs; d += nwarps) {
-        const int64_t tn = S.ntl(buf)[d * kChunkTiles + lane];
+        const int64_t tn = (int64_t)S.ntl(buf)[d * kChunkTiles + lane] - 1;
         const uint64_t rel = (uint64_t)(tn - (int64_t)c.t0);
         const bool inside = tn >= 0 && rel < c.nt;
         const uint32_t e1 = p.dir_start[d + 1];
@@ -386,7 +378,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
       const uint32_t j = j0 + my_jj;
       uint32_t nw = 0;
       if (j < K) {
-        const uint4 row = reinterpret_cast<const uint4*>(S.nbr)[j];
+        const uint4 row = __ldg(reinterpret_cast<const uint4*>(p.nbr) + j);  // shared table, L1-resident
         uint32_t x[8];
         x[0] = S.Z[row.x & 0xFFFFu];
         x[1] = S.Z[row.x >> 16];
@@ -449,8 +441,8 @@ using TileFn = void (*)(TileParams, const uint8_t*, uint8_t*);
 static TileFn pick(const TileParams& p, int threads) {
   const bool conway = (p.birth == (1u << 3)) && (p.survive == ((1u << 2) | (1u << 3)));
   if (threads <= 256) {
-    if (p.dmax <= 5) return conway ? k_step_tile<5, true, 256, 3> : k_step_tile<5, false, 256, 3>;
-    return conway ? k_step_tile<8, true, 256, 3> : k_step_tile<8, false, 256, 3>;
+    if (p.dmax <= 5) return conway ? k_step_tile<5, true, 256, 4> : k_step_tile<5, false, 256, 4>;
+    return conway ? k_step_tile<8, true, 256, 4> : k_step_tile<8, false, 256, 4>;
   }
   if (p.dmax <= 5) return conway ? k_step_tile<5, true, 1024, 1> : k_step_tile<5, false, 1024, 1>;
   return conway ? k_step_tile<8, true, 1024, 1> : k_step_tile<8, false, 1024, 1>;
