@@ -149,6 +149,7 @@ squeeze_status check_state(const Ctx* c, const void* p) {
 
 squeeze_status do_step(Ctx* c, const uint8_t* cur, uint8_t* next, cudaStream_t st) {
   if (c->nranks > 1 && !c->needs.empty() && c->d_recv == nullptr) return SQZ_E_CONFIG;
+  if (c->NT >= 0xFFFFFFFFull) return SQZ_E_OVERFLOW;  // the tile kernel keeps tile indices in 32 bits
   TileParams p{};
   p.coarse = c->d_coarse.view;
   p.K = c->tt.K;
@@ -256,7 +257,6 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
     build_level_maps(c->f, r, c->full);
     build_level_maps(c->f, r - g, c->coarse);
     checked_pow(c->f.k, r - g, ~0ull, c->NT);
-    if (c->NT >= 0xFFFFFFFFull) return fail(SQZ_E_OVERFLOW);  // tile indices are 32-bit in the tile kernel
     c->sr = shard_range(c->NT, c->tt.K, c->rank, c->nranks);
     c->Kp = (uint32_t)((c->tt.K + 15) & ~15ull);
     c->state_bytes = (c->sr.tile_hi - c->sr.tile_lo) * c->Kp;
@@ -271,7 +271,11 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       squeeze_status st;
       if ((st = upload_maps(c->full, c->d_full)) != SQZ_OK) return fail(st);
       if ((st = upload_maps(c->coarse, c->d_coarse)) != SQZ_OK) return fail(st);
-      if ((st = upload(&c->d_nbr, c->tt.nbr.data(), c->tt.nbr.size())) != SQZ_OK) return fail(st);
+      // the tile kernel reads neighbour slots as byte offsets into its Z word array
+      if ((uint64_t)c->tt.zero_slot * 4 > 0xFFFFu) return fail(SQZ_E_INVALID_LEVEL);
+      std::vector<uint16_t> nbr_bytes(c->tt.nbr.size());
+      for (size_t i = 0; i < nbr_bytes.size(); ++i) nbr_bytes[i] = (uint16_t)(c->tt.nbr[i] * 4u);
+      if ((st = upload(&c->d_nbr, nbr_bytes.data(), nbr_bytes.size())) != SQZ_OK) return fail(st);
       if ((st = upload(&c->d_link_j2, c->tt.link_j2.data(), c->tt.link_j2.size())) != SQZ_OK) return fail(st);
       if ((st = upload(&c->d_link_dir, c->tt.link_dir.data(), c->tt.link_dir.size())) != SQZ_OK) return fail(st);
       if ((st = upload(&c->d_dir_start, c->tt.dir_start.data(), c->tt.dir_start.size())) != SQZ_OK) return fail(st);

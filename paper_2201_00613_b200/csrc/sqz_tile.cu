@@ -261,7 +261,7 @@ __device__ __forceinline__ void chunk_store(const TileParams& p, const ChunkInfo
 // Dynamic j-block distribution: warps that carry extra work (coarse maps, TMA) take fewer blocks.
 __device__ __forceinline__ uint32_t grab(uint32_t* ctr, int lane) {
   uint32_t v = 0;
-  if (lane == 0) v = atomicAdd(ctr, 1u);
+  if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(v) : "r"(smem_u32(ctr)) : "memory");
   return __shfl_sync(0xFFFFFFFFu, v, 0);
 }
 
@@ -379,16 +379,17 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
       uint32_t nw = 0;
       if (j < K) {
         const uint4 row = __ldg(reinterpret_cast<const uint4*>(p.nbr) + j);  // shared table, L1-resident
+        const uint8_t* zb = reinterpret_cast<const uint8_t*>(S.Z);  // slots hold byte offsets into Z
         uint32_t x[8];
-        x[0] = S.Z[row.x & 0xFFFFu];
-        x[1] = S.Z[row.x >> 16];
-        x[2] = S.Z[row.y & 0xFFFFu];
-        x[3] = S.Z[row.y >> 16];
-        x[4] = S.Z[row.z & 0xFFFFu];
+        x[0] = *reinterpret_cast<const uint32_t*>(zb + (row.x & 0xFFFFu));
+        x[1] = *reinterpret_cast<const uint32_t*>(zb + (row.x >> 16));
+        x[2] = *reinterpret_cast<const uint32_t*>(zb + (row.y & 0xFFFFu));
+        x[3] = *reinterpret_cast<const uint32_t*>(zb + (row.y >> 16));
+        x[4] = *reinterpret_cast<const uint32_t*>(zb + (row.z & 0xFFFFu));
         if (DMAX > 5) {
-          x[5] = S.Z[row.z >> 16];
-          x[6] = S.Z[row.w & 0xFFFFu];
-          x[7] = S.Z[row.w >> 16];
+          x[5] = *reinterpret_cast<const uint32_t*>(zb + (row.z >> 16));
+          x[6] = *reinterpret_cast<const uint32_t*>(zb + (row.w & 0xFFFFu));
+          x[7] = *reinterpret_cast<const uint32_t*>(zb + (row.w >> 16));
         }
         uint32_t c0, c1, c2, c3;
         if (DMAX <= 5) {
