@@ -154,7 +154,7 @@ squeeze_status do_step(Ctx* c, const uint8_t* cur, uint8_t* next, cudaStream_t s
   p.coarse = c->d_coarse.view;
   p.K = c->tt.K;
   p.Kp = c->Kp;
-  p.St = (uint32_t)(((c->tt.K + 31) / 32) * 32 + 16);
+  p.St = c->Kp;
   p.E = c->tt.E;
   p.zslot = c->tt.zero_slot;
   p.dmax = c->tt.max_degree;
@@ -258,7 +258,9 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
     build_level_maps(c->f, r - g, c->coarse);
     checked_pow(c->f.k, r - g, ~0ull, c->NT);
     c->sr = shard_range(c->NT, c->tt.K, c->rank, c->nranks);
-    c->Kp = (uint32_t)((c->tt.K + 15) & ~15ull);
+    // tile-padded layout: Kp >= round_up(K, 32); Kp/16 not a multiple of 4 (bank conflicts <= 2-way)
+    c->Kp = (uint32_t)((c->tt.K + 31) & ~31ull);
+    if ((c->Kp / 16) % 4 == 0) c->Kp += 16;
     c->state_bytes = (c->sr.tile_hi - c->sr.tile_lo) * c->Kp;
     if (c->nranks > 1) {
       unsigned th = std::max(1u, std::thread::hardware_concurrency());

@@ -106,10 +106,10 @@ __device__ __forceinline__ uint32_t rule_bits(uint32_t mask, uint32_t c0, uint32
 __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
-// 32 tile slots of St bytes each (St = round_up(K, 32) + 16: an odd multiple of 16, so the
-// 16-byte accesses of 8 consecutive lanes hit distinct bank groups)
-__host__ __device__ inline uint32_t slot_bytes(uint64_t K) { return (uint32_t)(((K + 31) / 32) * 32 + 16); }
-__host__ __device__ inline size_t chunk_buf_bytes(uint64_t K) { return (size_t)slot_bytes(K) * kChunkTiles; }
+// A chunk is 32 consecutive tiles of Kp bytes, contiguous in HBM and in shared memory (one
+// bulk copy each way).  Kp >= round_up(K, 32) (whole 32-byte lane windows) and Kp/16 is not a
+// multiple of 4, so 128-bit lane accesses are at worst 2-way bank-conflicted.
+__host__ __device__ inline size_t chunk_buf_bytes(const TileParams& p) { return (size_t)p.Kp * kChunkTiles; }
 
 // Boundary links whose neighbour tile is outside the chunk are prefetched one chunk ahead
 // with 4-byte cp.async gathers into R; at most kMaxPrefetchLinks (larger E falls back to a
@@ -139,7 +139,7 @@ __host__ __device__ inline uint32_t prefetch_links(const TileParams& p) {
 
 __host__ __device__ inline size_t tile_layout(const TileParams& p, uint8_t* base, TileSmem* s) {
   size_t off = 0;
-  const size_t cb = chunk_buf_bytes(p.K);
+  const size_t cb = chunk_buf_bytes(p);
   if (s) {
     s->in0 = base;
     s->cb = (uint32_t)cb;
@@ -235,27 +235,15 @@ __device__ __forceinline__ void chunk_neighbours(const TileParams& p, const Tile
   cp_async_commit();
 }
 
-// Lanes of one warp: tile i of the chunk -> slot i (one bulk copy per tile, Kp bytes each).
+// One thread: the chunk's 32 tiles (nt * Kp contiguous bytes) -> shared memory, one bulk copy.
 __device__ __forceinline__ void chunk_load(const TileParams& p, const ChunkInfo& c, uint8_t* buf, uint64_t* bar,
-                                           const uint8_t* __restrict__ cur, int lane, uint32_t St) {
-  if (lane == 0) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(c.nt * p.Kp)
-                 : "memory");
-  }
-  __syncwarp();
-  if ((uint32_t)lane < c.nt) {
-    const uint8_t* src = cur + (c.t0 + lane - p.tile_lo) * p.Kp;
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(buf + (size_t)lane * St)),
-        "l"(src), "r"(p.Kp), "r"(smem_u32(bar))
-        : "memory");
-  }
+                                           const uint8_t* __restrict__ cur) {
+  tma_load_1d(buf, cur + (c.t0 - p.tile_lo) * p.Kp, c.nt * p.Kp, bar);
 }
 
 __device__ __forceinline__ void chunk_store(const TileParams& p, const ChunkInfo& c, const uint8_t* buf,
-                                            uint8_t* __restrict__ next, int lane, uint32_t St) {
-  if ((uint32_t)lane < c.nt) tma_store_1d(next + (c.t0 + lane - p.tile_lo) * p.Kp, buf + (size_t)lane * St, p.Kp);
+                                            uint8_t* __restrict__ next) {
+  tma_store_1d(next + (c.t0 - p.tile_lo) * p.Kp, buf, c.nt * p.Kp);
 }
 
 // Dynamic j-block distribution: warps that carry extra work (coarse maps, TMA) take fewer blocks.
@@ -284,8 +272,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
   }
   const uint32_t my_jj = 4 * (lane & 7) + (lane >> 3);  // cell offset this lane holds after a transpose
   const Transposer tr(lane);
-  const int lw = nwarps - 1;  // the last warp (fewest j-blocks) issues TMA and the coarse λ
-  const uint32_t St = slot_bytes(K);
+  const int lw = nwarps - 1;  // the last warp issues TMA and the coarse λ
+  const uint32_t St = p.Kp;   // tile stride in shared memory
+  const bool issuer = warp == lw && lane == 0;
 
   if (tid == 0) {
     S.Z[p.zslot] = 0;
@@ -301,8 +290,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
   const uint64_t G = gridDim.x;
   {  // prologue: chunk 0 loaded, λ of chunks 0 and 1, neighbours + prefetch of chunk 0
     const ChunkInfo c0 = chunk_info(p, chunk);
+    if (issuer) chunk_load(p, c0, S.in(0), &S.bar[0], cur);
     if (warp == lw) {
-      chunk_load(p, c0, S.in(0), &S.bar[0], cur, lane, St);
       chunk_lambda(p, c0, S.XY(0), lane);
       if (chunk + G < p.nchunks) chunk_lambda(p, chunk_info(p, chunk + G), S.XY(1), lane);
     }
@@ -317,10 +306,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     const bool has_next = chunk + G < p.nchunks;
     if (has_next) {
       const ChunkInfo cn = chunk_info(p, chunk + G);
-      if (warp == lw) {
-        bulk_wait_read_all();  // in(buf^1) held the previous chunk's output (each lane stored one tile)
+      if (issuer) {
+        bulk_wait_read_all();  // in(buf^1) held the previous chunk's output
         fence_proxy_async();
-        chunk_load(p, cn, S.in(buf ^ 1), &S.bar[buf ^ 1], cur, lane, St);
+        chunk_load(p, cn, S.in(buf ^ 1), &S.bar[buf ^ 1], cur);
       }
       chunk_neighbours(p, S, cn, buf ^ 1, cur, warp, nwarps, lane);  // reads XY(buf^1), written last iteration
     } else {
@@ -429,10 +418,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     fence_proxy_async();
     __syncthreads();
     if (tid == 0) S.ctr[2 + (buf ^ 1)] = 0;  // next chunk's count/write-back counter
-    if (warp == lw) chunk_store(p, c, inb, next, lane, St);
+    if (issuer) chunk_store(p, c, inb, next);
   }
   cp_async_wait_all();
-  if (warp == lw) bulk_wait_all();
+  if (issuer) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------------------
