@@ -287,6 +287,8 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       // tile kernel launch shape: persistent CTAs, threads ~ one per tile cell
       TileParams p{};
       p.K = c->tt.K;
+      p.Kp = c->Kp;
+      p.St = c->Kp;
       p.E = c->tt.E;
       p.ndirs = c->tt.ndirs;
       p.dmax = c->tt.max_degree;
