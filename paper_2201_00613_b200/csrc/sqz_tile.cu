@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
 
     // Phase A: lane = tile; 32 aligned bytes (cells j0..j0+31 of its slot) -> bits 8p+m =
     // cell 4m+p -> transpose, leaving lane L with the bit-sliced word of cell j0 + my_jj(L)
-    for (uint32_t jb = grab(&S.ctr[buf], lane); jb < nblk; jb = grab(&S.ctr[buf], lane)) {
+    for (uint32_t jb = warp; jb < nblk; jb = nwarps + grab(&S.ctr[buf], lane)) {  // first block static
       const uint32_t j0 = jb * 32;
       const uint4* src = reinterpret_cast<const uint4*>(inb + (size_t)lane * St + j0);
       const uint4 lo = src[0], hi = src[1];
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     // Phases C + D per j-block: lane L computes cell j0 + my_jj(L) of all 32 tiles (carry-save
     // count, rule), then the block is transposed back (lane = tile) and written in place
     const uint32_t live_lanes = c.nt >= 32 ? 0xFFFFFFFFu : ((1u << c.nt) - 1u);
-    for (uint32_t jb = grab(&S.ctr[2 + buf], lane); jb < nblk; jb = grab(&S.ctr[2 + buf], lane)) {
+    for (uint32_t jb = warp; jb < nblk; jb = nwarps + grab(&S.ctr[2 + buf], lane)) {
       const uint32_t j0 = jb * 32;
       const uint32_t j = j0 + my_jj;
       uint32_t nw = 0;
