@@ -119,18 +119,16 @@ constexpr uint32_t kMaxPrefetchLinks = 32;
 struct TileSmem {
   uint8_t* in0;    // 2 chunk buffers (input, then output in place)
   uint32_t cb;
-  uint32_t* Z;     // K state words | E link words | zero word
+  uint32_t* Z0;    // 2 x [K state words | E link words | zero word] (by chunk parity)
+  uint32_t zn;
   uint32_t* XY0;   // 2 x [32] coarse (X, Y) of a chunk's tiles (by chunk parity)
-  uint32_t* ntl0;  // 2 x [ndirs][32] neighbour tile + 1 of each lane's tile (0 = none)
-  uint32_t ntn;
-  uint32_t* R0;    // 2 x [E][32] prefetched words holding out-of-chunk neighbour bytes
-  uint32_t rn;
-  uint64_t* bar;   // 2 mbarriers (TMA loads)
+  uint32_t* ntl;   // [ndirs][32] neighbour tile + 1 of each lane's tile (0 = none) — next chunk
+  uint32_t* R;     // [E][32] prefetched words holding out-of-chunk neighbour bytes — next chunk
+  uint64_t* bar;   // [0,2) TMA loads landed, [2,4) all warps wrote the chunk's output
   uint32_t* ctr;   // [2] Phase-A and [2] count/write-back block counters, by chunk parity
   __device__ __forceinline__ uint8_t* in(int b) const { return in0 + (size_t)b * cb; }
   __device__ __forceinline__ uint32_t* XY(int b) const { return XY0 + (size_t)b * 64; }
-  __device__ __forceinline__ uint32_t* ntl(int b) const { return ntl0 + (size_t)b * ntn; }
-  __device__ __forceinline__ uint32_t* R(int b) const { return R0 + (size_t)b * rn; }
+  __device__ __forceinline__ uint32_t* Z(int b) const { return Z0 + (size_t)b * zn; }
 };
 
 __host__ __device__ inline uint32_t prefetch_links(const TileParams& p) {
@@ -145,24 +143,20 @@ __host__ __device__ inline size_t tile_layout(const TileParams& p, uint8_t* base
     s->cb = (uint32_t)cb;
   }
   off += 2 * cb;
-  if (s) s->Z = (uint32_t*)(base + off);
-  off += align16((size_t)(p.K + p.E + 1) * 4);
+  const size_t zn = align16((size_t)(p.K + p.E + 1) * 4) / 4;
+  if (s) {
+    s->Z0 = (uint32_t*)(base + off);
+    s->zn = (uint32_t)zn;
+  }
+  off += 2 * zn * 4;
   if (s) s->XY0 = (uint32_t*)(base + off);
   off += 2 * 64 * 4;
-  const size_t ntn = (size_t)(p.ndirs ? p.ndirs : 1) * kChunkTiles;
-  if (s) {
-    s->ntl0 = (uint32_t*)(base + off);
-    s->ntn = (uint32_t)ntn;
-  }
-  off += 2 * ntn * 4;
-  const size_t rn = (size_t)(prefetch_links(p) ? prefetch_links(p) : 1) * kChunkTiles;
-  if (s) {
-    s->R0 = (uint32_t*)(base + off);
-    s->rn = (uint32_t)rn;
-  }
-  off += 2 * rn * 4;
+  if (s) s->ntl = (uint32_t*)(base + off);
+  off += (size_t)(p.ndirs ? p.ndirs : 1) * kChunkTiles * 4;
+  if (s) s->R = (uint32_t*)(base + off);
+  off += (size_t)(prefetch_links(p) ? prefetch_links(p) : 1) * kChunkTiles * 4;
   if (s) s->bar = (uint64_t*)(base + off);
-  off += 16;
+  off += 32;
   if (s) s->ctr = (uint32_t*)(base + off);
   off += 16;
   return align16(off);
@@ -174,7 +168,9 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 struct ChunkInfo {
@@ -217,11 +213,11 @@ __device__ __forceinline__ void chunk_neighbours(const TileParams& p, const Tile
       const uint64_t nt = nu_level(p.coarse, (int64_t)X + dx, (int64_t)Y + dy);
       tn = nt == kNoneU64 ? -1 : (int64_t)nt;
     }
-    S.ntl(b)[d * kChunkTiles + lane] = (uint32_t)(tn + 1);  // tiles < 2^32 - 1 (checked on the host)
+    S.ntl[d * kChunkTiles + lane] = (uint32_t)(tn + 1);  // tiles < 2^32 - 1 (checked on the host)
     if (tn >= 0 && ((uint64_t)tn < c.t0 || (uint64_t)tn >= t_end)) {
       const uint32_t e1 = min((uint32_t)p.dir_start[d + 1], Epf);
       for (uint32_t e = p.dir_start[d]; e < e1; ++e) {
-        uint32_t* dst = &S.R(b)[e * kChunkTiles + lane];
+        uint32_t* dst = &S.R[e * kChunkTiles + lane];
         const uint32_t j2 = p.link_j2[e];
         if ((uint64_t)tn >= p.tile_lo && (uint64_t)tn < p.tile_hi) {
           const uint64_t off = ((uint64_t)tn - p.tile_lo) * p.Kp + j2;  // tile-padded layout
@@ -277,10 +273,13 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
   const bool issuer = warp == lw && lane == 0;
 
   if (tid == 0) {
-    S.Z[p.zslot] = 0;
+    S.Z(0)[p.zslot] = 0;
+    S.Z(1)[p.zslot] = 0;
     S.ctr[0] = S.ctr[1] = S.ctr[2] = S.ctr[3] = 0;
     mbar_init(&S.bar[0], 1);
     mbar_init(&S.bar[1], 1);
+    mbar_init(&S.bar[2], (uint32_t)nwarps);
+    mbar_init(&S.bar[3], (uint32_t)nwarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -311,12 +310,11 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
         fence_proxy_async();
         chunk_load(p, cn, S.in(buf ^ 1), &S.bar[buf ^ 1], cur);
       }
-      chunk_neighbours(p, S, cn, buf ^ 1, cur, warp, nwarps, lane);  // reads XY(buf^1), written last iteration
-    } else {
-      cp_async_commit();  // one group per iteration keeps wait_group 1 exact
     }
+    if (tid == 0) S.ctr[buf ^ 1] = 0;  // next chunk's Phase-A counter (idle since the last barrier)
     mbar_wait(&S.bar[buf], (it >> 1) & 1);
     uint8_t* inb = S.in(buf);
+    uint32_t* Zb = S.Z(buf);
     const bool active = (uint32_t)lane < c.nt;
 
     // Phase A: lane = tile; 32 aligned bytes (cells j0..j0+31 of its slot) -> bits 8p+m =
@@ -331,13 +329,14 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
       if (jb == nblk - 1) acc &= tail_mask;
       if (!active) acc = 0;
       const uint32_t x = tr(acc);
-      if (j0 + my_jj < K) S.Z[j0 + my_jj] = x;
+      if (j0 + my_jj < K) Zb[j0 + my_jj] = x;
     }
-    // Phase B: boundary-link words; warp w owns the links of directions w, w + nwarps, ...
+    // Phase B: boundary-link words; warp w owns the links of directions w, w + nwarps, ... (the
+    // same warp computed their neighbour tiles and issued their gathers last iteration)
     if (warp < (int)p.ndirs) {
-      cp_async_wait_prev();  // this chunk's gathers (issued last iteration) have landed
+      cp_async_wait_all();
       for (int d = warp; d < (int)p.ndirs; d += nwarps) {
-        const int64_t tn = (int64_t)S.ntl(buf)[d * kChunkTiles + lane] - 1;
+        const int64_t tn = (int64_t)S.ntl[d * kChunkTiles + lane] - 1;
         const uint64_t rel = (uint64_t)(tn - (int64_t)c.t0);
         const bool inside = tn >= 0 && rel < c.nt;
         const uint32_t e1 = p.dir_start[d + 1];
@@ -346,18 +345,20 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
           uint32_t v = 0;
           if (inside) v = inb[(uint32_t)rel * St + j2];
           else if (tn >= 0) {
-            if (e < Epf) v = (S.R(buf)[e * kChunkTiles + lane] >> (8 * (j2 & 3u))) & 0xFFu;
+            if (e < Epf) v = (S.R[e * kChunkTiles + lane] >> (8 * (j2 & 3u))) & 0xFFu;
             else v = fetch_cell(cur, (uint64_t)tn * p.K + j2, p.halo);
           }
           const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
-          if (lane == 0) S.Z[K + e] = bal;
+          if (lane == 0) Zb[K + e] = bal;
         }
       }
     }
-    __syncthreads();
-    if (tid == 0) S.ctr[buf ^ 1] = 0;  // next chunk's Phase-A counter (its last use ended at the barrier)
-    // λ two chunks ahead (XY(buf) is free: this chunk's ν ran last iteration); overlaps the blocks below
+    __syncthreads();  // the one CTA barrier per chunk: all state and link words are in Zb
+    if (tid == 0) S.ctr[2 + (buf ^ 1)] = 0;  // idle: every warp finished the previous chunk's blocks
+    // λ two chunks ahead (XY(buf) is free: this chunk's ν ran last iteration), and the next
+    // chunk's neighbour tiles + link prefetch; both overlap the count/write-back blocks
     if (warp == lw && chunk + 2 * G < p.nchunks) chunk_lambda(p, chunk_info(p, chunk + 2 * G), S.XY(buf), lane);
+    if (has_next) chunk_neighbours(p, S, chunk_info(p, chunk + G), buf ^ 1, cur, warp, nwarps, lane);
 
     // Phases C + D per j-block: lane L computes cell j0 + my_jj(L) of all 32 tiles (carry-save
     // count, rule), then the block is transposed back (lane = tile) and written in place
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
       uint32_t nw = 0;
       if (j < K) {
         const uint4 row = __ldg(reinterpret_cast<const uint4*>(p.nbr) + j);  // shared table, L1-resident
-        const uint8_t* zb = reinterpret_cast<const uint8_t*>(S.Z);  // slots hold byte offsets into Z
+        const uint8_t* zb = reinterpret_cast<const uint8_t*>(Zb);  // slots hold byte offsets into Z
         uint32_t x[8];
         x[0] = *reinterpret_cast<const uint32_t*>(zb + (row.x & 0xFFFFu));
         x[1] = *reinterpret_cast<const uint32_t*>(zb + (row.x >> 16));
@@ -400,7 +401,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
           c2 = ke ^ kf;
           c3 = ke & kf;
         }
-        const uint32_t alive = S.Z[j];
+        const uint32_t alive = Zb[j];
         if (CONWAY) {
           nw = c1 & ~c2 & ~c3 & (c0 | alive);  // B3/S23: count 3, or count 2 and alive
         } else {
@@ -415,10 +416,14 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
       dst[1] = make_uint4((xb >> 4) & 0x01010101u, (xb >> 5) & 0x01010101u, (xb >> 6) & 0x01010101u,
                           (xb >> 7) & 0x01010101u);
     }
+    // no CTA barrier: each warp publishes its part of the output; only the storing thread waits
     fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) S.ctr[2 + (buf ^ 1)] = 0;  // next chunk's count/write-back counter
-    if (issuer) chunk_store(p, c, inb, next);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.bar[2 + buf]);
+    if (issuer) {
+      mbar_wait(&S.bar[2 + buf], (it >> 1) & 1);
+      chunk_store(p, c, inb, next);
+    }
   }
   cp_async_wait_all();
   if (issuer) bulk_wait_all();
