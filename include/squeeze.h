@@ -13,10 +13,10 @@
  *    base k is the replica id at level μ.  A state buffer holds one uint8 per
  *    cell (0 dead / 1 alive, reading D10) in Ω order, TILE-PADDED: Ω = t·K + j
  *    (K = k^g cells per level-g tile) lives at byte offset
- *    (t - t_lo)·Kp + j, Kp = tile_bytes = K rounded up to 32 (plus 16 when that is a
- *    multiple of 64), so every tile starts on a 16-byte boundary and a run of tiles
- *    moves with one TMA bulk copy.  The Kp - K padding bytes of each tile are zero
- *    (≈1% of the buffer for K = 729).
+ *    (t - t_lo)·Kp + j, Kp = tile_bytes = K rounded up to 32, plus 16 when that is an
+ *    even multiple of 16, so every tile starts on a 16-byte boundary, a run of tiles
+ *    moves with one TMA bulk copy, and 128-bit lane accesses are bank-conflict-free.
+ *    The Kp - K padding bytes of each tile are zero (3.2% of the buffer for K = 729).
  *  - (x, y) is the expanded coordinate, origin upper-left, y downward.
  *  - Level μ of x/y has weight s^{μ-1}; axis parity per reading D1.
  *
@@ -101,7 +101,7 @@ typedef struct {
   uint32_t chunk_tiles;  /* tiles per CTA work unit (32: one bit-slice lane per tile) */
   uint32_t remote_links; /* tile-boundary neighbour links per tile (table size) */
   uint32_t max_degree;   /* largest neighbour-slot count of any cell of a tile (<= 8) */
-  uint32_t tile_bytes;   /* Kp: bytes per tile in a state buffer (>= K rounded up to 32) */
+  uint32_t tile_bytes;   /* Kp: bytes per tile in a state buffer (K rounded up to 32, odd multiple of 16) */
 } squeeze_geometry_t;
 
 const char* squeeze_strerror(squeeze_status st);

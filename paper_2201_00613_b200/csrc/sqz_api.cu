@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -258,9 +259,10 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
     build_level_maps(c->f, r - g, c->coarse);
     checked_pow(c->f.k, r - g, ~0ull, c->NT);
     c->sr = shard_range(c->NT, c->tt.K, c->rank, c->nranks);
-    // tile-padded layout: Kp >= round_up(K, 32); Kp/16 not a multiple of 4 (bank conflicts <= 2-way)
+    // tile-padded layout: Kp >= round_up(K, 32) and Kp/16 odd, so the 128-bit lane accesses of
+    // the tile kernel are bank-conflict-free (measured: 15.7 vs 16.1 ms at r=22 despite +2.2% bytes)
     c->Kp = (uint32_t)((c->tt.K + 31) & ~31ull);
-    if ((c->Kp / 16) % 4 == 0) c->Kp += 16;
+    if ((c->Kp / 16) % 2 == 0) c->Kp += 16;
     c->state_bytes = (c->sr.tile_hi - c->sr.tile_lo) * c->Kp;
     if (c->nranks > 1) {
       unsigned th = std::max(1u, std::thread::hardware_concurrency());

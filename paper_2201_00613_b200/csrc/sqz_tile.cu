@@ -107,8 +107,8 @@ __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { r
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
 // A chunk is 32 consecutive tiles of Kp bytes, contiguous in HBM and in shared memory (one
-// bulk copy each way).  Kp >= round_up(K, 32) (whole 32-byte lane windows) and Kp/16 is not a
-// multiple of 4, so 128-bit lane accesses are at worst 2-way bank-conflicted.
+// bulk copy each way).  Kp >= round_up(K, 32) (whole 32-byte lane windows) and Kp/16 is odd,
+// so the 128-bit accesses of 8 consecutive lanes hit distinct bank groups.
 __host__ __device__ inline size_t chunk_buf_bytes(const TileParams& p) { return (size_t)p.Kp * kChunkTiles; }
 
 // Boundary links whose neighbour tile is outside the chunk are prefetched one chunk ahead
