@@ -196,6 +196,7 @@ int build_tile_tables(const Spec& f, uint32_t g, TileTables& t) {
   // neighbour entries: local j' (< K) or remote link K + e; remote links are shared by
   // every tile because each level-g sub-fractal is a translated copy (NBB class)
   std::vector<std::vector<uint32_t>> entries(K);
+  std::map<uint64_t, uint32_t> remote_index;
   int dir_of[9];
   for (int i = 0; i < 9; ++i) dir_of[i] = -1;
   for (uint64_t j = 0; j < K; ++j) {
@@ -217,10 +218,21 @@ int build_tile_tables(const Spec& f, uint32_t g, TileTables& t) {
           t.dir_dy[t.ndirs] = dy;
           ++t.ndirs;
         }
-        t.link_j.push_back((uint32_t)j);
-        t.link_j2.push_back((uint32_t)jj);
-        t.link_dir.push_back((uint8_t)dir_of[key]);
-        entries[j].push_back((uint32_t)(K + t.link_j.size() - 1));
+        // one remote word per distinct (direction, neighbour-tile cell): several own cells
+        // that touch the same outside cell share it
+        const uint64_t rkey = (uint64_t)dir_of[key] * K + (uint64_t)jj;
+        auto found = remote_index.find(rkey);
+        uint32_t e;
+        if (found == remote_index.end()) {
+          e = (uint32_t)t.link_j2.size();
+          remote_index.emplace(rkey, e);
+          t.link_j.push_back((uint32_t)j);
+          t.link_j2.push_back((uint32_t)jj);
+          t.link_dir.push_back((uint8_t)dir_of[key]);
+        } else {
+          e = found->second;
+        }
+        entries[j].push_back((uint32_t)(K + e));
       }
     }
   }

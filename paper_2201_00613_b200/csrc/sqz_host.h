@@ -42,13 +42,13 @@ struct TileTables {
   uint32_t g = 0;
   uint64_t K = 1;          // k^g
   uint64_t h = 1;          // s^g
-  uint32_t E = 0;          // remote links per tile
+  uint32_t E = 0;          // distinct remote (direction, neighbour cell) words per tile
   uint32_t zero_slot = 0;  // index of the always-zero word in Z (= K + E)
   uint32_t max_degree = 0;
   uint32_t ndirs = 0;
   int dir_dx[8] = {0}, dir_dy[8] = {0};
   std::vector<uint16_t> nbr;       // K*8 indices into Z = [state words 0..K) | remote words | zero]
-  std::vector<uint32_t> link_j;    // E: own local cell
+  std::vector<uint32_t> link_j;    // E: (first) own local cell touching it
   std::vector<uint32_t> link_j2;   // E: local cell inside the neighbour tile
   std::vector<uint8_t> link_dir;   // E: index into dir_dx/dir_dy (links sorted by direction)
   std::vector<uint16_t> dir_start; // ndirs + 1: links of direction d are [dir_start[d], dir_start[d+1])

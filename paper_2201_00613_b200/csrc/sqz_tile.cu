@@ -114,7 +114,7 @@ __host__ __device__ inline size_t chunk_buf_bytes(const TileParams& p) { return 
 // Boundary links whose neighbour tile is outside the chunk are prefetched one chunk ahead
 // with 4-byte cp.async gathers into R; at most kMaxPrefetchLinks (larger E falls back to a
 // synchronous gather).
-constexpr uint32_t kMaxPrefetchLinks = 32;
+constexpr uint32_t kMaxPrefetchLinks = 160;
 
 struct TileSmem {
   uint8_t* in0;    // 2 chunk buffers (input, then output in place)

@@ -130,11 +130,12 @@ def test_host_only_context_rejects_device_calls():
 
 
 def test_tile_tables_sierpinski():
-    """Sierpinski level-g tiles: 10 boundary links (5 corner junction pairs per tile side,
-    DESIGN.md §5) and at most 5 member neighbours per cell (histogram pin)."""
+    """Sierpinski level-g tiles touch their neighbour tiles only at corners: 8 distinct outside
+    cells (UL 1, U 2, L 1, D 1, R 2, DR 1) and at most 5 member neighbours per cell
+    (histogram pin)."""
     for g in range(2, 8):
         p = product("sierpinski-triangle", 10, tile_level=g)
-        assert p.geometry.remote_links == 10
+        assert p.geometry.remote_links == 8
         assert p.geometry.max_degree == 5
         assert p.geometry.tile_cells == 3 ** g
 
