@@ -97,3 +97,12 @@ class ShardedSqueeze:
             cur, nxt = (a, b) if i % 2 == 0 else (b, a)
             self.step(cur, nxt)
         return b if steps % 2 else a
+
+    def run_host(self, h_state, a, b, steps: int):
+        """End to end from host memory: this rank's tile-padded shard in ``h_state`` (CPU,
+        ideally pinned) -> device, ``steps`` sharded steps, -> back into ``h_state``."""
+        a.copy_(h_state, non_blocking=True)
+        fin = self.run(a, b, steps)
+        h_state.copy_(fin, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return h_state
