@@ -317,22 +317,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     uint32_t* Zb = S.Z(buf);
     const bool active = (uint32_t)lane < c.nt;
 
-    // Phase A: lane = tile; 32 aligned bytes (cells j0..j0+31 of its slot) -> bits 8p+m =
-    // cell 4m+p -> transpose, leaving lane L with the bit-sliced word of cell j0 + my_jj(L)
-    for (uint32_t jb = warp; jb < nblk; jb = nwarps + grab(&S.ctr[buf], lane)) {  // first block static
-      const uint32_t j0 = jb * 32;
-      const uint4* src = reinterpret_cast<const uint4*>(inb + (size_t)lane * St + j0);
-      const uint4 lo = src[0], hi = src[1];
-      uint32_t acc = (lo.x & 0x01010101u) | ((lo.y & 0x01010101u) << 1) | ((lo.z & 0x01010101u) << 2) |
-                     ((lo.w & 0x01010101u) << 3) | ((hi.x & 0x01010101u) << 4) | ((hi.y & 0x01010101u) << 5) |
-                     ((hi.z & 0x01010101u) << 6) | ((hi.w & 0x01010101u) << 7);
-      if (jb == nblk - 1) acc &= tail_mask;
-      if (!active) acc = 0;
-      const uint32_t x = tr(acc);
-      if (j0 + my_jj < K) Zb[j0 + my_jj] = x;
-    }
-    // Phase B: boundary-link words; warp w owns the links of directions w, w + nwarps, ... (the
-    // same warp computed their neighbour tiles and issued their gathers last iteration)
+    // Phase B first: boundary-link words; warp w owns the links of directions w, w + nwarps, ...
+    // (the same warp computed their neighbour tiles and issued their gathers last iteration).
+    // Phase A's blocks are grabbed dynamically afterwards, so warps with heavy link work take fewer.
     if (warp < (int)p.ndirs) {
       cp_async_wait_all();
       for (int d = warp; d < (int)p.ndirs; d += nwarps) {
@@ -352,6 +339,20 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
           if (lane == 0) Zb[K + e] = bal;
         }
       }
+    }
+    // Phase A: lane = tile; 32 aligned bytes (cells j0..j0+31 of its slot) -> bits 8p+m =
+    // cell 4m+p -> transpose, leaving lane L with the bit-sliced word of cell j0 + my_jj(L)
+    for (uint32_t jb = grab(&S.ctr[buf], lane); jb < nblk; jb = grab(&S.ctr[buf], lane)) {  // all dynamic
+      const uint32_t j0 = jb * 32;
+      const uint4* src = reinterpret_cast<const uint4*>(inb + (size_t)lane * St + j0);
+      const uint4 lo = src[0], hi = src[1];
+      uint32_t acc = (lo.x & 0x01010101u) | ((lo.y & 0x01010101u) << 1) | ((lo.z & 0x01010101u) << 2) |
+                     ((lo.w & 0x01010101u) << 3) | ((hi.x & 0x01010101u) << 4) | ((hi.y & 0x01010101u) << 5) |
+                     ((hi.z & 0x01010101u) << 6) | ((hi.w & 0x01010101u) << 7);
+      if (jb == nblk - 1) acc &= tail_mask;
+      if (!active) acc = 0;
+      const uint32_t x = tr(acc);
+      if (j0 + my_jj < K) Zb[j0 + my_jj] = x;
     }
     __syncthreads();  // the one CTA barrier per chunk: all state and link words are in Zb
     if (tid == 0) S.ctr[2 + (buf ^ 1)] = 0;  // idle: every warp finished the previous chunk's blocks
