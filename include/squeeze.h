@@ -102,6 +102,9 @@ typedef struct {
   uint32_t remote_links; /* tile-boundary neighbour links per tile (table size) */
   uint32_t max_degree;   /* largest neighbour-slot count of any cell of a tile (<= 8) */
   uint32_t tile_bytes;   /* Kp: bytes per tile in a state buffer (K rounded up to 32, odd multiple of 16) */
+  uint64_t packed_bytes; /* bytes of a PACKED state buffer (squeeze_*_packed) */
+  uint32_t chunk_words;  /* Kw: 32-bit words per chunk in the packed layout (K rounded up to 4) */
+  uint32_t reserved;
 } squeeze_geometry_t;
 
 const char* squeeze_strerror(squeeze_status st);
@@ -184,6 +187,25 @@ squeeze_status squeeze_halo_set_sends(void* ctx, const uint64_t* omegas, uint64_
 squeeze_status squeeze_halo_bind(void* ctx, uint8_t* d_send, const uint8_t* d_recv);
 /* d_send[i] = state of cell sends[i] in d_cur. */
 squeeze_status squeeze_halo_pack(const void* ctx, const uint8_t* d_cur, squeeze_stream_t stream);
+
+/* ---- bit-sliced PACKED state (1 bit per cell) ----
+ * Layout: the shard's tiles are grouped in chunks of 32 consecutive tiles; chunk c holds Kw
+ * 32-bit words (packed_bytes = chunks x Kw x 4); word j bit i = cell j of tile 32c + i of the
+ * shard (j < K; padding words and bits of tiles past the shard end are zero).  It is the form
+ * the step computes on, so a packed step moves 0.25 B per cell instead of 2 B.  Unsharded
+ * contexts only (SQZ_E_CONFIG otherwise).  Buffers: 16-byte aligned device memory. */
+squeeze_status squeeze_pack(const void* ctx, const uint8_t* d_state, uint32_t* d_packed, squeeze_stream_t stream);
+squeeze_status squeeze_unpack(const void* ctx, const uint32_t* d_packed, uint8_t* d_state, squeeze_stream_t stream);
+/* D9 initial state written directly in the packed layout (same cells as squeeze_seed). */
+squeeze_status squeeze_seed_packed(const void* ctx, uint32_t* d_packed, uint64_t seed, uint64_t q,
+                                   squeeze_stream_t stream);
+/* One synchronous step on packed buffers (d_cur, d_next must not alias). */
+squeeze_status squeeze_step_packed(void* ctx, const uint32_t* d_cur, uint32_t* d_next, squeeze_stream_t stream);
+/* `steps` packed steps ping-ponging d_a / d_b (final state in d_b if steps is odd). */
+squeeze_status squeeze_run_packed(void* ctx, uint32_t* d_a, uint32_t* d_b, uint64_t steps, squeeze_stream_t stream);
+/* *d_out (device uint64) = number of alive cells in a packed buffer. */
+squeeze_status squeeze_count_alive_packed(const void* ctx, const uint32_t* d_packed, uint64_t* d_out,
+                                          squeeze_stream_t stream);
 
 /* ---- expanded bounding-box baseline (the paper's "BB" engine) ---- */
 /* n x n uint8 grid, row-major [y][x]: 0 dead, 1 alive, 2 hole (never changes).  Unsharded only. */

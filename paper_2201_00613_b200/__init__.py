@@ -85,7 +85,7 @@ class Squeeze:
         self.ctx = ctx
         g = _lib.GeometryC()
         _lib.check(self.lib.squeeze_geometry(self.ctx, ctypes.byref(g)))
-        self.geometry = Geometry(*[getattr(g, f[0]) for f in _lib.GeometryC._fields_])
+        self.geometry = Geometry(*[getattr(g, f[0]) for f in _lib.GeometryC._fields_ if f[0] != "reserved"])
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -215,6 +215,47 @@ class Squeeze:
 
     def halo_pack(self, cur, stream=None) -> None:
         _lib.check(self.lib.squeeze_halo_pack(self.ctx, _ptr(cur), _stream(stream, cur.device)), "halo_pack")
+
+    # ------------------------------------------------------------------ packed state (NEXT-1)
+    def new_packed(self):
+        import torch
+        return torch.empty(max(16, self.geometry.packed_bytes) // 4, dtype=torch.int32, device=f"cuda:{self.device}")
+
+    def pack(self, state, packed, stream=None):
+        _lib.check(self.lib.squeeze_pack(self.ctx, _ptr(state), _ptr(packed), _stream(stream, state.device)), "pack")
+
+    def unpack(self, packed, state, stream=None):
+        _lib.check(self.lib.squeeze_unpack(self.ctx, _ptr(packed), _ptr(state), _stream(stream, state.device)),
+                   "unpack")
+
+    def seed_packed(self, packed, seed: int = 42, density: float = 0.5, stream=None):
+        _lib.check(self.lib.squeeze_seed_packed(self.ctx, _ptr(packed), seed, density_q(density),
+                                                _stream(stream, packed.device)), "seed_packed")
+
+    def step_packed(self, cur, nxt, stream=None):
+        _lib.check(self.lib.squeeze_step_packed(self.ctx, _ptr(cur), _ptr(nxt), _stream(stream, cur.device)),
+                   "step_packed")
+
+    def run_packed(self, a, b, steps: int, stream=None):
+        _lib.check(self.lib.squeeze_run_packed(self.ctx, _ptr(a), _ptr(b), steps, _stream(stream, a.device)),
+                   "run_packed")
+        return b if steps % 2 else a
+
+    def count_alive_packed(self, packed, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.zeros(1, dtype=torch.int64, device=packed.device)
+        _lib.check(self.lib.squeeze_count_alive_packed(self.ctx, _ptr(packed), _ptr(out),
+                                                       _stream(stream, packed.device)), "count_alive_packed")
+        return out
+
+    def packed_to_cells(self, packed):
+        """Ω-ordered cells of this shard from a packed buffer (host-side decode, for tests)."""
+        import numpy as np
+        g = self.geometry
+        w = packed.cpu().numpy().view(np.uint32)[:g.packed_bytes // 4].reshape(-1, g.chunk_words)[:, :g.tile_cells]
+        bits = (w[:, None, :] >> np.arange(32, dtype=np.uint32)[None, :, None]) & 1  # [chunk, tile, j]
+        return bits.reshape(-1, g.tile_cells)[:g.local_tiles].reshape(-1).astype(np.uint8)
 
     # ------------------------------------------------------------------ BB baseline
     def bb_bytes(self) -> int:

@@ -47,7 +47,8 @@ class GeometryC(ctypes.Structure):
                 ("state_bytes", ctypes.c_uint64), ("n", ctypes.c_uint64), ("compact_w", ctypes.c_uint64),
                 ("compact_h", ctypes.c_uint64), ("r", ctypes.c_uint32), ("tile_level", ctypes.c_uint32),
                 ("tile_cells", ctypes.c_uint64), ("num_tiles", ctypes.c_uint64), ("chunk_tiles", ctypes.c_uint32),
-                ("remote_links", ctypes.c_uint32), ("max_degree", ctypes.c_uint32), ("tile_bytes", ctypes.c_uint32)]
+                ("remote_links", ctypes.c_uint32), ("max_degree", ctypes.c_uint32), ("tile_bytes", ctypes.c_uint32),
+                ("packed_bytes", ctypes.c_uint64), ("chunk_words", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 vp = ctypes.c_void_p
@@ -78,6 +79,12 @@ SIGNATURES = {
     "squeeze_halo_set_sends": ([vp, u64p, ctypes.c_uint64], st),
     "squeeze_halo_bind": ([vp, vp, vp], st),
     "squeeze_halo_pack": ([vp, vp, vp], st),
+    "squeeze_pack": ([vp, vp, vp, vp], st),
+    "squeeze_unpack": ([vp, vp, vp, vp], st),
+    "squeeze_seed_packed": ([vp, vp, ctypes.c_uint64, ctypes.c_uint64, vp], st),
+    "squeeze_step_packed": ([vp, vp, vp, vp], st),
+    "squeeze_run_packed": ([vp, vp, vp, ctypes.c_uint64, vp], st),
+    "squeeze_count_alive_packed": ([vp, vp, vp, vp], st),
     "squeeze_bb_bytes": ([vp, u64p], st),
     "squeeze_bb_seed": ([vp, vp, ctypes.c_uint64, ctypes.c_uint64, vp], st),
     "squeeze_bb_step": ([vp, vp, vp, vp], st),
@@ -131,6 +138,8 @@ class Geometry:
     remote_links: int
     max_degree: int
     tile_bytes: int
+    packed_bytes: int
+    chunk_words: int
 
     @property
     def local_cells(self) -> int:

@@ -44,6 +44,11 @@ struct Ctx {
   int device = -1;
   DeviceLUTs d_full, d_coarse;
   uint16_t* d_nbr = nullptr;
+  uint16_t* d_nbr_packed = nullptr;  // neighbour slots for the packed kernel (links after Kw words)
+  uint32_t Kw = 4;                    // packed words per chunk
+  uint64_t packed_bytes = 0;
+  int packed_grid = 0;
+  size_t packed_smem = 0;
   uint32_t* d_link_j2 = nullptr;
   uint8_t* d_link_dir = nullptr;
   uint16_t* d_dir_start = nullptr;
@@ -110,6 +115,7 @@ void free_device(Ctx* c) {
   cudaFree(c->d_full.d);
   cudaFree(c->d_coarse.d);
   cudaFree(c->d_nbr);
+  cudaFree(c->d_nbr_packed);
   cudaFree(c->d_link_j2);
   cudaFree(c->d_link_dir);
   cudaFree(c->d_dir_start);
@@ -148,9 +154,7 @@ squeeze_status check_state(const Ctx* c, const void* p) {
   return SQZ_OK;
 }
 
-squeeze_status do_step(Ctx* c, const uint8_t* cur, uint8_t* next, cudaStream_t st) {
-  if (c->nranks > 1 && !c->needs.empty() && c->d_recv == nullptr) return SQZ_E_CONFIG;
-  if (c->NT >= 0xFFFFFFFFull) return SQZ_E_OVERFLOW;  // the tile kernel keeps tile indices in 32 bits
+TileParams tile_params(const Ctx* c) {
   TileParams p{};
   p.coarse = c->d_coarse.view;
   p.K = c->tt.K;
@@ -172,9 +176,26 @@ squeeze_status do_step(Ctx* c, const uint8_t* cur, uint8_t* next, cudaStream_t s
   p.nchunks = (c->sr.tile_hi - c->sr.tile_lo + kChunkTiles - 1) / kChunkTiles;
   p.birth = c->rule.birth_mask;
   p.survive = c->rule.survive_mask;
+  p.Kw = c->Kw;
   p.halo = halo_view(c);
+  return p;
+}
+
+squeeze_status do_step(Ctx* c, const uint8_t* cur, uint8_t* next, cudaStream_t st) {
+  if (c->nranks > 1 && !c->needs.empty() && c->d_recv == nullptr) return SQZ_E_CONFIG;
+  if (c->NT >= 0xFFFFFFFFull) return SQZ_E_OVERFLOW;  // the tile kernel keeps tile indices in 32 bits
+  TileParams p = tile_params(c);
   int grid = (int)std::min<uint64_t>((uint64_t)c->tile_grid, p.nchunks ? p.nchunks : 1);
   return cu(launch_step_tile(p, cur, next, grid, c->tile_threads, c->tile_smem, st));
+}
+
+squeeze_status do_step_packed(Ctx* c, const uint32_t* cur, uint32_t* next, cudaStream_t st) {
+  if (c->nranks > 1) return SQZ_E_CONFIG;
+  if (c->NT >= 0xFFFFFFFFull) return SQZ_E_OVERFLOW;
+  TileParams p = tile_params(c);
+  p.nbr = c->d_nbr_packed;
+  int grid = (int)std::min<uint64_t>((uint64_t)c->packed_grid, p.nchunks ? p.nchunks : 1);
+  return cu(launch_step_packed(p, cur, next, grid, 256, c->packed_smem, st));
 }
 
 template <class F>
@@ -264,6 +285,8 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
     c->Kp = (uint32_t)((c->tt.K + 31) & ~31ull);
     if ((c->Kp / 16) % 2 == 0) c->Kp += 16;
     c->state_bytes = (c->sr.tile_hi - c->sr.tile_lo) * c->Kp;
+    c->Kw = (uint32_t)((c->tt.K + 3) & ~3ull);
+    c->packed_bytes = ((c->sr.tile_hi - c->sr.tile_lo + kChunkTiles - 1) / kChunkTiles) * c->Kw * 4;
     if (c->nranks > 1) {
       unsigned th = std::max(1u, std::thread::hardware_concurrency());
       halo_needs(c->tt, c->coarse.view, c->sr, c->needs, th);
@@ -277,9 +300,16 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       if ((st = upload_maps(c->coarse, c->d_coarse)) != SQZ_OK) return fail(st);
       // the tile kernel reads neighbour slots as byte offsets into its Z word array
       if ((uint64_t)c->tt.zero_slot * 4 > 0xFFFFu) return fail(SQZ_E_INVALID_LEVEL);
-      std::vector<uint16_t> nbr_bytes(c->tt.nbr.size());
-      for (size_t i = 0; i < nbr_bytes.size(); ++i) nbr_bytes[i] = (uint16_t)(c->tt.nbr[i] * 4u);
+      std::vector<uint16_t> nbr_bytes(c->tt.nbr.size()), nbr_packed(c->tt.nbr.size());
+      for (size_t i = 0; i < nbr_bytes.size(); ++i) {
+        const uint32_t v = c->tt.nbr[i];
+        nbr_bytes[i] = (uint16_t)(v * 4u);
+        // packed kernel: state words fill [0, Kw), link words follow at Kw + e
+        nbr_packed[i] = (uint16_t)((v < c->tt.K ? v : v - c->tt.K + c->Kw) * 4u);
+      }
+      if ((uint64_t)(c->Kw + c->tt.E + 1) * 4 > 0xFFFFu) return fail(SQZ_E_INVALID_LEVEL);
       if ((st = upload(&c->d_nbr, nbr_bytes.data(), nbr_bytes.size())) != SQZ_OK) return fail(st);
+      if ((st = upload(&c->d_nbr_packed, nbr_packed.data(), nbr_packed.size())) != SQZ_OK) return fail(st);
       if ((st = upload(&c->d_link_j2, c->tt.link_j2.data(), c->tt.link_j2.size())) != SQZ_OK) return fail(st);
       if ((st = upload(&c->d_link_dir, c->tt.link_dir.data(), c->tt.link_dir.size())) != SQZ_OK) return fail(st);
       if ((st = upload(&c->d_dir_start, c->tt.dir_start.data(), c->tt.dir_start.size())) != SQZ_OK) return fail(st);
@@ -307,6 +337,11 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
       c->tile_grid = sms * std::max(1, occ);
+      p.Kw = c->Kw;
+      c->packed_smem = packed_smem_bytes(p);
+      int pocc = 0;
+      if (packed_prepare(p, c->packed_smem, 256, &pocc) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
+      c->packed_grid = sms * std::max(1, pocc);
     }
     *out_ctx = c;
     return SQZ_OK;
@@ -339,6 +374,8 @@ squeeze_status squeeze_geometry(const void* ctx, squeeze_geometry_t* out) {
   out->remote_links = c->tt.E;
   out->max_degree = c->tt.max_degree;
   out->tile_bytes = c->Kp;
+  out->packed_bytes = c->packed_bytes;
+  out->chunk_words = c->Kw;
   return SQZ_OK;
 }
 
@@ -556,6 +593,73 @@ squeeze_status squeeze_halo_pack(const void* ctx, const uint8_t* d_cur, squeeze_
   if (!c->sends.empty() && !c->d_send) return SQZ_E_CONFIG;
   DevGuard g(c->device);
   return cu(launch_halo_pack(d_cur, c->d_sends, c->sends.size(), c->d_send, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_pack(const void* ctx, const uint8_t* d_state, uint32_t* d_packed, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_state);
+  if (st == SQZ_OK) st = check_state(c, d_packed);
+  if (st != SQZ_OK) return st;
+  DevGuard g(c->device);
+  return cu(launch_pack(tile_params(c), d_state, d_packed, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_unpack(const void* ctx, const uint32_t* d_packed, uint8_t* d_state, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_state);
+  if (st == SQZ_OK) st = check_state(c, d_packed);
+  if (st != SQZ_OK) return st;
+  DevGuard g(c->device);
+  return cu(launch_unpack(tile_params(c), d_packed, d_state, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_seed_packed(const void* ctx, uint32_t* d_packed, uint64_t seed, uint64_t q,
+                                   squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_packed);
+  if (st != SQZ_OK) return st;
+  if (q > (1ull << 32)) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return cu(launch_seed_packed(tile_params(c), c->d_full.view, d_packed, seed, q, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_step_packed(void* ctx, const uint32_t* d_cur, uint32_t* d_next, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_cur);
+  if (st == SQZ_OK) st = check_state(c, d_next);
+  if (st != SQZ_OK) return st;
+  if ((const void*)d_cur == (const void*)d_next) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return do_step_packed(c, d_cur, d_next, (cudaStream_t)stream);
+}
+
+squeeze_status squeeze_run_packed(void* ctx, uint32_t* d_a, uint32_t* d_b, uint64_t steps, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_a);
+  if (st == SQZ_OK) st = check_state(c, d_b);
+  if (st != SQZ_OK) return st;
+  if (d_a == d_b) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  for (uint64_t i = 0; i < steps; ++i) {
+    st = (i & 1) ? do_step_packed(c, d_b, d_a, (cudaStream_t)stream) : do_step_packed(c, d_a, d_b, (cudaStream_t)stream);
+    if (st != SQZ_OK) return st;
+  }
+  return SQZ_OK;
+}
+
+squeeze_status squeeze_count_alive_packed(const void* ctx, const uint32_t* d_packed, uint64_t* d_out,
+                                          squeeze_stream_t stream) {
+  if (!ctx || !d_out) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_packed);
+  if (st != SQZ_OK) return st;
+  DevGuard g(c->device);
+  return cu(launch_count_packed(d_packed, c->packed_bytes / 4, d_out, (cudaStream_t)stream));
 }
 
 squeeze_status squeeze_bb_bytes(const void* ctx, uint64_t* bytes) {

@@ -1,0 +1,193 @@
+// sqz_bits.cuh — device building blocks shared by the byte-state and packed-state tile kernels
+// (internal): TMA/mbarrier/cp.async wrappers, the warp bit transpose, bit-sliced counting and
+// rule evaluation, chunk bookkeeping and the coarse maps of a chunk's 32 tiles.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sqz_device.cuh"
+#include "sqz_kernels.cuh"
+
+namespace sqz {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_store_1d(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 32x32 bit transpose across the warp: afterwards lane L bit i = (lane i bit L) before.
+// Stage s swaps the off-diagonal s x s blocks: each lane sends the block its partner keeps
+// (a rotate of x & sel) and keeps x & ~sel; 4 instructions per stage.
+struct Transposer {
+  uint32_t sel[5], amt[5];
+  __device__ __forceinline__ explicit Transposer(int lane) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const int s = 16 >> k;
+      const uint32_t m = (s == 16) ? 0x0000FFFFu : (s == 8) ? 0x00FF00FFu : (s == 4) ? 0x0F0F0F0Fu
+                         : (s == 2) ? 0x33333333u : 0x55555555u;
+      const bool hi = lane & s;
+      sel[k] = hi ? m : ~m;
+      amt[k] = hi ? (uint32_t)s : (uint32_t)(32 - s);
+    }
+  }
+  __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const uint32_t v = x & sel[k];
+      const uint32_t send = __funnelshift_l(v, v, amt[k]);
+      x = (x & ~sel[k]) | __shfl_xor_sync(0xFFFFFFFFu, send, 16 >> k);
+    }
+    return x;
+  }
+};
+
+// Bit-sliced rule f(c) = bit c of `mask` (c <= 8), a mux tree on the count bits.
+__device__ __forceinline__ uint32_t mask_word(uint32_t mask, int v) { return ((mask >> v) & 1u) ? 0xFFFFFFFFu : 0u; }
+
+__device__ __forceinline__ uint32_t rule_bits(uint32_t mask, uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
+  uint32_t m0 = (mask_word(mask, 0) & ~c0) | (mask_word(mask, 1) & c0);
+  uint32_t m1 = (mask_word(mask, 2) & ~c0) | (mask_word(mask, 3) & c0);
+  uint32_t m2 = (mask_word(mask, 4) & ~c0) | (mask_word(mask, 5) & c0);
+  uint32_t m3 = (mask_word(mask, 6) & ~c0) | (mask_word(mask, 7) & c0);
+  uint32_t m4 = mask_word(mask, 8) & ~c0;
+  uint32_t n0 = (m0 & ~c1) | (m1 & c1);
+  uint32_t n1 = (m2 & ~c1) | (m3 & c1);
+  uint32_t n2 = m4 & ~c1;
+  uint32_t o0 = (n0 & ~c2) | (n1 & c2);
+  uint32_t o1 = n2 & ~c2;
+  return (o0 & ~c3) | (o1 & c3);
+}
+
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
+
+__host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
+
+// Boundary links whose neighbour tile is outside the chunk are prefetched one chunk ahead
+// with 4-byte cp.async gathers into R; at most kMaxPrefetchLinks (larger E falls back to a
+// synchronous gather).
+constexpr uint32_t kMaxPrefetchLinks = 160;
+
+__host__ __device__ inline uint32_t prefetch_links(const TileParams& p) {
+  return p.E <= kMaxPrefetchLinks ? p.E : 0;
+}
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+struct ChunkInfo {
+  uint64_t chunk, t0;
+  uint32_t nt;
+};
+
+__device__ __forceinline__ ChunkInfo chunk_info(const TileParams& p, uint64_t chunk) {
+  ChunkInfo c;
+  c.chunk = chunk;
+  c.t0 = p.tile_lo + chunk * kChunkTiles;
+  c.nt = (uint32_t)min((uint64_t)kChunkTiles, p.tile_hi - c.t0);
+  return c;
+}
+
+// Coarse λ of each lane's tile (P:212-230 at tile level), one warp.
+__device__ __forceinline__ void chunk_lambda(const TileParams& p, const ChunkInfo& c, uint32_t* XY, int lane) {
+  const uint64_t t = c.t0 + lane;
+  uint32_t X = 0, Y = 0;
+  if (t < p.tile_hi) lambda_level(p.coarse, t, X, Y);
+  XY[2 * lane] = X;
+  XY[2 * lane + 1] = Y;
+}
+
+// Dynamic j-block distribution: warps that carry extra work (coarse maps, TMA) take fewer blocks.
+__device__ __forceinline__ uint32_t grab(uint32_t* ctr, int lane) {
+  uint32_t v = 0;
+  if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(v) : "r"(smem_u32(ctr)) : "memory");
+  return __shfl_sync(0xFFFFFFFFu, v, 0);
+}
+
+// Warp w, directions d = w, w + nwarps, ...: neighbour tile of each lane's tile (coarse ν,
+// P:252-278 at tile level) and, for each link of direction d whose neighbour tile is outside
+// the chunk, a 4-byte cp.async gather of the word holding the neighbour cell's byte.  The same
+// warp consumes them in Phase B of that chunk.  Always commits exactly one group.
+// PACKED = false: tile-padded byte layout (gather the word holding the byte); true: bit-sliced
+// packed layout (gather the word holding the bit).
+template <bool PACKED>
+__device__ __forceinline__ void chunk_neighbours(const TileParams& p, const uint32_t* XY, uint32_t* ntl, uint32_t* R,
+                                                 const ChunkInfo& c, const uint8_t* __restrict__ cur, int warp,
+                                                 int nwarps, int lane) {
+  const uint64_t t = c.t0 + lane;
+  const uint64_t t_end = c.t0 + c.nt;
+  const uint32_t X = XY[2 * lane], Y = XY[2 * lane + 1];
+  const uint32_t Epf = prefetch_links(p);
+  for (int d = warp; d < (int)p.ndirs; d += nwarps) {
+    int64_t tn = -1;
+    if (t < p.tile_hi) {
+      const uint32_t code = (p.dir_code >> (4 * d)) & 0xFu;
+      const int dx = (int)(code & 3u) - 1, dy = (int)(code >> 2) - 1;
+      const uint64_t nt = nu_level(p.coarse, (int64_t)X + dx, (int64_t)Y + dy);
+      tn = nt == kNoneU64 ? -1 : (int64_t)nt;
+    }
+    ntl[d * kChunkTiles + lane] = (uint32_t)(tn + 1);  // tiles < 2^32 - 1 (checked on the host)
+    if (tn >= 0 && ((uint64_t)tn < c.t0 || (uint64_t)tn >= t_end)) {
+      const uint32_t e1 = min((uint32_t)p.dir_start[d + 1], Epf);
+      for (uint32_t e = p.dir_start[d]; e < e1; ++e) {
+        uint32_t* dst = &R[e * kChunkTiles + lane];
+        const uint32_t j2 = p.link_j2[e];
+        if ((uint64_t)tn >= p.tile_lo && (uint64_t)tn < p.tile_hi) {
+          if (PACKED) {  // word j2 of the neighbour tile's chunk
+            const uint64_t w = (((uint64_t)tn - p.tile_lo) >> 5) * p.Kw + j2;
+            cp_async4(dst, cur + 4 * w);
+          } else {  // tile-padded byte layout: the aligned word holding the byte
+            const uint64_t off = ((uint64_t)tn - p.tile_lo) * p.Kp + j2;
+            cp_async4(dst, cur + (off & ~3ull));
+          }
+        } else if (PACKED) {
+          *dst = fetch_cell(cur, (uint64_t)tn * p.K + j2, p.halo) << (((uint64_t)tn - p.tile_lo) & 31);
+        } else {
+          *dst = fetch_cell(cur, (uint64_t)tn * p.K + j2, p.halo) << (8 * (j2 & 3u));  // halo: rare, synchronous
+        }
+      }
+    }
+  }
+  cp_async_commit();
+}
+
+}  // namespace sqz

@@ -32,6 +32,7 @@ struct TileParams {
   uint64_t K;        // cells per tile
   uint32_t Kp;       // bytes per tile in a state buffer (K rounded up to 16)
   uint32_t St;       // bytes per tile slot in shared memory (odd multiple of 16, >= round_up(K, 32))
+  uint32_t Kw;       // words per chunk in the packed layout (K rounded up to 4)
   uint32_t E;        // remote links per tile
   uint32_t zslot;    // index of the zero word in Z
   uint32_t dmax;     // max neighbour entries per cell
@@ -51,6 +52,16 @@ size_t tile_smem_bytes(const TileParams& p);
 // Sets the shared-memory attribute of the kernel variant `p` selects and returns its
 // occupancy (CTAs per SM) at `threads` threads.
 cudaError_t tile_prepare(const TileParams& p, size_t smem, int threads, int* occupancy);
+
+size_t packed_smem_bytes(const TileParams& p);
+cudaError_t packed_prepare(const TileParams& p, size_t smem, int threads, int* occupancy);
+cudaError_t launch_step_packed(const TileParams& p, const uint32_t* cur, uint32_t* next, int grid, int threads,
+                               size_t smem, cudaStream_t st);
+cudaError_t launch_pack(const TileParams& p, const uint8_t* st, uint32_t* packed, cudaStream_t s);
+cudaError_t launch_unpack(const TileParams& p, const uint32_t* packed, uint8_t* st, cudaStream_t s);
+cudaError_t launch_seed_packed(const TileParams& p, const LevelMaps& full, uint32_t* packed, uint64_t seed, uint64_t q,
+                               cudaStream_t s);
+cudaError_t launch_count_packed(const uint32_t* w, uint64_t nwords, uint64_t* out, cudaStream_t s);
 
 cudaError_t launch_map_lambda(const LevelMaps& m, const uint64_t* om, uint32_t* x, uint32_t* y, uint64_t count,
                               cudaStream_t st);

@@ -1,0 +1,147 @@
+"""GPU parity of the bit-sliced PACKED state path against the CPU oracle.
+
+Every expected value comes from ``oracle/`` or a closed form; the packed buffers are decoded
+on the host (``Squeeze.packed_to_cells``) and compared bit-exactly.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2201_00613_b200 as sq
+import sqz_inputs
+from oracle import automaton as A
+from oracle.fractals import BUILTINS, SIERPINSKI
+
+pytestmark = pytest.mark.gpu
+
+
+def mk(name, r, **kw):
+    return sq.Squeeze(sq.builtin_fractal(name), r, device=0, **kw)
+
+
+def oracle_run(name, r, seed, density, steps, rule=A.B3S23):
+    o = BUILTINS[name]
+    cur = A.seed_compact(o, r, seed, density)
+    out = [cur]
+    for _ in range(steps):
+        cur = A.compact_step(o, r, cur, rule)
+        out.append(cur)
+    return out
+
+
+def cells(p, packed):
+    torch.cuda.synchronize()
+    return p.packed_to_cells(packed)
+
+
+CASES = [("sierpinski-triangle", 0, 0), ("sierpinski-triangle", 1, 1), ("sierpinski-triangle", 2, 1),
+         ("sierpinski-triangle", 5, 2), ("sierpinski-triangle", 8, 0), ("sierpinski-triangle", 10, 6),
+         ("sierpinski-triangle", 11, 7), ("sierpinski-triangle", 12, 5), ("sierpinski-carpet", 4, 3),
+         ("sierpinski-carpet", 5, 2), ("vicsek", 5, 4), ("empty-bottles", 5, 3), ("full-square", 7, 3)]
+
+
+@pytest.mark.parametrize("name,r,g", CASES)
+def test_seed_pack_unpack(name, r, g):
+    p = mk(name, r, tile_level=g)
+    want = A.seed_compact(BUILTINS[name], r, 7, 0.4)
+    st = p.new_state()
+    p.seed(st, 7, 0.4)
+    pk, pk2 = p.new_packed(), p.new_packed()
+    p.pack(st, pk)
+    p.seed_packed(pk2, 7, 0.4)
+    assert np.array_equal(cells(p, pk), want)
+    assert torch.equal(pk, pk2)  # padding words and bits included
+    back = p.new_state()
+    back.fill_(0xAB)
+    p.unpack(pk, back)
+    torch.cuda.synchronize()
+    g_ = p.geometry
+    assert torch.equal(back[:g_.state_bytes], st[:g_.state_bytes])
+
+
+@pytest.mark.parametrize("name,r,g", CASES)
+def test_packed_step_vs_oracle(name, r, g):
+    p = mk(name, r, tile_level=g)
+    steps = 4
+    want = oracle_run(name, r, 7, 0.4, steps)
+    a, b = p.new_packed(), p.new_packed()
+    p.seed_packed(a, 7, 0.4)
+    for t in range(steps):
+        p.step_packed(a, b)
+        assert np.array_equal(cells(p, b), want[t + 1]), f"step {t + 1}"
+        a, b = b, a
+
+
+RULES = [(1 << 3 | 1 << 6, 1 << 2 | 1 << 3), (1 << 1, 0x1FF), (0x1FF, 0), (1 << 0 | 1 << 4, 1 << 5 | 1 << 8)]
+
+
+@pytest.mark.parametrize("rule", RULES)
+def test_packed_rules(rule):
+    r = 9
+    p = mk("sierpinski-triangle", r, rule=rule)
+    want = oracle_run("sierpinski-triangle", r, 3, 0.5, 3, rule)
+    a, b = p.new_packed(), p.new_packed()
+    p.seed_packed(a, 3, 0.5)
+    fin = p.run_packed(a, b, 3)
+    assert np.array_equal(cells(p, fin), want[3])
+
+
+def test_packed_count_and_run():
+    r = 10
+    p = mk("sierpinski-triangle", r)
+    want = oracle_run("sierpinski-triangle", r, 11, 0.5, 7)
+    a, b = p.new_packed(), p.new_packed()
+    p.seed_packed(a, 11, 0.5)
+    assert int(p.count_alive_packed(a).item()) == int(want[0].sum())
+    fin = p.run_packed(a, b, 7)
+    assert fin is b
+    assert np.array_equal(cells(p, fin), want[7])
+    assert int(p.count_alive_packed(fin).item()) == int(want[7].sum())
+
+
+def test_packed_equals_byte_path_r16():
+    """Two CUDA formulations (byte-state tile kernel, packed kernel) agree for 20 steps at r=16."""
+    p = mk("sierpinski-triangle", 16)
+    a, b = p.new_state(), p.new_state()
+    p.seed(a, 42, 0.5)
+    pa, pb = p.new_packed(), p.new_packed()
+    p.seed_packed(pa, 42, 0.5)
+    fin = p.run(a, b, 20)
+    pfin = p.run_packed(pa, pb, 20)
+    chk = p.new_packed()
+    p.pack(fin, chk)
+    torch.cuda.synchronize()
+    assert torch.equal(chk, pfin)
+
+
+def test_packed_full_size_sampled_and_histogram():
+    """r=22 (BASELINE configs[2]): one packed step vs the oracle at 2e5 sampled cells (the oracle
+    computes its own inputs); all alive + survive={c} gives the closed-form neighbour histogram."""
+    r = 22
+    p = mk("sierpinski-triangle", r)
+    g = p.geometry
+    a, b = p.new_packed(), p.new_packed()
+    p.seed_packed(a, 42, 0.5)
+    p.step_packed(a, b)
+    torch.cuda.synchronize()
+    om = np.unique(sqz_inputs.random_indices(200_000, 3 ** r, seed=99).astype(np.int64))
+    om = np.concatenate([om, [0, 1, 2, 3 ** r - 1]]).astype(np.int64)
+    t = om // g.tile_cells
+    j = om - t * g.tile_cells
+    widx = torch.from_numpy((t // 32) * g.chunk_words + j).cuda()
+    bit = torch.from_numpy(t % 32).cuda()
+
+    def bits(buf):
+        return ((buf[widx].to(torch.int64) >> bit) & 1).cpu().numpy().astype(np.uint8)
+
+    assert np.array_equal(bits(a), A.seed_at(SIERPINSKI, r, om, 42, 0.5))
+    want = A.compact_step_sampled(SIERPINSKI, r, om, lambda q: A.seed_at(SIERPINSKI, r, q, 42, 0.5))
+    assert np.array_equal(bits(b), want)
+    tt = 3 ** (r - 2)
+    hist = {2: 3, 3: 4 * tt - 2, 4: 4 * tt, 5: tt - 1}
+    p.seed_packed(a, 1, 1.0)  # density 1: every cell alive
+    assert int(p.count_alive_packed(a).item()) == 3 ** r
+    for c in (2, 3, 5, 6):
+        pc = mk("sierpinski-triangle", r, rule=(0, 1 << c))
+        pc.step_packed(a, b)
+        assert int(pc.count_alive_packed(b).item()) == hist.get(c, 0), c
