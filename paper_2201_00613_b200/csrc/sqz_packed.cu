@@ -111,7 +111,6 @@ __global__ void __launch_bounds__(256, 4) k_step_packed(TileParams p, const uint
         tma_load_1d(S.Zin(buf ^ 1), cur + (chunk + G) * Kw, cbytes, &S.bar[buf ^ 1]);
       }
     }
-    if (tid == 0) S.ctr[buf ^ 1] = 0;  // next chunk's block counter (idle since the last barrier)
     mbar_wait(&S.bar[buf], (it >> 1) & 1);
     uint32_t* Z = S.Zin(buf);
 
@@ -139,6 +138,7 @@ __global__ void __launch_bounds__(256, 4) k_step_packed(TileParams p, const uint
     }
     if (issuer) bulk_wait_read_all();  // Zout(buf) was last stored two chunks ago
     __syncthreads();  // the one CTA barrier per chunk
+    if (tid == 0) S.ctr[buf ^ 1] = 0;  // idle: every warp finished the previous chunk's blocks
     if (warp == lw && chunk + 2 * G < p.nchunks) chunk_lambda(p, chunk_info(p, chunk + 2 * G), S.XY(buf), lane);
     if (has_next)
       chunk_neighbours<true>(p, S.XY(buf ^ 1), S.ntl, S.R, chunk_info(p, chunk + G), cur8, warp, nwarps, lane);

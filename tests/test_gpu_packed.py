@@ -34,10 +34,12 @@ def cells(p, packed):
     return p.packed_to_cells(packed)
 
 
+# the last cases span several chunks per CTA (the persistent pipeline's multi-iteration path)
 CASES = [("sierpinski-triangle", 0, 0), ("sierpinski-triangle", 1, 1), ("sierpinski-triangle", 2, 1),
          ("sierpinski-triangle", 5, 2), ("sierpinski-triangle", 8, 0), ("sierpinski-triangle", 10, 6),
          ("sierpinski-triangle", 11, 7), ("sierpinski-triangle", 12, 5), ("sierpinski-carpet", 4, 3),
-         ("sierpinski-carpet", 5, 2), ("vicsek", 5, 4), ("empty-bottles", 5, 3), ("full-square", 7, 3)]
+         ("sierpinski-carpet", 5, 2), ("vicsek", 5, 4), ("empty-bottles", 5, 3), ("full-square", 7, 3),
+         ("sierpinski-triangle", 15, 3), ("sierpinski-carpet", 7, 2)]
 
 
 @pytest.mark.parametrize("name,r,g", CASES)
