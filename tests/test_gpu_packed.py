@@ -39,7 +39,7 @@ CASES = [("sierpinski-triangle", 0, 0), ("sierpinski-triangle", 1, 1), ("sierpin
          ("sierpinski-triangle", 5, 2), ("sierpinski-triangle", 8, 0), ("sierpinski-triangle", 10, 6),
          ("sierpinski-triangle", 11, 7), ("sierpinski-triangle", 12, 5), ("sierpinski-carpet", 4, 3),
          ("sierpinski-carpet", 5, 2), ("vicsek", 5, 4), ("empty-bottles", 5, 3), ("full-square", 7, 3),
-         ("sierpinski-triangle", 15, 3), ("sierpinski-carpet", 7, 2)]
+         ("sierpinski-triangle", 14, 3), ("sierpinski-carpet", 6, 2)]
 
 
 @pytest.mark.parametrize("name,r,g", CASES)
