@@ -45,6 +45,8 @@ struct Ctx {
   DeviceLUTs d_full, d_coarse;
   uint16_t* d_nbr = nullptr;
   uint16_t* d_nbr_packed = nullptr;  // neighbour slots for the packed kernel (links after Kw words)
+  uint32_t* d_adj = nullptr;         // tile adjacency [ndirs][local tiles], built once at init
+  int packed_threads = 256;
   uint32_t Kw = 4;                    // packed words per chunk
   uint64_t packed_bytes = 0;
   int packed_grid = 0;
@@ -116,6 +118,7 @@ void free_device(Ctx* c) {
   cudaFree(c->d_coarse.d);
   cudaFree(c->d_nbr);
   cudaFree(c->d_nbr_packed);
+  cudaFree(c->d_adj);
   cudaFree(c->d_link_j2);
   cudaFree(c->d_link_dir);
   cudaFree(c->d_dir_start);
@@ -178,6 +181,8 @@ TileParams tile_params(const Ctx* c) {
   p.survive = c->rule.survive_mask;
   p.Kw = c->Kw;
   p.halo = halo_view(c);
+  p.adj = c->d_adj;
+  p.adj_stride = c->sr.tile_hi - c->sr.tile_lo;
   return p;
 }
 
@@ -195,7 +200,7 @@ squeeze_status do_step_packed(Ctx* c, const uint32_t* cur, uint32_t* next, cudaS
   TileParams p = tile_params(c);
   p.nbr = c->d_nbr_packed;
   int grid = (int)std::min<uint64_t>((uint64_t)c->packed_grid, p.nchunks ? p.nchunks : 1);
-  return cu(launch_step_packed(p, cur, next, grid, 256, c->packed_smem, st));
+  return cu(launch_step_packed(p, cur, next, grid, c->packed_threads, c->packed_smem, st));
 }
 
 template <class F>
@@ -339,9 +344,20 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       c->tile_grid = sms * std::max(1, occ);
       p.Kw = c->Kw;
       c->packed_smem = packed_smem_bytes(p);
+      if (const char* e = getenv("SQZ_PACKED_THREADS")) c->packed_threads = atoi(e);  // tuning experiments
+      if (c->packed_threads < 64 || c->packed_threads > 256 || c->packed_threads % 32) return fail(SQZ_E_CONFIG);
       int pocc = 0;
-      if (packed_prepare(p, c->packed_smem, 256, &pocc) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
+      if (packed_prepare(p, c->packed_smem, c->packed_threads, &pocc) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
       c->packed_grid = sms * std::max(1, pocc);
+      // tile adjacency: the coarse λ and one coarse ν per link direction of every local tile,
+      // evaluated once here instead of every step
+      const uint64_t ntl = c->sr.tile_hi - c->sr.tile_lo;
+      if (ntl && c->tt.ndirs && c->NT < 0xFFFFFFFFull) {
+        if (cudaMalloc((void**)&c->d_adj, ntl * c->tt.ndirs * sizeof(uint32_t)) != cudaSuccess) return fail(SQZ_E_NOMEM);
+        TileParams q = tile_params(c);
+        if (launch_tile_adjacency(q, c->d_adj, nullptr) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+          return fail(SQZ_E_CUDA);
+      }
     }
     *out_ctx = c;
     return SQZ_OK;

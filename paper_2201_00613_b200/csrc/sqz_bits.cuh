@@ -127,15 +127,6 @@ __device__ __forceinline__ ChunkInfo chunk_info(const TileParams& p, uint64_t ch
   return c;
 }
 
-// Coarse λ of each lane's tile (P:212-230 at tile level), one warp.
-__device__ __forceinline__ void chunk_lambda(const TileParams& p, const ChunkInfo& c, uint32_t* XY, int lane) {
-  const uint64_t t = c.t0 + lane;
-  uint32_t X = 0, Y = 0;
-  if (t < p.tile_hi) lambda_level(p.coarse, t, X, Y);
-  XY[2 * lane] = X;
-  XY[2 * lane + 1] = Y;
-}
-
 // Dynamic j-block distribution: warps that carry extra work (coarse maps, TMA) take fewer blocks.
 __device__ __forceinline__ uint32_t grab(uint32_t* ctr, int lane) {
   uint32_t v = 0;
@@ -143,29 +134,23 @@ __device__ __forceinline__ uint32_t grab(uint32_t* ctr, int lane) {
   return __shfl_sync(0xFFFFFFFFu, v, 0);
 }
 
-// Warp w, directions d = w, w + nwarps, ...: neighbour tile of each lane's tile (coarse ν,
-// P:252-278 at tile level) and, for each link of direction d whose neighbour tile is outside
-// the chunk, a 4-byte cp.async gather of the word holding the neighbour cell's byte.  The same
-// warp consumes them in Phase B of that chunk.  Always commits exactly one group.
+// Warp w, directions d = w, w + nwarps, ...: neighbour tile of each lane's tile (from the
+// adjacency table: coarse λ then coarse ν, P:189 at tile level, evaluated once at init) and,
+// for each link of direction d whose neighbour tile is outside the chunk, a 4-byte cp.async
+// gather of the word holding the neighbour cell.  The same warp consumes them in Phase B of
+// that chunk.  Always commits exactly one group.
 // PACKED = false: tile-padded byte layout (gather the word holding the byte); true: bit-sliced
 // packed layout (gather the word holding the bit).
 template <bool PACKED>
-__device__ __forceinline__ void chunk_neighbours(const TileParams& p, const uint32_t* XY, uint32_t* ntl, uint32_t* R,
-                                                 const ChunkInfo& c, const uint8_t* __restrict__ cur, int warp,
-                                                 int nwarps, int lane) {
+__device__ __forceinline__ void chunk_neighbours(const TileParams& p, uint32_t* ntl, uint32_t* R, const ChunkInfo& c,
+                                                 const uint8_t* __restrict__ cur, int warp, int nwarps, int lane) {
   const uint64_t t = c.t0 + lane;
   const uint64_t t_end = c.t0 + c.nt;
-  const uint32_t X = XY[2 * lane], Y = XY[2 * lane + 1];
   const uint32_t Epf = prefetch_links(p);
   for (int d = warp; d < (int)p.ndirs; d += nwarps) {
-    int64_t tn = -1;
-    if (t < p.tile_hi) {
-      const uint32_t code = (p.dir_code >> (4 * d)) & 0xFu;
-      const int dx = (int)(code & 3u) - 1, dy = (int)(code >> 2) - 1;
-      const uint64_t nt = nu_level(p.coarse, (int64_t)X + dx, (int64_t)Y + dy);
-      tn = nt == kNoneU64 ? -1 : (int64_t)nt;
-    }
-    ntl[d * kChunkTiles + lane] = (uint32_t)(tn + 1);  // tiles < 2^32 - 1 (checked on the host)
+    const uint32_t a1 = (t < p.tile_hi) ? __ldg(p.adj + d * p.adj_stride + (t - p.tile_lo)) : 0u;
+    const int64_t tn = (int64_t)a1 - 1;
+    ntl[d * kChunkTiles + lane] = a1;  // tiles < 2^32 - 1 (checked on the host)
     if (tn >= 0 && ((uint64_t)tn < c.t0 || (uint64_t)tn >= t_end)) {
       const uint32_t e1 = min((uint32_t)p.dir_start[d + 1], Epf);
       for (uint32_t e = p.dir_start[d]; e < e1; ++e) {

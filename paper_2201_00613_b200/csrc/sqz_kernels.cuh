@@ -45,6 +45,10 @@ struct TileParams {
   uint64_t tile_lo, tile_hi, nchunks;
   uint32_t birth, survive;
   HaloView halo;
+  // tile adjacency, built once at init: adj[d * adj_stride + (t - tile_lo)] = neighbour tile of
+  // local tile t in link direction d, plus 1 (0 = none)
+  const uint32_t* adj;
+  uint64_t adj_stride;
 };
 
 // Shared-memory bytes the tile kernel needs for these parameters.
@@ -53,6 +57,7 @@ size_t tile_smem_bytes(const TileParams& p);
 // occupancy (CTAs per SM) at `threads` threads.
 cudaError_t tile_prepare(const TileParams& p, size_t smem, int threads, int* occupancy);
 
+cudaError_t launch_tile_adjacency(const TileParams& p, uint32_t* adj, cudaStream_t st);
 size_t packed_smem_bytes(const TileParams& p);
 cudaError_t packed_prepare(const TileParams& p, size_t smem, int threads, int* occupancy);
 cudaError_t launch_step_packed(const TileParams& p, const uint32_t* cur, uint32_t* next, int grid, int threads,

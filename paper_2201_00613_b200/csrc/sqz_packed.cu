@@ -18,14 +18,12 @@ struct PackedSmem {
   uint32_t* Zin0;   // 2 x [Kw state words (TMA target) | E link words | zero word]
   uint32_t zn;
   uint32_t* Zout0;  // 2 x [Kw next-state words] (TMA source)
-  uint32_t* XY0;    // 2 x [32] coarse (X, Y) of a chunk's tiles (by chunk parity)
   uint32_t* ntl;    // [ndirs][32] neighbour tile + 1 (next chunk)
   uint32_t* R;      // [E][32] prefetched words (next chunk)
   uint64_t* bar;    // [0,2) TMA load landed, [2,4) all warps wrote Zout
   uint32_t* ctr;    // [2] block counters by chunk parity
   __device__ __forceinline__ uint32_t* Zin(int b) const { return Zin0 + (size_t)b * zn; }
   __device__ __forceinline__ uint32_t* Zout(int b) const { return Zout0 + (size_t)b * zn; }
-  __device__ __forceinline__ uint32_t* XY(int b) const { return XY0 + (size_t)b * 64; }
 };
 
 __host__ __device__ inline size_t packed_layout(const TileParams& p, uint8_t* base, PackedSmem* s) {
@@ -38,8 +36,6 @@ __host__ __device__ inline size_t packed_layout(const TileParams& p, uint8_t* ba
   off += 2 * zn * 4;
   if (s) s->Zout0 = (uint32_t*)(base + off);
   off += 2 * zn * 4;
-  if (s) s->XY0 = (uint32_t*)(base + off);
-  off += 2 * 64 * 4;
   if (s) s->ntl = (uint32_t*)(base + off);
   off += (size_t)(p.ndirs ? p.ndirs : 1) * kChunkTiles * 4;
   if (s) s->R = (uint32_t*)(base + off);
@@ -88,12 +84,7 @@ __global__ void __launch_bounds__(256, 4) k_step_packed(TileParams p, const uint
   {  // prologue: chunk 0 loaded, λ of chunks 0 and 1, neighbours + prefetch of chunk 0
     const ChunkInfo c0 = chunk_info(p, chunk);
     if (issuer) tma_load_1d(S.Zin(0), cur + chunk * Kw, cbytes, &S.bar[0]);
-    if (warp == lw) {
-      chunk_lambda(p, c0, S.XY(0), lane);
-      if (chunk + G < p.nchunks) chunk_lambda(p, chunk_info(p, chunk + G), S.XY(1), lane);
-    }
-    __syncthreads();
-    chunk_neighbours<true>(p, S.XY(0), S.ntl, S.R, c0, cur8, warp, nwarps, lane);
+    chunk_neighbours<true>(p, S.ntl, S.R, c0, cur8, warp, nwarps, lane);
   }
 
   uint32_t it = 0;
@@ -139,9 +130,8 @@ __global__ void __launch_bounds__(256, 4) k_step_packed(TileParams p, const uint
     if (issuer) bulk_wait_read_all();  // Zout(buf) was last stored two chunks ago
     __syncthreads();  // the one CTA barrier per chunk
     if (tid == 0) S.ctr[buf ^ 1] = 0;  // idle: every warp finished the previous chunk's blocks
-    if (warp == lw && chunk + 2 * G < p.nchunks) chunk_lambda(p, chunk_info(p, chunk + 2 * G), S.XY(buf), lane);
     if (has_next)
-      chunk_neighbours<true>(p, S.XY(buf ^ 1), S.ntl, S.R, chunk_info(p, chunk + G), cur8, warp, nwarps, lane);
+      chunk_neighbours<true>(p, S.ntl, S.R, chunk_info(p, chunk + G), cur8, warp, nwarps, lane);
 
     // count + rule, one word (32 cells) per lane
     const uint32_t live_lanes = c.nt >= 32 ? 0xFFFFFFFFu : ((1u << c.nt) - 1u);

@@ -32,13 +32,11 @@ struct TileSmem {
   uint32_t cb;
   uint32_t* Z0;    // 2 x [K state words | E link words | zero word] (by chunk parity)
   uint32_t zn;
-  uint32_t* XY0;   // 2 x [32] coarse (X, Y) of a chunk's tiles (by chunk parity)
   uint32_t* ntl;   // [ndirs][32] neighbour tile + 1 of each lane's tile (0 = none) — next chunk
   uint32_t* R;     // [E][32] prefetched words holding out-of-chunk neighbour bytes — next chunk
   uint64_t* bar;   // [0,2) TMA loads landed, [2,4) all warps wrote the chunk's output
   uint32_t* ctr;   // [2] Phase-A and [2] count/write-back block counters, by chunk parity
   __device__ __forceinline__ uint8_t* in(int b) const { return in0 + (size_t)b * cb; }
-  __device__ __forceinline__ uint32_t* XY(int b) const { return XY0 + (size_t)b * 64; }
   __device__ __forceinline__ uint32_t* Z(int b) const { return Z0 + (size_t)b * zn; }
 };
 
@@ -57,8 +55,6 @@ __host__ __device__ inline size_t tile_layout(const TileParams& p, uint8_t* base
     s->zn = (uint32_t)zn;
   }
   off += 2 * zn * 4;
-  if (s) s->XY0 = (uint32_t*)(base + off);
-  off += 2 * 64 * 4;
   if (s) s->ntl = (uint32_t*)(base + off);
   off += (size_t)(p.ndirs ? p.ndirs : 1) * kChunkTiles * 4;
   if (s) s->R = (uint32_t*)(base + off);
@@ -121,15 +117,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
   uint64_t chunk = blockIdx.x;
   if (chunk >= p.nchunks) return;
   const uint64_t G = gridDim.x;
-  {  // prologue: chunk 0 loaded, λ of chunks 0 and 1, neighbours + prefetch of chunk 0
+  {  // prologue: chunk 0 loaded, neighbours + link prefetch of chunk 0
     const ChunkInfo c0 = chunk_info(p, chunk);
     if (issuer) chunk_load(p, c0, S.in(0), &S.bar[0], cur);
-    if (warp == lw) {
-      chunk_lambda(p, c0, S.XY(0), lane);
-      if (chunk + G < p.nchunks) chunk_lambda(p, chunk_info(p, chunk + G), S.XY(1), lane);
-    }
-    __syncthreads();
-    chunk_neighbours<false>(p, S.XY(0), S.ntl, S.R, c0, cur, warp, nwarps, lane);
+    chunk_neighbours<false>(p, S.ntl, S.R, c0, cur, warp, nwarps, lane);
   }
 
   uint32_t it = 0;
@@ -190,10 +181,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     }
     __syncthreads();  // the one CTA barrier per chunk: all state and link words are in Zb
     if (tid == 0) S.ctr[2 + (buf ^ 1)] = 0;  // idle: every warp finished the previous chunk's blocks
-    // λ two chunks ahead (XY(buf) is free: this chunk's ν ran last iteration), and the next
-    // chunk's neighbour tiles + link prefetch; both overlap the count/write-back blocks
-    if (warp == lw && chunk + 2 * G < p.nchunks) chunk_lambda(p, chunk_info(p, chunk + 2 * G), S.XY(buf), lane);
-    if (has_next) chunk_neighbours<false>(p, S.XY(buf ^ 1), S.ntl, S.R, chunk_info(p, chunk + G), cur, warp, nwarps, lane);
+    // the next chunk's neighbour tiles + link prefetch overlap the count/write-back blocks
+    if (has_next) chunk_neighbours<false>(p, S.ntl, S.R, chunk_info(p, chunk + G), cur, warp, nwarps, lane);
 
     // Phases C + D per j-block: lane L computes cell j0 + my_jj(L) of all 32 tiles (carry-save
     // count, rule), then the block is transposed back (lane = tile) and written in place
@@ -265,6 +254,30 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
 }
 
 // ---------------------------------------------------------------------------------------
+
+// Tile adjacency (init): one thread per local tile, coarse λ then one coarse ν per direction.
+__global__ void k_tile_adjacency(TileParams p, uint32_t* __restrict__ adj) {
+  const uint64_t n = p.tile_hi - p.tile_lo;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t X, Y;
+    lambda_level(p.coarse, p.tile_lo + i, X, Y);
+    for (uint32_t d = 0; d < p.ndirs; ++d) {
+      const uint32_t code = (p.dir_code >> (4 * d)) & 0xFu;
+      const int dx = (int)(code & 3u) - 1, dy = (int)(code >> 2) - 1;
+      const uint64_t nt = nu_level(p.coarse, (int64_t)X + dx, (int64_t)Y + dy);
+      adj[d * p.adj_stride + i] = nt == kNoneU64 ? 0u : (uint32_t)(nt + 1);
+    }
+  }
+}
+
+cudaError_t launch_tile_adjacency(const TileParams& p, uint32_t* adj, cudaStream_t st) {
+  const uint64_t n = p.tile_hi - p.tile_lo;
+  if (n == 0 || p.ndirs == 0) return cudaSuccess;
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 148ull * 32) blocks = 148ull * 32;
+  k_tile_adjacency<<<(unsigned)blocks, 256, 0, st>>>(p, adj);
+  return cudaGetLastError();
+}
 
 using TileFn = void (*)(TileParams, const uint8_t*, uint8_t*);
 

@@ -18,13 +18,20 @@ ap.add_argument("--level", type=int, default=20)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--naive", action="store_true")
 ap.add_argument("--bb", action="store_true")
+ap.add_argument("--packed", action="store_true")
 ap.add_argument("--tile-level", type=int, default=0)
 ap.add_argument("--block-threads", type=int, default=0)
 ap.add_argument("--ctas-per-sm", type=int, default=0)
 a = ap.parse_args()
 p = pkg.Squeeze(pkg.builtin_fractal(a.fractal), a.level, device=0, tile_level=a.tile_level,
                 block_threads=a.block_threads, ctas_per_sm=a.ctas_per_sm)
-if a.bb:
+if a.packed:
+    x, y = p.new_packed(), p.new_packed()
+    p.seed_packed(x, 42, 0.5)
+    for i in range(a.steps):
+        p.step_packed(x, y)
+        x, y = y, x
+elif a.bb:
     x, y = p.new_bb(), p.new_bb()
     p.bb_seed(x, 42, 0.5)
     for i in range(a.steps):
