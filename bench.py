@@ -339,6 +339,33 @@ def main():
                                   "tile_speedup": naive_ms / (ms / K)}
         del a, b
         torch.cuda.empty_cache()
+        # --- bit-sliced packed state: same step, 1 bit per cell in HBM
+        pa, pb = sq.new_packed(), sq.new_packed()
+        sq.seed_packed(pa, args.seed, args.density)
+        for i in range(args.warmup):
+            sq.step_packed(pa if i % 2 == 0 else pb, pb if i % 2 == 0 else pa)
+        torch.cuda.synchronize()
+        pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for i in range(K):
+            pev[i][0].record(stream)
+            sq.step_packed(pa if i % 2 == 0 else pb, pb if i % 2 == 0 else pa)
+            pev[i][1].record(stream)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        p_ms = s0.elapsed_time(s1)
+        p_kern = sum(e0.elapsed_time(e1) for e0, e1 in pev) / K
+        p_bytes = 2 * g.packed_bytes
+        extras["packed_state"] = {
+            "value": cells_per_s(g.cells_total, K, p_ms), "unit": "cells/s", "ms_per_step": p_ms / K,
+            "bytes_per_cell_per_step": p_bytes / g.cells_total, "state_bytes": g.packed_bytes,
+            "kernel": "sqz::k_step_packed", "avg_launch_ms": p_kern,
+            "hbm_achieved_GBps": p_bytes / (p_kern / 1e3) / 1e9, "hbm_frac": p_bytes / (p_kern / 1e3) / 1e9 / peak,
+            "note": "1 bit per cell, bit-sliced chunk layout (squeeze_*_packed); compute/latency-bound, "
+                    "bit-exact with the byte path (tests/test_gpu_packed.py)"}
+        del pa, pb
+        torch.cuda.empty_cache()
         # --- GPU expanded bounding-box baseline vs compact at r=16 (BASELINE configs[1])
         r16 = 16
         p16 = pkg.Squeeze(f, r16, device=local, **opts)

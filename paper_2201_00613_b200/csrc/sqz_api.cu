@@ -46,7 +46,7 @@ struct Ctx {
   uint16_t* d_nbr = nullptr;
   uint16_t* d_nbr_packed = nullptr;  // neighbour slots for the packed kernel (links after Kw words)
   uint32_t* d_adj = nullptr;         // tile adjacency [ndirs][local tiles], built once at init
-  int packed_threads = 256;
+  int packed_threads = 128;  // tools/packed_timing.py: 4 warps per CTA is fastest at r=22
   uint32_t Kw = 4;                    // packed words per chunk
   uint64_t packed_bytes = 0;
   int packed_grid = 0;

@@ -1,0 +1,28 @@
+"""Times the packed-state step at level r (CUDA events after warm-up)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2201_00613_b200 as pkg  # noqa: E402
+
+fr = sys.argv[1] if len(sys.argv) > 1 else "sierpinski-triangle"
+for r in [int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "22").split(",")]:
+    p = pkg.Squeeze(pkg.builtin_fractal(fr), r, device=0)
+    a, b = p.new_packed(), p.new_packed()
+    p.seed_packed(a, 42, 0.5)
+    for _ in range(3):
+        p.step_packed(a, b)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    p.run_packed(a, b, 20)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 20
+    c = p.geometry.cells_total
+    print(fr, r, os.environ.get("SQZ_PACKED_THREADS", "256"), round(ms, 3), "ms", round(c / ms / 1e9, 3), "Tcells/s",
+          round(2 * p.geometry.packed_bytes / ms / 1e6, 1), "GB/s", flush=True)
+    del a, b, p
+    torch.cuda.empty_cache()
