@@ -207,6 +207,20 @@ squeeze_status squeeze_run_packed(void* ctx, uint32_t* d_a, uint32_t* d_b, uint6
 squeeze_status squeeze_count_alive_packed(const void* ctx, const uint32_t* d_packed, uint64_t* d_out,
                                           squeeze_stream_t stream);
 
+/* ---- the paper's comparison engines ---- */
+/* λ(ω) engine ("compact grid and expanded fractal"): one thread per compact cell computes
+ * λ(Ω) and updates that cell of an EXPANDED grid in the BB layout (squeeze_bb_*; 2 = hole). */
+squeeze_status squeeze_lambda_engine_step(const void* ctx, const uint8_t* d_cur_grid, uint8_t* d_next_grid,
+                                          squeeze_stream_t stream);
+/* Block-level Squeeze with rho = s^m (m <= level, rho <= 32): k^(r-m) blocks, block b
+ * holding the rho x rho expanded micro-embedding of its level-m sub-fractal at expanded origin
+ * λ_{r-m}(b)·rho; byte (b·rho + y)·rho + x; 0 dead, 1 alive, 2 hole.  Unsharded contexts only. */
+squeeze_status squeeze_block_bytes(const void* ctx, uint32_t rho, uint64_t* bytes);
+squeeze_status squeeze_block_seed(void* ctx, uint32_t rho, uint8_t* d_blocks, uint64_t seed, uint64_t q,
+                                  squeeze_stream_t stream);
+squeeze_status squeeze_block_step(void* ctx, uint32_t rho, const uint8_t* d_cur, uint8_t* d_next,
+                                  squeeze_stream_t stream);
+
 /* ---- expanded bounding-box baseline (the paper's "BB" engine) ---- */
 /* n x n uint8 grid, row-major [y][x]: 0 dead, 1 alive, 2 hole (never changes).  Unsharded only. */
 squeeze_status squeeze_bb_bytes(const void* ctx, uint64_t* bytes);

@@ -257,6 +257,30 @@ class Squeeze:
         bits = (w[:, None, :] >> np.arange(32, dtype=np.uint32)[None, :, None]) & 1  # [chunk, tile, j]
         return bits.reshape(-1, g.tile_cells)[:g.local_tiles].reshape(-1).astype(np.uint8)
 
+    # ------------------------------------------------------------------ paper comparison engines (NEXT-2)
+    def lambda_engine_step(self, cur_grid, next_grid, stream=None):
+        """λ(ω) engine: compact thread grid over an expanded BB-layout grid."""
+        _lib.check(self.lib.squeeze_lambda_engine_step(self.ctx, _ptr(cur_grid), _ptr(next_grid),
+                                                       _stream(stream, cur_grid.device)), "lambda_engine_step")
+
+    def block_bytes(self, rho: int) -> int:
+        b = ctypes.c_uint64()
+        _lib.check(self.lib.squeeze_block_bytes(self.ctx, rho, ctypes.byref(b)), "block_bytes")
+        return b.value
+
+    def new_blocks(self, rho: int):
+        import torch
+        return torch.empty(max(16, self.block_bytes(rho)), dtype=torch.uint8, device=f"cuda:{self.device}")
+
+    def block_seed(self, rho: int, blocks, seed: int = 42, density: float = 0.5, stream=None):
+        _lib.check(self.lib.squeeze_block_seed(self.ctx, rho, _ptr(blocks), seed, density_q(density),
+                                               _stream(stream, blocks.device)), "block_seed")
+
+    def block_step(self, rho: int, cur, nxt, stream=None):
+        """Block-level Squeeze with rho x rho expanded micro-embeddings per block."""
+        _lib.check(self.lib.squeeze_block_step(self.ctx, rho, _ptr(cur), _ptr(nxt), _stream(stream, cur.device)),
+                   "block_step")
+
     # ------------------------------------------------------------------ BB baseline
     def bb_bytes(self) -> int:
         b = ctypes.c_uint64()

@@ -85,6 +85,10 @@ SIGNATURES = {
     "squeeze_step_packed": ([vp, vp, vp, vp], st),
     "squeeze_run_packed": ([vp, vp, vp, ctypes.c_uint64, vp], st),
     "squeeze_count_alive_packed": ([vp, vp, vp, vp], st),
+    "squeeze_lambda_engine_step": ([vp, vp, vp, vp], st),
+    "squeeze_block_bytes": ([vp, ctypes.c_uint32, u64p], st),
+    "squeeze_block_seed": ([vp, ctypes.c_uint32, vp, ctypes.c_uint64, ctypes.c_uint64, vp], st),
+    "squeeze_block_step": ([vp, ctypes.c_uint32, vp, vp, vp], st),
     "squeeze_bb_bytes": ([vp, u64p], st),
     "squeeze_bb_seed": ([vp, vp, ctypes.c_uint64, ctypes.c_uint64, vp], st),
     "squeeze_bb_step": ([vp, vp, vp, vp], st),

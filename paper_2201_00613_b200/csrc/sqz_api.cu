@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <new>
 #include <string>
 #include <thread>
@@ -24,6 +25,13 @@ namespace {
 struct DeviceLUTs {
   uint32_t* d = nullptr;
   LevelMaps view{};
+};
+
+// Block-level Squeeze at rho = s^m: maps at level r - m and the rho x rho micro-fractal mask.
+struct BlockLevel {
+  HostLevelMaps host;
+  DeviceLUTs dev;
+  uint8_t* d_micro = nullptr;
 };
 
 struct Ctx {
@@ -61,6 +69,7 @@ struct Ctx {
   const uint8_t* d_recv = nullptr;
   int tile_threads = 0, tile_grid = 0;
   size_t tile_smem = 0;
+  std::map<uint32_t, BlockLevel> blocks;  // by m = log_s rho
   // CUDA graph of the two-step ping-pong
   cudaGraphExec_t graph = nullptr;
   const uint8_t* graph_a = nullptr;
@@ -119,6 +128,10 @@ void free_device(Ctx* c) {
   cudaFree(c->d_nbr);
   cudaFree(c->d_nbr_packed);
   cudaFree(c->d_adj);
+  for (auto& kv : c->blocks) {
+    cudaFree(kv.second.dev.d);
+    cudaFree(kv.second.d_micro);
+  }
   cudaFree(c->d_link_j2);
   cudaFree(c->d_link_dir);
   cudaFree(c->d_dir_start);
@@ -201,6 +214,42 @@ squeeze_status do_step_packed(Ctx* c, const uint32_t* cur, uint32_t* next, cudaS
   p.nbr = c->d_nbr_packed;
   int grid = (int)std::min<uint64_t>((uint64_t)c->packed_grid, p.nchunks ? p.nchunks : 1);
   return cu(launch_step_packed(p, cur, next, grid, c->packed_threads, c->packed_smem, st));
+}
+
+// m = log_s rho, or -1 if rho is not a power of s (or exceeds the level / 32).
+int block_m(const Ctx* c, uint32_t rho) {
+  uint64_t v = 1;
+  for (int m = 0; m <= (int)c->r; ++m) {
+    if (v == rho) return (rho <= 32) ? m : -1;
+    v *= c->f.s;
+  }
+  return -1;
+}
+
+squeeze_status block_level(Ctx* c, uint32_t rho, BlockLevel** out) {
+  const int m = block_m(c, rho);
+  if (m < 0) return SQZ_E_INVALID_LEVEL;
+  auto it = c->blocks.find((uint32_t)m);
+  if (it == c->blocks.end()) {
+    BlockLevel bl;
+    build_level_maps(c->f, c->r - (uint32_t)m, bl.host);
+    HostLevelMaps micro_maps;
+    build_level_maps(c->f, (uint32_t)m, micro_maps);
+    std::vector<uint8_t> mask((size_t)rho * rho);
+    for (uint32_t y = 0; y < rho; ++y)
+      for (uint32_t x = 0; x < rho; ++x) mask[(size_t)y * rho + x] = nu_level(micro_maps.view, x, y) != kNoneU64;
+    squeeze_status st = upload_maps(bl.host, bl.dev);
+    if (st == SQZ_OK) st = upload(&bl.d_micro, mask.data(), mask.size());
+    if (st != SQZ_OK) return st;
+    bl.dev.view = bl.host.view;  // re-point the view at the device copies
+    bl.dev.view.lam_full = bl.dev.d;
+    bl.dev.view.lam_tail = bl.dev.d + bl.host.lam_full.size();
+    bl.dev.view.nu_full = bl.dev.d + bl.host.lam_full.size() + bl.host.lam_tail.size();
+    bl.dev.view.nu_tail = bl.dev.view.nu_full + bl.host.nu_full.size();
+    it = c->blocks.emplace((uint32_t)m, std::move(bl)).first;
+  }
+  *out = &it->second;
+  return SQZ_OK;
 }
 
 template <class F>
@@ -676,6 +725,62 @@ squeeze_status squeeze_count_alive_packed(const void* ctx, const uint32_t* d_pac
   if (st != SQZ_OK) return st;
   DevGuard g(c->device);
   return cu(launch_count_packed(d_packed, c->packed_bytes / 4, d_out, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_lambda_engine_step(const void* ctx, const uint8_t* d_cur_grid, uint8_t* d_next_grid,
+                                          squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_cur_grid);
+  if (st == SQZ_OK) st = check_state(c, d_next_grid);
+  if (st != SQZ_OK) return st;
+  if (c->nranks > 1 || d_cur_grid == d_next_grid || c->n > (1ull << 20)) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return cu(launch_lambda_engine(c->d_full.view, d_cur_grid, d_next_grid, c->rule.birth_mask, c->rule.survive_mask,
+                                 (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_block_bytes(const void* ctx, uint32_t rho, uint64_t* bytes) {
+  if (!ctx || !bytes) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  const int m = block_m(c, rho);
+  if (m < 0) return SQZ_E_INVALID_LEVEL;
+  uint64_t nb;
+  if (!checked_pow(c->f.k, c->r - (uint32_t)m, 1ull << 56, nb)) return SQZ_E_OVERFLOW;
+  *bytes = nb * rho * rho;
+  return SQZ_OK;
+}
+
+squeeze_status squeeze_block_seed(void* ctx, uint32_t rho, uint8_t* d_blocks, uint64_t seed, uint64_t q,
+                                  squeeze_stream_t stream) {
+  return guarded([&]() -> squeeze_status {
+    if (!ctx) return SQZ_E_CONFIG;
+    Ctx* c = static_cast<Ctx*>(ctx);
+    squeeze_status st = check_state(c, d_blocks);
+    if (st != SQZ_OK) return st;
+    if (c->nranks > 1 || q > (1ull << 32)) return SQZ_E_CONFIG;
+    DevGuard g(c->device);
+    BlockLevel* bl;
+    if ((st = block_level(c, rho, &bl)) != SQZ_OK) return st;
+    return cu(launch_block_seed(bl->dev.view, rho, bl->d_micro, d_blocks, seed, q, (cudaStream_t)stream));
+  });
+}
+
+squeeze_status squeeze_block_step(void* ctx, uint32_t rho, const uint8_t* d_cur, uint8_t* d_next,
+                                  squeeze_stream_t stream) {
+  return guarded([&]() -> squeeze_status {
+    if (!ctx) return SQZ_E_CONFIG;
+    Ctx* c = static_cast<Ctx*>(ctx);
+    squeeze_status st = check_state(c, d_cur);
+    if (st == SQZ_OK) st = check_state(c, d_next);
+    if (st != SQZ_OK) return st;
+    if (c->nranks > 1 || d_cur == d_next) return SQZ_E_CONFIG;
+    DevGuard g(c->device);
+    BlockLevel* bl;
+    if ((st = block_level(c, rho, &bl)) != SQZ_OK) return st;
+    return cu(launch_block_step(bl->dev.view, rho, bl->d_micro, c->rule.birth_mask, c->rule.survive_mask, d_cur,
+                                d_next, (cudaStream_t)stream));
+  });
 }
 
 squeeze_status squeeze_bb_bytes(const void* ctx, uint64_t* bytes) {

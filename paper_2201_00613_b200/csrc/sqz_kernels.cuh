@@ -57,6 +57,12 @@ size_t tile_smem_bytes(const TileParams& p);
 // occupancy (CTAs per SM) at `threads` threads.
 cudaError_t tile_prepare(const TileParams& p, size_t smem, int threads, int* occupancy);
 
+cudaError_t launch_lambda_engine(const LevelMaps& m, const uint8_t* cur, uint8_t* next, uint32_t birth,
+                                 uint32_t survive, cudaStream_t st);
+cudaError_t launch_block_step(const LevelMaps& coarse, uint32_t rho, const uint8_t* micro, uint32_t birth,
+                              uint32_t survive, const uint8_t* cur, uint8_t* next, cudaStream_t st);
+cudaError_t launch_block_seed(const LevelMaps& coarse, uint32_t rho, const uint8_t* micro, uint8_t* blocks,
+                              uint64_t seed, uint64_t q, cudaStream_t st);
 cudaError_t launch_tile_adjacency(const TileParams& p, uint32_t* adj, cudaStream_t st);
 size_t packed_smem_bytes(const TileParams& p);
 cudaError_t packed_prepare(const TileParams& p, size_t smem, int threads, int* occupancy);
