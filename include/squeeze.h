@@ -17,6 +17,10 @@
  *    even multiple of 16, so every tile starts on a 16-byte boundary, a run of tiles
  *    moves with one TMA bulk copy, and 128-bit lane accesses are bank-conflict-free.
  *    The Kp - K padding bytes of each tile are zero (3.2% of the buffer for K = 729).
+ *    INPUT CONTRACT of the stepping kernels: every cell byte is 0 or 1 and every padding
+ *    byte is 0 (squeeze_seed, squeeze_step, squeeze_unpack and the binding's from_cells
+ *    keep it; the kernels pack bytes with shifted adds).  A buffer breaking it yields
+ *    unspecified cell values, never an out-of-bounds access.
  *  - (x, y) is the expanded coordinate, origin upper-left, y downward.
  *  - Level μ of x/y has weight s^{μ-1}; axis parity per reading D1.
  *

@@ -49,27 +49,43 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // 32x32 bit transpose across the warp: afterwards lane L bit i = (lane i bit L) before.
-// Stage s swaps the off-diagonal s x s blocks: each lane sends the block its partner keeps
-// (a rotate of x & sel) and keeps x & ~sel; 4 instructions per stage.
+// Stage s exchanges the off-diagonal s x s bit blocks between lanes L and L^s: the lane with
+// (L & s) == 0 keeps its bits {b : (b & s) == 0} and takes the partner's same bits moved up by
+// s; the other lane keeps {b : b & s} and takes the partner's moved down by s.  Every lane
+// sends its raw word.  s = 16, 8 move whole bytes: one PRMT picks the kept and received bytes.
+// s = 4, 2, 1: rotate the received word by +-s (per-lane amount) and merge with one LOP3.
 struct Transposer {
-  uint32_t sel[5], amt[5];
+  uint32_t perm16, perm8;  // PRMT selectors
+  uint32_t keep[3], amt[3];
   __device__ __forceinline__ explicit Transposer(int lane) {
+    perm16 = (lane & 16) ? 0x3276u : 0x5410u;  // hi: [r2 r3 x2 x3]   lo: [x0 x1 r0 r1]
+    perm8 = (lane & 8) ? 0x3715u : 0x6240u;    // hi: [r1 x1 r3 x3]   lo: [x0 r0 x2 r2]
 #pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      const int s = 16 >> k;
-      const uint32_t m = (s == 16) ? 0x0000FFFFu : (s == 8) ? 0x00FF00FFu : (s == 4) ? 0x0F0F0F0Fu
-                         : (s == 2) ? 0x33333333u : 0x55555555u;
+    for (int k = 0; k < 3; ++k) {
+      const int s = 4 >> k;
+      const uint32_t m = (s == 4) ? 0x0F0F0F0Fu : (s == 2) ? 0x33333333u : 0x55555555u;
       const bool hi = lane & s;
-      sel[k] = hi ? m : ~m;
-      amt[k] = hi ? (uint32_t)s : (uint32_t)(32 - s);
+      keep[k] = hi ? ~m : m;
+      amt[k] = hi ? (uint32_t)(32 - s) : (uint32_t)s;
+    }
+    // Identity shuffles make the constants opaque, so ptxas keeps them in registers instead
+    // of re-deriving them from the lane id inside the hot loops.
+    perm16 = __shfl_sync(0xFFFFFFFFu, perm16, lane);
+    perm8 = __shfl_sync(0xFFFFFFFFu, perm8, lane);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      keep[k] = __shfl_sync(0xFFFFFFFFu, keep[k], lane);
+      amt[k] = __shfl_sync(0xFFFFFFFFu, amt[k], lane);
     }
   }
   __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+    x = __byte_perm(x, __shfl_xor_sync(0xFFFFFFFFu, x, 16), perm16);
+    x = __byte_perm(x, __shfl_xor_sync(0xFFFFFFFFu, x, 8), perm8);
 #pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      const uint32_t v = x & sel[k];
-      const uint32_t send = __funnelshift_l(v, v, amt[k]);
-      x = (x & ~sel[k]) | __shfl_xor_sync(0xFFFFFFFFu, send, 16 >> k);
+    for (int k = 0; k < 3; ++k) {
+      const uint32_t r = __shfl_xor_sync(0xFFFFFFFFu, x, 4 >> k);
+      const uint32_t rot = __funnelshift_l(r, r, amt[k]);
+      x = (x & keep[k]) | (rot & ~keep[k]);
     }
     return x;
   }
@@ -90,6 +106,37 @@ __device__ __forceinline__ uint32_t rule_bits(uint32_t mask, uint32_t c0, uint32
   uint32_t o0 = (n0 & ~c2) | (n1 & c2);
   uint32_t o1 = n2 & ~c2;
   return (o0 & ~c3) | (o1 & c3);
+}
+
+// Shared-memory accesses by 32-bit shared-window address (no generic->shared conversion per use).
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// 32 state bytes (cells c..c+31 of one tile, each 0 or 1 by the input contract) -> 32 bits,
+// bit 8p+m = cell 4m+p.  Shifted adds (LEA) never carry between bytes for 0/1 inputs.
+__device__ __forceinline__ uint32_t pack01(const uint4& lo, const uint4& hi) {
+  uint32_t a = lo.x + (lo.y << 1);
+  a += lo.z << 2;
+  a += lo.w << 3;
+  a += hi.x << 4;
+  a += hi.y << 5;
+  a += hi.z << 6;
+  a += hi.w << 7;
+  return a;
 }
 
 __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
@@ -128,11 +175,12 @@ __device__ __forceinline__ ChunkInfo chunk_info(const TileParams& p, uint64_t ch
 }
 
 // Dynamic j-block distribution: warps that carry extra work (coarse maps, TMA) take fewer blocks.
-__device__ __forceinline__ uint32_t grab(uint32_t* ctr, int lane) {
+__device__ __forceinline__ uint32_t grab(uint32_t ctr_s, int lane) {  // ctr_s: shared-window address
   uint32_t v = 0;
-  if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(v) : "r"(smem_u32(ctr)) : "memory");
+  if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(v) : "r"(ctr_s) : "memory");
   return __shfl_sync(0xFFFFFFFFu, v, 0);
 }
+__device__ __forceinline__ uint32_t grab(uint32_t* ctr, int lane) { return grab(smem_u32(ctr), lane); }
 
 // Warp w, directions d = w, w + nwarps, ...: neighbour tile of each lane's tile (from the
 // adjacency table: coarse λ then coarse ν, P:189 at tile level, evaluated once at init) and,

@@ -79,7 +79,7 @@ __device__ __forceinline__ void chunk_store(const TileParams& p, const ChunkInfo
   tma_store_1d(next + (c.t0 - p.tile_lo) * p.Kp, buf, c.nt * p.Kp);
 }
 
-template <int DMAX, bool CONWAY, int MAXT, int MINB>
+template <int DMAX, bool CONWAY, int MAXT, int MINB, int RB>
 __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const uint8_t* __restrict__ cur,
                                                          uint8_t* __restrict__ next) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -89,15 +89,14 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
   const uint32_t K = (uint32_t)p.K;
   const uint32_t nblk = (K + 31) / 32;
   const uint32_t Epf = prefetch_links(p);
-  uint32_t tail_mask = 0;  // packed bits (bit 8p+m = cell 4m+p) valid in the last j-block
-  {
-    const uint32_t nv = K - (nblk - 1) * 32;
-#pragma unroll
-    for (int b = 0; b < 32; ++b)
-      if ((uint32_t)(4 * (b & 7) + (b >> 3)) < nv) tail_mask |= 1u << b;
-  }
   const uint32_t my_jj = 4 * (lane & 7) + (lane >> 3);  // cell offset this lane holds after a transpose
   const Transposer tr(lane);
+  uint4 rows[RB];  // neighbour-table rows of this lane's static C+D blocks (L1 once per launch)
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    const uint32_t j = ((uint32_t)warp + (uint32_t)(i * nwarps)) * 32 + my_jj;
+    rows[i] = j < K ? __ldg(reinterpret_cast<const uint4*>(p.nbr) + j) : make_uint4(0, 0, 0, 0);
+  }
   const int lw = nwarps - 1;  // the last warp issues TMA and the coarse λ
   const uint32_t St = p.Kp;   // tile stride in shared memory
   const bool issuer = warp == lw && lane == 0;
@@ -167,43 +166,40 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     }
     // Phase A: lane = tile; 32 aligned bytes (cells j0..j0+31 of its slot) -> bits 8p+m =
     // cell 4m+p -> transpose, leaving lane L with the bit-sliced word of cell j0 + my_jj(L)
-    for (uint32_t jb = grab(&S.ctr[buf], lane); jb < nblk; jb = grab(&S.ctr[buf], lane)) {  // all dynamic
+    const uint32_t in_s = smem_u32(inb) + (uint32_t)lane * St;  // this lane's tile slot
+    const uint32_t z_s = smem_u32(Zb);
+    const uint32_t ctr_s = smem_u32(&S.ctr[buf]);
+    for (uint32_t jb = grab(ctr_s, lane); jb < nblk; jb = grab(ctr_s, lane)) {  // all dynamic
       const uint32_t j0 = jb * 32;
-      const uint4* src = reinterpret_cast<const uint4*>(inb + (size_t)lane * St + j0);
-      const uint4 lo = src[0], hi = src[1];
-      uint32_t acc = (lo.x & 0x01010101u) | ((lo.y & 0x01010101u) << 1) | ((lo.z & 0x01010101u) << 2) |
-                     ((lo.w & 0x01010101u) << 3) | ((hi.x & 0x01010101u) << 4) | ((hi.y & 0x01010101u) << 5) |
-                     ((hi.z & 0x01010101u) << 6) | ((hi.w & 0x01010101u) << 7);
-      if (jb == nblk - 1) acc &= tail_mask;
-      if (!active) acc = 0;
-      const uint32_t x = tr(acc);
-      if (j0 + my_jj < K) Zb[j0 + my_jj] = x;
+      // Padding bytes (j >= K) and the slots of lanes past a ragged chunk's end only reach
+      // words j >= K (not stored) and bit positions of dead tiles (masked at the output).
+      const uint32_t x = tr(pack01(lds128(in_s + j0), lds128(in_s + j0 + 16)));
+      if (j0 + my_jj < K) sts32(z_s + 4 * (j0 + my_jj), x);
     }
     __syncthreads();  // the one CTA barrier per chunk: all state and link words are in Zb
-    if (tid == 0) S.ctr[2 + (buf ^ 1)] = 0;  // idle: every warp finished the previous chunk's blocks
     // the next chunk's neighbour tiles + link prefetch overlap the count/write-back blocks
     if (has_next) chunk_neighbours<false>(p, S.ntl, S.R, chunk_info(p, chunk + G), cur, warp, nwarps, lane);
 
     // Phases C + D per j-block: lane L computes cell j0 + my_jj(L) of all 32 tiles (carry-save
-    // count, rule), then the block is transposed back (lane = tile) and written in place
+    // count, rule), then the block is transposed back (lane = tile) and written in place.
+    // Blocks are static (jb = warp + i * nwarps) so the first RB rows of the shared neighbour
+    // table stay in registers for the whole launch.
     const uint32_t live_lanes = c.nt >= 32 ? 0xFFFFFFFFu : ((1u << c.nt) - 1u);
-    for (uint32_t jb = warp; jb < nblk; jb = nwarps + grab(&S.ctr[2 + buf], lane)) {
+    auto block = [&](uint32_t jb, const uint4& row) {
       const uint32_t j0 = jb * 32;
       const uint32_t j = j0 + my_jj;
       uint32_t nw = 0;
       if (j < K) {
-        const uint4 row = __ldg(reinterpret_cast<const uint4*>(p.nbr) + j);  // shared table, L1-resident
-        const uint8_t* zb = reinterpret_cast<const uint8_t*>(Zb);  // slots hold byte offsets into Z
-        uint32_t x[8];
-        x[0] = *reinterpret_cast<const uint32_t*>(zb + (row.x & 0xFFFFu));
-        x[1] = *reinterpret_cast<const uint32_t*>(zb + (row.x >> 16));
-        x[2] = *reinterpret_cast<const uint32_t*>(zb + (row.y & 0xFFFFu));
-        x[3] = *reinterpret_cast<const uint32_t*>(zb + (row.y >> 16));
-        x[4] = *reinterpret_cast<const uint32_t*>(zb + (row.z & 0xFFFFu));
+        uint32_t x[8];  // slots hold byte offsets into Z
+        x[0] = lds32(z_s + (row.x & 0xFFFFu));
+        x[1] = lds32(z_s + (row.x >> 16));
+        x[2] = lds32(z_s + (row.y & 0xFFFFu));
+        x[3] = lds32(z_s + (row.y >> 16));
+        x[4] = lds32(z_s + (row.z & 0xFFFFu));
         if (DMAX > 5) {
-          x[5] = *reinterpret_cast<const uint32_t*>(zb + (row.z >> 16));
-          x[6] = *reinterpret_cast<const uint32_t*>(zb + (row.w & 0xFFFFu));
-          x[7] = *reinterpret_cast<const uint32_t*>(zb + (row.w >> 16));
+          x[5] = lds32(z_s + (row.z >> 16));
+          x[6] = lds32(z_s + (row.w & 0xFFFFu));
+          x[7] = lds32(z_s + (row.w >> 16));
         }
         uint32_t c0, c1, c2, c3;
         if (DMAX <= 5) {
@@ -225,7 +221,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
           c2 = ke ^ kf;
           c3 = ke & kf;
         }
-        const uint32_t alive = Zb[j];
+        const uint32_t alive = lds32(z_s + 4 * j);
         if (CONWAY) {
           nw = c1 & ~c2 & ~c3 & (c0 | alive);  // B3/S23: count 3, or count 2 and alive
         } else {
@@ -234,11 +230,20 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
         nw &= live_lanes;
       }
       const uint32_t xb = tr(nw);  // bit 8p+m = cell j0 + 4m + p of this lane's tile (0 past K)
-      if (!active) continue;
-      uint4* dst = reinterpret_cast<uint4*>(inb + (size_t)lane * St + j0);
-      dst[0] = make_uint4(xb & 0x01010101u, (xb >> 1) & 0x01010101u, (xb >> 2) & 0x01010101u, (xb >> 3) & 0x01010101u);
-      dst[1] = make_uint4((xb >> 4) & 0x01010101u, (xb >> 5) & 0x01010101u, (xb >> 6) & 0x01010101u,
-                          (xb >> 7) & 0x01010101u);
+      if (active) {
+        const uint32_t m = 0x01010101u;
+        sts128(in_s + j0, xb & m, (xb >> 1) & m, (xb >> 2) & m, (xb >> 3) & m);
+        sts128(in_s + j0 + 16, (xb >> 4) & m, (xb >> 5) & m, (xb >> 6) & m, (xb >> 7) & m);
+      }
+    };
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      const uint32_t jb = (uint32_t)warp + (uint32_t)(i * nwarps);
+      if (jb < nblk) block(jb, rows[i]);
+    }
+    for (uint32_t jb = (uint32_t)warp + (uint32_t)(RB * nwarps); jb < nblk; jb += (uint32_t)nwarps) {
+      const uint32_t j = jb * 32 + my_jj;
+      block(jb, j < K ? __ldg(reinterpret_cast<const uint4*>(p.nbr) + j) : make_uint4(0, 0, 0, 0));
     }
     // no CTA barrier: each warp publishes its part of the output; only the storing thread waits
     fence_proxy_async();
@@ -284,11 +289,11 @@ using TileFn = void (*)(TileParams, const uint8_t*, uint8_t*);
 static TileFn pick(const TileParams& p, int threads) {
   const bool conway = (p.birth == (1u << 3)) && (p.survive == ((1u << 2) | (1u << 3)));
   if (threads <= 256) {
-    if (p.dmax <= 5) return conway ? k_step_tile<5, true, 256, 4> : k_step_tile<5, false, 256, 4>;
-    return conway ? k_step_tile<8, true, 256, 4> : k_step_tile<8, false, 256, 4>;
+    if (p.dmax <= 5) return conway ? k_step_tile<5, true, 256, 4, 3> : k_step_tile<5, false, 256, 4, 3>;
+    return conway ? k_step_tile<8, true, 256, 4, 3> : k_step_tile<8, false, 256, 4, 3>;
   }
-  if (p.dmax <= 5) return conway ? k_step_tile<5, true, 1024, 1> : k_step_tile<5, false, 1024, 1>;
-  return conway ? k_step_tile<8, true, 1024, 1> : k_step_tile<8, false, 1024, 1>;
+  if (p.dmax <= 5) return conway ? k_step_tile<5, true, 1024, 1, 1> : k_step_tile<5, false, 1024, 1, 1>;
+  return conway ? k_step_tile<8, true, 1024, 1, 1> : k_step_tile<8, false, 1024, 1, 1>;
 }
 
 cudaError_t tile_prepare(const TileParams& p, size_t smem, int threads, int* occupancy) {
