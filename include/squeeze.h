@@ -107,8 +107,8 @@ typedef struct {
   uint32_t max_degree;   /* largest neighbour-slot count of any cell of a tile (<= 8) */
   uint32_t tile_bytes;   /* Kp: bytes per tile in a state buffer (K rounded up to 32, odd multiple of 16) */
   uint64_t packed_bytes; /* bytes of a PACKED state buffer (squeeze_*_packed) */
-  uint32_t chunk_words;  /* Kw: 32-bit words per chunk in the packed layout (K rounded up to 4) */
-  uint32_t reserved;
+  uint32_t chunk_words;  /* Kw: 128-bit words per chunk in the packed layout (K rounded up to 4) */
+  uint32_t packed_tiles; /* tiles per chunk of the packed layout (128) */
 } squeeze_geometry_t;
 
 const char* squeeze_strerror(squeeze_status st);
@@ -193,11 +193,12 @@ squeeze_status squeeze_halo_bind(void* ctx, uint8_t* d_send, const uint8_t* d_re
 squeeze_status squeeze_halo_pack(const void* ctx, const uint8_t* d_cur, squeeze_stream_t stream);
 
 /* ---- bit-sliced PACKED state (1 bit per cell) ----
- * Layout: the shard's tiles are grouped in chunks of 32 consecutive tiles; chunk c holds Kw
- * 32-bit words (packed_bytes = chunks x Kw x 4); word j bit i = cell j of tile 32c + i of the
- * shard (j < K; padding words and bits of tiles past the shard end are zero).  It is the form
- * the step computes on, so a packed step moves 0.25 B per cell instead of 2 B.  Unsharded
- * contexts only (SQZ_E_CONFIG otherwise).  Buffers: 16-byte aligned device memory. */
+ * Layout: the shard's tiles are grouped in chunks of packed_tiles = 128 consecutive tiles;
+ * chunk c holds Kw 128-bit words (packed_bytes = chunks x Kw x 16); 32-bit lane q (0..3) of
+ * word j, bit i = cell j of tile 128c + 32q + i of the shard, i.e. the u32 at index
+ * (c x Kw + j) x 4 + q (j < K; padding words and bits of tiles past the shard end are zero).
+ * It is the form the step computes on, so a packed step moves 0.25 B per cell instead of 2 B.
+ * Unsharded contexts only (SQZ_E_CONFIG otherwise).  Buffers: 16-byte aligned device memory. */
 squeeze_status squeeze_pack(const void* ctx, const uint8_t* d_state, uint32_t* d_packed, squeeze_stream_t stream);
 squeeze_status squeeze_unpack(const void* ctx, const uint32_t* d_packed, uint8_t* d_state, squeeze_stream_t stream);
 /* D9 initial state written directly in the packed layout (same cells as squeeze_seed). */

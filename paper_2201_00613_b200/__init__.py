@@ -85,7 +85,7 @@ class Squeeze:
         self.ctx = ctx
         g = _lib.GeometryC()
         _lib.check(self.lib.squeeze_geometry(self.ctx, ctypes.byref(g)))
-        self.geometry = Geometry(*[getattr(g, f[0]) for f in _lib.GeometryC._fields_ if f[0] != "reserved"])
+        self.geometry = Geometry(*[getattr(g, f[0]) for f in _lib.GeometryC._fields_])
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -253,8 +253,9 @@ class Squeeze:
         """Ω-ordered cells of this shard from a packed buffer (host-side decode, for tests)."""
         import numpy as np
         g = self.geometry
-        w = packed.cpu().numpy().view(np.uint32)[:g.packed_bytes // 4].reshape(-1, g.chunk_words)[:, :g.tile_cells]
-        bits = (w[:, None, :] >> np.arange(32, dtype=np.uint32)[None, :, None]) & 1  # [chunk, tile, j]
+        w = packed.cpu().numpy().view(np.uint32)[:g.packed_bytes // 4].reshape(-1, g.chunk_words, 4)
+        w = w[:, :g.tile_cells, :].transpose(0, 2, 1)  # [chunk, lane group q, j]
+        bits = (w[:, :, None, :] >> np.arange(32, dtype=np.uint32)[None, None, :, None]) & 1  # [chunk, q, i, j]
         return bits.reshape(-1, g.tile_cells)[:g.local_tiles].reshape(-1).astype(np.uint8)
 
     # ------------------------------------------------------------------ paper comparison engines (NEXT-2)

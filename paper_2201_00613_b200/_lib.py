@@ -48,7 +48,7 @@ class GeometryC(ctypes.Structure):
                 ("compact_h", ctypes.c_uint64), ("r", ctypes.c_uint32), ("tile_level", ctypes.c_uint32),
                 ("tile_cells", ctypes.c_uint64), ("num_tiles", ctypes.c_uint64), ("chunk_tiles", ctypes.c_uint32),
                 ("remote_links", ctypes.c_uint32), ("max_degree", ctypes.c_uint32), ("tile_bytes", ctypes.c_uint32),
-                ("packed_bytes", ctypes.c_uint64), ("chunk_words", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("packed_bytes", ctypes.c_uint64), ("chunk_words", ctypes.c_uint32), ("packed_tiles", ctypes.c_uint32)]
 
 
 vp = ctypes.c_void_p
@@ -144,6 +144,7 @@ class Geometry:
     tile_bytes: int
     packed_bytes: int
     chunk_words: int
+    packed_tiles: int
 
     @property
     def local_cells(self) -> int:

@@ -54,7 +54,8 @@ struct Ctx {
   uint16_t* d_nbr = nullptr;
   uint16_t* d_nbr_packed = nullptr;  // neighbour slots for the packed kernel (links after Kw words)
   uint32_t* d_adj = nullptr;         // tile adjacency [ndirs][local tiles], built once at init
-  int packed_threads = 128;  // tools/packed_timing.py: 4 warps per CTA is fastest at r=22
+  int packed_threads = 256;
+  uint32_t packed_stages = 3;
   uint32_t Kw = 4;                    // packed words per chunk
   uint64_t packed_bytes = 0;
   int packed_grid = 0;
@@ -170,6 +171,11 @@ squeeze_status check_state(const Ctx* c, const void* p) {
   return SQZ_OK;
 }
 
+// Rows of the adjacency table are padded to whole packed chunks (the packed kernel bulk-copies them).
+uint64_t adj_stride(const Ctx* c) {
+  return (c->sr.tile_hi - c->sr.tile_lo + kPackTiles - 1) / kPackTiles * kPackTiles;
+}
+
 TileParams tile_params(const Ctx* c) {
   TileParams p{};
   p.coarse = c->d_coarse.view;
@@ -195,7 +201,8 @@ TileParams tile_params(const Ctx* c) {
   p.Kw = c->Kw;
   p.halo = halo_view(c);
   p.adj = c->d_adj;
-  p.adj_stride = c->sr.tile_hi - c->sr.tile_lo;
+  p.adj_stride = adj_stride(c);
+  p.pstages = c->packed_stages;
   return p;
 }
 
@@ -212,7 +219,8 @@ squeeze_status do_step_packed(Ctx* c, const uint32_t* cur, uint32_t* next, cudaS
   if (c->NT >= 0xFFFFFFFFull) return SQZ_E_OVERFLOW;
   TileParams p = tile_params(c);
   p.nbr = c->d_nbr_packed;
-  int grid = (int)std::min<uint64_t>((uint64_t)c->packed_grid, p.nchunks ? p.nchunks : 1);
+  const uint64_t pch = (p.tile_hi - p.tile_lo + kPackTiles - 1) / kPackTiles;
+  int grid = (int)std::min<uint64_t>((uint64_t)c->packed_grid, pch ? pch : 1);
   return cu(launch_step_packed(p, cur, next, grid, c->packed_threads, c->packed_smem, st));
 }
 
@@ -340,7 +348,7 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
     if ((c->Kp / 16) % 2 == 0) c->Kp += 16;
     c->state_bytes = (c->sr.tile_hi - c->sr.tile_lo) * c->Kp;
     c->Kw = (uint32_t)((c->tt.K + 3) & ~3ull);
-    c->packed_bytes = ((c->sr.tile_hi - c->sr.tile_lo + kChunkTiles - 1) / kChunkTiles) * c->Kw * 4;
+    c->packed_bytes = ((c->sr.tile_hi - c->sr.tile_lo + kPackTiles - 1) / kPackTiles) * c->Kw * 16;
     if (c->nranks > 1) {
       unsigned th = std::max(1u, std::thread::hardware_concurrency());
       halo_needs(c->tt, c->coarse.view, c->sr, c->needs, th);
@@ -358,10 +366,10 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       for (size_t i = 0; i < nbr_bytes.size(); ++i) {
         const uint32_t v = c->tt.nbr[i];
         nbr_bytes[i] = (uint16_t)(v * 4u);
-        // packed kernel: state words fill [0, Kw), link words follow at Kw + e
-        nbr_packed[i] = (uint16_t)((v < c->tt.K ? v : v - c->tt.K + c->Kw) * 4u);
+        // packed kernel: word slots; state words fill [0, Kw), link words follow at Kw + e
+        nbr_packed[i] = (uint16_t)(v < c->tt.K ? v : v - c->tt.K + c->Kw);
       }
-      if ((uint64_t)(c->Kw + c->tt.E + 1) * 4 > 0xFFFFu) return fail(SQZ_E_INVALID_LEVEL);
+      if ((uint64_t)(c->Kw + c->tt.E + 1) > 0xFFFFu) return fail(SQZ_E_INVALID_LEVEL);
       if ((st = upload(&c->d_nbr, nbr_bytes.data(), nbr_bytes.size())) != SQZ_OK) return fail(st);
       if ((st = upload(&c->d_nbr_packed, nbr_packed.data(), nbr_packed.size())) != SQZ_OK) return fail(st);
       if ((st = upload(&c->d_link_j2, c->tt.link_j2.data(), c->tt.link_j2.size())) != SQZ_OK) return fail(st);
@@ -392,9 +400,19 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
       c->tile_grid = sms * std::max(1, occ);
       p.Kw = c->Kw;
-      c->packed_smem = packed_smem_bytes(p);
+      // packed step: 8 warps while a chunk's words fit the registers of 3 blocks per warp, else
+      // 16; 3 pipeline stages if two CTAs still fit an SM, else 2
+      c->packed_threads = ((c->Kw + 31) / 32 <= 24) ? 256 : 512;
       if (const char* e = getenv("SQZ_PACKED_THREADS")) c->packed_threads = atoi(e);  // tuning experiments
-      if (c->packed_threads < 64 || c->packed_threads > 256 || c->packed_threads % 32) return fail(SQZ_E_CONFIG);
+      if (c->packed_threads < 64 || c->packed_threads > 512 || c->packed_threads % 32) return fail(SQZ_E_CONFIG);
+      // stages: 4 if three CTAs still fit an SM, else 3 if two do, else 2
+      p.pstages = 4;
+      if (3 * packed_smem_bytes(p) > 220 * 1024) p.pstages = 3;
+      if (p.pstages == 3 && 2 * packed_smem_bytes(p) > 220 * 1024) p.pstages = 2;
+      if (const char* e = getenv("SQZ_PACKED_STAGES")) p.pstages = (uint32_t)atoi(e);
+      if (p.pstages < 2 || p.pstages > 4) return fail(SQZ_E_CONFIG);
+      c->packed_stages = p.pstages;
+      c->packed_smem = packed_smem_bytes(p);
       int pocc = 0;
       if (packed_prepare(p, c->packed_smem, c->packed_threads, &pocc) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
       c->packed_grid = sms * std::max(1, pocc);
@@ -402,7 +420,9 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       // evaluated once here instead of every step
       const uint64_t ntl = c->sr.tile_hi - c->sr.tile_lo;
       if (ntl && c->tt.ndirs && c->NT < 0xFFFFFFFFull) {
-        if (cudaMalloc((void**)&c->d_adj, ntl * c->tt.ndirs * sizeof(uint32_t)) != cudaSuccess) return fail(SQZ_E_NOMEM);
+        const size_t adj_bytes = adj_stride(c) * c->tt.ndirs * sizeof(uint32_t);
+        if (cudaMalloc((void**)&c->d_adj, adj_bytes) != cudaSuccess) return fail(SQZ_E_NOMEM);
+        if (cudaMemset(c->d_adj, 0, adj_bytes) != cudaSuccess) return fail(SQZ_E_CUDA);
         TileParams q = tile_params(c);
         if (launch_tile_adjacency(q, c->d_adj, nullptr) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
           return fail(SQZ_E_CUDA);
@@ -441,6 +461,7 @@ squeeze_status squeeze_geometry(const void* ctx, squeeze_geometry_t* out) {
   out->tile_bytes = c->Kp;
   out->packed_bytes = c->packed_bytes;
   out->chunk_words = c->Kw;
+  out->packed_tiles = kPackTiles;
   return SQZ_OK;
 }
 

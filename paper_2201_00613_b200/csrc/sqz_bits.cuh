@@ -187,9 +187,7 @@ __device__ __forceinline__ uint32_t grab(uint32_t* ctr, int lane) { return grab(
 // for each link of direction d whose neighbour tile is outside the chunk, a 4-byte cp.async
 // gather of the word holding the neighbour cell.  The same warp consumes them in Phase B of
 // that chunk.  Always commits exactly one group.
-// PACKED = false: tile-padded byte layout (gather the word holding the byte); true: bit-sliced
-// packed layout (gather the word holding the bit).
-template <bool PACKED>
+// Tile-padded byte layout: the gather fetches the aligned word holding the byte.
 __device__ __forceinline__ void chunk_neighbours(const TileParams& p, uint32_t* ntl, uint32_t* R, const ChunkInfo& c,
                                                  const uint8_t* __restrict__ cur, int warp, int nwarps, int lane) {
   const uint64_t t = c.t0 + lane;
@@ -205,15 +203,8 @@ __device__ __forceinline__ void chunk_neighbours(const TileParams& p, uint32_t* 
         uint32_t* dst = &R[e * kChunkTiles + lane];
         const uint32_t j2 = p.link_j2[e];
         if ((uint64_t)tn >= p.tile_lo && (uint64_t)tn < p.tile_hi) {
-          if (PACKED) {  // word j2 of the neighbour tile's chunk
-            const uint64_t w = (((uint64_t)tn - p.tile_lo) >> 5) * p.Kw + j2;
-            cp_async4(dst, cur + 4 * w);
-          } else {  // tile-padded byte layout: the aligned word holding the byte
-            const uint64_t off = ((uint64_t)tn - p.tile_lo) * p.Kp + j2;
-            cp_async4(dst, cur + (off & ~3ull));
-          }
-        } else if (PACKED) {
-          *dst = fetch_cell(cur, (uint64_t)tn * p.K + j2, p.halo) << (((uint64_t)tn - p.tile_lo) & 31);
+          const uint64_t off = ((uint64_t)tn - p.tile_lo) * p.Kp + j2;
+          cp_async4(dst, cur + (off & ~3ull));
         } else {
           *dst = fetch_cell(cur, (uint64_t)tn * p.K + j2, p.halo) << (8 * (j2 & 3u));  // halo: rare, synchronous
         }

@@ -15,6 +15,7 @@ namespace sqz {
 constexpr uint32_t kHoleU32 = 0xFFFFFFFFu;
 constexpr uint64_t kNoneU64 = ~0ull;
 constexpr int kChunkTiles = 32;  // one bit-slice lane per tile
+constexpr uint32_t kPackTiles = 128;  // tiles per chunk of the packed layout (a 128-bit word per cell)
 
 // ---------------------------------------------------------------------------
 // Exact unsigned 64-bit division by a runtime-constant divisor, by multiply-high

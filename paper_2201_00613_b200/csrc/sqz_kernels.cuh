@@ -48,7 +48,8 @@ struct TileParams {
   // tile adjacency, built once at init: adj[d * adj_stride + (t - tile_lo)] = neighbour tile of
   // local tile t in link direction d, plus 1 (0 = none)
   const uint32_t* adj;
-  uint64_t adj_stride;
+  uint64_t adj_stride;  // a multiple of kPackTiles
+  uint32_t pstages;     // pipeline stages of the packed step
 };
 
 // Shared-memory bytes the tile kernel needs for these parameters.

@@ -1,11 +1,12 @@
 // sqz_packed.cu — the automaton step on the BIT-SLICED PACKED state.
 //
-// Packed layout (include/squeeze.h): chunk c of a shard = its 32 consecutive level-g tiles;
-// Kw = round_up(K, 4) 32-bit words per chunk; word j bit i = cell j of tile 32c + i.  This is
-// exactly the bit-sliced form the byte-state kernel (sqz_tile.cu) builds in shared memory, so
-// here a step is: TMA the chunk's words in, add one word per tile-boundary link, carry-save
-// count + rule per word (32 cells), TMA the words out.  1 bit per cell in HBM (0.25 B/cell of
-// traffic per step instead of 2 B) and no byte<->bit staging.
+// Packed layout (include/squeeze.h): the shard's level-g tiles in chunks of kPackTiles = 128
+// consecutive tiles; chunk c holds Kw = round_up(K, 4) 128-bit words; u32 lane q of word j,
+// bit i = cell j of tile 128c + 32q + i.  It is the bit-sliced form the byte-state kernel
+// (sqz_tile.cu) builds in shared memory, four 32-tile slices side by side, so a step is:
+// bulk-copy the chunk's words in, add one word per tile-boundary link, carry-save count + rule
+// per word (one 128-bit word = 128 cells per lane), store the words.  1 bit per cell in HBM
+// (0.25 B of traffic per cell per step instead of 2 B) and no byte<->bit staging.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -14,186 +15,294 @@
 namespace sqz {
 
 // ------------------------------------------------------------------------------------ layout
-struct PackedSmem {
-  uint32_t* Zin0;   // 2 x [Kw state words (TMA target) | E link words | zero word]
-  uint32_t zn;
-  uint32_t* Zout0;  // 2 x [Kw next-state words] (TMA source)
-  uint32_t* ntl;    // [ndirs][32] neighbour tile + 1 (next chunk)
-  uint32_t* R;      // [E][32] prefetched words (next chunk)
-  uint64_t* bar;    // [0,2) TMA load landed, [2,4) all warps wrote Zout
-  uint32_t* ctr;    // [2] block counters by chunk parity
-  __device__ __forceinline__ uint32_t* Zin(int b) const { return Zin0 + (size_t)b * zn; }
-  __device__ __forceinline__ uint32_t* Zout(int b) const { return Zout0 + (size_t)b * zn; }
+// CTA work unit = one chunk.  Two rings of bulk copies, each with its own mbarriers:
+//  * state stages (p.pstages): [Kw state words (TMA target) | E link words | zero word], 16 B
+//    each; chunk i+pstages-1 is issued when chunk i's barrier frees the stage of chunk i-1;
+//  * adjacency slots (kAdjSlots): the chunk's rows of the tile adjacency table (128 words per
+//    link direction), issued kAdjSlots-1 chunks ahead, so the out-of-chunk link gathers of the
+//    next chunk never wait for its state copy.
+// Results go straight from registers to HBM (coalesced 512-byte warp stores): no output staging
+// and one CTA barrier per chunk.
+constexpr uint32_t kAdjSlots = 4;
+
+__host__ __device__ inline uint32_t pack_zw(const TileParams& p) { return (p.Kw + p.E + 1) * 4; }
+
+struct PackSmem {
+  uint32_t* Z0;   // pstages x zw u32 (state/link/zero words)
+  uint32_t zw;
+  uint32_t* A0;   // kAdjSlots x ndirs x 128 adjacency words
+  uint32_t* R;    // [4E][32] prefetched words holding out-of-chunk neighbour bits (next chunk)
+  uint32_t* lk;   // [E] link e: j2 << 8 | direction
+  uint64_t* bar;  // [pstages] state copies landed, then [kAdjSlots] adjacency copies landed
+  uint32_t ndirs, ns;
+  __device__ __forceinline__ uint32_t* Z(uint32_t s) const { return Z0 + s * zw; }
+  __device__ __forceinline__ const uint32_t* ntl(uint32_t a) const { return A0 + a * ndirs * kPackTiles; }
+  __device__ __forceinline__ uint64_t* abar(uint32_t a) const { return bar + ns + a; }
 };
 
-__host__ __device__ inline size_t packed_layout(const TileParams& p, uint8_t* base, PackedSmem* s) {
-  const size_t zn = align16((size_t)(p.Kw + p.E + 1) * 4) / 4;
+__host__ __device__ inline size_t packed_layout(const TileParams& p, uint8_t* base, PackSmem* s) {
+  const size_t zw = pack_zw(p);
+  const size_t ns = p.pstages ? p.pstages : 2;
   size_t off = 0;
   if (s) {
-    s->Zin0 = (uint32_t*)base;
-    s->zn = (uint32_t)zn;
+    s->Z0 = (uint32_t*)base;
+    s->zw = (uint32_t)zw;
+    s->ndirs = p.ndirs;
+    s->ns = (uint32_t)ns;
   }
-  off += 2 * zn * 4;
-  if (s) s->Zout0 = (uint32_t*)(base + off);
-  off += 2 * zn * 4;
-  if (s) s->ntl = (uint32_t*)(base + off);
-  off += (size_t)(p.ndirs ? p.ndirs : 1) * kChunkTiles * 4;
+  off += ns * zw * 4;
+  if (s) s->A0 = (uint32_t*)(base + off);
+  off += (size_t)kAdjSlots * p.ndirs * kPackTiles * 4;
   if (s) s->R = (uint32_t*)(base + off);
-  off += (size_t)(prefetch_links(p) ? prefetch_links(p) : 1) * kChunkTiles * 4;
+  off += (size_t)4 * (prefetch_links(p) ? prefetch_links(p) : 1) * 32 * 4;
+  if (s) s->lk = (uint32_t*)(base + off);
+  off += align16((size_t)(p.E ? p.E : 1) * 4);
   if (s) s->bar = (uint64_t*)(base + off);
-  off += 32;
-  if (s) s->ctr = (uint32_t*)(base + off);
-  off += 16;
+  off += (ns + kAdjSlots) * 8;
   return align16(off);
 }
 
 size_t packed_smem_bytes(const TileParams& p) { return packed_layout(p, nullptr, nullptr); }
 
-// ------------------------------------------------------------------------------------ step
+__host__ __device__ inline uint64_t pack_chunks(const TileParams& p) {
+  return (p.tile_hi - p.tile_lo + kPackTiles - 1) / kPackTiles;
+}
+
+struct PackChunk {
+  uint64_t c;
+  uint32_t t0;  // first tile (tile indices < 2^32, checked on the host)
+  uint32_t nt;  // tiles in the chunk
+};
+
+__device__ __forceinline__ PackChunk pack_chunk(const TileParams& p, uint64_t c) {
+  PackChunk pc;
+  pc.c = c;
+  const uint64_t t0 = p.tile_lo + c * kPackTiles;
+  pc.t0 = (uint32_t)t0;
+  pc.nt = (uint32_t)min((uint64_t)kPackTiles, p.tile_hi - t0);
+  return pc;
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// One thread: the chunk's Kw words -> state stage s.
+__device__ __forceinline__ void state_load(const TileParams& p, const PackSmem& S, const PackChunk& pc, uint32_t s,
+                                           const uint4* __restrict__ cur) {
+  const uint32_t bytes = p.Kw * 16;
+  uint64_t* bar = &S.bar[s];
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  bulk_g2s(smem_u32(S.Z(s)), cur + pc.c * p.Kw, bytes, bar);
+}
+
+// One thread: the chunk's 128 adjacency words per link direction -> adjacency slot a.
+// (Adjacency rows are padded to whole chunks on the host, so every copy is 512 bytes.)
+__device__ __forceinline__ void adj_load(const TileParams& p, const PackSmem& S, const PackChunk& pc, uint32_t a) {
+  const uint32_t abytes = kPackTiles * 4;
+  uint64_t* bar = S.abar(a);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(abytes * p.ndirs)
+               : "memory");
+  const uint32_t dst = smem_u32(S.ntl(a));
+  for (uint32_t d = 0; d < p.ndirs; ++d)
+    bulk_g2s(dst + d * abytes, p.adj + d * p.adj_stride + (pc.t0 - p.tile_lo), abytes, bar);
+}
+
+// Link slot u = 4e + q: link e for the 32 tiles of lane group q (tiles 32q..32q+31 of the chunk).
+// Slots belong to warp u mod W, here and in the link phase of the next iteration (same thread:
+// program order suffices).  For a link whose neighbour tile is outside the chunk: a 4-byte
+// cp.async of the packed word holding the neighbour bit.  `ntl` = the chunk's adjacency words
+// (neighbour tile + 1, from the coarse λ + ν at init: P:189 at tile level).  Commits one group.
+__device__ __forceinline__ void chunk_prefetch(const TileParams& p, const PackSmem& S, const PackChunk& pc,
+                                               const uint32_t* ntl, const uint32_t* __restrict__ cur32, int warp,
+                                               int nwarps, int lane) {
+  const uint32_t E = prefetch_links(p);
+  for (uint32_t u = (uint32_t)warp; u < 4 * E; u += (uint32_t)nwarps) {
+    const uint32_t q = u & 3u, e = u >> 2;
+    const uint32_t lk = S.lk[e];
+    const uint32_t a1 = ntl[(lk & 7u) * kPackTiles + q * 32 + lane];
+    const uint32_t tl = a1 - 1u - (uint32_t)p.tile_lo;
+    if (a1 != 0 && a1 - 1u - pc.t0 >= pc.nt)
+      cp_async4(&S.R[u * 32 + lane], cur32 + ((uint64_t)(tl >> 7) * p.Kw + (lk >> 8)) * 4 + ((tl >> 5) & 3u));
+  }
+  cp_async_commit();
+}
+
+// Carry-save count of DMAX neighbour words and the rule, on one 32-bit lane of the word.
 template <int DMAX, bool CONWAY>
-__global__ void __launch_bounds__(256, 4) k_step_packed(TileParams p, const uint32_t* __restrict__ cur,
-                                                        uint32_t* __restrict__ next) {
+__device__ __forceinline__ uint32_t cell_rule(const uint32_t* x, uint32_t alive, uint32_t birth, uint32_t survive) {
+  uint32_t c0, c1, c2, c3;
+  if (DMAX <= 5) {
+    const uint32_t s1 = x[0] ^ x[1] ^ x[2], k1 = maj3(x[0], x[1], x[2]);
+    const uint32_t s2 = s1 ^ x[3] ^ x[4], k2 = maj3(s1, x[3], x[4]);
+    c0 = s2;
+    c1 = k1 ^ k2;
+    c2 = k1 & k2;
+    c3 = 0;
+  } else {
+    const uint32_t sa = x[0] ^ x[1] ^ x[2], ka = maj3(x[0], x[1], x[2]);
+    const uint32_t sb = x[3] ^ x[4] ^ x[5], kb = maj3(x[3], x[4], x[5]);
+    const uint32_t sc = sa ^ sb ^ x[6], kc = maj3(sa, sb, x[6]);
+    c0 = sc ^ x[7];
+    const uint32_t kd = sc & x[7];
+    const uint32_t se = ka ^ kb ^ kc, ke = maj3(ka, kb, kc);
+    c1 = se ^ kd;
+    const uint32_t kf = se & kd;
+    c2 = ke ^ kf;
+    c3 = ke & kf;
+  }
+  if (CONWAY) return c1 & ~c2 & ~c3 & (c0 | alive);  // B3/S23: count 3, or count 2 and alive
+  return (alive & rule_bits(survive, c0, c1, c2, c3)) | (~alive & rule_bits(birth, c0, c1, c2, c3));
+}
+
+// ------------------------------------------------------------------------------------ step
+// DMAX: neighbour slots per cell (5 for the Sierpinski triangle, else 8).  RB: j-blocks per warp
+// whose neighbour slots stay in registers for the whole launch (block jb = warp + i * W); later
+// blocks read their slots through L1.
+template <int DMAX, bool CONWAY, int RB, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const uint4* __restrict__ cur,
+                                                        uint4* __restrict__ next) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  PackedSmem S;
+  PackSmem S;
   packed_layout(p, smem_raw, &S);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const uint32_t K = (uint32_t)p.K, Kw = p.Kw;
-  const uint32_t nblk = (K + 31) / 32;
+  const uint32_t K = (uint32_t)p.K, Kw = p.Kw, E = p.E, NS = p.pstages;
   const uint32_t Epf = prefetch_links(p);
-  const int lw = nwarps - 1;
-  const bool issuer = warp == lw && lane == 0;
-  const uint8_t* cur8 = reinterpret_cast<const uint8_t*>(cur);
+  const uint64_t nch = pack_chunks(p);
+  const bool issuer = warp == nwarps - 1 && lane == 0;
+  const uint32_t* cur32 = reinterpret_cast<const uint32_t*>(cur);
 
-  for (uint32_t i = tid; i < 2 * S.zn; i += blockDim.x) S.Zout0[i] = 0;  // padding words stay 0
+  uint32_t off[RB][DMAX];  // byte offsets of this lane's neighbour words in a stage (slot x 16)
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    const uint32_t j = ((uint32_t)warp + (uint32_t)(i * nwarps)) * 32 + lane;
+    const uint4 row = j < K ? __ldg(reinterpret_cast<const uint4*>(p.nbr) + j) : make_uint4(0, 0, 0, 0);
+    const uint32_t w[4] = {row.x, row.y, row.z, row.w};
+#pragma unroll
+    for (int k = 0; k < DMAX; ++k) off[i][k] = ((w[k >> 1] >> (16 * (k & 1))) & 0xFFFFu) * 16;
+  }
+
+  for (uint32_t i = tid; i < NS * 4; i += blockDim.x) S.Z(i >> 2)[(Kw + E) * 4 + (i & 3)] = 0;  // zero slot
+  for (uint32_t e = tid; e < E; e += blockDim.x) S.lk[e] = (p.link_j2[e] << 8) | p.link_dir[e];
   if (tid == 0) {
-    S.Zin(0)[Kw + p.E] = 0;
-    S.Zin(1)[Kw + p.E] = 0;
-    S.ctr[0] = S.ctr[1] = 0;
-    mbar_init(&S.bar[0], 1);
-    mbar_init(&S.bar[1], 1);
-    mbar_init(&S.bar[2], (uint32_t)nwarps);
-    mbar_init(&S.bar[3], (uint32_t)nwarps);
+    for (uint32_t s = 0; s < NS + kAdjSlots; ++s) mbar_init(&S.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  uint64_t chunk = blockIdx.x;
-  if (chunk >= p.nchunks) return;
+  uint64_t c = blockIdx.x;
+  if (c >= nch) return;
   const uint64_t G = gridDim.x;
-  const uint32_t cbytes = Kw * 4;
-  {  // prologue: chunk 0 loaded, λ of chunks 0 and 1, neighbours + prefetch of chunk 0
-    const ChunkInfo c0 = chunk_info(p, chunk);
-    if (issuer) tma_load_1d(S.Zin(0), cur + chunk * Kw, cbytes, &S.bar[0]);
-    chunk_neighbours<true>(p, S.ntl, S.R, c0, cur8, warp, nwarps, lane);
+  if (issuer) {
+    for (uint32_t s = 0; s + 1 < NS && c + s * G < nch; ++s) state_load(p, S, pack_chunk(p, c + s * G), s, cur);
+    for (uint32_t a = 0; a + 1 < kAdjSlots && c + a * G < nch; ++a) adj_load(p, S, pack_chunk(p, c + a * G), a);
   }
+  mbar_wait(S.abar(0), 0);
+  chunk_prefetch(p, S, pack_chunk(p, c), S.ntl(0), cur32, warp, nwarps, lane);
 
-  uint32_t it = 0;
-  for (; chunk < p.nchunks; chunk += G, ++it) {
-    const int buf = it & 1;
-    const ChunkInfo c = chunk_info(p, chunk);
-    const bool has_next = chunk + G < p.nchunks;
-    if (issuer) {
-      if (it >= 1) {  // the previous chunk is complete: write it out, then reuse its input buffer
-        mbar_wait(&S.bar[2 + (buf ^ 1)], ((it - 1) >> 1) & 1);
-        tma_store_1d(next + (chunk - G) * Kw, S.Zout(buf ^ 1), cbytes);
-      }
-      if (has_next) {
-        fence_proxy_async();
-        tma_load_1d(S.Zin(buf ^ 1), cur + (chunk + G) * Kw, cbytes, &S.bar[buf ^ 1]);
-      }
-    }
-    mbar_wait(&S.bar[buf], (it >> 1) & 1);
-    uint32_t* Z = S.Zin(buf);
+  uint32_t it = 0, s = 0, sphase = 0;  // sphase bit s: parity of state stage s's next completion
+  for (; c < nch; c += G, ++it, s = (s + 1 == NS) ? 0 : s + 1) {
+    const PackChunk pc = pack_chunk(p, c);
+    uint32_t* Z = S.Z(s);
+    const uint32_t zs = smem_u32(Z);
+    const uint32_t a = it & (kAdjSlots - 1);
+    const uint32_t* ntl = S.ntl(a);
+    mbar_wait(&S.bar[s], (sphase >> s) & 1);
+    sphase ^= 1u << s;
 
-    // link words: bit i of Z[Kw + e] = cell j2 of lane i's neighbour tile in the link's direction
-    if (warp < (int)p.ndirs) {
+    // link words: bit i of u32 lane q of word Kw + e = cell j2 of the neighbour tile (link e)
+    // of tile 32q + i
+    if ((uint32_t)warp < 4 * E) {
+      mbar_wait(S.abar(a), (it / kAdjSlots) & 1);  // (already complete when the prefetch ran)
       cp_async_wait_all();
-      for (int d = warp; d < (int)p.ndirs; d += nwarps) {
-        const int64_t tn = (int64_t)S.ntl[d * kChunkTiles + lane] - 1;
-        const uint64_t rel = (uint64_t)(tn - (int64_t)c.t0);
-        const bool inside = tn >= 0 && rel < c.nt;
-        const uint32_t bit = (uint32_t)(((uint64_t)tn - p.tile_lo) & 31);
-        const uint32_t e1 = p.dir_start[d + 1];
-        for (uint32_t e = p.dir_start[d]; e < e1; ++e) {
-          const uint32_t j2 = p.link_j2[e];
-          uint32_t v = 0;
-          if (inside) v = (Z[j2] >> (uint32_t)rel) & 1u;
-          else if (tn >= 0) {
-            if (e < Epf) v = (S.R[e * kChunkTiles + lane] >> bit) & 1u;
-            else v = fetch_cell(cur8, (uint64_t)tn * p.K + j2, p.halo);
-          }
-          const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
-          if (lane == 0) Z[Kw + e] = bal;
-        }
+      const uint32_t rs = smem_u32(S.R);
+      for (uint32_t u = (uint32_t)warp; u < 4 * E; u += (uint32_t)nwarps) {
+        const uint32_t q = u & 3u, e = u >> 2;
+        const uint32_t lk = S.lk[e], j2 = lk >> 8;
+        const uint32_t a1 = ntl[(lk & 7u) * kPackTiles + q * 32 + lane];
+        const uint32_t rel = a1 - 1u - pc.t0, tl = a1 - 1u - (uint32_t)p.tile_lo;
+        uint32_t v = 0;
+        if (rel < pc.nt) v = lds32(zs + (j2 * 4 + (rel >> 5)) * 4) >> (rel & 31);
+        else if (a1 != 0)
+          v = (e < Epf ? lds32(rs + (u * 32 + lane) * 4)
+                       : __ldg(cur32 + ((uint64_t)(tl >> 7) * Kw + j2) * 4 + ((tl >> 5) & 3u))) >>
+              (tl & 31);
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v & 1u);
+        if (lane == 0) Z[(Kw + e) * 4 + q] = bal;
       }
     }
-    if (issuer) bulk_wait_read_all();  // Zout(buf) was last stored two chunks ago
-    __syncthreads();  // the one CTA barrier per chunk
-    if (tid == 0) S.ctr[buf ^ 1] = 0;  // idle: every warp finished the previous chunk's blocks
-    if (has_next)
-      chunk_neighbours<true>(p, S.ntl, S.R, chunk_info(p, chunk + G), cur8, warp, nwarps, lane);
+    __syncthreads();  // the one CTA barrier per chunk: state + link words in place, chunk it-1 done
+    if (issuer) {
+      if (c + (NS - 1) * G < nch) {
+        fence_proxy_async();
+        state_load(p, S, pack_chunk(p, c + (NS - 1) * G), (s + NS - 1) % NS, cur);
+      }
+      if (c + (kAdjSlots - 1) * G < nch)
+        adj_load(p, S, pack_chunk(p, c + (kAdjSlots - 1) * G), (it + kAdjSlots - 1) & (kAdjSlots - 1));
+    }
+    if (c + G < nch) {  // out-of-chunk link gathers of the next chunk (its adjacency was issued long ago)
+      const uint32_t a1 = (it + 1) & (kAdjSlots - 1);
+      if ((uint32_t)warp < 4 * Epf) mbar_wait(S.abar(a1), ((it + 1) / kAdjSlots) & 1);
+      chunk_prefetch(p, S, pack_chunk(p, c + G), S.ntl(a1), cur32, warp, nwarps, lane);
+    }
 
-    // count + rule, one word (32 cells) per lane
-    const uint32_t live_lanes = c.nt >= 32 ? 0xFFFFFFFFu : ((1u << c.nt) - 1u);
-    const uint8_t* zb = reinterpret_cast<const uint8_t*>(Z);
-    uint32_t* out = S.Zout(buf);
-    for (uint32_t jb = grab(&S.ctr[buf], lane); jb < nblk; jb = grab(&S.ctr[buf], lane)) {
-      const uint32_t j = jb * 32 + lane;
-      if (j >= K) continue;
-      const uint4 row = __ldg(reinterpret_cast<const uint4*>(p.nbr) + j);  // byte offsets into Z
-      uint32_t x[8];
-      x[0] = *reinterpret_cast<const uint32_t*>(zb + (row.x & 0xFFFFu));
-      x[1] = *reinterpret_cast<const uint32_t*>(zb + (row.x >> 16));
-      x[2] = *reinterpret_cast<const uint32_t*>(zb + (row.y & 0xFFFFu));
-      x[3] = *reinterpret_cast<const uint32_t*>(zb + (row.y >> 16));
-      x[4] = *reinterpret_cast<const uint32_t*>(zb + (row.z & 0xFFFFu));
-      if (DMAX > 5) {
-        x[5] = *reinterpret_cast<const uint32_t*>(zb + (row.z >> 16));
-        x[6] = *reinterpret_cast<const uint32_t*>(zb + (row.w & 0xFFFFu));
-        x[7] = *reinterpret_cast<const uint32_t*>(zb + (row.w >> 16));
-      }
-      uint32_t c0, c1, c2, c3;
-      if (DMAX <= 5) {
-        const uint32_t s1 = x[0] ^ x[1] ^ x[2], k1 = maj3(x[0], x[1], x[2]);
-        const uint32_t s2 = s1 ^ x[3] ^ x[4], k2 = maj3(s1, x[3], x[4]);
-        c0 = s2;
-        c1 = k1 ^ k2;
-        c2 = k1 & k2;
-        c3 = 0;
-      } else {
-        const uint32_t sa = x[0] ^ x[1] ^ x[2], ka = maj3(x[0], x[1], x[2]);
-        const uint32_t sb = x[3] ^ x[4] ^ x[5], kb = maj3(x[3], x[4], x[5]);
-        const uint32_t sc = sa ^ sb ^ x[6], kc = maj3(sa, sb, x[6]);
-        c0 = sc ^ x[7];
-        const uint32_t kd = sc & x[7];
-        const uint32_t se = ka ^ kb ^ kc, ke = maj3(ka, kb, kc);
-        c1 = se ^ kd;
-        const uint32_t kf = se & kd;
-        c2 = ke ^ kf;
-        c3 = ke & kf;
-      }
-      const uint32_t alive = Z[j];
-      uint32_t nw;
-      if (CONWAY) nw = c1 & ~c2 & ~c3 & (c0 | alive);
-      else nw = (alive & rule_bits(p.survive, c0, c1, c2, c3)) | (~alive & rule_bits(p.birth, c0, c1, c2, c3));
-      out[j] = nw & live_lanes;
+    // count + rule: lane = word j (128 cells), straight to HBM
+    uint4 lm = make_uint4(~0u, ~0u, ~0u, ~0u);
+    if (pc.nt < kPackTiles) {  // the shard's last chunk: bits of tiles past its end stay 0
+      const uint32_t n = pc.nt;
+      lm.x = n >= 32 ? ~0u : (1u << n) - 1u;
+      lm.y = n >= 64 ? ~0u : (n <= 32 ? 0u : (1u << (n - 32)) - 1u);
+      lm.z = n >= 96 ? ~0u : (n <= 64 ? 0u : (1u << (n - 64)) - 1u);
+      lm.w = n <= 96 ? 0u : (1u << (n - 96)) - 1u;
     }
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&S.bar[2 + buf]);
-  }
-  if (issuer) {  // write out the last chunk
-    const int lb = (int)((it - 1) & 1);
-    mbar_wait(&S.bar[2 + lb], ((it - 1) >> 1) & 1);
-    tma_store_1d(next + (chunk - G) * Kw, S.Zout(lb), cbytes);
-    bulk_wait_all();
+    uint4* outc = next + pc.c * Kw;
+    auto word = [&](uint32_t j, const uint32_t* o) {
+      if (j >= Kw) return;
+      uint4 nw = make_uint4(0, 0, 0, 0);
+      if (j < K) {
+        uint32_t x0[DMAX], x1[DMAX], x2[DMAX], x3[DMAX];
+#pragma unroll
+        for (int k = 0; k < DMAX; ++k) {
+          const uint4 v = lds128(zs + o[k]);
+          x0[k] = v.x;
+          x1[k] = v.y;
+          x2[k] = v.z;
+          x3[k] = v.w;
+        }
+        const uint4 al = lds128(zs + j * 16);
+        nw.x = cell_rule<DMAX, CONWAY>(x0, al.x, p.birth, p.survive) & lm.x;
+        nw.y = cell_rule<DMAX, CONWAY>(x1, al.y, p.birth, p.survive) & lm.y;
+        nw.z = cell_rule<DMAX, CONWAY>(x2, al.z, p.birth, p.survive) & lm.z;
+        nw.w = cell_rule<DMAX, CONWAY>(x3, al.w, p.birth, p.survive) & lm.w;
+      }
+      outc[j] = nw;  // padding words K..Kw-1 are written 0
+    };
+#pragma unroll
+    for (int i = 0; i < RB; ++i) word(((uint32_t)warp + (uint32_t)(i * nwarps)) * 32 + lane, off[i]);
+    for (uint32_t jb = (uint32_t)warp + (uint32_t)(RB * nwarps); jb * 32 < Kw; jb += (uint32_t)nwarps) {
+      const uint32_t j = jb * 32 + lane;
+      const uint4 row = j < K ? __ldg(reinterpret_cast<const uint4*>(p.nbr) + j) : make_uint4(0, 0, 0, 0);
+      const uint32_t w[4] = {row.x, row.y, row.z, row.w};
+      uint32_t o[DMAX];
+#pragma unroll
+      for (int k = 0; k < DMAX; ++k) o[k] = ((w[k >> 1] >> (16 * (k & 1))) & 0xFFFFu) * 16;
+      word(j, o);
+    }
   }
   cp_async_wait_all();
 }
 
 // ------------------------------------------------------------------------------------ conversions
+// The conversions walk 32-tile slices: slice v = 4c + q of the shard is u32 lane q of chunk c,
+// so u32 word j of slice v sits at index (c * Kw + j) * 4 + q of the packed buffer.
+__device__ __forceinline__ uint64_t slice_word(const TileParams& p, uint64_t v, uint32_t j) {
+  return ((v >> 2) * p.Kw + j) * 4 + (v & 3);
+}
+
 // byte layout -> packed: lane = tile reads its 32-byte window (two 128-bit loads), packs, and
-// the warp transposes so lane L holds word j0 + my_jj(L).  One warp per (chunk, j-block).
+// the warp transposes so lane L holds word j0 + my_jj(L).  One warp per (slice, j-block).
 __global__ void k_pack(TileParams p, const uint8_t* __restrict__ st, uint32_t* __restrict__ packed) {
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -201,11 +310,11 @@ __global__ void k_pack(TileParams p, const uint8_t* __restrict__ st, uint32_t* _
   const uint32_t K = (uint32_t)p.K, nblk = (K + 31) / 32, wpc = (p.Kw + 31) / 32;  // blocks incl. padding words
   const uint32_t my_jj = 4 * (lane & 7) + (lane >> 3);
   const Transposer tr(lane);
-  const uint64_t ntiles = p.tile_hi - p.tile_lo;
-  for (uint64_t wi = gw; wi < p.nchunks * wpc; wi += nw) {
-    const uint64_t c = wi / wpc;
-    const uint32_t jb = (uint32_t)(wi - c * wpc), j0 = jb * 32;
-    const uint64_t t = c * kChunkTiles + lane;
+  const uint64_t ntiles = p.tile_hi - p.tile_lo, nslices = pack_chunks(p) * 4;
+  for (uint64_t wi = gw; wi < nslices * wpc; wi += nw) {
+    const uint64_t v = wi / wpc;
+    const uint32_t jb = (uint32_t)(wi - v * wpc), j0 = jb * 32;
+    const uint64_t t = v * 32 + lane;
     uint32_t acc = 0;
     if (jb < nblk && t < ntiles) {
       const uint4* src = reinterpret_cast<const uint4*>(st + t * p.Kp + j0);
@@ -215,7 +324,7 @@ __global__ void k_pack(TileParams p, const uint8_t* __restrict__ st, uint32_t* _
             ((hi.z & 0x01010101u) << 6) | ((hi.w & 0x01010101u) << 7);
     }
     const uint32_t x = tr(acc);  // bytes past K are zero in the byte layout
-    if (j0 + my_jj < p.Kw) packed[c * p.Kw + j0 + my_jj] = x;
+    if (j0 + my_jj < p.Kw) packed[slice_word(p, v, j0 + my_jj)] = x;
   }
 }
 
@@ -228,14 +337,14 @@ __global__ void k_unpack(TileParams p, const uint32_t* __restrict__ packed, uint
   const uint32_t nblk = (K + 31) / 32;
   const uint32_t my_jj = 4 * (lane & 7) + (lane >> 3);
   const Transposer tr(lane);
-  const uint64_t ntiles = p.tile_hi - p.tile_lo;
+  const uint64_t ntiles = p.tile_hi - p.tile_lo, nslices = (ntiles + 31) / 32;
   const uint32_t jobs = (wpt + 1) / 2;  // 32-byte windows per tile (the last may be 16 bytes)
-  for (uint64_t wi = gw; wi < p.nchunks * jobs; wi += nw) {
-    const uint64_t c = wi / jobs;
-    const uint32_t jb = (uint32_t)(wi - c * jobs), j0 = jb * 32;
-    uint32_t x = (jb < nblk && j0 + my_jj < K) ? packed[c * p.Kw + j0 + my_jj] : 0u;
+  for (uint64_t wi = gw; wi < nslices * jobs; wi += nw) {
+    const uint64_t v = wi / jobs;
+    const uint32_t jb = (uint32_t)(wi - v * jobs), j0 = jb * 32;
+    uint32_t x = (jb < nblk && j0 + my_jj < K) ? packed[slice_word(p, v, j0 + my_jj)] : 0u;
     x = tr(x);
-    const uint64_t t = c * kChunkTiles + lane;
+    const uint64_t t = v * 32 + lane;
     if (t >= ntiles) continue;
     uint4* dst = reinterpret_cast<uint4*>(st + t * p.Kp + j0);
     dst[0] = make_uint4(x & 0x01010101u, (x >> 1) & 0x01010101u, (x >> 2) & 0x01010101u, (x >> 3) & 0x01010101u);
@@ -250,12 +359,12 @@ __global__ void k_seed_packed(TileParams p, LevelMaps gm, uint32_t* __restrict__
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t)gridDim.x * blockDim.x >> 5;
-  const uint64_t ntiles = p.tile_hi - p.tile_lo;
-  for (uint64_t wi = gw; wi < p.nchunks * p.Kw; wi += nw) {
-    const uint64_t c = wi / p.Kw;
-    const uint32_t j = (uint32_t)(wi - c * p.Kw);
-    const uint64_t t = c * kChunkTiles + lane;
-    uint32_t v = 0;
+  const uint64_t ntiles = p.tile_hi - p.tile_lo, nslices = pack_chunks(p) * 4;
+  for (uint64_t wi = gw; wi < nslices * p.Kw; wi += nw) {
+    const uint64_t v = wi / p.Kw;
+    const uint32_t j = (uint32_t)(wi - v * p.Kw);
+    const uint64_t t = v * 32 + lane;
+    uint32_t a = 0;
     if (j < p.K && t < ntiles) {
       uint32_t x, y;
       lambda_level(gm, (p.tile_lo + t) * p.K + j, x, y);
@@ -268,10 +377,10 @@ __global__ void k_seed_packed(TileParams p, LevelMaps gm, uint32_t* __restrict__
         z ^= z >> 31;
         return z;
       }();
-      v = (h >> 32) < q ? 1u : 0u;
+      a = (h >> 32) < q ? 1u : 0u;
     }
-    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
-    if (lane == 0) packed[wi] = bal;
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, a != 0);
+    if (lane == 0) packed[slice_word(p, v, j)] = bal;
   }
 }
 
@@ -291,16 +400,26 @@ __global__ void k_count_packed(const uint32_t* __restrict__ w, uint64_t n, unsig
 }
 
 // ------------------------------------------------------------------------------------ launchers
-using PackedFn = void (*)(TileParams, const uint32_t*, uint32_t*);
+using PackedFn = void (*)(TileParams, const uint4*, uint4*);
 
-static PackedFn pick_packed(const TileParams& p) {
+// RB = j-blocks per warp with register-resident neighbour slots (ceil(nblk / W), capped).
+static PackedFn pick_packed(const TileParams& p, int threads) {
   const bool conway = (p.birth == (1u << 3)) && (p.survive == ((1u << 2) | (1u << 3)));
-  if (p.dmax <= 5) return conway ? k_step_packed<5, true> : k_step_packed<5, false>;
-  return conway ? k_step_packed<8, true> : k_step_packed<8, false>;
+  const uint32_t nblk = (uint32_t)((p.Kw + 31) / 32), W = (uint32_t)threads / 32;
+  const uint32_t rb = (nblk + W - 1) / W;
+  if (threads <= 256) {
+    if (p.dmax <= 5) return conway ? k_step_packed<5, true, 3, 256, 3> : k_step_packed<5, false, 3, 256, 3>;
+    return conway ? k_step_packed<8, true, 2, 256, 3> : k_step_packed<8, false, 2, 256, 3>;
+  }
+  if (p.dmax <= 5) {
+    if (rb <= 3) return conway ? k_step_packed<5, true, 3, 512, 1> : k_step_packed<5, false, 3, 512, 1>;
+    return conway ? k_step_packed<5, true, 5, 512, 2> : k_step_packed<5, false, 5, 512, 2>;
+  }
+  return conway ? k_step_packed<8, true, 3, 512, 1> : k_step_packed<8, false, 3, 512, 1>;
 }
 
 cudaError_t packed_prepare(const TileParams& p, size_t smem, int threads, int* occupancy) {
-  PackedFn fn = pick_packed(p);
+  PackedFn fn = pick_packed(p, threads);
   cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int blocks = 0;
@@ -312,8 +431,9 @@ cudaError_t packed_prepare(const TileParams& p, size_t smem, int threads, int* o
 
 cudaError_t launch_step_packed(const TileParams& p, const uint32_t* cur, uint32_t* next, int grid, int threads,
                                size_t smem, cudaStream_t st) {
-  if (p.nchunks == 0) return cudaSuccess;
-  pick_packed(p)<<<grid, threads, smem, st>>>(p, cur, next);
+  if (pack_chunks(p) == 0) return cudaSuccess;
+  pick_packed(p, threads)<<<grid, threads, smem, st>>>(p, reinterpret_cast<const uint4*>(cur),
+                                                      reinterpret_cast<uint4*>(next));
   return cudaGetLastError();
 }
 
@@ -324,27 +444,27 @@ static unsigned warps_grid(uint64_t warps) {
 }
 
 cudaError_t launch_pack(const TileParams& p, const uint8_t* st, uint32_t* packed, cudaStream_t s) {
-  if (p.nchunks == 0) return cudaSuccess;
-  k_pack<<<warps_grid(p.nchunks * ((p.Kw + 31) / 32)), 256, 0, s>>>(p, st, packed);
+  if (pack_chunks(p) == 0) return cudaSuccess;
+  k_pack<<<warps_grid(pack_chunks(p) * 4 * ((p.Kw + 31) / 32)), 256, 0, s>>>(p, st, packed);
   return cudaGetLastError();
 }
 
 cudaError_t launch_unpack(const TileParams& p, const uint32_t* packed, uint8_t* st, cudaStream_t s) {
-  if (p.nchunks == 0) return cudaSuccess;
-  k_unpack<<<warps_grid(p.nchunks * ((p.Kp / 16 + 1) / 2)), 256, 0, s>>>(p, packed, st);
+  if (pack_chunks(p) == 0) return cudaSuccess;
+  k_unpack<<<warps_grid(pack_chunks(p) * 4 * ((p.Kp / 16 + 1) / 2)), 256, 0, s>>>(p, packed, st);
   return cudaGetLastError();
 }
 
 cudaError_t launch_seed_packed(const TileParams& p, const LevelMaps& full, uint32_t* packed, uint64_t seed, uint64_t q,
                                cudaStream_t s) {
-  if (p.nchunks == 0) return cudaSuccess;
+  if (pack_chunks(p) == 0) return cudaSuccess;
   uint64_t z = seed;
   z ^= z >> 30;
   z *= 0xBF58476D1CE4E5B9ull;
   z ^= z >> 27;
   z *= 0x94D049BB133111EBull;
   z ^= z >> 31;
-  k_seed_packed<<<warps_grid(p.nchunks * p.Kw), 256, 0, s>>>(p, full, packed, z, q);
+  k_seed_packed<<<warps_grid(pack_chunks(p) * 4 * p.Kw), 256, 0, s>>>(p, full, packed, z, q);
   return cudaGetLastError();
 }
 

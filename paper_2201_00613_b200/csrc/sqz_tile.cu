@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
   {  // prologue: chunk 0 loaded, neighbours + link prefetch of chunk 0
     const ChunkInfo c0 = chunk_info(p, chunk);
     if (issuer) chunk_load(p, c0, S.in(0), &S.bar[0], cur);
-    chunk_neighbours<false>(p, S.ntl, S.R, c0, cur, warp, nwarps, lane);
+    chunk_neighbours(p, S.ntl, S.R, c0, cur, warp, nwarps, lane);
   }
 
   uint32_t it = 0;
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     }
     __syncthreads();  // the one CTA barrier per chunk: all state and link words are in Zb
     // the next chunk's neighbour tiles + link prefetch overlap the count/write-back blocks
-    if (has_next) chunk_neighbours<false>(p, S.ntl, S.R, chunk_info(p, chunk + G), cur, warp, nwarps, lane);
+    if (has_next) chunk_neighbours(p, S.ntl, S.R, chunk_info(p, chunk + G), cur, warp, nwarps, lane);
 
     // Phases C + D per j-block: lane L computes cell j0 + my_jj(L) of all 32 tiles (carry-save
     // count, rule), then the block is transposed back (lane = tile) and written in place.

@@ -130,7 +130,7 @@ def test_packed_full_size_sampled_and_histogram():
     om = np.concatenate([om, [0, 1, 2, 3 ** r - 1]]).astype(np.int64)
     t = om // g.tile_cells
     j = om - t * g.tile_cells
-    widx = torch.from_numpy((t // 32) * g.chunk_words + j).cuda()
+    widx = torch.from_numpy(((t // 128) * g.chunk_words + j) * 4 + (t // 32) % 4).cuda()
     bit = torch.from_numpy(t % 32).cuda()
 
     def bits(buf):

@@ -1,4 +1,5 @@
-"""Times the packed-state step at level r (CUDA events after warm-up)."""
+"""Times the packed-state step (CUDA events after warm-up).
+    python tools/packed_timing.py [fractal] [levels,comma-separated] [tile_level]"""
 import os
 import sys
 
@@ -8,8 +9,9 @@ import torch  # noqa: E402
 import paper_2201_00613_b200 as pkg  # noqa: E402
 
 fr = sys.argv[1] if len(sys.argv) > 1 else "sierpinski-triangle"
+g = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 for r in [int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "22").split(",")]:
-    p = pkg.Squeeze(pkg.builtin_fractal(fr), r, device=0)
+    p = pkg.Squeeze(pkg.builtin_fractal(fr), r, device=0, tile_level=g)
     a, b = p.new_packed(), p.new_packed()
     p.seed_packed(a, 42, 0.5)
     for _ in range(3):
@@ -22,7 +24,7 @@ for r in [int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "22").split(","
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 20
     c = p.geometry.cells_total
-    print(fr, r, os.environ.get("SQZ_PACKED_THREADS", "256"), round(ms, 3), "ms", round(c / ms / 1e9, 3), "Tcells/s",
-          round(2 * p.geometry.packed_bytes / ms / 1e6, 1), "GB/s", flush=True)
+    print(fr, r, "g", p.geometry.tile_level, os.environ.get("SQZ_PACKED_THREADS", "auto"), round(ms, 3), "ms",
+          round(c / ms / 1e9, 3), "Tcells/s", round(2 * p.geometry.packed_bytes / ms / 1e6, 1), "GB/s", flush=True)
     del a, b, p
     torch.cuda.empty_cache()
