@@ -43,6 +43,7 @@ def parse_args():
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--density", type=float, default=0.5)
     ap.add_argument("--tile-level", type=int, default=0)
+    ap.add_argument("--packed-tile-level", type=int, default=7, help="tile level of the packed leg (0 = same ctx)")
     ap.add_argument("--block-threads", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--no-extras", action="store_true", help="skip BB / naive / cpu / e2e legs")
@@ -339,32 +340,45 @@ def main():
                                   "tile_speedup": naive_ms / (ms / K)}
         del a, b
         torch.cuda.empty_cache()
-        # --- bit-sliced packed state: same step, 1 bit per cell in HBM
-        pa, pb = sq.new_packed(), sq.new_packed()
-        sq.seed_packed(pa, args.seed, args.density)
+        # --- bit-sliced packed state: same step, 1 bit per cell in HBM.  Its own
+        # context at the packed kernel's tile level (level-7 tiles: 3x fewer boundary links per
+        # cell than the byte kernel's level 6)
+        pq = sq
+        if args.packed_tile_level and args.packed_tile_level != g.tile_level:
+            try:
+                pq = pkg.Squeeze(f, args.level, device=local, tile_level=args.packed_tile_level)
+            except pkg.SqueezeError:
+                pq = sq
+        gq = pq.geometry
+        pa, pb = pq.new_packed(), pq.new_packed()
+        pq.seed_packed(pa, args.seed, args.density)
         for i in range(args.warmup):
-            sq.step_packed(pa if i % 2 == 0 else pb, pb if i % 2 == 0 else pa)
+            pq.step_packed(pa if i % 2 == 0 else pb, pb if i % 2 == 0 else pa)
         torch.cuda.synchronize()
         pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         for i in range(K):
             pev[i][0].record(stream)
-            sq.step_packed(pa if i % 2 == 0 else pb, pb if i % 2 == 0 else pa)
+            pq.step_packed(pa if i % 2 == 0 else pb, pb if i % 2 == 0 else pa)
             pev[i][1].record(stream)
         s1.record(stream)
         torch.cuda.synchronize()
         p_ms = s0.elapsed_time(s1)
         p_kern = sum(e0.elapsed_time(e1) for e0, e1 in pev) / K
-        p_bytes = 2 * g.packed_bytes
+        p_bytes = 2 * gq.packed_bytes
         extras["packed_state"] = {
-            "value": cells_per_s(g.cells_total, K, p_ms), "unit": "cells/s", "ms_per_step": p_ms / K,
-            "bytes_per_cell_per_step": p_bytes / g.cells_total, "state_bytes": g.packed_bytes,
+            "value": cells_per_s(gq.cells_total, K, p_ms), "unit": "cells/s", "ms_per_step": p_ms / K,
+            "tile_level": gq.tile_level, "tile_cells": gq.tile_cells,
+            "bytes_per_cell_per_step": p_bytes / gq.cells_total, "state_bytes": gq.packed_bytes,
             "kernel": "sqz::k_step_packed", "avg_launch_ms": p_kern,
             "hbm_achieved_GBps": p_bytes / (p_kern / 1e3) / 1e9, "hbm_frac": p_bytes / (p_kern / 1e3) / 1e9 / peak,
-            "note": "1 bit per cell, bit-sliced chunk layout (squeeze_*_packed); compute/latency-bound, "
-                    "bit-exact with the byte path (tests/test_gpu_packed.py)"}
+            "note": "1 bit per cell, 128-tile bit-sliced chunks (squeeze_*_packed); algorithmic bytes = state "
+                    "read + write; the tile adjacency rows add 4 B x link directions per tile; bit-exact with "
+                    "the byte path (tests/test_gpu_packed.py)"}
         del pa, pb
+        if pq is not sq:
+            pq.close()
         torch.cuda.empty_cache()
         # --- GPU expanded bounding-box baseline vs compact at r=16 (BASELINE configs[1])
         r16 = 16
