@@ -20,10 +20,13 @@ automaton     Game of Life on the expanded embedding (the definition) and
               on the compact form through λ/ν, plus transport
 metrics       V = k^r, compact size, MRF (Table 2)
 mma           the paper's MMA encoding of ν, exact integer product
+heat          second workload (reading D16): explicit heat diffusion on the
+              fractal's Moore graph, definition on the embedding and λ/ν compact form
 
 Parity status: every function here is pinned by ``tests/test_oracle_*.py``
 against values the paper prints, closed forms (Pascal's triangle mod 2, Morton
-order, textbook Game-of-Life patterns, the Sierpinski neighbour histogram) or
-brute force, except where its docstring says "parity unpinned" (the empty-bottles
+order, textbook Game-of-Life patterns, the Sierpinski neighbour histogram; for
+``heat``: conservation, a brute-force Laplacian matrix power, scipy's 3x3 stencil on
+the full square) or brute force, except where its docstring says "parity unpinned" (the empty-bottles
 and Vicsek replica layouts, D11; the paper's unstated "adapted" rule, D6).
 """

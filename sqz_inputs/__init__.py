@@ -83,3 +83,22 @@ def random_coords(count: int, side: int, seed: int) -> tuple[np.ndarray, np.ndar
     x = rng.integers(0, side, size=count, dtype=np.uint64).astype(np.uint32)
     y = rng.integers(0, side, size=count, dtype=np.uint64).astype(np.uint32)
     return x, y
+
+
+# ---------------------------------------------------------------- NEXT-4 initial field
+HEAT_BITS = 24  # the initial temperature is k * 2^-24, exactly representable in float32
+
+
+def heat_value(x: int, y: int, seed: int) -> float:
+    """Initial temperature at expanded (X, Y): (mix(((X << 32) | Y) ^ mix(seed)) >> 40) * 2^-24,
+    in [0, 1) with 24 significant bits (the same splitmix64 draw as D9, top 24 bits)."""
+    h = mix((((x & 0xFFFFFFFF) << 32) | (y & 0xFFFFFFFF)) ^ mix(seed))
+    return (h >> (64 - HEAT_BITS)) / float(1 << HEAT_BITS)
+
+
+def heat_values(x: np.ndarray, y: np.ndarray, seed: int) -> np.ndarray:
+    """Vectorised ``heat_value`` -> float64."""
+    x = np.asarray(x, dtype=np.uint64)
+    y = np.asarray(y, dtype=np.uint64)
+    h = _mix_np(((x << np.uint64(32)) | y) ^ np.uint64(mix(seed)))
+    return (h >> np.uint64(64 - HEAT_BITS)).astype(np.float64) / float(1 << HEAT_BITS)
