@@ -109,6 +109,9 @@ typedef struct {
   uint64_t packed_bytes; /* bytes of a PACKED state buffer (squeeze_*_packed) */
   uint32_t chunk_words;  /* Kw: 128-bit words per chunk in the packed layout (K rounded up to 4) */
   uint32_t packed_tiles; /* tiles per chunk of the packed layout (128) */
+  uint64_t heat_bytes;   /* bytes of a HEAT field buffer (squeeze_heat_*) */
+  uint32_t heat_tile_floats; /* Kf: floats per tile in a heat buffer (K rounded up to 4) */
+  uint32_t heat_pairs;   /* remote (own cell, neighbour) pairs per tile of the heat kernel */
 } squeeze_geometry_t;
 
 const char* squeeze_strerror(squeeze_status st);
@@ -211,6 +214,23 @@ squeeze_status squeeze_run_packed(void* ctx, uint32_t* d_a, uint32_t* d_b, uint6
 /* *d_out (device uint64) = number of alive cells in a packed buffer. */
 squeeze_status squeeze_count_alive_packed(const void* ctx, const uint32_t* d_packed, uint64_t* d_out,
                                           squeeze_stream_t stream);
+
+/* ---- second workload: heat diffusion on the compact fractal ----
+ * Squeeze serves "PDE solvers, cellular-automata, spin-model simulations ... as they rely
+ * on accessing neighboring cells".  One explicit step of the graph heat equation (D16):
+ *     u'(Ω) = u(Ω) + α Σ_{n ∈ N(Ω)} (u(n) − u(Ω)),  N(Ω) = member Moore neighbours,
+ * i.e. an insulated boundary; α·max_degree <= 1 keeps it a convex combination (stable).
+ * Layout: float32, tile-padded: local tile t at float offset t x heat_tile_floats, padding 0;
+ * heat_bytes per buffer; 16-byte aligned caller-owned device memory.  Unsharded contexts only
+ * (SQZ_E_CONFIG otherwise); d_cur and d_next must not alias. */
+/* Initial field: u(Ω) = (mix(((X<<32)|Y) ^ mix(seed)) >> 40) x 2^-24 at (X, Y) = λ(Ω). */
+squeeze_status squeeze_heat_seed(const void* ctx, float* d_u, uint64_t seed, squeeze_stream_t stream);
+squeeze_status squeeze_heat_step(void* ctx, const float* d_cur, float* d_next, float alpha, squeeze_stream_t stream);
+/* `steps` steps ping-ponging d_a / d_b (final field in d_b if steps is odd). */
+squeeze_status squeeze_heat_run(void* ctx, float* d_a, float* d_b, uint64_t steps, float alpha,
+                                squeeze_stream_t stream);
+/* *d_out (device double) = Σ u over the buffer (conserved by the step up to rounding). */
+squeeze_status squeeze_heat_sum(const void* ctx, const float* d_u, double* d_out, squeeze_stream_t stream);
 
 /* ---- the paper's comparison engines ---- */
 /* λ(ω) engine ("compact grid and expanded fractal"): one thread per compact cell computes

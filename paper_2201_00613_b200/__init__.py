@@ -258,6 +258,37 @@ class Squeeze:
         bits = (w[:, :, None, :] >> np.arange(32, dtype=np.uint32)[None, None, :, None]) & 1  # [chunk, q, i, j]
         return bits.reshape(-1, g.tile_cells)[:g.local_tiles].reshape(-1).astype(np.uint8)
 
+    # ------------------------------------------------------------------ heat diffusion (NEXT-4)
+    def new_heat(self):
+        """A float32 field buffer in the tile-padded heat layout (include/squeeze.h)."""
+        import torch
+        return torch.zeros(max(4, self.geometry.heat_bytes // 4), dtype=torch.float32, device=f"cuda:{self.device}")
+
+    def heat_seed(self, u, seed: int = 42, stream=None):
+        _lib.check(self.lib.squeeze_heat_seed(self.ctx, _ptr(u), seed, _stream(stream, u.device)), "heat_seed")
+
+    def heat_step(self, cur, nxt, alpha: float = 0.125, stream=None):
+        _lib.check(self.lib.squeeze_heat_step(self.ctx, _ptr(cur), _ptr(nxt), alpha, _stream(stream, cur.device)),
+                   "heat_step")
+
+    def heat_run(self, a, b, steps: int, alpha: float = 0.125, stream=None):
+        _lib.check(self.lib.squeeze_heat_run(self.ctx, _ptr(a), _ptr(b), steps, alpha, _stream(stream, a.device)),
+                   "heat_run")
+        return b if steps % 2 else a
+
+    def heat_sum(self, u, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.zeros(1, dtype=torch.float64, device=u.device)
+        _lib.check(self.lib.squeeze_heat_sum(self.ctx, _ptr(u), _ptr(out), _stream(stream, u.device)), "heat_sum")
+        return out
+
+    def heat_to_cells(self, u):
+        """Ω-ordered float32 values of this shard from a heat buffer (host-side decode)."""
+        g = self.geometry
+        kf = g.heat_tile_floats
+        return u[:g.local_tiles * kf].reshape(g.local_tiles, kf)[:, :g.tile_cells].reshape(-1)
+
     # ------------------------------------------------------------------ paper comparison engines (NEXT-2)
     def lambda_engine_step(self, cur_grid, next_grid, stream=None):
         """λ(ω) engine: compact thread grid over an expanded BB-layout grid."""

@@ -48,7 +48,8 @@ class GeometryC(ctypes.Structure):
                 ("compact_h", ctypes.c_uint64), ("r", ctypes.c_uint32), ("tile_level", ctypes.c_uint32),
                 ("tile_cells", ctypes.c_uint64), ("num_tiles", ctypes.c_uint64), ("chunk_tiles", ctypes.c_uint32),
                 ("remote_links", ctypes.c_uint32), ("max_degree", ctypes.c_uint32), ("tile_bytes", ctypes.c_uint32),
-                ("packed_bytes", ctypes.c_uint64), ("chunk_words", ctypes.c_uint32), ("packed_tiles", ctypes.c_uint32)]
+                ("packed_bytes", ctypes.c_uint64), ("chunk_words", ctypes.c_uint32), ("packed_tiles", ctypes.c_uint32),
+                ("heat_bytes", ctypes.c_uint64), ("heat_tile_floats", ctypes.c_uint32), ("heat_pairs", ctypes.c_uint32)]
 
 
 vp = ctypes.c_void_p
@@ -85,6 +86,10 @@ SIGNATURES = {
     "squeeze_step_packed": ([vp, vp, vp, vp], st),
     "squeeze_run_packed": ([vp, vp, vp, ctypes.c_uint64, vp], st),
     "squeeze_count_alive_packed": ([vp, vp, vp, vp], st),
+    "squeeze_heat_seed": ([vp, vp, ctypes.c_uint64, vp], st),
+    "squeeze_heat_step": ([vp, vp, vp, ctypes.c_float, vp], st),
+    "squeeze_heat_run": ([vp, vp, vp, ctypes.c_uint64, ctypes.c_float, vp], st),
+    "squeeze_heat_sum": ([vp, vp, vp, vp], st),
     "squeeze_lambda_engine_step": ([vp, vp, vp, vp], st),
     "squeeze_block_bytes": ([vp, ctypes.c_uint32, u64p], st),
     "squeeze_block_seed": ([vp, ctypes.c_uint32, vp, ctypes.c_uint64, ctypes.c_uint64, vp], st),
@@ -145,6 +150,9 @@ class Geometry:
     packed_bytes: int
     chunk_words: int
     packed_tiles: int
+    heat_bytes: int
+    heat_tile_floats: int
+    heat_pairs: int
 
     @property
     def local_cells(self) -> int:

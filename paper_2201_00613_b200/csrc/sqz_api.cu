@@ -16,6 +16,7 @@
 
 #include "../../include/squeeze.h"
 #include "sqz_host.h"
+#include "sqz_heat.cuh"
 #include "sqz_kernels.cuh"
 
 using namespace sqz;
@@ -60,6 +61,13 @@ struct Ctx {
   uint64_t packed_bytes = 0;
   int packed_grid = 0;
   size_t packed_smem = 0;
+  // heat workload (NEXT-4): neighbour slots, remote pairs, launch shape
+  uint32_t Kf = 4, heat_P = 0, heat_stages = 3;
+  uint64_t heat_bytes = 0;
+  int heat_grid = 0;
+  uint16_t* d_heat_nbr = nullptr;
+  uint32_t* d_heat_pairs = nullptr;
+  uint32_t* d_heat_j2 = nullptr;
   uint32_t* d_link_j2 = nullptr;
   uint8_t* d_link_dir = nullptr;
   uint16_t* d_dir_start = nullptr;
@@ -128,6 +136,9 @@ void free_device(Ctx* c) {
   cudaFree(c->d_coarse.d);
   cudaFree(c->d_nbr);
   cudaFree(c->d_nbr_packed);
+  cudaFree(c->d_heat_nbr);
+  cudaFree(c->d_heat_pairs);
+  cudaFree(c->d_heat_j2);
   cudaFree(c->d_adj);
   for (auto& kv : c->blocks) {
     cudaFree(kv.second.dev.d);
@@ -204,6 +215,24 @@ TileParams tile_params(const Ctx* c) {
   p.adj_stride = adj_stride(c);
   p.pstages = c->packed_stages;
   return p;
+}
+
+HeatParams heat_params(const Ctx* c, float alpha) {
+  HeatParams h{};
+  h.Kf = c->Kf;
+  h.P = c->heat_P;
+  h.stages = c->heat_stages;
+  h.alpha = alpha;
+  h.nbr = c->d_heat_nbr;
+  h.pairs = c->d_heat_pairs;
+  h.pair_j2 = c->d_heat_j2;
+  return h;
+}
+
+squeeze_status do_heat_step(Ctx* c, const float* cur, float* next, float alpha, cudaStream_t st) {
+  if (c->nranks > 1) return SQZ_E_CONFIG;
+  if (c->NT >= 0xFFFFFFFFull) return SQZ_E_OVERFLOW;
+  return cu(launch_heat_step(heat_params(c, alpha), tile_params(c), cur, next, c->heat_grid, st));
 }
 
 squeeze_status do_step(Ctx* c, const uint8_t* cur, uint8_t* next, cudaStream_t st) {
@@ -349,6 +378,8 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
     c->state_bytes = (c->sr.tile_hi - c->sr.tile_lo) * c->Kp;
     c->Kw = (uint32_t)((c->tt.K + 3) & ~3ull);
     c->packed_bytes = ((c->sr.tile_hi - c->sr.tile_lo + kPackTiles - 1) / kPackTiles) * c->Kw * 16;
+    c->Kf = (uint32_t)((c->tt.K + 3) & ~3ull);
+    c->heat_bytes = (c->sr.tile_hi - c->sr.tile_lo) * c->Kf * 4;
     if (c->nranks > 1) {
       unsigned th = std::max(1u, std::thread::hardware_concurrency());
       halo_needs(c->tt, c->coarse.view, c->sr, c->needs, th);
@@ -416,6 +447,41 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       int pocc = 0;
       if (packed_prepare(p, c->packed_smem, c->packed_threads, &pocc) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
       c->packed_grid = sms * std::max(1, pocc);
+      // heat workload: slots = byte offsets into a tile's [Kf state | P pairs] shared slot; an
+      // absent neighbour is the cell itself, a remote neighbour a per-(cell, link) pair
+      {
+        std::vector<uint16_t> hn(c->tt.nbr.size());
+        std::vector<uint32_t> hp, hj2;
+        for (uint64_t j = 0; j < c->tt.K; ++j)
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t v = c->tt.nbr[j * 8 + k];
+            uint64_t slot;
+            if (v < c->tt.K) slot = v;
+            else if (v == c->tt.zero_slot) slot = j;
+            else {
+              const uint32_t e = v - (uint32_t)c->tt.K;
+              slot = c->Kf + hp.size();
+              hp.push_back((uint32_t)j | ((uint32_t)c->tt.link_dir[e] << 16));
+              hj2.push_back(c->tt.link_j2[e]);
+            }
+            if (slot * 4 > 0xFFFFu) return fail(SQZ_E_INVALID_LEVEL);
+            hn[j * 8 + k] = (uint16_t)(slot * 4);
+          }
+        c->heat_P = (uint32_t)hp.size();
+        if ((st = upload(&c->d_heat_nbr, hn.data(), hn.size())) != SQZ_OK) return fail(st);
+        if ((st = upload(&c->d_heat_pairs, hp.data(), hp.size())) != SQZ_OK) return fail(st);
+        if ((st = upload(&c->d_heat_j2, hj2.data(), hj2.size())) != SQZ_OK) return fail(st);
+        HeatParams h = heat_params(c, 0.125f);
+        TileParams q = tile_params(c);
+        for (c->heat_stages = 3; c->heat_stages > 2; --c->heat_stages) {  // 3 CTAs per SM if they fit
+          h.stages = c->heat_stages;
+          if (3 * heat_smem_bytes(h, q) <= 220 * 1024) break;
+        }  // (at least 2 stages: a unit's successor is filled while the unit is computed)
+        h.stages = c->heat_stages;
+        int hocc = 0;
+        if (heat_prepare(h, q, &hocc) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
+        c->heat_grid = sms * std::max(1, hocc);
+      }
       // tile adjacency: the coarse λ and one coarse ν per link direction of every local tile,
       // evaluated once here instead of every step
       const uint64_t ntl = c->sr.tile_hi - c->sr.tile_lo;
@@ -462,6 +528,9 @@ squeeze_status squeeze_geometry(const void* ctx, squeeze_geometry_t* out) {
   out->packed_bytes = c->packed_bytes;
   out->chunk_words = c->Kw;
   out->packed_tiles = kPackTiles;
+  out->heat_bytes = c->heat_bytes;
+  out->heat_tile_floats = c->Kf;
+  out->heat_pairs = c->heat_P;
   return SQZ_OK;
 }
 
@@ -746,6 +815,51 @@ squeeze_status squeeze_count_alive_packed(const void* ctx, const uint32_t* d_pac
   if (st != SQZ_OK) return st;
   DevGuard g(c->device);
   return cu(launch_count_packed(d_packed, c->packed_bytes / 4, d_out, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_heat_seed(const void* ctx, float* d_u, uint64_t seed, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_u);
+  if (st != SQZ_OK) return st;
+  if (c->nranks > 1) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return cu(launch_heat_seed(c->d_full.view, tile_params(c), c->Kf, d_u, seed, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_heat_step(void* ctx, const float* d_cur, float* d_next, float alpha, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_cur);
+  if (st == SQZ_OK) st = check_state(c, d_next);
+  if (st != SQZ_OK) return st;
+  if (d_cur == d_next || !(alpha == alpha)) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return do_heat_step(c, d_cur, d_next, alpha, (cudaStream_t)stream);
+}
+
+squeeze_status squeeze_heat_run(void* ctx, float* d_a, float* d_b, uint64_t steps, float alpha,
+                                squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_a);
+  if (st == SQZ_OK) st = check_state(c, d_b);
+  if (st != SQZ_OK) return st;
+  if (d_a == d_b || !(alpha == alpha)) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  for (uint64_t i = 0; i < steps && st == SQZ_OK; ++i)
+    st = (i & 1) ? do_heat_step(c, d_b, d_a, alpha, (cudaStream_t)stream)
+                 : do_heat_step(c, d_a, d_b, alpha, (cudaStream_t)stream);
+  return st;
+}
+
+squeeze_status squeeze_heat_sum(const void* ctx, const float* d_u, double* d_out, squeeze_stream_t stream) {
+  if (!ctx || !d_out) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_u);
+  if (st != SQZ_OK) return st;
+  DevGuard g(c->device);
+  return cu(launch_heat_sum(d_u, c->heat_bytes / 4, d_out, (cudaStream_t)stream));
 }
 
 squeeze_status squeeze_lambda_engine_step(const void* ctx, const uint8_t* d_cur_grid, uint8_t* d_next_grid,

@@ -1,0 +1,29 @@
+// sqz_heat.cuh — parameters and launchers of the heat-diffusion workload (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sqz_kernels.cuh"
+
+namespace sqz {
+
+struct HeatParams {
+  uint32_t Kf;              // floats per tile in a heat buffer (K rounded up to 4)
+  uint32_t P;               // remote (own cell, neighbour) pairs per tile
+  uint32_t stages;          // pipeline stages
+  float alpha;              // diffusion number α
+  const uint16_t* nbr;      // K x 8 byte offsets into a tile's [Kf state | P pairs] slot
+  const uint32_t* pairs;    // P: own cell j | link direction << 16
+  const uint32_t* pair_j2;  // P: the neighbour's cell in the neighbour tile
+};
+
+size_t heat_smem_bytes(const HeatParams& h, const TileParams& p);
+cudaError_t heat_prepare(const HeatParams& h, const TileParams& p, int* occupancy);
+cudaError_t launch_heat_step(const HeatParams& h, const TileParams& p, const float* cur, float* next, int grid,
+                             cudaStream_t st);
+cudaError_t launch_heat_seed(const LevelMaps& full, const TileParams& p, uint32_t Kf, float* u, uint64_t seed,
+                             cudaStream_t st);
+cudaError_t launch_heat_sum(const float* u, uint64_t n, double* out, cudaStream_t st);
+
+}  // namespace sqz
