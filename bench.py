@@ -44,6 +44,7 @@ def parse_args():
     ap.add_argument("--density", type=float, default=0.5)
     ap.add_argument("--tile-level", type=int, default=0)
     ap.add_argument("--packed-tile-level", type=int, default=7, help="tile level of the packed leg (0 = same ctx)")
+    ap.add_argument("--heat-level", type=int, default=21, help="level of the heat-diffusion leg (0 = skip)")
     ap.add_argument("--block-threads", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--no-extras", action="store_true", help="skip BB / naive / cpu / e2e legs")
@@ -379,6 +380,66 @@ def main():
         del pa, pb
         if pq is not sq:
             pq.close()
+        torch.cuda.empty_cache()
+        # --- second workload: heat diffusion on the compact fractal, float32 field
+        if args.heat_level:
+            ph = pkg.Squeeze(f, args.heat_level, device=local)
+            gh = ph.geometry
+            ha, hb = ph.new_heat(), ph.new_heat()
+            ph.heat_seed(ha, args.seed)
+            for i in range(args.warmup):
+                ph.heat_step(ha if i % 2 == 0 else hb, hb if i % 2 == 0 else ha)
+            torch.cuda.synchronize()
+            hsteps = max(2, min(K, 20))
+            hev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(hsteps)]
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            for i in range(hsteps):
+                hev[i][0].record(stream)
+                ph.heat_step(ha if i % 2 == 0 else hb, hb if i % 2 == 0 else ha)
+                hev[i][1].record(stream)
+            s1.record(stream)
+            torch.cuda.synchronize()
+            h_ms = s0.elapsed_time(s1)
+            h_kern = sum(e0.elapsed_time(e1) for e0, e1 in hev) / hsteps
+            h_bytes = 8 * gh.cells_total  # 4 B read + 4 B written per cell (algorithmic)
+            extras["heat_diffusion"] = {
+                "level": args.heat_level, "cells": gh.cells_total, "steps": hsteps,
+                "value": cells_per_s(gh.cells_total, hsteps, h_ms), "unit": "cells/s", "ms_per_step": h_ms / hsteps,
+                "kernel": "sqz::k_heat_step", "avg_launch_ms": h_kern, "bytes_per_cell_per_step": 8,
+                "hbm_achieved_GBps": h_bytes / (h_kern / 1e3) / 1e9,
+                "hbm_frac": h_bytes / (h_kern / 1e3) / 1e9 / peak, "dtype": "f32",
+                "note": "u' = u + alpha * sum over member Moore neighbours (u_n - u), alpha = 1/8, insulated edge "
+                        "(DESIGN.md D16); float32 field, parity vs the float64 oracle within the derived bound "
+                        "(tests/test_gpu_heat.py)"}
+            del ha, hb
+            ph.close()
+            torch.cuda.empty_cache()
+        torch.cuda.empty_cache()
+        # --- NEXT-3 ablation: batched ν map, LUT kernel vs integer tensor-core product
+        nmap = 1 << 27
+        gen = torch.Generator(device=f"cuda:{local}").manual_seed(1)
+        om_ = torch.randint(0, g.cells_total, (nmap,), device=f"cuda:{local}", generator=gen)
+        mx, my = sq.map_lambda(om_)
+        abl = {"elements": nmap, "level": args.level, "bytes_per_element": 16,
+               "note": "nu of member coordinates (lambda of random Omega); LUT = multi-digit tables (one lookup per "
+                       "6 levels), mma = mma.sync m16n8k32 u8 (A = H_nu per level, B = bytes of k^(mu-1)); both "
+                       "bit-exact (tests/test_gpu_mma.py); the hot path keeps the LUT (DESIGN.md §9)"}
+        for name, fn in (("lut", sq.map_nu), ("mma", sq.map_nu_mma)):
+            fn(mx, my)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(5):
+                res = fn(mx, my)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            mms = e0.elapsed_time(e1) / 5
+            abl[name] = {"ms": mms, "maps_per_s": nmap / (mms / 1e3), "GBps": 16 * nmap / (mms / 1e3) / 1e9,
+                         "exact": bool(torch.equal(res, om_))}
+        abl["mma_over_lut_time"] = abl["mma"]["ms"] / abl["lut"]["ms"]
+        extras["map_ablation"] = abl
+        del om_, mx, my, res
         torch.cuda.empty_cache()
         # --- GPU expanded bounding-box baseline vs compact at r=16 (BASELINE configs[1])
         r16 = 16

@@ -152,6 +152,13 @@ squeeze_status squeeze_map_lambda(const void* ctx, const uint64_t* d_omega, uint
 /* d_omega[i] = ν(d_x[i], d_y[i]); holes and out-of-range coordinates yield UINT64_MAX. */
 squeeze_status squeeze_map_nu(const void* ctx, const uint32_t* d_x, const uint32_t* d_y, uint64_t* d_omega,
                               uint64_t count, squeeze_stream_t stream);
+/* ν as an exact integer tensor-core product (SURVEY §8f NEXT-3 ablation of P:296-332):
+ * Ω = Σ_b (A·B)[c][b] 256^b with A[c][μ] = H_ν[θ_μ(c)] (u8) and B[μ][b] = byte b of k^(μ-1),
+ * one mma.sync m16n8k32 u8 per 16 coordinates.  Same contract and output as squeeze_map_nu;
+ * SQZ_E_CONFIG when s^2 > 256 or k > 256 (no u8 encoding).  Not on the hot path: bench.py
+ * times it beside the LUT map. */
+squeeze_status squeeze_map_nu_mma(const void* ctx, const uint32_t* d_x, const uint32_t* d_y, uint64_t* d_omega,
+                                  uint64_t count, squeeze_stream_t stream);
 
 /* ---- automaton ---- */
 /* Initial state (reading D9): cell Ω alive iff (mix(((X<<32)|Y) ^ mix(seed)) >> 32) < q at

@@ -177,6 +177,16 @@ class Squeeze:
                                            _stream(stream, x.device)), "map_nu")
         return om
 
+    def map_nu_mma(self, x, y, stream=None):
+        """ν through the integer tensor-core product (NEXT-3 ablation); same output as map_nu."""
+        import torch
+        x = x.contiguous()
+        y = y.contiguous()
+        om = torch.empty(x.numel(), dtype=torch.int64, device=x.device)
+        _lib.check(self.lib.squeeze_map_nu_mma(self.ctx, _ptr(x), _ptr(y), _ptr(om), x.numel(),
+                                               _stream(stream, x.device)), "map_nu_mma")
+        return om
+
     def seed(self, state, seed: int = 42, density: float = 0.5, stream=None):
         _lib.check(self.lib.squeeze_seed(self.ctx, _ptr(state), seed, density_q(density),
                                          _stream(stream, state.device)), "seed")

@@ -69,6 +69,7 @@ SIGNATURES = {
     "squeeze_nu_host": ([vp, ctypes.c_uint64, ctypes.c_uint64, u64p], st),
     "squeeze_map_lambda": ([vp, vp, vp, vp, ctypes.c_uint64, vp], st),
     "squeeze_map_nu": ([vp, vp, vp, vp, ctypes.c_uint64, vp], st),
+    "squeeze_map_nu_mma": ([vp, vp, vp, vp, ctypes.c_uint64, vp], st),
     "squeeze_seed": ([vp, vp, ctypes.c_uint64, ctypes.c_uint64, vp], st),
     "squeeze_step": ([vp, vp, vp, vp], st),
     "squeeze_step_naive": ([vp, vp, vp, vp], st),

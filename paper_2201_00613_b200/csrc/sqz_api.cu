@@ -68,6 +68,8 @@ struct Ctx {
   uint16_t* d_heat_nbr = nullptr;
   uint32_t* d_heat_pairs = nullptr;
   uint32_t* d_heat_j2 = nullptr;
+  int16_t* d_mma_h = nullptr;   // ν tensor-core ablation tables (NEXT-3)
+  uint8_t* d_mma_B = nullptr;
   uint32_t* d_link_j2 = nullptr;
   uint8_t* d_link_dir = nullptr;
   uint16_t* d_dir_start = nullptr;
@@ -137,6 +139,8 @@ void free_device(Ctx* c) {
   cudaFree(c->d_nbr);
   cudaFree(c->d_nbr_packed);
   cudaFree(c->d_heat_nbr);
+  cudaFree(c->d_mma_h);
+  cudaFree(c->d_mma_B);
   cudaFree(c->d_heat_pairs);
   cudaFree(c->d_heat_j2);
   cudaFree(c->d_adj);
@@ -447,6 +451,18 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       int pocc = 0;
       if (packed_prepare(p, c->packed_smem, c->packed_threads, &pocc) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
       c->packed_grid = sms * std::max(1, pocc);
+      // ν tensor-core ablation: H_ν as int16 and the per-level weight bytes of k^(μ-1)
+      if (c->f.s * c->f.s <= kMmaMaxS2 && c->f.k <= 256 && r <= 32) {
+        std::vector<int16_t> hh(c->f.hnu.begin(), c->f.hnu.end());
+        std::vector<uint8_t> B(32 * 8, 0);
+        uint64_t w = 1;
+        for (uint32_t m = 0; m < r; ++m) {
+          for (int b = 0; b < 8; ++b) B[m * 8 + b] = (uint8_t)(w >> (8 * b));
+          w *= c->f.k;
+        }
+        if ((st = upload(&c->d_mma_h, hh.data(), hh.size())) != SQZ_OK) return fail(st);
+        if ((st = upload(&c->d_mma_B, B.data(), B.size())) != SQZ_OK) return fail(st);
+      }
       // heat workload: slots = byte offsets into a tile's [Kf state | P pairs] shared slot; an
       // absent neighbour is the cell itself, a remote neighbour a per-(cell, link) pair
       {
@@ -580,6 +596,25 @@ squeeze_status squeeze_map_nu(const void* ctx, const uint32_t* d_x, const uint32
   if (count && (!d_omega || !d_x || !d_y)) return SQZ_E_CONFIG;
   DevGuard g(c->device);
   return cu(launch_map_nu(c->d_full.view, d_x, d_y, d_omega, count, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_map_nu_mma(const void* ctx, const uint32_t* d_x, const uint32_t* d_y, uint64_t* d_omega,
+                                  uint64_t count, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (c->device < 0) return SQZ_E_NO_DEVICE;
+  if (!c->d_mma_B) return SQZ_E_CONFIG;  // s^2 > 256 or k > 256: no u8 encoding
+  if (count && (!d_omega || !d_x || !d_y)) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  MmaNuParams q{};
+  q.r = c->r;
+  q.s = c->f.s;
+  q.k = c->f.k;
+  q.s_log2 = c->full.view.s_log2;
+  q.n = c->n;
+  q.hnu = c->d_mma_h;
+  q.B = c->d_mma_B;
+  return cu(launch_map_nu_mma(q, d_x, d_y, d_omega, count, (cudaStream_t)stream));
 }
 
 squeeze_status squeeze_seed(const void* ctx, uint8_t* d_state, uint64_t seed, uint64_t q, squeeze_stream_t stream) {

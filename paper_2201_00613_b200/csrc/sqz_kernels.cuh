@@ -52,6 +52,18 @@ struct TileParams {
   uint32_t pstages;     // pipeline stages of the packed step
 };
 
+// ν as an integer tensor-core product (sqz_mma.cu, SURVEY NEXT-3 ablation).
+constexpr uint32_t kMmaMaxS2 = 256;  // s^2 <= 256 (H_ν staged in shared memory), k <= 256 (u8 A)
+struct MmaNuParams {
+  uint32_t r, s, k;
+  uint32_t s_log2;       // log2 s if s is a power of two, else 0
+  uint64_t n;            // s^r
+  const int16_t* hnu;    // s*s: H_ν[θy * s + θx] or -1 (hole)
+  const uint8_t* B;      // 32 x 8: B[μ-1][b] = byte b of k^(μ-1) (0 for μ > r)
+};
+cudaError_t launch_map_nu_mma(const MmaNuParams& q, const uint32_t* x, const uint32_t* y, uint64_t* om,
+                              uint64_t count, cudaStream_t st);
+
 // Shared-memory bytes the tile kernel needs for these parameters.
 size_t tile_smem_bytes(const TileParams& p);
 // Sets the shared-memory attribute of the kernel variant `p` selects and returns its
