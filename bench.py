@@ -209,9 +209,18 @@ def main():
     import paper_2201_00613_b200 as pkg
     from paper_2201_00613_b200.sharded import ShardedSqueeze
 
+    # SQZ_DIST_BACKEND=gloo with SQZ_SHARE_GPU=1 runs every rank on cuda:0 with host-staged
+    # collectives: a single-GPU check of the multi-rank path (never a reported number)
+    backend = os.environ.get("SQZ_DIST_BACKEND", "nccl")
+    if os.environ.get("SQZ_SHARE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
+    red_dev = "cuda" if backend == "nccl" else "cpu"
     f = pkg.builtin_fractal(args.fractal)
     opts = dict(tile_level=args.tile_level, block_threads=args.block_threads, ctas_per_sm=args.ctas_per_sm)
     if world > 1:
@@ -258,7 +267,7 @@ def main():
     kern_ms = [e0.elapsed_time(e1) for e0, e1 in ev_k]
     kern_avg = sum(kern_ms) / K
     if world > 1:
-        t = torch.tensor([ms, kern_avg], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms, kern_avg], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, kern_avg_max = float(t[0]), float(t[1])
     else:
@@ -291,7 +300,7 @@ def main():
         sh.run_host(h, a[:g.state_bytes], b[:g.state_bytes], K)
         e1.record(stream)
         torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e_ms = float(t[0])
         extras["e2e"] = {"value": cells_per_s(g.cells_total, K, e_ms), "unit": "cells/s",

@@ -10,7 +10,9 @@ out-of-shard neighbour states per step (the halo plan, squeeze_halo_needs).  Per
 
 ``HaloExchange`` is the pure plumbing (who sends which Ω to whom, and the per-step
 collective); it works on CPU tensors with gloo as on CUDA tensors with NCCL, so the
-multi-rank logic is tested without GPUs.  ``ShardedSqueeze`` binds it to the library.
+multi-rank logic is tested without GPUs.  Under a gloo group with CUDA buffers (several
+ranks sharing one GPU, the single-GPU test of the multi-rank bench path) the collectives
+run on host copies.  ``ShardedSqueeze`` binds it to the library.
 """
 from __future__ import annotations
 
@@ -33,6 +35,9 @@ class HaloExchange:
 
     def __init__(self, needs: np.ndarray, ranges: list, rank: int, nranks: int, device, group=None):
         self.rank, self.nranks, self.group, self.device = rank, nranks, group, device
+        dev = torch.device(device)
+        # gloo moves CPU tensors only: stage through the host when the buffers live on a GPU
+        self.comm = torch.device("cpu") if dist.get_backend(group) == "gloo" else dev
         needs = np.asarray(needs, dtype=np.int64)
         his = np.array([hi for _, hi in ranges], dtype=np.int64)
         owner = np.searchsorted(his, needs, side="right")
@@ -42,12 +47,12 @@ class HaloExchange:
             raise ValueError("halo plan lists an owned cell")
         # needs are sorted and shards contiguous, so grouping by owner keeps the needs order
         self.recv_counts = [int((owner == p).sum()) for p in range(nranks)]
-        req_counts = torch.tensor(self.recv_counts, dtype=torch.int64, device=device)
-        got_counts = torch.empty(nranks, dtype=torch.int64, device=device)
+        req_counts = torch.tensor(self.recv_counts, dtype=torch.int64, device=self.comm)
+        got_counts = torch.empty(nranks, dtype=torch.int64, device=self.comm)
         dist.all_to_all_single(got_counts, req_counts, group=group)
         self.send_counts = [int(v) for v in got_counts.cpu()]
-        req = torch.from_numpy(needs).to(device)
-        sends = torch.empty(sum(self.send_counts), dtype=torch.int64, device=device)
+        req = torch.from_numpy(needs).to(self.comm)
+        sends = torch.empty(sum(self.send_counts), dtype=torch.int64, device=self.comm)
         dist.all_to_all_single(sends, req, output_split_sizes=self.send_counts,
                                input_split_sizes=self.recv_counts, group=group)
         self.sends = sends.cpu().numpy().astype(np.uint64)
@@ -63,6 +68,12 @@ class HaloExchange:
         if self.nranks == 1:
             return
         n_send = int(self.sends.size)
+        if self.comm != self.send_buf.device:  # gloo with device buffers: host staging
+            recv = torch.empty(self.nneeds, dtype=torch.uint8)
+            dist.all_to_all_single(recv, self.send_buf[:n_send].cpu(), output_split_sizes=self.recv_counts,
+                                   input_split_sizes=self.send_counts, group=self.group)
+            self.recv_buf[:self.nneeds].copy_(recv)
+            return
         dist.all_to_all_single(self.recv_buf[:self.nneeds], self.send_buf[:n_send],
                                output_split_sizes=self.recv_counts, input_split_sizes=self.send_counts,
                                group=self.group)

@@ -1,0 +1,60 @@
+"""Multi-PROCESS sharded run on one GPU: every rank is its own process with its own shard
+context on cuda:0, the halo travels through ``ShardedSqueeze`` / ``HaloExchange`` over a gloo
+group (host-staged; NCCL refuses two ranks on one device).  The union of the shards after
+T steps must equal the unsharded run byte for byte (itself pinned to the oracle).  This is
+the full product path of bench.py's N > 1 leg except the NCCL transport itself."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, name, r, steps, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2201_00613_b200 as pkg
+        from paper_2201_00613_b200.sharded import ShardedSqueeze
+
+        torch.cuda.set_device(0)
+        sh = ShardedSqueeze(pkg.builtin_fractal(name), r, rank, world, 0)
+        a, b = sh.new_state(), sh.new_state()
+        sh.seed(a, 42, 0.5)
+        fin = sh.run(a, b, steps)
+        torch.cuda.synchronize()
+        out[rank] = sh.sq.to_cells(fin).cpu().numpy().copy()
+        assert sh.sq.device_error() == 0
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,r,world,steps", [("sierpinski-triangle", 12, 2, 5), ("sierpinski-triangle", 13, 4, 4),
+                                                ("sierpinski-carpet", 6, 3, 3)])
+def test_multiprocess_shards_equal_unsharded(name, r, world, steps):
+    import paper_2201_00613_b200 as pkg
+
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    mp.start_processes(_worker, args=(world, _free_port(), name, r, steps, out), nprocs=world, join=True,
+                       start_method="spawn")
+    got = np.concatenate([out[p] for p in range(world)])
+    p = pkg.Squeeze(pkg.builtin_fractal(name), r, device=0)
+    a, b = p.new_state(), p.new_state()
+    p.seed(a, 42, 0.5)
+    fin = p.run(a, b, steps)
+    torch.cuda.synchronize()
+    assert np.array_equal(got, p.to_cells(fin).cpu().numpy())
