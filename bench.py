@@ -383,6 +383,7 @@ def main():
             "bytes_per_cell_per_step": p_bytes / gq.cells_total, "state_bytes": gq.packed_bytes,
             "kernel": "sqz::k_step_packed", "avg_launch_ms": p_kern,
             "hbm_achieved_GBps": p_bytes / (p_kern / 1e3) / 1e9, "hbm_frac": p_bytes / (p_kern / 1e3) / 1e9 / peak,
+            "traffic": ncu_traffic(f"{args.fractal}-r{args.level}-g{gq.tile_level}-packed"),
             "note": "1 bit per cell, 128-tile bit-sliced chunks (squeeze_*_packed); algorithmic bytes = state "
                     "read + write; the tile adjacency rows add 4 B x link directions per tile; bit-exact with "
                     "the byte path (tests/test_gpu_packed.py)"}
@@ -418,6 +419,7 @@ def main():
                 "kernel": "sqz::k_heat_step", "avg_launch_ms": h_kern, "bytes_per_cell_per_step": 8,
                 "hbm_achieved_GBps": h_bytes / (h_kern / 1e3) / 1e9,
                 "hbm_frac": h_bytes / (h_kern / 1e3) / 1e9 / peak, "dtype": "f32",
+                "traffic": ncu_traffic(f"{args.fractal}-r{args.heat_level}-heat"),
                 "note": "u' = u + alpha * sum over member Moore neighbours (u_n - u), alpha = 1/8, insulated edge "
                         "(DESIGN.md D16); float32 field, parity vs the float64 oracle within the derived bound "
                         "(tests/test_gpu_heat.py)"}
