@@ -32,7 +32,7 @@ struct PackSmem {
   uint32_t zw;
   uint32_t* A0;   // kAdjSlots x ndirs x 128 adjacency words
   uint32_t* R;    // [4E][32] prefetched words holding out-of-chunk neighbour bits (next chunk)
-  uint32_t* lk;   // [E] link e: j2 << 8 | direction
+  uint32_t* sl;   // [4E] link slot u = 4e + q: j2 << 10 | (direction * 128 + 32 q)
   uint64_t* bar;  // [pstages] state copies landed, then [kAdjSlots] adjacency copies landed
   uint32_t ndirs, ns;
   __device__ __forceinline__ uint32_t* Z(uint32_t s) const { return Z0 + s * zw; }
@@ -55,8 +55,8 @@ __host__ __device__ inline size_t packed_layout(const TileParams& p, uint8_t* ba
   off += (size_t)kAdjSlots * p.ndirs * kPackTiles * 4;
   if (s) s->R = (uint32_t*)(base + off);
   off += (size_t)4 * (prefetch_links(p) ? prefetch_links(p) : 1) * 32 * 4;
-  if (s) s->lk = (uint32_t*)(base + off);
-  off += align16((size_t)(p.E ? p.E : 1) * 4);
+  if (s) s->sl = (uint32_t*)(base + off);
+  off += align16((size_t)(p.E ? 4 * p.E : 1) * 4);
   if (s) s->bar = (uint64_t*)(base + off);
   off += (ns + kAdjSlots) * 8;
   return align16(off);
@@ -120,12 +120,11 @@ __device__ __forceinline__ void chunk_prefetch(const TileParams& p, const PackSm
                                                int nwarps, int lane) {
   const uint32_t E = prefetch_links(p);
   for (uint32_t u = (uint32_t)warp; u < 4 * E; u += (uint32_t)nwarps) {
-    const uint32_t q = u & 3u, e = u >> 2;
-    const uint32_t lk = S.lk[e];
-    const uint32_t a1 = ntl[(lk & 7u) * kPackTiles + q * 32 + lane];
+    const uint32_t sl = S.sl[u];
+    const uint32_t a1 = ntl[(sl & 1023u) + lane];
     const uint32_t tl = a1 - 1u - (uint32_t)p.tile_lo;
     if (a1 != 0 && a1 - 1u - pc.t0 >= pc.nt)
-      cp_async4(&S.R[u * 32 + lane], cur32 + ((uint64_t)(tl >> 7) * p.Kw + (lk >> 8)) * 4 + ((tl >> 5) & 3u));
+      cp_async4(&S.R[u * 32 + lane], cur32 + ((uint64_t)(tl >> 7) * p.Kw + (sl >> 10)) * 4 + ((tl >> 5) & 3u));
   }
   cp_async_commit();
 }
@@ -185,7 +184,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
   }
 
   for (uint32_t i = tid; i < NS * 4; i += blockDim.x) S.Z(i >> 2)[(Kw + E) * 4 + (i & 3)] = 0;  // zero slot
-  for (uint32_t e = tid; e < E; e += blockDim.x) S.lk[e] = (p.link_j2[e] << 8) | p.link_dir[e];
+  for (uint32_t u = tid; u < 4 * E; u += blockDim.x)
+    S.sl[u] = (p.link_j2[u >> 2] << 10) | (p.link_dir[u >> 2] * kPackTiles + 32 * (u & 3u));
   if (tid == 0) {
     for (uint32_t s = 0; s < NS + kAdjSlots; ++s) mbar_init(&S.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -217,20 +217,24 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
     if ((uint32_t)warp < 4 * E) {
       mbar_wait(S.abar(a), (it / kAdjSlots) & 1);  // (already complete when the prefetch ran)
       cp_async_wait_all();
-      const uint32_t rs = smem_u32(S.R);
+      const uint32_t rs = smem_u32(S.R) + lane * 4;
+      const uint32_t ntl_s = smem_u32(ntl) + lane * 4;
       for (uint32_t u = (uint32_t)warp; u < 4 * E; u += (uint32_t)nwarps) {
-        const uint32_t q = u & 3u, e = u >> 2;
-        const uint32_t lk = S.lk[e], j2 = lk >> 8;
-        const uint32_t a1 = ntl[(lk & 7u) * kPackTiles + q * 32 + lane];
+        const uint32_t sl = S.sl[u], j2 = sl >> 10;
+        const uint32_t a1 = lds32(ntl_s + (sl & 1023u) * 4);
         const uint32_t rel = a1 - 1u - pc.t0, tl = a1 - 1u - (uint32_t)p.tile_lo;
-        uint32_t v = 0;
-        if (rel < pc.nt) v = lds32(zs + (j2 * 4 + (rel >> 5)) * 4) >> (rel & 31);
-        else if (a1 != 0)
-          v = (e < Epf ? lds32(rs + (u * 32 + lane) * 4)
-                       : __ldg(cur32 + ((uint64_t)(tl >> 7) * Kw + j2) * 4 + ((tl >> 5) & 3u))) >>
-              (tl & 31);
+        uint32_t v;
+        if (Epf) {  // branch-free: the word from this chunk's stage, or the prefetched one
+          const bool in = rel < pc.nt;
+          v = lds32(in ? zs + (j2 * 4 + (rel >> 5)) * 4 : rs + u * 128) >> ((in ? rel : tl) & 31u);
+          v &= a1 != 0 ? 1u : 0u;
+        } else {  // more links than the prefetch holds: synchronous gathers
+          v = rel < pc.nt ? lds32(zs + (j2 * 4 + (rel >> 5)) * 4) >> (rel & 31u)
+              : a1 != 0   ? __ldg(cur32 + ((uint64_t)(tl >> 7) * Kw + j2) * 4 + ((tl >> 5) & 3u)) >> (tl & 31u)
+                          : 0u;
+        }
         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v & 1u);
-        if (lane == 0) Z[(Kw + e) * 4 + q] = bal;
+        if (lane == 0) Z[(Kw + (u >> 2)) * 4 + (u & 3u)] = bal;
       }
     }
     __syncthreads();  // the one CTA barrier per chunk: state + link words in place, chunk it-1 done
