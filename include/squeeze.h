@@ -110,7 +110,7 @@ typedef struct {
   uint32_t chunk_words;  /* Kw: 128-bit words per chunk in the packed layout (K rounded up to 4) */
   uint32_t packed_tiles; /* tiles per chunk of the packed layout (128) */
   uint64_t heat_bytes;   /* bytes of a HEAT field buffer (squeeze_heat_*) */
-  uint32_t heat_tile_floats; /* Kf: floats per tile in a heat buffer (K rounded up to 4) */
+  uint32_t heat_chunk_tiles; /* tiles per chunk of the heat layout (4: one float4 word per cell) */
   uint32_t heat_pairs;   /* remote (own cell, neighbour) pairs per tile of the heat kernel */
 } squeeze_geometry_t;
 
@@ -227,8 +227,10 @@ squeeze_status squeeze_count_alive_packed(const void* ctx, const uint32_t* d_pac
  * on accessing neighboring cells".  One explicit step of the graph heat equation (D16):
  *     u'(Ω) = u(Ω) + α Σ_{n ∈ N(Ω)} (u(n) − u(Ω)),  N(Ω) = member Moore neighbours,
  * i.e. an insulated boundary; α·max_degree <= 1 keeps it a convex combination (stable).
- * Layout: float32, tile-padded: local tile t at float offset t x heat_tile_floats, padding 0;
- * heat_bytes per buffer; 16-byte aligned caller-owned device memory.  Unsharded contexts only
+ * Layout: float32 in chunks of heat_chunk_tiles = 4 consecutive tiles; chunk c holds K float4
+ * words, word j = cell j of tiles 4c..4c+3, i.e. the float at index (c x K + j) x 4 + (t mod 4)
+ * for local tile t (lanes of tiles past the shard end are 0); heat_bytes per buffer; 16-byte
+ * aligned caller-owned device memory.  Unsharded contexts only
  * (SQZ_E_CONFIG otherwise); d_cur and d_next must not alias. */
 /* Initial field: u(Ω) = (mix(((X<<32)|Y) ^ mix(seed)) >> 40) x 2^-24 at (X, Y) = λ(Ω). */
 squeeze_status squeeze_heat_seed(const void* ctx, float* d_u, uint64_t seed, squeeze_stream_t stream);

@@ -270,7 +270,7 @@ class Squeeze:
 
     # ------------------------------------------------------------------ heat diffusion (NEXT-4)
     def new_heat(self):
-        """A float32 field buffer in the tile-padded heat layout (include/squeeze.h)."""
+        """A float32 field buffer in the 4-tile-chunk heat layout (include/squeeze.h)."""
         import torch
         return torch.zeros(max(4, self.geometry.heat_bytes // 4), dtype=torch.float32, device=f"cuda:{self.device}")
 
@@ -296,8 +296,9 @@ class Squeeze:
     def heat_to_cells(self, u):
         """Ω-ordered float32 values of this shard from a heat buffer (host-side decode)."""
         g = self.geometry
-        kf = g.heat_tile_floats
-        return u[:g.local_tiles * kf].reshape(g.local_tiles, kf)[:, :g.tile_cells].reshape(-1)
+        nch = (g.local_tiles + 3) // 4
+        w = u[:nch * g.tile_cells * 4].reshape(nch, g.tile_cells, 4).transpose(1, 2)  # [chunk, lane, j]
+        return w.reshape(nch * 4, g.tile_cells)[:g.local_tiles].reshape(-1)
 
     # ------------------------------------------------------------------ paper comparison engines (NEXT-2)
     def lambda_engine_step(self, cur_grid, next_grid, stream=None):

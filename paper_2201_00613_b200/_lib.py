@@ -49,7 +49,7 @@ class GeometryC(ctypes.Structure):
                 ("tile_cells", ctypes.c_uint64), ("num_tiles", ctypes.c_uint64), ("chunk_tiles", ctypes.c_uint32),
                 ("remote_links", ctypes.c_uint32), ("max_degree", ctypes.c_uint32), ("tile_bytes", ctypes.c_uint32),
                 ("packed_bytes", ctypes.c_uint64), ("chunk_words", ctypes.c_uint32), ("packed_tiles", ctypes.c_uint32),
-                ("heat_bytes", ctypes.c_uint64), ("heat_tile_floats", ctypes.c_uint32), ("heat_pairs", ctypes.c_uint32)]
+                ("heat_bytes", ctypes.c_uint64), ("heat_chunk_tiles", ctypes.c_uint32), ("heat_pairs", ctypes.c_uint32)]
 
 
 vp = ctypes.c_void_p
@@ -152,7 +152,7 @@ class Geometry:
     chunk_words: int
     packed_tiles: int
     heat_bytes: int
-    heat_tile_floats: int
+    heat_chunk_tiles: int
     heat_pairs: int
 
     @property

@@ -62,7 +62,7 @@ struct Ctx {
   int packed_grid = 0;
   size_t packed_smem = 0;
   // heat workload (NEXT-4): neighbour slots, remote pairs, launch shape
-  uint32_t Kf = 4, heat_P = 0, heat_stages = 3;
+  uint32_t heat_P = 0, heat_stages = 3;
   uint64_t heat_bytes = 0;
   int heat_grid = 0;
   uint16_t* d_heat_nbr = nullptr;
@@ -223,7 +223,7 @@ TileParams tile_params(const Ctx* c) {
 
 HeatParams heat_params(const Ctx* c, float alpha) {
   HeatParams h{};
-  h.Kf = c->Kf;
+  h.K = (uint32_t)c->tt.K;
   h.P = c->heat_P;
   h.stages = c->heat_stages;
   h.alpha = alpha;
@@ -382,8 +382,7 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
     c->state_bytes = (c->sr.tile_hi - c->sr.tile_lo) * c->Kp;
     c->Kw = (uint32_t)((c->tt.K + 3) & ~3ull);
     c->packed_bytes = ((c->sr.tile_hi - c->sr.tile_lo + kPackTiles - 1) / kPackTiles) * c->Kw * 16;
-    c->Kf = (uint32_t)((c->tt.K + 3) & ~3ull);
-    c->heat_bytes = (c->sr.tile_hi - c->sr.tile_lo) * c->Kf * 4;
+    c->heat_bytes = ((c->sr.tile_hi - c->sr.tile_lo + 3) / 4) * c->tt.K * 16;  // 4-tile float4 chunks
     if (c->nranks > 1) {
       unsigned th = std::max(1u, std::thread::hardware_concurrency());
       halo_needs(c->tt, c->coarse.view, c->sr, c->needs, th);
@@ -463,7 +462,7 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
         if ((st = upload(&c->d_mma_h, hh.data(), hh.size())) != SQZ_OK) return fail(st);
         if ((st = upload(&c->d_mma_B, B.data(), B.size())) != SQZ_OK) return fail(st);
       }
-      // heat workload: slots = byte offsets into a tile's [Kf state | P pairs] shared slot; an
+      // heat workload: slots = float4 words of a chunk's [K state | P pairs] shared slot; an
       // absent neighbour is the cell itself, a remote neighbour a per-(cell, link) pair
       {
         std::vector<uint16_t> hn(c->tt.nbr.size());
@@ -476,12 +475,12 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
             else if (v == c->tt.zero_slot) slot = j;
             else {
               const uint32_t e = v - (uint32_t)c->tt.K;
-              slot = c->Kf + hp.size();
+              slot = c->tt.K + hp.size();
               hp.push_back((uint32_t)j | ((uint32_t)c->tt.link_dir[e] << 16));
               hj2.push_back(c->tt.link_j2[e]);
             }
-            if (slot * 4 > 0xFFFFu) return fail(SQZ_E_INVALID_LEVEL);
-            hn[j * 8 + k] = (uint16_t)(slot * 4);
+            if (slot > 0xFFFFu) return fail(SQZ_E_INVALID_LEVEL);
+            hn[j * 8 + k] = (uint16_t)slot;
           }
         c->heat_P = (uint32_t)hp.size();
         if ((st = upload(&c->d_heat_nbr, hn.data(), hn.size())) != SQZ_OK) return fail(st);
@@ -545,7 +544,7 @@ squeeze_status squeeze_geometry(const void* ctx, squeeze_geometry_t* out) {
   out->chunk_words = c->Kw;
   out->packed_tiles = kPackTiles;
   out->heat_bytes = c->heat_bytes;
-  out->heat_tile_floats = c->Kf;
+  out->heat_chunk_tiles = 4;
   out->heat_pairs = c->heat_P;
   return SQZ_OK;
 }
@@ -859,7 +858,7 @@ squeeze_status squeeze_heat_seed(const void* ctx, float* d_u, uint64_t seed, squ
   if (st != SQZ_OK) return st;
   if (c->nranks > 1) return SQZ_E_CONFIG;
   DevGuard g(c->device);
-  return cu(launch_heat_seed(c->d_full.view, tile_params(c), c->Kf, d_u, seed, (cudaStream_t)stream));
+  return cu(launch_heat_seed(c->d_full.view, tile_params(c), d_u, seed, (cudaStream_t)stream));
 }
 
 squeeze_status squeeze_heat_step(void* ctx, const float* d_cur, float* d_next, float alpha, squeeze_stream_t stream) {

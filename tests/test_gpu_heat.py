@@ -67,7 +67,9 @@ def test_heat_padding_stays_zero_and_run_matches_steps():
         c, d = d, c
     torch.cuda.synchronize()
     assert torch.equal(fin, c)
-    pad = fin[:g.local_tiles * g.heat_tile_floats].reshape(g.local_tiles, -1)[:, g.tile_cells:]
+    nch = (g.local_tiles + 3) // 4
+    lanes = fin[:nch * g.tile_cells * 4].reshape(nch, g.tile_cells, 4)
+    pad = lanes[-1, :, g.local_tiles - 4 * (nch - 1):]  # lanes of tiles past the shard end
     assert torch.count_nonzero(pad).item() == 0
 
 
@@ -115,11 +117,10 @@ def test_heat_full_size_sampled():
     torch.cuda.synchronize()
     om = np.unique(sqz_inputs.random_indices(200_000, 3 ** r, seed=5).astype(np.int64))
     om = np.concatenate([om, [0, 1, 2, 3 ** r - 1]]).astype(np.int64)
-    kf = g.heat_tile_floats
 
     def fetch(buf, q):
         t = q // g.tile_cells
-        idx = torch.from_numpy(t * kf + (q - t * g.tile_cells)).cuda()
+        idx = torch.from_numpy(((t // 4) * g.tile_cells + (q - t * g.tile_cells)) * 4 + t % 4).cuda()
         return buf[idx].double().cpu().numpy()
 
     assert np.array_equal(fetch(a, om), heat.seed_heat_at(SIERPINSKI, r, om, 42))
