@@ -276,10 +276,16 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
           x3[k] = v.w;
         }
         const uint4 al = lds128(zs + j * 16);
-        nw.x = cell_rule<DMAX, CONWAY>(x0, al.x, p.birth, p.survive) & lm.x;
-        nw.y = cell_rule<DMAX, CONWAY>(x1, al.y, p.birth, p.survive) & lm.y;
-        nw.z = cell_rule<DMAX, CONWAY>(x2, al.z, p.birth, p.survive) & lm.z;
-        nw.w = cell_rule<DMAX, CONWAY>(x3, al.w, p.birth, p.survive) & lm.w;
+        nw.x = cell_rule<DMAX, CONWAY>(x0, al.x, p.birth, p.survive);
+        nw.y = cell_rule<DMAX, CONWAY>(x1, al.y, p.birth, p.survive);
+        nw.z = cell_rule<DMAX, CONWAY>(x2, al.z, p.birth, p.survive);
+        nw.w = cell_rule<DMAX, CONWAY>(x3, al.w, p.birth, p.survive);
+        if (pc.nt < kPackTiles) {  // the shard's last chunk only
+          nw.x &= lm.x;
+          nw.y &= lm.y;
+          nw.z &= lm.z;
+          nw.w &= lm.w;
+        }
       }
       outc[j] = nw;  // padding words K..Kw-1 are written 0
     };
