@@ -434,11 +434,10 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
       c->tile_grid = sms * std::max(1, occ);
       p.Kw = c->Kw;
-      // packed step: 8 warps while a chunk's words fit the registers of 3 blocks per warp, else
-      // 16; 3 pipeline stages if two CTAs still fit an SM, else 2
-      c->packed_threads = ((c->Kw + 31) / 32 <= 24) ? 256 : 512;
-      if (const char* e = getenv("SQZ_PACKED_THREADS")) c->packed_threads = atoi(e);  // tuning experiments
-      if (c->packed_threads < 64 || c->packed_threads > 512 || c->packed_threads % 32) return fail(SQZ_E_CONFIG);
+      // packed step: 8 warps (tools/packed_timing.py: 8 warps with every block's slots in
+      // registers beat 16 warps at 64 registers); 4 stages if three CTAs fit an SM, else 3 if
+      // two do, else 2
+      c->packed_threads = 256;
       // stages: 4 if three CTAs still fit an SM, else 3 if two do, else 2
       p.pstages = 4;
       if (3 * packed_smem_bytes(p) > 220 * 1024) p.pstages = 3;

@@ -417,15 +417,14 @@ static PackedFn pick_packed(const TileParams& p, int threads) {
   const bool conway = (p.birth == (1u << 3)) && (p.survive == ((1u << 2) | (1u << 3)));
   const uint32_t nblk = (uint32_t)((p.Kw + 31) / 32), W = (uint32_t)threads / 32;
   const uint32_t rb = (nblk + W - 1) / W;
-  if (threads <= 256) {
-    if (p.dmax <= 5) return conway ? k_step_packed<5, true, 3, 256, 3> : k_step_packed<5, false, 3, 256, 3>;
-    return conway ? k_step_packed<8, true, 2, 256, 3> : k_step_packed<8, false, 2, 256, 3>;
-  }
+  // small tiles: 3 blocks per warp, 3 CTAs per SM; large tiles (level 7 Sierpinski: 69 blocks):
+  // all 9 blocks' slots in registers (108 registers), 2 CTAs per SM (tools/packed_timing.py)
   if (p.dmax <= 5) {
-    if (rb <= 3) return conway ? k_step_packed<5, true, 3, 512, 1> : k_step_packed<5, false, 3, 512, 1>;
-    return conway ? k_step_packed<5, true, 5, 512, 2> : k_step_packed<5, false, 5, 512, 2>;
+    if (rb <= 3) return conway ? k_step_packed<5, true, 3, 256, 3> : k_step_packed<5, false, 3, 256, 3>;
+    return conway ? k_step_packed<5, true, 9, 256, 2> : k_step_packed<5, false, 9, 256, 2>;
   }
-  return conway ? k_step_packed<8, true, 3, 512, 1> : k_step_packed<8, false, 3, 512, 1>;
+  if (rb <= 2) return conway ? k_step_packed<8, true, 2, 256, 3> : k_step_packed<8, false, 2, 256, 3>;
+  return conway ? k_step_packed<8, true, 6, 256, 2> : k_step_packed<8, false, 6, 256, 2>;
 }
 
 cudaError_t packed_prepare(const TileParams& p, size_t smem, int threads, int* occupancy) {
