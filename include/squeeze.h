@@ -208,9 +208,13 @@ squeeze_status squeeze_halo_pack(const void* ctx, const uint8_t* d_cur, squeeze_
  * word j, bit i = cell j of tile 128c + 32q + i of the shard, i.e. the u32 at index
  * (c x Kw + j) x 4 + q (j < K; padding words and bits of tiles past the shard end are zero).
  * It is the form the step computes on, so a packed step moves 0.25 B per cell instead of 2 B.
- * Unsharded contexts only (SQZ_E_CONFIG otherwise).  Buffers: 16-byte aligned device memory. */
+ * Sharded contexts: squeeze_step_packed reads out-of-shard neighbours from the bound halo receive
+ * buffer (fill it as for squeeze_step, packing with squeeze_halo_pack_packed); squeeze_run_packed
+ * is unsharded only (SQZ_E_CONFIG otherwise).  Buffers: 16-byte aligned device memory. */
 squeeze_status squeeze_pack(const void* ctx, const uint8_t* d_state, uint32_t* d_packed, squeeze_stream_t stream);
 squeeze_status squeeze_unpack(const void* ctx, const uint32_t* d_packed, uint8_t* d_state, squeeze_stream_t stream);
+/* d_send[i] = state of cell sends[i] in a packed buffer (the packed twin of squeeze_halo_pack). */
+squeeze_status squeeze_halo_pack_packed(const void* ctx, const uint32_t* d_cur, squeeze_stream_t stream);
 /* D9 initial state written directly in the packed layout (same cells as squeeze_seed). */
 squeeze_status squeeze_seed_packed(const void* ctx, uint32_t* d_packed, uint64_t seed, uint64_t q,
                                    squeeze_stream_t stream);

@@ -231,6 +231,10 @@ class Squeeze:
         import torch
         return torch.empty(max(16, self.geometry.packed_bytes) // 4, dtype=torch.int32, device=f"cuda:{self.device}")
 
+    def halo_pack_packed(self, cur, stream=None) -> None:
+        _lib.check(self.lib.squeeze_halo_pack_packed(self.ctx, _ptr(cur), _stream(stream, cur.device)),
+                   "halo_pack_packed")
+
     def pack(self, state, packed, stream=None):
         _lib.check(self.lib.squeeze_pack(self.ctx, _ptr(state), _ptr(packed), _stream(stream, state.device)), "pack")
 

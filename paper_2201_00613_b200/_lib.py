@@ -11,7 +11,7 @@ import os
 from dataclasses import dataclass
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsqueeze.so")
+LIB_PATH = os.environ.get("SQZ_LIB", os.path.join(HERE, "libsqueeze.so"))  # SQZ_LIB: A/B builds (tools/)
 
 u8p = ctypes.POINTER(ctypes.c_uint8)
 u32p = ctypes.POINTER(ctypes.c_uint32)
@@ -81,6 +81,7 @@ SIGNATURES = {
     "squeeze_halo_set_sends": ([vp, u64p, ctypes.c_uint64], st),
     "squeeze_halo_bind": ([vp, vp, vp], st),
     "squeeze_halo_pack": ([vp, vp, vp], st),
+    "squeeze_halo_pack_packed": ([vp, vp, vp], st),
     "squeeze_pack": ([vp, vp, vp, vp], st),
     "squeeze_unpack": ([vp, vp, vp, vp], st),
     "squeeze_seed_packed": ([vp, vp, ctypes.c_uint64, ctypes.c_uint64, vp], st),
@@ -112,6 +113,8 @@ def load() -> ctypes.CDLL:
             raise SqueezeError(-7, f"{LIB_PATH} missing — run __graft_entry__.build()")
         lib = ctypes.CDLL(LIB_PATH)
         for name, (args, res) in SIGNATURES.items():
+            if "SQZ_LIB" in os.environ and not hasattr(lib, name):
+                continue  # an older A/B build may predate a symbol
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = res

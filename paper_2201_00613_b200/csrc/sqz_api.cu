@@ -49,6 +49,7 @@ struct Ctx {
   uint64_t state_bytes = 0;
   uint32_t Kp = 16;  // bytes per tile in a state buffer (tile-padded layout)
   std::vector<uint64_t> needs, sends, send_offsets;
+  std::vector<uint64_t> send_bits;  // packed layout: u32 index << 5 | bit of each send cell
   // device
   int device = -1;
   DeviceLUTs d_full, d_coarse;
@@ -75,6 +76,7 @@ struct Ctx {
   uint16_t* d_dir_start = nullptr;
   uint64_t* d_needs = nullptr;
   uint64_t* d_sends = nullptr;
+  uint64_t* d_send_bits = nullptr;
   int* d_err = nullptr;
   uint8_t* d_send = nullptr;
   const uint8_t* d_recv = nullptr;
@@ -152,6 +154,7 @@ void free_device(Ctx* c) {
   cudaFree(c->d_link_dir);
   cudaFree(c->d_dir_start);
   cudaFree(c->d_needs);
+  cudaFree(c->d_send_bits);
   cudaFree(c->d_sends);
   cudaFree(c->d_err);
 }
@@ -248,7 +251,7 @@ squeeze_status do_step(Ctx* c, const uint8_t* cur, uint8_t* next, cudaStream_t s
 }
 
 squeeze_status do_step_packed(Ctx* c, const uint32_t* cur, uint32_t* next, cudaStream_t st) {
-  if (c->nranks > 1) return SQZ_E_CONFIG;
+  if (c->nranks > 1 && !c->needs.empty() && c->d_recv == nullptr) return SQZ_E_CONFIG;
   if (c->NT >= 0xFFFFFFFFull) return SQZ_E_OVERFLOW;
   TileParams p = tile_params(c);
   p.nbr = c->d_nbr_packed;
@@ -749,15 +752,21 @@ squeeze_status squeeze_halo_set_sends(void* ctx, const uint64_t* omegas, uint64_
       if (omegas[i] < c->sr.omega_lo || omegas[i] >= c->sr.omega_hi) return SQZ_E_CONFIG;
     c->sends.assign(omegas, omegas + count);
     c->send_offsets.resize(count);
-    for (uint64_t i = 0; i < count; ++i) {  // tile-padded byte offsets of the cells to send
-      const uint64_t t = omegas[i] / c->tt.K;
-      c->send_offsets[i] = (t - c->sr.tile_lo) * c->Kp + (omegas[i] - t * c->tt.K);
+    c->send_bits.resize(count);
+    for (uint64_t i = 0; i < count; ++i) {  // tile-padded byte offsets / packed bits of the cells to send
+      const uint64_t t = omegas[i] / c->tt.K, j = omegas[i] - t * c->tt.K, tl = t - c->sr.tile_lo;
+      c->send_offsets[i] = tl * c->Kp + j;
+      c->send_bits[i] = ((((tl / kPackTiles) * c->Kw + j) * 4 + (tl / 32) % 4) << 5) | (tl % 32);
     }
     if (c->device >= 0) {
       DevGuard g(c->device);
       cudaFree(c->d_sends);
+      cudaFree(c->d_send_bits);
       c->d_sends = nullptr;
-      return upload(&c->d_sends, c->send_offsets.data(), c->send_offsets.size());
+      c->d_send_bits = nullptr;
+      squeeze_status st = upload(&c->d_sends, c->send_offsets.data(), c->send_offsets.size());
+      if (st == SQZ_OK) st = upload(&c->d_send_bits, c->send_bits.data(), c->send_bits.size());
+      return st;
     }
     return SQZ_OK;
   });
@@ -781,6 +790,16 @@ squeeze_status squeeze_halo_pack(const void* ctx, const uint8_t* d_cur, squeeze_
   if (!c->sends.empty() && !c->d_send) return SQZ_E_CONFIG;
   DevGuard g(c->device);
   return cu(launch_halo_pack(d_cur, c->d_sends, c->sends.size(), c->d_send, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_halo_pack_packed(const void* ctx, const uint32_t* d_cur, squeeze_stream_t stream) {
+  if (!ctx) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_cur);
+  if (st != SQZ_OK) return st;
+  if (!c->sends.empty() && !c->d_send) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return cu(launch_halo_pack_packed(d_cur, c->d_send_bits, c->sends.size(), c->d_send, (cudaStream_t)stream));
 }
 
 squeeze_status squeeze_pack(const void* ctx, const uint8_t* d_state, uint32_t* d_packed, squeeze_stream_t stream) {
@@ -831,7 +850,7 @@ squeeze_status squeeze_run_packed(void* ctx, uint32_t* d_a, uint32_t* d_b, uint6
   squeeze_status st = check_state(c, d_a);
   if (st == SQZ_OK) st = check_state(c, d_b);
   if (st != SQZ_OK) return st;
-  if (d_a == d_b) return SQZ_E_CONFIG;
+  if (d_a == d_b || c->nranks > 1) return SQZ_E_CONFIG;  // sharded: step + halo exchange per step
   DevGuard g(c->device);
   for (uint64_t i = 0; i < steps; ++i) {
     st = (i & 1) ? do_step_packed(c, d_b, d_a, (cudaStream_t)stream) : do_step_packed(c, d_a, d_b, (cudaStream_t)stream);

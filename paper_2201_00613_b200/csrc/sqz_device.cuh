@@ -30,4 +30,18 @@ __device__ __forceinline__ uint32_t fetch_cell(const uint8_t* __restrict__ cur, 
   return 0;
 }
 
+// State of an out-of-shard Ω from the halo receive buffer (binary search over the sorted
+// needs list); a miss sets the error flag and reads as dead.
+__device__ __forceinline__ uint32_t halo_fetch(const HaloView& h, uint64_t om) {
+  uint64_t lo = 0, hi = h.nneeds;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (h.needs[mid] < om) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < h.nneeds && h.needs[lo] == om && h.recv != nullptr) return h.recv[lo];
+  if (h.err) atomicExch(h.err, 1);
+  return 0;
+}
+
 }  // namespace sqz

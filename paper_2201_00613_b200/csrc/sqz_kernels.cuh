@@ -98,6 +98,8 @@ cudaError_t launch_step_naive(const LevelMaps& m, const uint8_t* cur, uint8_t* n
 cudaError_t launch_step_tile(const TileParams& p, const uint8_t* cur, uint8_t* next, int grid, int threads,
                              size_t smem, cudaStream_t st);
 cudaError_t launch_count_alive(const uint8_t* state, uint64_t bytes, uint64_t* out, cudaStream_t st);
+cudaError_t launch_halo_pack_packed(const uint32_t* cur, const uint64_t* send_bits, uint64_t nsends, uint8_t* out,
+                                   cudaStream_t st);
 cudaError_t launch_halo_pack(const uint8_t* cur, const uint64_t* send_offsets, uint64_t nsends, uint8_t* out,
                              cudaStream_t st);
 cudaError_t launch_bb_seed(const LevelMaps& m, uint8_t* grid, uint64_t seed, uint64_t q, cudaStream_t st);

@@ -115,6 +115,7 @@ __device__ __forceinline__ void adj_load(const TileParams& p, const PackSmem& S,
 // program order suffices).  For a link whose neighbour tile is outside the chunk: a 4-byte
 // cp.async of the packed word holding the neighbour bit.  `ntl` = the chunk's adjacency words
 // (neighbour tile + 1, from the coarse λ + ν at init: P:189 at tile level).  Commits one group.
+template <bool SHARDED>
 __device__ __forceinline__ void chunk_prefetch(const TileParams& p, const PackSmem& S, const PackChunk& pc,
                                                const uint32_t* ntl, const uint32_t* __restrict__ cur32, int warp,
                                                int nwarps, int lane) {
@@ -123,8 +124,12 @@ __device__ __forceinline__ void chunk_prefetch(const TileParams& p, const PackSm
     const uint32_t sl = S.sl[u];
     const uint32_t a1 = ntl[(sl & 1023u) + lane];
     const uint32_t tl = a1 - 1u - (uint32_t)p.tile_lo;
-    if (a1 != 0 && a1 - 1u - pc.t0 >= pc.nt)
-      cp_async4(&S.R[u * 32 + lane], cur32 + ((uint64_t)(tl >> 7) * p.Kw + (sl >> 10)) * 4 + ((tl >> 5) & 3u));
+    if (a1 != 0 && a1 - 1u - pc.t0 >= pc.nt) {
+      if (!SHARDED || tl < (uint32_t)(p.tile_hi - p.tile_lo))
+        cp_async4(&S.R[u * 32 + lane], cur32 + ((uint64_t)(tl >> 7) * p.Kw + (sl >> 10)) * 4 + ((tl >> 5) & 3u));
+      else  // another shard's tile (sharded contexts): the bit from the halo, placed where the link reads it
+        S.R[u * 32 + lane] = halo_fetch(p.halo, (uint64_t)(a1 - 1u) * p.K + (sl >> 10)) << (tl & 31u);
+    }
   }
   cp_async_commit();
 }
@@ -160,7 +165,7 @@ __device__ __forceinline__ uint32_t cell_rule(const uint32_t* x, uint32_t alive,
 // DMAX: neighbour slots per cell (5 for the Sierpinski triangle, else 8).  RB: j-blocks per warp
 // whose neighbour slots stay in registers for the whole launch (block jb = warp + i * W); later
 // blocks read their slots through L1.
-template <int DMAX, bool CONWAY, int RB, int MAXT, int MINB>
+template <int DMAX, bool CONWAY, int RB, int MAXT, int MINB, bool SHARDED>
 __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const uint4* __restrict__ cur,
                                                         uint4* __restrict__ next) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -172,6 +177,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
   const uint64_t nch = pack_chunks(p);
   const bool issuer = warp == nwarps - 1 && lane == 0;
   const uint32_t* cur32 = reinterpret_cast<const uint32_t*>(cur);
+  const uint32_t nloc = (uint32_t)(p.tile_hi - p.tile_lo);  // local tiles
 
   uint32_t off[RB][DMAX];  // byte offsets of this lane's neighbour words in a stage (slot x 16)
 #pragma unroll
@@ -200,7 +206,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
     for (uint32_t a = 0; a + 1 < kAdjSlots && c + a * G < nch; ++a) adj_load(p, S, pack_chunk(p, c + a * G), a);
   }
   mbar_wait(S.abar(0), 0);
-  chunk_prefetch(p, S, pack_chunk(p, c), S.ntl(0), cur32, warp, nwarps, lane);
+  chunk_prefetch<SHARDED>(p, S, pack_chunk(p, c), S.ntl(0), cur32, warp, nwarps, lane);
 
   uint32_t it = 0, s = 0, sphase = 0;  // sphase bit s: parity of state stage s's next completion
   for (; c < nch; c += G, ++it, s = (s + 1 == NS) ? 0 : s + 1) {
@@ -229,9 +235,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
           v = lds32(in ? zs + (j2 * 4 + (rel >> 5)) * 4 : rs + u * 128) >> ((in ? rel : tl) & 31u);
           v &= a1 != 0 ? 1u : 0u;
         } else {  // more links than the prefetch holds: synchronous gathers
-          v = rel < pc.nt ? lds32(zs + (j2 * 4 + (rel >> 5)) * 4) >> (rel & 31u)
-              : a1 != 0   ? __ldg(cur32 + ((uint64_t)(tl >> 7) * Kw + j2) * 4 + ((tl >> 5) & 3u)) >> (tl & 31u)
-                          : 0u;
+          v = rel < pc.nt         ? lds32(zs + (j2 * 4 + (rel >> 5)) * 4) >> (rel & 31u)
+              : a1 == 0             ? 0u
+              : !SHARDED || tl < nloc ? __ldg(cur32 + ((uint64_t)(tl >> 7) * Kw + j2) * 4 + ((tl >> 5) & 3u)) >> (tl & 31u)
+                                    : halo_fetch(p.halo, (uint64_t)(a1 - 1u) * K + j2);  // another shard's tile
         }
         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v & 1u);
         if (lane == 0) Z[(Kw + (u >> 2)) * 4 + (u & 3u)] = bal;
@@ -249,7 +256,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
     if (c + G < nch) {  // out-of-chunk link gathers of the next chunk (its adjacency was issued long ago)
       const uint32_t a1 = (it + 1) & (kAdjSlots - 1);
       if ((uint32_t)warp < 4 * Epf) mbar_wait(S.abar(a1), ((it + 1) / kAdjSlots) & 1);
-      chunk_prefetch(p, S, pack_chunk(p, c + G), S.ntl(a1), cur32, warp, nwarps, lane);
+      chunk_prefetch<SHARDED>(p, S, pack_chunk(p, c + G), S.ntl(a1), cur32, warp, nwarps, lane);
     }
 
     // count + rule: lane = word j (128 cells), straight to HBM
@@ -409,30 +416,47 @@ __global__ void k_count_packed(const uint32_t* __restrict__ w, uint64_t n, unsig
   }
 }
 
+// send[i] = state bit i of the packed state (sharded contexts: the halo this shard sends).
+__global__ void k_halo_pack_packed(const uint32_t* __restrict__ cur, const uint64_t* __restrict__ bits, uint64_t n,
+                                   uint8_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = bits[i];
+    out[i] = (uint8_t)((cur[b >> 5] >> (b & 31)) & 1u);
+  }
+}
+
 // ------------------------------------------------------------------------------------ launchers
 using PackedFn = void (*)(TileParams, const uint4*, uint4*);
 
 // RB = j-blocks per warp with register-resident neighbour slots (ceil(nblk / W), capped).
-static PackedFn pick_packed(const TileParams& p, int threads) {
+template <bool SH>
+static PackedFn pick_packed_t(const TileParams& p, int threads) {
   const bool conway = (p.birth == (1u << 3)) && (p.survive == ((1u << 2) | (1u << 3)));
   const uint32_t nblk = (uint32_t)((p.Kw + 31) / 32), W = (uint32_t)threads / 32;
   const uint32_t rb = (nblk + W - 1) / W;
   // small tiles: 3 blocks per warp, 3 CTAs per SM; large tiles (level 7 Sierpinski: 69 blocks):
   // all 9 blocks' slots in registers (108 registers), 2 CTAs per SM (tools/packed_timing.py)
   if (p.dmax <= 5) {
-    if (rb <= 3) return conway ? k_step_packed<5, true, 3, 256, 3> : k_step_packed<5, false, 3, 256, 3>;
-    return conway ? k_step_packed<5, true, 9, 256, 2> : k_step_packed<5, false, 9, 256, 2>;
+    if (rb <= 3) return conway ? k_step_packed<5, true, 3, 256, 3, SH> : k_step_packed<5, false, 3, 256, 3, SH>;
+    return conway ? k_step_packed<5, true, 9, 256, 2, SH> : k_step_packed<5, false, 9, 256, 2, SH>;
   }
-  if (rb <= 2) return conway ? k_step_packed<8, true, 2, 256, 3> : k_step_packed<8, false, 2, 256, 3>;
-  return conway ? k_step_packed<8, true, 6, 256, 2> : k_step_packed<8, false, 6, 256, 2>;
+  if (rb <= 2) return conway ? k_step_packed<8, true, 2, 256, 3, SH> : k_step_packed<8, false, 2, 256, 3, SH>;
+  return conway ? k_step_packed<8, true, 6, 256, 2, SH> : k_step_packed<8, false, 6, 256, 2, SH>;
+}
+
+// SHARDED variants also read another shard's cells from the halo receive buffer.
+static PackedFn pick_packed(const TileParams& p, int threads) {
+  return p.halo.nneeds != 0 ? pick_packed_t<true>(p, threads) : pick_packed_t<false>(p, threads);
 }
 
 cudaError_t packed_prepare(const TileParams& p, size_t smem, int threads, int* occupancy) {
-  PackedFn fn = pick_packed(p, threads);
-  cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  for (PackedFn fn : {pick_packed_t<false>(p, threads), pick_packed_t<true>(p, threads)}) {
+    e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   int blocks = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, threads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick_packed_t<false>(p, threads), threads, smem);
   if (e != cudaSuccess) return e;
   *occupancy = blocks;
   return blocks > 0 ? cudaSuccess : cudaErrorInvalidConfiguration;
@@ -474,6 +498,15 @@ cudaError_t launch_seed_packed(const TileParams& p, const LevelMaps& full, uint3
   z *= 0x94D049BB133111EBull;
   z ^= z >> 31;
   k_seed_packed<<<warps_grid(pack_chunks(p) * 4 * p.Kw), 256, 0, s>>>(p, full, packed, z, q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_halo_pack_packed(const uint32_t* cur, const uint64_t* send_bits, uint64_t nsends, uint8_t* out,
+                                   cudaStream_t st) {
+  if (nsends == 0) return cudaSuccess;
+  uint64_t blocks = (nsends + 255) / 256;
+  if (blocks > 1024) blocks = 1024;
+  k_halo_pack_packed<<<(unsigned)blocks, 256, 0, st>>>(cur, send_bits, nsends, out);
   return cudaGetLastError();
 }
 

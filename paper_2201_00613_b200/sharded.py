@@ -103,6 +103,24 @@ class ShardedSqueeze:
         self.halo.exchange()
         (self.sq.step_naive if naive else self.sq.step)(cur, nxt)
 
+    # 1-bit-per-cell state (NEXT-1): same halo plan, the packed halo pack and packed step
+    def new_packed(self):
+        return self.sq.new_packed()
+
+    def seed_packed(self, packed, seed=42, density=0.5):
+        self.sq.seed_packed(packed, seed, density)
+
+    def step_packed(self, cur, nxt):
+        self.sq.halo_pack_packed(cur)
+        self.halo.exchange()
+        self.sq.step_packed(cur, nxt)
+
+    def run_packed(self, a, b, steps: int):
+        for i in range(steps):
+            cur, nxt = (a, b) if i % 2 == 0 else (b, a)
+            self.step_packed(cur, nxt)
+        return b if steps % 2 else a
+
     def run(self, a, b, steps: int):
         for i in range(steps):
             cur, nxt = (a, b) if i % 2 == 0 else (b, a)

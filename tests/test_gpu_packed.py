@@ -147,3 +147,72 @@ def test_packed_full_size_sampled_and_histogram():
         pc = mk("sierpinski-triangle", r, rule=(0, 1 << c))
         pc.step_packed(a, b)
         assert int(pc.count_alive_packed(b).item()) == hist.get(c, 0), c
+
+
+# ---------------------------------------------------------------------------- sharded packed state
+def packed_bits(p, buf, omegas):
+    """Bits of global cells ``omegas`` (inside p's shard) read from p's packed buffer."""
+    g = p.geometry
+    om = np.asarray(omegas, dtype=np.int64)
+    tl = om // g.tile_cells - g.omega_lo // g.tile_cells
+    j = om % g.tile_cells
+    widx = torch.from_numpy(((tl // 128) * g.chunk_words + j) * 4 + (tl // 32) % 4).cuda()
+    bit = torch.from_numpy(tl % 32).cuda()
+    return ((buf[widx].to(torch.int64) >> bit) & 1).to(torch.uint8)
+
+
+def run_sharded_packed_local(name, r, nranks, steps, g=0):
+    """Packed shards on one device; the halo (what NCCL moves) gathered from the owners' buffers."""
+    f = sq.builtin_fractal(name)
+    parts = [sq.Squeeze(f, r, rank=i, nranks=nranks, device=0, tile_level=g) for i in range(nranks)]
+    ranges = [p.shard_range(i) for i, p in enumerate(parts)]
+    bufs = []
+    for p in parts:
+        a, b = p.new_packed(), p.new_packed()
+        p.seed_packed(a, 42, 0.5)
+        bufs.append([a, b])
+    needs = [p.halo_needs() for p in parts]
+    recv = [torch.zeros(max(1, len(nd)), dtype=torch.uint8, device="cuda") for nd in needs]
+    for p, rv in zip(parts, recv):
+        p.halo_set_sends(np.zeros(0, np.uint64))
+        p.halo_bind(None, rv)
+    for _ in range(steps):
+        for i, nd in enumerate(needs):
+            for j, (lo, hi) in enumerate(ranges):
+                sel = np.nonzero((nd >= lo) & (nd < hi))[0]
+                if sel.size:
+                    recv[i][torch.from_numpy(sel).cuda()] = packed_bits(parts[j], bufs[j][0], nd[sel])
+        for p, bf in zip(parts, bufs):
+            p.step_packed(bf[0], bf[1])
+        for bf in bufs:
+            bf.reverse()
+    torch.cuda.synchronize()
+    for p in parts:
+        assert p.device_error() == 0
+    return np.concatenate([cells(pp, bf[0]) for pp, bf in zip(parts, bufs)])
+
+
+@pytest.mark.parametrize("name,r,nranks,g", [("sierpinski-triangle", 10, 2, 3), ("sierpinski-triangle", 12, 3, 4),
+                                             ("sierpinski-triangle", 13, 8, 5), ("sierpinski-carpet", 5, 4, 2),
+                                             ("empty-bottles", 6, 5, 2), ("sierpinski-triangle", 14, 2, 7)])
+def test_sharded_packed_equals_oracle(name, r, nranks, g):
+    got = run_sharded_packed_local(name, r, nranks, 5, g)
+    assert np.array_equal(got, oracle_run(name, r, 42, 0.5, 5)[5])
+
+
+def test_halo_pack_packed_kernel():
+    p = sq.Squeeze(sq.builtin_fractal("sierpinski-triangle"), 12, rank=1, nranks=3, device=0, tile_level=4)
+    lo, hi = p.shard_range(1)
+    sends = np.array([lo, lo + 5, hi - 1, lo + 77, (lo + hi) // 2], dtype=np.uint64)
+    p.halo_set_sends(sends)
+    cur = p.new_packed()
+    p.seed_packed(cur, 42, 0.5)
+    send = torch.zeros(sends.size, dtype=torch.uint8, device="cuda")
+    recv = torch.zeros(max(1, len(p.halo_needs())), dtype=torch.uint8, device="cuda")
+    p.halo_bind(send, recv)
+    p.halo_pack_packed(cur)
+    torch.cuda.synchronize()
+    assert np.array_equal(send.cpu().numpy(), A.seed_at(SIERPINSKI, 12, sends.astype(np.int64), 42, 0.5))
+    a, b = p.new_packed(), p.new_packed()
+    with pytest.raises(sq.SqueezeError):
+        p.run_packed(a, b, 2)  # sharded: one step at a time with the halo exchange

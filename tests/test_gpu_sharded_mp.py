@@ -21,7 +21,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, name, r, steps, out):
+def _worker(rank, world, port, name, r, steps, out, packed=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -31,11 +31,18 @@ def _worker(rank, world, port, name, r, steps, out):
 
         torch.cuda.set_device(0)
         sh = ShardedSqueeze(pkg.builtin_fractal(name), r, rank, world, 0)
-        a, b = sh.new_state(), sh.new_state()
-        sh.seed(a, 42, 0.5)
-        fin = sh.run(a, b, steps)
-        torch.cuda.synchronize()
-        out[rank] = sh.sq.to_cells(fin).cpu().numpy().copy()
+        if packed:
+            a, b = sh.new_packed(), sh.new_packed()
+            sh.seed_packed(a, 42, 0.5)
+            fin = sh.run_packed(a, b, steps)
+            torch.cuda.synchronize()
+            out[rank] = sh.sq.packed_to_cells(fin).copy()
+        else:
+            a, b = sh.new_state(), sh.new_state()
+            sh.seed(a, 42, 0.5)
+            fin = sh.run(a, b, steps)
+            torch.cuda.synchronize()
+            out[rank] = sh.sq.to_cells(fin).cpu().numpy().copy()
         assert sh.sq.device_error() == 0
     finally:
         dist.destroy_process_group()
@@ -43,13 +50,14 @@ def _worker(rank, world, port, name, r, steps, out):
 
 @pytest.mark.parametrize("name,r,world,steps", [("sierpinski-triangle", 12, 2, 5), ("sierpinski-triangle", 13, 4, 4),
                                                 ("sierpinski-carpet", 6, 3, 3)])
-def test_multiprocess_shards_equal_unsharded(name, r, world, steps):
+@pytest.mark.parametrize("packed", [False, True])
+def test_multiprocess_shards_equal_unsharded(name, r, world, steps, packed):
     import paper_2201_00613_b200 as pkg
 
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     out = mgr.dict()
-    mp.start_processes(_worker, args=(world, _free_port(), name, r, steps, out), nprocs=world, join=True,
+    mp.start_processes(_worker, args=(world, _free_port(), name, r, steps, out, packed), nprocs=world, join=True,
                        start_method="spawn")
     got = np.concatenate([out[p] for p in range(world)])
     p = pkg.Squeeze(pkg.builtin_fractal(name), r, device=0)
