@@ -44,6 +44,8 @@ def parse_args():
     ap.add_argument("--density", type=float, default=0.5)
     ap.add_argument("--tile-level", type=int, default=0)
     ap.add_argument("--packed-tile-level", type=int, default=7, help="tile level of the packed leg (0 = same ctx)")
+    ap.add_argument("--state", default="bytes", choices=["bytes", "packed"],
+                    help="state of the timed step: uint8 (default) or 1 bit per cell (NEXT-1; extras skipped)")
     ap.add_argument("--heat-level", type=int, default=21, help="level of the heat-diffusion leg (0 = skip)")
     ap.add_argument("--block-threads", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
@@ -223,6 +225,8 @@ def main():
     red_dev = "cuda" if backend == "nccl" else "cpu"
     f = pkg.builtin_fractal(args.fractal)
     opts = dict(tile_level=args.tile_level, block_threads=args.block_threads, ctas_per_sm=args.ctas_per_sm)
+    if args.state == "packed" and not args.tile_level:
+        opts["tile_level"] = args.packed_tile_level  # the packed kernel's level
     if world > 1:
         sh = ShardedSqueeze(f, args.level, rank, world, local, **opts)
         sq = sh.sq
@@ -230,17 +234,24 @@ def main():
         sh = None
         sq = pkg.Squeeze(f, args.level, device=local, **opts)
     g = sq.geometry
-    a, b = sq.new_state(), sq.new_state()
-    sq.seed(a, args.seed, args.density)
+    packed = args.state == "packed"  # 1 bit per cell (NEXT-1): e.g. r=24 on 2 GPUs
+    if packed:
+        args.no_extras = True  # the extra legs use the byte state
+    if packed:
+        a, b = sq.new_packed(), sq.new_packed()
+        sq.seed_packed(a, args.seed, args.density)
+    else:
+        a, b = sq.new_state(), sq.new_state()
+        sq.seed(a, args.seed, args.density)
     stream = torch.cuda.current_stream()
 
     def step(cur, nxt, ev0=None, ev1=None):
         if sh is not None:
-            sq.halo_pack(cur)
+            (sq.halo_pack_packed if packed else sq.halo_pack)(cur)
             sh.halo.exchange()
         if ev0 is not None:
             ev0.record(stream)
-        sq.step(cur, nxt)
+        (sq.step_packed if packed else sq.step)(cur, nxt)
         if ev1 is not None:
             ev1.record(stream)
 
@@ -276,11 +287,13 @@ def main():
         raise RuntimeError("device error flag set (halo miss)")
     value = cells_per_s(g.cells_total, K, ms)
     peak, peak_src = measured_hbm_peak()
-    alg_bytes = 2 * g.local_cells  # 1 B read + 1 B written per compact cell (uint8, D10)
+    # 1 B read + 1 B written per compact cell (uint8, D10); packed: the 1-bit words read + written
+    alg_bytes = 2 * g.packed_bytes if packed else 2 * g.local_cells
     achieved = alg_bytes / (kern_avg / 1e3) / 1e9
     wl_key = f"{args.fractal}-r{args.level}-n{world}"
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(wl_key), "kernel": "sqz::k_step_tile",
+                "traffic": None if packed else ncu_traffic(wl_key),
+                "kernel": "sqz::k_step_packed" if packed else "sqz::k_step_tile",
                 "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": kern_avg, "peak_source": peak_src}
     extras = {}
     launches = K * (1 + (1 if (sh is not None and sh.halo.sends.size) else 0))
@@ -522,15 +535,16 @@ def main():
         line = {
             "metric": "compact cell updates/s", "value": value, "unit": "cells/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "scaling": "strong", "vs_baseline": None, "dtype": "b1" if packed else "u8",
             "data": "synthetic",
             "config": {"workload": f"{args.fractal} r={args.level} ({g.cells_total} compact cells), B3/S23, "
-                                   f"seed {args.seed} density {args.density}",
+                                   f"seed {args.seed} density {args.density}" + (", packed state" if packed else ""),
                        "fractal": args.fractal, "level": args.level, "cells": g.cells_total,
                        "tile_level": g.tile_level, "tile_cells": g.tile_cells,
                        "parallelism": f"{world} shard(s) of contiguous Omega ranges" + (
                            ", NCCL halo exchange" if world > 1 else ""),
-                       "l2": f"inputs larger than L2 ({2 * g.state_bytes / 1e9:.1f} GB double buffer per GPU)"},
+                       "l2": f"inputs larger than L2 ({2 * (g.packed_bytes if packed else g.state_bytes) / 1e9:.1f} GB "
+                             f"double buffer per GPU)"},
             "roofline": roofline,
             "clocks": clocks,
             "gpu_launches": launches,
