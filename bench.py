@@ -44,6 +44,9 @@ def parse_args():
     ap.add_argument("--density", type=float, default=0.5)
     ap.add_argument("--tile-level", type=int, default=0)
     ap.add_argument("--packed-tile-level", type=int, default=7, help="tile level of the packed leg (0 = same ctx)")
+    ap.add_argument("--halo", default="peer", choices=["peer", "collective"],
+                    help="N > 1 halo transport: the step kernel stores it into the peers over CUDA IPC "
+                         "(default) or squeeze_halo_pack + all_to_all")
     ap.add_argument("--state", default="bytes", choices=["bytes", "packed"],
                     help="state of the timed step: uint8 (default) or 1 bit per cell (NEXT-1; extras skipped)")
     ap.add_argument("--heat-level", type=int, default=21, help="level of the heat-diffusion leg (0 = skip)")
@@ -228,7 +231,14 @@ def main():
     if args.state == "packed" and not args.tile_level:
         opts["tile_level"] = args.packed_tile_level  # the packed kernel's level
     if world > 1:
-        sh = ShardedSqueeze(f, args.level, rank, world, local, **opts)
+        transport = args.halo if args.state == "bytes" else "collective"
+        try:
+            sh = ShardedSqueeze(f, args.level, rank, world, local, transport=transport, **opts)
+        except Exception as exc:  # no CUDA IPC between these GPUs: the collective transport
+            if transport != "peer":
+                raise
+            print(f"peer halo unavailable ({exc}); using the collective", file=sys.stderr)
+            sh = ShardedSqueeze(f, args.level, rank, world, local, transport="collective", **opts)
         sq = sh.sq
     else:
         sh = None
@@ -246,8 +256,10 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step(cur, nxt, ev0=None, ev1=None):
+        if sh is not None and not packed:  # byte state: the shard's own transport
+            return sh.step(cur, nxt, ev0=ev0, ev1=ev1)
         if sh is not None:
-            (sq.halo_pack_packed if packed else sq.halo_pack)(cur)
+            sq.halo_pack_packed(cur)
             sh.halo.exchange()
         if ev0 is not None:
             ev0.record(stream)
@@ -296,7 +308,8 @@ def main():
                 "kernel": "sqz::k_step_packed" if packed else "sqz::k_step_tile",
                 "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": kern_avg, "peak_source": peak_src}
     extras = {}
-    launches = K * (1 + (1 if (sh is not None and sh.halo.sends.size) else 0))
+    pack_launch = sh is not None and sh.halo.sends.size and (packed or sh.transport != "peer")
+    launches = K * (1 + (1 if pack_launch else 0))
 
     if world > 1 and not args.no_extras and not args.no_e2e:
         # end to end through the public sharded API: H2D of each shard, K steps with the halo
@@ -440,6 +453,40 @@ def main():
             ph.close()
             torch.cuda.empty_cache()
         torch.cuda.empty_cache()
+        # --- BASELINE configs[3]: other NBB fractals through the generic H-table
+        fr_rows = {}
+        for fname, lvl in (("sierpinski-carpet", 10), ("empty-bottles", 11)):
+            pf = pkg.Squeeze(pkg.builtin_fractal(fname), lvl, device=local)
+            gf = pf.geometry
+            row = {"level": lvl, "cells": gf.cells_total, "tile_level": gf.tile_level, "remote_links": gf.remote_links}
+            for mode in ("bytes", "packed"):
+                if mode == "bytes":
+                    fa, fb = pf.new_state(), pf.new_state()
+                    pf.seed(fa, args.seed, args.density)
+                    fn, nbytes = pf.step, 2 * gf.cells_total
+                else:
+                    fa, fb = pf.new_packed(), pf.new_packed()
+                    pf.seed_packed(fa, args.seed, args.density)
+                    fn, nbytes = pf.step_packed, 2 * gf.packed_bytes
+                for i in range(3):
+                    fn(fa if i % 2 == 0 else fb, fb if i % 2 == 0 else fa)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for i in range(20):
+                    fn(fa if i % 2 == 0 else fb, fb if i % 2 == 0 else fa)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                fms = e0.elapsed_time(e1) / 20
+                row[mode] = {"ms_per_step": fms, "cells_per_s": cells_per_s(gf.cells_total, 1, fms),
+                             "hbm_frac": nbytes / (fms / 1e3) / 1e9 / peak}
+                del fa, fb
+            pf.close()
+            fr_rows[fname] = row
+        extras["fractal_configs"] = {"note": "BASELINE configs[3]: carpet (D11 row-major minus centre) and empty "
+                                             "bottles (D11 assumed silhouette), 20 steps each, B3/S23",
+                                     "rows": fr_rows}
+        torch.cuda.empty_cache()
         # --- NEXT-3 ablation: batched ν map, LUT kernel vs integer tensor-core product
         nmap = 1 << 27
         gen = torch.Generator(device=f"cuda:{local}").manual_seed(1)
@@ -542,7 +589,9 @@ def main():
                        "fractal": args.fractal, "level": args.level, "cells": g.cells_total,
                        "tile_level": g.tile_level, "tile_cells": g.tile_cells,
                        "parallelism": f"{world} shard(s) of contiguous Omega ranges" + (
-                           ", NCCL halo exchange" if world > 1 else ""),
+                           (", halo stored by the step kernel into the peers (CUDA IPC over NVLink)"
+                            if sh.transport == "peer" and not packed else ", halo: pack kernel + all_to_all")
+                           if world > 1 else ""),
                        "l2": f"inputs larger than L2 ({2 * (g.packed_bytes if packed else g.state_bytes) / 1e9:.1f} GB "
                              f"double buffer per GPU)"},
             "roofline": roofline,

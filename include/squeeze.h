@@ -202,6 +202,31 @@ squeeze_status squeeze_halo_bind(void* ctx, uint8_t* d_send, const uint8_t* d_re
 /* d_send[i] = state of cell sends[i] in d_cur. */
 squeeze_status squeeze_halo_pack(const void* ctx, const uint8_t* d_cur, squeeze_stream_t stream);
 
+/* ---- peer-memory halo: the step kernel stores the halo itself (fused transport) ----
+ * Instead of squeeze_halo_pack + a collective, squeeze_step's epilogue writes each send cell of
+ * its OUTPUT straight into the receiving rank's buffer over NVLink (CUDA IPC mappings), so the
+ * next step's halo is in place when the step ends; the caller only orders steps across ranks
+ * (e.g. a barrier after each step) and alternates two receive buffers by step parity.
+ * squeeze_ipc_handle / _open / _close: cudaIpc{Get,Open,Close}MemHandle (64-byte handles).
+ * squeeze_halo_peer_plan: destination of every send (squeeze_halo_set_sends order): peer slot
+ *   send_peer[i] and byte position send_pos[i] in that peer's receive buffer.
+ * squeeze_halo_peer_bind: device pointers (IPC-opened) of the peers' receive buffers for one
+ *   parity, indexed by peer slot.  squeeze_halo_peer_select: parity the next squeeze_step writes
+ *   (-1 = off, the default).  Byte state only (squeeze_step). */
+squeeze_status squeeze_ipc_handle(const void* d_ptr, uint8_t* handle);
+squeeze_status squeeze_ipc_open(const uint8_t* handle, int device, void** d_ptr);
+squeeze_status squeeze_ipc_close(void* d_ptr);
+/* Receive buffers for the peer halo: plain cudaMalloc'd, zeroed (an IPC handle names a whole
+ * allocation, so these are not sub-allocations of a caching allocator). */
+squeeze_status squeeze_ipc_alloc(uint64_t bytes, int device, void** d_ptr);
+squeeze_status squeeze_ipc_free(void* d_ptr);
+/* The halo of d_cur written into the peers' receive buffers of `parity` (the first step's halo;
+ * afterwards squeeze_step's epilogue writes it). */
+squeeze_status squeeze_halo_peer_push(const void* ctx, const uint8_t* d_cur, int parity, squeeze_stream_t stream);
+squeeze_status squeeze_halo_peer_plan(void* ctx, const uint32_t* send_peer, const uint64_t* send_pos);
+squeeze_status squeeze_halo_peer_bind(void* ctx, uint32_t parity, uint32_t npeers, void* const* peer_recv);
+squeeze_status squeeze_halo_peer_select(void* ctx, int parity);
+
 /* ---- bit-sliced PACKED state (1 bit per cell) ----
  * Layout: the shard's tiles are grouped in chunks of packed_tiles = 128 consecutive tiles;
  * chunk c holds Kw 128-bit words (packed_bytes = chunks x Kw x 16); 32-bit lane q (0..3) of

@@ -52,7 +52,37 @@ def density_q(density: float) -> int:
 
 
 def _ptr(t) -> int:
-    return 0 if t is None else int(t.data_ptr())
+    if t is None:
+        return 0
+    return int(t) if isinstance(t, int) else int(t.data_ptr())
+
+
+# ---------------------------------------------------------------- CUDA IPC (peer-memory halo)
+def ipc_alloc(nbytes: int, device: int) -> int:
+    p = ctypes.c_void_p()
+    _lib.check(_lib.load().squeeze_ipc_alloc(nbytes, device, ctypes.byref(p)), "ipc_alloc")
+    return int(p.value)
+
+
+def ipc_free(ptr: int) -> None:
+    _lib.check(_lib.load().squeeze_ipc_free(ptr), "ipc_free")
+
+
+def ipc_handle(ptr: int) -> bytes:
+    buf = (ctypes.c_uint8 * 64)()
+    _lib.check(_lib.load().squeeze_ipc_handle(ptr, buf), "ipc_handle")
+    return bytes(buf)
+
+
+def ipc_open(handle: bytes, device: int) -> int:
+    buf = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    p = ctypes.c_void_p()
+    _lib.check(_lib.load().squeeze_ipc_open(buf, device, ctypes.byref(p)), "ipc_open")
+    return int(p.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _lib.check(_lib.load().squeeze_ipc_close(ptr), "ipc_close")
 
 
 def _stream(stream, device):
@@ -222,6 +252,23 @@ class Squeeze:
 
     def halo_bind(self, send, recv) -> None:
         _lib.check(self.lib.squeeze_halo_bind(self.ctx, _ptr(send), _ptr(recv)), "halo_bind")
+
+    def halo_peer_plan(self, send_peer, send_pos) -> None:
+        sp = np.ascontiguousarray(send_peer, dtype=np.uint32)
+        ps = np.ascontiguousarray(send_pos, dtype=np.uint64)
+        _lib.check(self.lib.squeeze_halo_peer_plan(self.ctx, sp.ctypes.data_as(_lib.u32p), ps.ctypes.data_as(_lib.u64p)),
+                   "halo_peer_plan")
+
+    def halo_peer_bind(self, parity: int, peer_ptrs) -> None:
+        arr = (ctypes.c_void_p * max(1, len(peer_ptrs)))(*[int(p) for p in peer_ptrs])
+        _lib.check(self.lib.squeeze_halo_peer_bind(self.ctx, parity, len(peer_ptrs), arr), "halo_peer_bind")
+
+    def halo_peer_select(self, parity: int) -> None:
+        _lib.check(self.lib.squeeze_halo_peer_select(self.ctx, parity), "halo_peer_select")
+
+    def halo_peer_push(self, cur, parity: int, stream=None) -> None:
+        _lib.check(self.lib.squeeze_halo_peer_push(self.ctx, _ptr(cur), parity, _stream(stream, cur.device)),
+                   "halo_peer_push")
 
     def halo_pack(self, cur, stream=None) -> None:
         _lib.check(self.lib.squeeze_halo_pack(self.ctx, _ptr(cur), _stream(stream, cur.device)), "halo_pack")

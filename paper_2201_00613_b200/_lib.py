@@ -82,6 +82,15 @@ SIGNATURES = {
     "squeeze_halo_bind": ([vp, vp, vp], st),
     "squeeze_halo_pack": ([vp, vp, vp], st),
     "squeeze_halo_pack_packed": ([vp, vp, vp], st),
+    "squeeze_ipc_handle": ([vp, u8p], st),
+    "squeeze_ipc_open": ([u8p, ctypes.c_int, ctypes.POINTER(vp)], st),
+    "squeeze_ipc_close": ([vp], st),
+    "squeeze_ipc_alloc": ([ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(vp)], st),
+    "squeeze_ipc_free": ([vp], st),
+    "squeeze_halo_peer_push": ([vp, vp, ctypes.c_int, vp], st),
+    "squeeze_halo_peer_plan": ([vp, u32p, u64p], st),
+    "squeeze_halo_peer_bind": ([vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(vp)], st),
+    "squeeze_halo_peer_select": ([vp, ctypes.c_int], st),
     "squeeze_pack": ([vp, vp, vp, vp], st),
     "squeeze_unpack": ([vp, vp, vp, vp], st),
     "squeeze_seed_packed": ([vp, vp, ctypes.c_uint64, ctypes.c_uint64, vp], st),

@@ -77,6 +77,15 @@ struct Ctx {
   uint64_t* d_needs = nullptr;
   uint64_t* d_sends = nullptr;
   uint64_t* d_send_bits = nullptr;
+  // peer-memory halo: per-chunk CSR of the send cells and their destinations (squeeze_halo_peer_*)
+  uint32_t* d_peer_chunk_start = nullptr;
+  uint32_t* d_peer_cell = nullptr;
+  uint32_t* d_peer_of = nullptr;
+  uint64_t* d_peer_pos = nullptr;
+  uint8_t** d_peer_recv[2] = {nullptr, nullptr};
+  uint32_t* d_send_peer = nullptr;  // the same destinations in send order (squeeze_halo_peer_push)
+  uint64_t* d_send_pos = nullptr;
+  int peer_parity = -1;  // -1: fused stores off
   int* d_err = nullptr;
   uint8_t* d_send = nullptr;
   const uint8_t* d_recv = nullptr;
@@ -155,6 +164,14 @@ void free_device(Ctx* c) {
   cudaFree(c->d_dir_start);
   cudaFree(c->d_needs);
   cudaFree(c->d_send_bits);
+  cudaFree(c->d_peer_chunk_start);
+  cudaFree(c->d_peer_cell);
+  cudaFree(c->d_peer_of);
+  cudaFree(c->d_peer_pos);
+  cudaFree(c->d_send_peer);
+  cudaFree(c->d_send_pos);
+  cudaFree(c->d_peer_recv[0]);
+  cudaFree(c->d_peer_recv[1]);
   cudaFree(c->d_sends);
   cudaFree(c->d_err);
 }
@@ -221,6 +238,13 @@ TileParams tile_params(const Ctx* c) {
   p.adj = c->d_adj;
   p.adj_stride = adj_stride(c);
   p.pstages = c->packed_stages;
+  if (c->peer_parity >= 0 && c->d_peer_chunk_start) {
+    p.peer_recv = c->d_peer_recv[c->peer_parity];
+    p.peer_chunk_start = c->d_peer_chunk_start;
+    p.peer_cell = c->d_peer_cell;
+    p.peer_of = c->d_peer_of;
+    p.peer_pos = c->d_peer_pos;
+  }
   return p;
 }
 
@@ -790,6 +814,118 @@ squeeze_status squeeze_halo_pack(const void* ctx, const uint8_t* d_cur, squeeze_
   if (!c->sends.empty() && !c->d_send) return SQZ_E_CONFIG;
   DevGuard g(c->device);
   return cu(launch_halo_pack(d_cur, c->d_sends, c->sends.size(), c->d_send, (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_ipc_handle(const void* d_ptr, uint8_t* handle) {
+  if (!d_ptr || !handle) return SQZ_E_CONFIG;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)) != cudaSuccess) return SQZ_E_CUDA;
+  std::memcpy(handle, &h, sizeof(h));
+  return SQZ_OK;
+}
+
+squeeze_status squeeze_ipc_open(const uint8_t* handle, int device, void** d_ptr) {
+  if (!handle || !d_ptr) return SQZ_E_CONFIG;
+  DevGuard g(device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  return cu(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+}
+
+squeeze_status squeeze_ipc_close(void* d_ptr) { return d_ptr ? cu(cudaIpcCloseMemHandle(d_ptr)) : SQZ_OK; }
+
+squeeze_status squeeze_ipc_alloc(uint64_t bytes, int device, void** d_ptr) {
+  if (!d_ptr) return SQZ_E_CONFIG;
+  DevGuard g(device);
+  if (cudaMalloc(d_ptr, bytes ? bytes : 1) != cudaSuccess) return SQZ_E_NOMEM;
+  return cu(cudaMemset(*d_ptr, 0, bytes ? bytes : 1));
+}
+
+squeeze_status squeeze_ipc_free(void* d_ptr) { return d_ptr ? cu(cudaFree(d_ptr)) : SQZ_OK; }
+
+squeeze_status squeeze_halo_peer_push(const void* ctx, const uint8_t* d_cur, int parity, squeeze_stream_t stream) {
+  if (!ctx || parity < 0 || parity > 1) return SQZ_E_CONFIG;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_cur);
+  if (st != SQZ_OK) return st;
+  if (c->sends.empty()) return SQZ_OK;
+  if (!c->d_peer_recv[parity] || !c->d_peer_chunk_start) return SQZ_E_CONFIG;
+  DevGuard g(c->device);
+  return cu(launch_halo_peer_push(d_cur, c->d_sends, c->d_send_peer, c->d_send_pos, c->sends.size(),
+                                  c->d_peer_recv[parity], (cudaStream_t)stream));
+}
+
+squeeze_status squeeze_halo_peer_plan(void* ctx, const uint32_t* send_peer, const uint64_t* send_pos) {
+  return guarded([&]() -> squeeze_status {
+    if (!ctx) return SQZ_E_CONFIG;
+    Ctx* c = static_cast<Ctx*>(ctx);
+    if (c->device < 0) return SQZ_E_NO_DEVICE;
+    const uint64_t n = c->sends.size();
+    if (n && (!send_peer || !send_pos)) return SQZ_E_CONFIG;
+    // CSR over the tile kernel's 32-tile chunks; cell = tile in chunk << 16 | j
+    const uint64_t nch = (c->sr.tile_hi - c->sr.tile_lo + kChunkTiles - 1) / kChunkTiles;
+    std::vector<uint32_t> start(nch + 1, 0), cell(n), of(n);
+    std::vector<uint64_t> pos(n);
+    std::vector<uint64_t> order(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint64_t tl = c->sends[i] / c->tt.K - c->sr.tile_lo;
+      start[tl / kChunkTiles + 1]++;
+      order[i] = i;
+    }
+    for (uint64_t k = 0; k < nch; ++k) start[k + 1] += start[k];
+    std::vector<uint32_t> fill(start.begin(), start.end() - 1);
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint64_t t = c->sends[i] / c->tt.K, tl = t - c->sr.tile_lo;
+      const uint32_t e = fill[tl / kChunkTiles]++;
+      cell[e] = (uint32_t)((tl % kChunkTiles) << 16 | (c->sends[i] - t * c->tt.K));
+      of[e] = send_peer[i];
+      pos[e] = send_pos[i];
+    }
+    DevGuard g(c->device);
+    cudaFree(c->d_peer_chunk_start);
+    cudaFree(c->d_peer_cell);
+    cudaFree(c->d_peer_of);
+    cudaFree(c->d_peer_pos);
+    cudaFree(c->d_send_peer);
+    cudaFree(c->d_send_pos);
+    c->d_send_peer = nullptr;
+    c->d_send_pos = nullptr;
+    c->d_peer_chunk_start = nullptr;
+    c->d_peer_cell = c->d_peer_of = nullptr;
+    c->d_peer_pos = nullptr;
+    squeeze_status st = upload(&c->d_peer_chunk_start, start.data(), start.size());
+    if (st == SQZ_OK) st = upload(&c->d_peer_cell, cell.data(), cell.size());
+    if (st == SQZ_OK) st = upload(&c->d_peer_of, of.data(), of.size());
+    if (st == SQZ_OK) st = upload(&c->d_peer_pos, pos.data(), pos.size());
+    if (st == SQZ_OK) st = upload(&c->d_send_peer, send_peer, n);
+    if (st == SQZ_OK) st = upload(&c->d_send_pos, send_pos, n);
+    return st;
+  });
+}
+
+squeeze_status squeeze_halo_peer_bind(void* ctx, uint32_t parity, uint32_t npeers, void* const* peer_recv) {
+  if (!ctx || parity > 1 || (npeers && !peer_recv)) return SQZ_E_CONFIG;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (c->device < 0) return SQZ_E_NO_DEVICE;
+  DevGuard g(c->device);
+  cudaFree(c->d_peer_recv[parity]);
+  c->d_peer_recv[parity] = nullptr;
+  if (npeers == 0) return SQZ_OK;
+  return upload(&c->d_peer_recv[parity], reinterpret_cast<uint8_t* const*>(peer_recv), npeers);
+}
+
+squeeze_status squeeze_halo_peer_select(void* ctx, int parity) {
+  if (!ctx || parity > 1 || parity < -1) return SQZ_E_CONFIG;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (parity >= 0 && (!c->d_peer_chunk_start || (!c->d_peer_recv[parity] && !c->sends.empty())))
+    return SQZ_E_CONFIG;
+  c->peer_parity = parity;
+  if (c->graph) {  // a captured run would replay the old parameters
+    cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+  }
+  return SQZ_OK;
 }
 
 squeeze_status squeeze_halo_pack_packed(const void* ctx, const uint32_t* d_cur, squeeze_stream_t stream) {

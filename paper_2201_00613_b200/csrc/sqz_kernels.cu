@@ -168,6 +168,15 @@ __global__ void k_count_alive(const uint4* __restrict__ st, uint64_t n16, const 
   }
 }
 
+// peer_recv[peer[i]][pos[i]] = cur[off_i]: the halo of a state written into the peers' buffers.
+__global__ void k_halo_peer_push(const uint8_t* __restrict__ cur, const uint64_t* __restrict__ offs,
+                                 const uint32_t* __restrict__ peer, const uint64_t* __restrict__ pos, uint64_t n,
+                                 uint8_t* const* __restrict__ peer_recv) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    peer_recv[peer[i]][pos[i]] = cur[offs[i]];
+  __threadfence_system();
+}
+
 __global__ void k_halo_pack(const uint8_t* __restrict__ cur, const uint64_t* __restrict__ offs, uint64_t n,
                             uint8_t* __restrict__ out) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
@@ -375,6 +384,13 @@ cudaError_t launch_count_alive(const uint8_t* state, uint64_t bytes, uint64_t* o
   k_count_alive<<<grid_for(n16 ? n16 : 1, 256, 4), 256, 0, st>>>(reinterpret_cast<const uint4*>(state), n16,
                                                                   state + n16 * 16, ntail,
                                                                   reinterpret_cast<unsigned long long*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_halo_peer_push(const uint8_t* cur, const uint64_t* send_offsets, const uint32_t* send_peer,
+                                  const uint64_t* send_pos, uint64_t nsends, uint8_t* const* peer_recv, cudaStream_t st) {
+  if (nsends == 0) return cudaSuccess;
+  k_halo_peer_push<<<grid_for(nsends, 256), 256, 0, st>>>(cur, send_offsets, send_peer, send_pos, nsends, peer_recv);
   return cudaGetLastError();
 }
 

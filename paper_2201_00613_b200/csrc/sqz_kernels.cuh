@@ -45,6 +45,14 @@ struct TileParams {
   uint64_t tile_lo, tile_hi, nchunks;
   uint32_t birth, survive;
   HaloView halo;
+  // peer-memory halo (sqz_tile.cu epilogue): send entries of chunk c are
+  // [peer_chunk_start[c], peer_chunk_start[c+1]); entry e stores byte (tile << 16 | j) of the
+  // chunk's output into peer_recv[peer_of[e]][peer_pos[e]] (IPC-mapped receive buffers).
+  uint8_t* const* peer_recv;
+  const uint32_t* peer_chunk_start;
+  const uint32_t* peer_cell;
+  const uint32_t* peer_of;
+  const uint64_t* peer_pos;
   // tile adjacency, built once at init: adj[d * adj_stride + (t - tile_lo)] = neighbour tile of
   // local tile t in link direction d, plus 1 (0 = none)
   const uint32_t* adj;
@@ -98,6 +106,8 @@ cudaError_t launch_step_naive(const LevelMaps& m, const uint8_t* cur, uint8_t* n
 cudaError_t launch_step_tile(const TileParams& p, const uint8_t* cur, uint8_t* next, int grid, int threads,
                              size_t smem, cudaStream_t st);
 cudaError_t launch_count_alive(const uint8_t* state, uint64_t bytes, uint64_t* out, cudaStream_t st);
+cudaError_t launch_halo_peer_push(const uint8_t* cur, const uint64_t* send_offsets, const uint32_t* send_peer,
+                                  const uint64_t* send_pos, uint64_t nsends, uint8_t* const* peer_recv, cudaStream_t st);
 cudaError_t launch_halo_pack_packed(const uint32_t* cur, const uint64_t* send_bits, uint64_t nsends, uint8_t* out,
                                    cudaStream_t st);
 cudaError_t launch_halo_pack(const uint8_t* cur, const uint64_t* send_offsets, uint64_t nsends, uint8_t* out,

@@ -251,6 +251,14 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     if (lane == 0) mbar_arrive(&S.bar[2 + buf]);
     if (issuer) {
       mbar_wait(&S.bar[2 + buf], (it >> 1) & 1);
+      if (p.peer_recv) {  // fused halo: this chunk's send cells go straight into the peers' buffers
+        const uint32_t e1 = p.peer_chunk_start[chunk + 1];
+        for (uint32_t e = p.peer_chunk_start[chunk]; e < e1; ++e) {
+          const uint32_t cell = p.peer_cell[e];
+          p.peer_recv[p.peer_of[e]][p.peer_pos[e]] = inb[(cell >> 16) * St + (cell & 0xFFFFu)];
+        }
+        __threadfence_system();
+      }
       chunk_store(p, c, inb, next);
     }
   }

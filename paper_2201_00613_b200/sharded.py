@@ -59,6 +59,15 @@ class HaloExchange:
         lo, hi = ranges[rank]
         if self.sends.size and ((self.sends < lo).any() or (self.sends >= hi).any()):
             raise ValueError("peer requested a cell this rank does not own")
+        # where this rank's sends land in each destination's receive buffer (peer-memory halo):
+        # destination d keeps the cells it needs from source p at offset sum(recv_counts[:p])
+        offs = np.concatenate([[0], np.cumsum(self.recv_counts)[:-1]]).astype(np.int64)
+        got = torch.empty(nranks, dtype=torch.int64, device=self.comm)
+        dist.all_to_all_single(got, torch.from_numpy(offs).to(self.comm), group=group)
+        base = got.cpu().numpy()
+        self.send_peer = np.repeat(np.arange(nranks, dtype=np.uint32), self.send_counts)
+        self.send_pos = np.concatenate([base[d] + np.arange(self.send_counts[d], dtype=np.int64)
+                                        for d in range(nranks)]).astype(np.uint64) if nranks else np.zeros(0, np.uint64)
         self.send_buf = torch.zeros(max(1, int(self.sends.size)), dtype=torch.uint8, device=device)
         self.recv_buf = torch.zeros(max(1, int(needs.size)), dtype=torch.uint8, device=device)
         self.nneeds = int(needs.size)
@@ -80,28 +89,112 @@ class HaloExchange:
 
 
 class ShardedSqueeze:
-    """One rank's shard of a level-r fractal: library context + halo exchange."""
+    """One rank's shard of a level-r fractal: library context + halo exchange.
+
+    transport="collective": per step squeeze_halo_pack + all_to_all (NCCL on GPUs).
+    transport="peer": the step kernel itself stores the next state's halo into the peers'
+    receive buffers over NVLink (CUDA IPC; squeeze_halo_peer_*), two receive buffers by step
+    parity, and a barrier between steps orders the ranks — no pack kernel, no collective.
+    Byte state only; packed steps always use the collective."""
 
     def __init__(self, fractal: Fractal, r: int, rank: int, nranks: int, device: int, rule=B3S23,
-                 group=None, **opts):
+                 group=None, transport: str = "collective", **opts):
         self.sq = Squeeze(fractal, r, rule=rule, rank=rank, nranks=nranks, device=device, **opts)
         self.geometry = self.sq.geometry
+        self.rank, self.nranks, self.group, self.device = rank, nranks, group, device
         ranges = [self.sq.shard_range(p) for p in range(nranks)]
         self.halo = HaloExchange(self.sq.halo_needs(), ranges, rank, nranks, torch.device(f"cuda:{device}"),
                                  group)
         self.sq.halo_set_sends(self.halo.sends)
         self.sq.halo_bind(self.halo.send_buf, self.halo.recv_buf)
+        self.transport = transport
+        self.parity = 0
+        self._peer_bufs, self._peer_open = [], []
+        if transport == "peer":
+            self._init_peer()
+        elif transport != "collective":
+            raise ValueError(f"unknown halo transport {transport!r}")
+
+    def _init_peer(self):
+        from . import ipc_alloc, ipc_handle, ipc_open
+        n = max(1, self.halo.nneeds)
+        self._peer_bufs = [ipc_alloc(n, self.device), ipc_alloc(n, self.device)]
+        mine = [ipc_handle(p) for p in self._peer_bufs]
+        allh = [None] * self.nranks
+        dist.all_gather_object(allh, mine, group=self.group)
+        ptrs = [[0] * self.nranks, [0] * self.nranks]
+        for d in range(self.nranks):
+            if d == self.rank:
+                continue
+            for par in range(2):
+                ptrs[par][d] = ipc_open(allh[d][par], self.device)
+                self._peer_open.append(ptrs[par][d])
+        self.sq.halo_peer_plan(self.halo.send_peer, self.halo.send_pos)
+        for par in range(2):
+            self.sq.halo_peer_bind(par, ptrs[par])
+        self.primed = False
+
+    def close(self):
+        from . import ipc_close, ipc_free
+        if not self._peer_bufs:
+            return
+        torch.cuda.synchronize(self.device)
+        for p in self._peer_open:
+            ipc_close(p)
+        dist.barrier(group=self.group)  # every importer has unmapped before the buffers are freed
+        for p in self._peer_bufs:
+            ipc_free(p)
+        self._peer_open, self._peer_bufs = [], []
 
     def new_state(self):
         return self.sq.new_state()
 
     def seed(self, state, seed=42, density=0.5):
         self.sq.seed(state, seed, density)
+        self.primed = False  # the peer halo is pushed again from the new state
 
-    def step(self, cur, nxt, naive: bool = False):
+    def step(self, cur, nxt, naive: bool = False, ev0=None, ev1=None):
+        """One sharded step; ev0/ev1 (optional CUDA events) bracket the step kernel itself."""
+        if self.transport == "peer" and not naive:
+            return self._step_peer(cur, nxt, ev0, ev1)
         self.sq.halo_pack(cur)
         self.halo.exchange()
+        if ev0 is not None:
+            ev0.record()
         (self.sq.step_naive if naive else self.sq.step)(cur, nxt)
+        if ev1 is not None:
+            ev1.record()
+
+    def _barrier(self):
+        """Orders every rank's previous step before anyone's next one.  NCCL: a one-element
+        all_reduce on the stream (asynchronous for the host; the current stream waits on it, and
+        it completes only after every rank's preceding step kernel — whose peer stores end with a
+        system-scope fence — has finished).  gloo (ranks sharing one GPU in tests): host sync."""
+        if dist.get_backend(self.group) == "nccl":
+            if not hasattr(self, "_flag"):
+                self._flag = torch.zeros(1, dtype=torch.int32, device=f"cuda:{self.device}")
+            dist.all_reduce(self._flag, group=self.group)
+            return
+        torch.cuda.current_stream(self.device).synchronize()
+        dist.barrier(group=self.group)
+
+    def _step_peer(self, cur, nxt, ev0=None, ev1=None):
+        if not self.primed:  # the first halo: pushed from the current state into parity 0
+            self.parity = 0
+            self.sq.halo_peer_push(cur, 0)
+            self._barrier()
+            self.primed = True
+        p = self.parity
+        self.sq.halo_bind(self.halo.send_buf, self._peer_bufs[p])  # this step reads parity p
+        self.sq.halo_peer_select(1 - p)  # and writes the next state's halo into parity 1-p
+        if ev0 is not None:
+            ev0.record()
+        self.sq.step(cur, nxt)
+        if ev1 is not None:
+            ev1.record()
+        self.sq.halo_peer_select(-1)
+        self._barrier()
+        self.parity = 1 - p
 
     # 1-bit-per-cell state (NEXT-1): same halo plan, the packed halo pack and packed step
     def new_packed(self):
@@ -122,6 +215,7 @@ class ShardedSqueeze:
         return b if steps % 2 else a
 
     def run(self, a, b, steps: int):
+        self.primed = False  # a run starts from `a`: its halo is pushed before the first step
         for i in range(steps):
             cur, nxt = (a, b) if i % 2 == 0 else (b, a)
             self.step(cur, nxt)

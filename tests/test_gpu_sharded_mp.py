@@ -21,7 +21,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, name, r, steps, out, packed=False):
+def _worker(rank, world, port, name, r, steps, out, packed=False, transport="collective"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -30,7 +30,7 @@ def _worker(rank, world, port, name, r, steps, out, packed=False):
         from paper_2201_00613_b200.sharded import ShardedSqueeze
 
         torch.cuda.set_device(0)
-        sh = ShardedSqueeze(pkg.builtin_fractal(name), r, rank, world, 0)
+        sh = ShardedSqueeze(pkg.builtin_fractal(name), r, rank, world, 0, transport=transport)
         if packed:
             a, b = sh.new_packed(), sh.new_packed()
             sh.seed_packed(a, 42, 0.5)
@@ -44,20 +44,22 @@ def _worker(rank, world, port, name, r, steps, out, packed=False):
             torch.cuda.synchronize()
             out[rank] = sh.sq.to_cells(fin).cpu().numpy().copy()
         assert sh.sq.device_error() == 0
+        sh.close()
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("name,r,world,steps", [("sierpinski-triangle", 12, 2, 5), ("sierpinski-triangle", 13, 4, 4),
                                                 ("sierpinski-carpet", 6, 3, 3)])
-@pytest.mark.parametrize("packed", [False, True])
-def test_multiprocess_shards_equal_unsharded(name, r, world, steps, packed):
+@pytest.mark.parametrize("packed,transport", [(False, "collective"), (True, "collective"), (False, "peer")])
+def test_multiprocess_shards_equal_unsharded(name, r, world, steps, packed, transport):
     import paper_2201_00613_b200 as pkg
 
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     out = mgr.dict()
-    mp.start_processes(_worker, args=(world, _free_port(), name, r, steps, out, packed), nprocs=world, join=True,
+    mp.start_processes(_worker, args=(world, _free_port(), name, r, steps, out, packed, transport), nprocs=world,
+                       join=True,
                        start_method="spawn")
     got = np.concatenate([out[p] for p in range(world)])
     p = pkg.Squeeze(pkg.builtin_fractal(name), r, device=0)
