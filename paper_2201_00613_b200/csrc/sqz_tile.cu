@@ -79,7 +79,7 @@ __device__ __forceinline__ void chunk_store(const TileParams& p, const ChunkInfo
   tma_store_1d(next + (c.t0 - p.tile_lo) * p.Kp, buf, c.nt * p.Kp);
 }
 
-template <int DMAX, bool CONWAY, int MAXT, int MINB, int RB>
+template <int DMAX, bool CONWAY, int MAXT, int MINB, int RB, bool PEER>
 __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const uint8_t* __restrict__ cur,
                                                          uint8_t* __restrict__ next) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     if (lane == 0) mbar_arrive(&S.bar[2 + buf]);
     if (issuer) {
       mbar_wait(&S.bar[2 + buf], (it >> 1) & 1);
-      if (p.peer_recv) {  // fused halo: this chunk's send cells go straight into the peers' buffers
+      if (PEER) {  // fused halo: this chunk's send cells go straight into the peers' buffers
         const uint32_t e1 = p.peer_chunk_start[chunk + 1];
         for (uint32_t e = p.peer_chunk_start[chunk]; e < e1; ++e) {
           const uint32_t cell = p.peer_cell[e];
@@ -294,22 +294,29 @@ cudaError_t launch_tile_adjacency(const TileParams& p, uint32_t* adj, cudaStream
 
 using TileFn = void (*)(TileParams, const uint8_t*, uint8_t*);
 
-static TileFn pick(const TileParams& p, int threads) {
+template <bool PEER>
+static TileFn pick_t(const TileParams& p, int threads) {
   const bool conway = (p.birth == (1u << 3)) && (p.survive == ((1u << 2) | (1u << 3)));
   if (threads <= 256) {
-    if (p.dmax <= 5) return conway ? k_step_tile<5, true, 256, 4, 3> : k_step_tile<5, false, 256, 4, 3>;
-    return conway ? k_step_tile<8, true, 256, 4, 3> : k_step_tile<8, false, 256, 4, 3>;
+    if (p.dmax <= 5) return conway ? k_step_tile<5, true, 256, 4, 3, PEER> : k_step_tile<5, false, 256, 4, 3, PEER>;
+    return conway ? k_step_tile<8, true, 256, 4, 3, PEER> : k_step_tile<8, false, 256, 4, 3, PEER>;
   }
-  if (p.dmax <= 5) return conway ? k_step_tile<5, true, 1024, 1, 1> : k_step_tile<5, false, 1024, 1, 1>;
-  return conway ? k_step_tile<8, true, 1024, 1, 1> : k_step_tile<8, false, 1024, 1, 1>;
+  if (p.dmax <= 5) return conway ? k_step_tile<5, true, 1024, 1, 1, PEER> : k_step_tile<5, false, 1024, 1, 1, PEER>;
+  return conway ? k_step_tile<8, true, 1024, 1, 1, PEER> : k_step_tile<8, false, 1024, 1, 1, PEER>;
+}
+
+// PEER variants carry the fused peer-memory halo epilogue (sharded contexts with the peer transport).
+static TileFn pick(const TileParams& p, int threads) {
+  return p.peer_recv ? pick_t<true>(p, threads) : pick_t<false>(p, threads);
 }
 
 cudaError_t tile_prepare(const TileParams& p, size_t smem, int threads, int* occupancy) {
-  TileFn fn = pick(p, threads);
-  cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  for (TileFn fn : {pick_t<false>(p, threads), pick_t<true>(p, threads)}) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   int blocks = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, threads, smem);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick_t<false>(p, threads), threads, smem);
   if (e != cudaSuccess) return e;
   *occupancy = blocks;
   return blocks > 0 ? cudaSuccess : cudaErrorInvalidConfiguration;

@@ -123,12 +123,22 @@ class ShardedSqueeze:
         allh = [None] * self.nranks
         dist.all_gather_object(allh, mine, group=self.group)
         ptrs = [[0] * self.nranks, [0] * self.nranks]
-        for d in range(self.nranks):
-            if d == self.rank:
-                continue
-            for par in range(2):
-                ptrs[par][d] = ipc_open(allh[d][par], self.device)
-                self._peer_open.append(ptrs[par][d])
+        ok = 1
+        try:
+            for d in range(self.nranks):
+                if d == self.rank:
+                    continue
+                for par in range(2):
+                    ptrs[par][d] = ipc_open(allh[d][par], self.device)
+                    self._peer_open.append(ptrs[par][d])
+        except Exception:
+            ok = 0
+        # every rank takes the same decision (a rank that cannot map a peer fails them all)
+        flag = torch.tensor([ok], dtype=torch.int32, device=self.halo.comm)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        if int(flag.item()) == 0:
+            self.close()
+            raise RuntimeError("CUDA IPC mapping of a peer's receive buffer failed on some rank")
         self.sq.halo_peer_plan(self.halo.send_peer, self.halo.send_pos)
         for par in range(2):
             self.sq.halo_peer_bind(par, ptrs[par])
