@@ -120,6 +120,15 @@ def measured_hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_pipes(workload_key: str):
+    """integer/LSU pipe utilisation of the stencil kernel from the committed ncu summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh).get(workload_key, {}).get("pipes_pct_active")
+    except (OSError, ValueError):
+        return None
+
+
 def ncu_traffic(workload_key: str):
     """dram bytes per launch of the stencil kernel from a committed `ncu --set full` summary."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -306,7 +315,8 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": None if packed else ncu_traffic(wl_key),
                 "kernel": "sqz::k_step_packed" if packed else "sqz::k_step_tile",
-                "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": kern_avg, "peak_source": peak_src}
+                "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": kern_avg, "peak_source": peak_src,
+                "pipes_pct_active": None if packed else ncu_pipes(wl_key)}
     extras = {}
     pack_launch = sh is not None and sh.halo.sends.size and (packed or sh.transport != "peer")
     launches = K * (1 + (1 if pack_launch else 0))
