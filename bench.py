@@ -54,6 +54,7 @@ def parse_args():
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--no-extras", action="store_true", help="skip BB / naive / cpu / e2e legs")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--reps", type=int, default=5, help="repetitions of the K-step run reported (mean, stderr)")
     ap.add_argument("--cpu-sample", type=int, default=1 << 21, help="cells in the cpu_baseline sample")
     ap.add_argument("--ref-sample", type=int, default=1 << 16, help="cells per --impl reference step")
     return ap.parse_args()
@@ -345,6 +346,20 @@ def main():
                                  f"halo exchange, D2H; max over ranks", "ms": e_ms}
         del h
     if rank == 0 and world == 1 and not args.no_extras:
+        # repetitions of the K-step run (the first is the timed run above)
+        reps = [ms / K]
+        for _ in range(args.reps - 1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(K):
+                step(bufs[i % 2], bufs[(i + 1) % 2])
+            e1.record(stream)
+            torch.cuda.synchronize()
+            reps.append(e0.elapsed_time(e1) / K)
+        mean = statistics.fmean(reps)
+        extras["repetitions"] = {"n": len(reps), "steps_each": K, "ms_per_step_mean": mean,
+                                 "ms_per_step_stderr": (statistics.stdev(reps) / len(reps) ** 0.5) if len(reps) > 1
+                                 else None, "ms_per_step": reps}
         del bufs
         # --- end to end through the public API from (pinned) host memory
         if not args.no_e2e:
