@@ -49,6 +49,7 @@ def parse_args():
                          "(default) or squeeze_halo_pack + all_to_all")
     ap.add_argument("--state", default="bytes", choices=["bytes", "packed"],
                     help="state of the timed step: uint8 (default) or 1 bit per cell (NEXT-1; extras skipped)")
+    ap.add_argument("--r24-packed", type=int, default=1, help="time the r=24 packed step on this GPU (0 = skip)")
     ap.add_argument("--heat-level", type=int, default=21, help="level of the heat-diffusion leg (0 = skip)")
     ap.add_argument("--block-threads", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
@@ -442,6 +443,34 @@ def main():
         if pq is not sq:
             pq.close()
         torch.cuda.empty_cache()
+        # --- r=24 (BASELINE configs[4]: "2.8e11 cells ... across 8 B200") on ONE GPU: 1 bit per cell is
+        # 70.6 GB double-buffered, where the byte state would need 565 GB
+        if args.r24_packed and args.fractal == "sierpinski-triangle":
+            p24 = pkg.Squeeze(f, 24, device=local, tile_level=args.packed_tile_level)
+            g24 = p24.geometry
+            a24, b24 = p24.new_packed(), p24.new_packed()
+            p24.seed_packed(a24, args.seed, args.density)
+            for i in range(args.warmup):
+                p24.step_packed(a24 if i % 2 == 0 else b24, b24 if i % 2 == 0 else a24)
+            torch.cuda.synchronize()
+            steps24 = max(2, min(K, 20))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(steps24):
+                p24.step_packed(a24 if i % 2 == 0 else b24, b24 if i % 2 == 0 else a24)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms24 = e0.elapsed_time(e1) / steps24
+            extras["packed_r24_one_gpu"] = {
+                "level": 24, "cells": g24.cells_total, "steps": steps24, "ms_per_step": ms24,
+                "value": cells_per_s(g24.cells_total, 1, ms24), "unit": "cells/s",
+                "state_bytes_double_buffered": 2 * g24.packed_bytes,
+                "hbm_frac": 2 * g24.packed_bytes / (ms24 / 1e3) / 1e9 / peak,
+                "note": "BASELINE configs[4] level on a single B200 thanks to the 1-bit state (the byte state needs "
+                        "565 GB); parity: tests/test_gpu_packed.py::test_packed_r24_on_one_gpu_histogram_and_sampled"}
+            del a24, b24
+            p24.close()
+            torch.cuda.empty_cache()
         # --- second workload: heat diffusion on the compact fractal, float32 field
         if args.heat_level:
             ph = pkg.Squeeze(f, args.heat_level, device=local)

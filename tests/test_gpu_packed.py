@@ -216,3 +216,38 @@ def test_halo_pack_packed_kernel():
     a, b = p.new_packed(), p.new_packed()
     with pytest.raises(sq.SqueezeError):
         p.run_packed(a, b, 2)  # sharded: one step at a time with the halo exchange
+
+
+def test_packed_r24_on_one_gpu_histogram_and_sampled():
+    """r=24 (2.8e11 cells; 70.6 GB double-buffered at 1 bit/cell — 565 GB as bytes) on ONE GPU:
+    the closed-form neighbour histogram pin (SURVEY §8c pin 7) from all-alive, and one B3/S23
+    step vs the oracle at 1e5 sampled cells."""
+    r = 24
+    tt = 3 ** (r - 2)
+    hist = {2: 3, 3: 4 * tt - 2, 4: 4 * tt, 5: tt - 1}
+    p = mk("sierpinski-triangle", r, tile_level=7)
+    g = p.geometry
+    a, b = p.new_packed(), p.new_packed()
+    p.seed_packed(a, 1, 1.0)
+    assert int(p.count_alive_packed(a).item()) == 3 ** r
+    for c in (2, 5):
+        pc = mk("sierpinski-triangle", r, tile_level=7, rule=(0, 1 << c))
+        pc.step_packed(a, b)
+        assert int(pc.count_alive_packed(b).item()) == hist[c], c
+        pc.close()
+    p.seed_packed(a, 42, 0.5)
+    p.step_packed(a, b)
+    torch.cuda.synchronize()
+    om = np.unique(sqz_inputs.random_indices(100_000, 3 ** r, seed=24).astype(np.int64))
+    om = np.concatenate([om, [0, 3 ** r - 1]]).astype(np.int64)
+    t = om // g.tile_cells
+    j = om - t * g.tile_cells
+    widx = torch.from_numpy(((t // 128) * g.chunk_words + j) * 4 + (t // 32) % 4).cuda()
+    bit = torch.from_numpy(t % 32).cuda()
+
+    def bits(buf, idx=widx, sh=bit):
+        return ((buf[idx].to(torch.int64) >> sh) & 1).cpu().numpy().astype(np.uint8)
+
+    assert np.array_equal(bits(a), A.seed_at(SIERPINSKI, r, om, 42, 0.5))
+    want = A.compact_step_sampled(SIERPINSKI, r, om, lambda q: A.seed_at(SIERPINSKI, r, q, 42, 0.5))
+    assert np.array_equal(bits(b), want)
