@@ -1,13 +1,17 @@
-"""Small multi-chunk runs of every step kernel, for compute-sanitizer (memcheck/racecheck/synccheck)."""
+"""Small multi-chunk runs of every step kernel, for compute-sanitizer (memcheck/racecheck/synccheck):
+byte tile step (+ literal step), packed step at small and level-7 tiles, packed/byte conversions,
+heat step, sharded packed step with a halo, tensor-core ν map."""
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2201_00613_b200 as pkg  # noqa: E402
 
-for name, r, g in [("sierpinski-triangle", 11, 3), ("sierpinski-carpet", 5, 2), ("empty-bottles", 6, 2)]:
+for name, r, g in [("sierpinski-triangle", 11, 3), ("sierpinski-triangle", 12, 7), ("sierpinski-carpet", 5, 2),
+                   ("empty-bottles", 6, 2)]:
     p = pkg.Squeeze(pkg.builtin_fractal(name), r, device=0, tile_level=g, ctas_per_sm=1)
     a, b = p.new_state(), p.new_state()
     p.seed(a, 42, 0.5)
@@ -18,5 +22,27 @@ for name, r, g in [("sierpinski-triangle", 11, 3), ("sierpinski-carpet", 5, 2), 
     p.run_packed(pa, pb, 3)
     p.unpack(pb, a)
     p.count_alive(a)
+    ha, hb = p.new_heat(), p.new_heat()
+    p.heat_seed(ha, 3)
+    p.heat_run(ha, hb, 3)
+    x, y = p.map_lambda(torch.arange(min(4096, p.geometry.cells_total), device="cuda"))
+    p.map_nu_mma(x, y)
     torch.cuda.synchronize()
     print("ok", name, r, g, flush=True)
+
+# sharded packed step with a bound halo (2 shards on one device)
+f = pkg.builtin_fractal("sierpinski-triangle")
+parts = [pkg.Squeeze(f, 11, rank=i, nranks=2, device=0, tile_level=4) for i in range(2)]
+for p in parts:
+    nd = p.halo_needs()
+    rv = torch.zeros(max(1, len(nd)), dtype=torch.uint8, device="cuda")
+    p.halo_set_sends(np.zeros(0, np.uint64))
+    p.halo_bind(None, rv)
+    a, b = p.new_packed(), p.new_packed()
+    p.seed_packed(a, 42, 0.5)
+    p.step_packed(a, b)
+    s, st = p.new_state(), p.new_state()
+    p.seed(s, 42, 0.5)
+    p.step(s, st)
+torch.cuda.synchronize()
+print("ok sharded", flush=True)
