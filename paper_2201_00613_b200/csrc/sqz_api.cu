@@ -431,6 +431,9 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
         nbr_packed[i] = (uint16_t)(v < c->tt.K ? v : v - c->tt.K + c->Kw);
       }
       if ((uint64_t)(c->Kw + c->tt.E + 1) > 0xFFFFu) return fail(SQZ_E_INVALID_LEVEL);
+      // 128-bit neighbour loads of the packed step: spread each quarter-warp's words over the
+      // shared-memory bank groups (sqz_host.h optimize_slot_order)
+      optimize_slot_order(nbr_packed, c->tt.K, c->tt.max_degree <= 5 ? 5 : 8);
       if ((st = upload(&c->d_nbr, nbr_bytes.data(), nbr_bytes.size())) != SQZ_OK) return fail(st);
       if ((st = upload(&c->d_nbr_packed, nbr_packed.data(), nbr_packed.size())) != SQZ_OK) return fail(st);
       if ((st = upload(&c->d_link_j2, c->tt.link_j2.data(), c->tt.link_j2.size())) != SQZ_OK) return fail(st);

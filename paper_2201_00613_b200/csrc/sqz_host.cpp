@@ -269,6 +269,68 @@ int build_tile_tables(const Spec& f, uint32_t g, TileTables& t) {
   return SQZ_OK;
 }
 
+namespace {
+// wavefronts of one slot across the lanes of a quarter: the largest number of DISTINCT words
+// that share a 16-byte bank group (word mod 8); equal words are one broadcast
+int slot_wavefronts(const uint16_t* w, int n) {
+  uint16_t seen[8];
+  int ns = 0, cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, best = 0;
+  for (int l = 0; l < n; ++l) {
+    bool dup = false;
+    for (int s = 0; s < ns; ++s) dup |= seen[s] == w[l];
+    if (dup) continue;
+    seen[ns++] = w[l];
+    best = std::max(best, ++cnt[w[l] & 7]);
+  }
+  return best;
+}
+}  // namespace
+
+void optimize_slot_order(std::vector<uint16_t>& rows, uint64_t K, int D) {
+  for (uint64_t q0 = 0; q0 < K; q0 += 8) {
+    const int n = (int)std::min<uint64_t>(8, K - q0);
+    auto cost = [&]() {
+      int c = 0;
+      for (int k = 0; k < D; ++k) {
+        uint16_t w[8];
+        for (int l = 0; l < n; ++l) w[l] = rows[(q0 + l) * 8 + k];
+        c += slot_wavefronts(w, n);
+      }
+      return c;
+    };
+    int best = cost();
+    for (int pass = 0; pass < 8; ++pass) {
+      const int before = best;
+      for (int l = 0; l < n; ++l) {
+        uint16_t* r = &rows[(q0 + l) * 8];
+        if (D <= 5) {  // every permutation of this lane's D slots
+          int idx[5] = {0, 1, 2, 3, 4};
+          uint16_t orig[5], keep[5];
+          for (int k = 0; k < D; ++k) orig[k] = keep[k] = r[k];
+          do {
+            for (int k = 0; k < D; ++k) r[k] = orig[idx[k]];
+            const int c = cost();
+            if (c < best) {
+              best = c;
+              for (int k = 0; k < D; ++k) keep[k] = r[k];
+            }
+          } while (std::next_permutation(idx, idx + D));
+          for (int k = 0; k < D; ++k) r[k] = keep[k];
+        } else {  // pairwise swaps
+          for (int a = 0; a < D; ++a)
+            for (int b = a + 1; b < D; ++b) {
+              std::swap(r[a], r[b]);
+              const int c = cost();
+              if (c < best) best = c;
+              else std::swap(r[a], r[b]);
+            }
+        }
+      }
+      if (best == before) break;
+    }
+  }
+}
+
 ShardRange shard_range(uint64_t num_tiles, uint64_t K, uint32_t rank, uint32_t nranks) {
   uint64_t nchunks = (num_tiles + kChunkTiles - 1) / kChunkTiles;
   uint64_t c_lo = (uint64_t)((unsigned __int128)nchunks * rank / nranks);

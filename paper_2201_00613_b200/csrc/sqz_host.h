@@ -57,6 +57,14 @@ struct TileTables {
 // Builds the tables for level-g tiles.  Returns 0 or an error code.
 int build_tile_tables(const Spec& f, uint32_t g, TileTables& t);
 
+// Reorders the first D slots of every row (K rows x 8 word slots; the step sums them, so any
+// order is correct) so that, for each group of 8 consecutive rows (the 8 lanes a 128-bit shared
+// load serves per wavefront), the words each slot index reads fall on distinct 16-byte bank
+// groups (word mod 8) as often as possible: fewer bank-conflict replays of the neighbour loads
+// (DESIGN.md §5.1b).  Coordinate descent over the lanes (all permutations for D <= 5, swaps
+// otherwise); deterministic.
+void optimize_slot_order(std::vector<uint16_t>& rows, uint64_t K, int D);
+
 // Largest g <= r with k^g <= max_cells and s^(2g) <= 1<<20 (auto tile level).
 uint32_t auto_tile_level(const Spec& f, uint32_t r, uint64_t max_cells);
 
