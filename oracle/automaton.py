@@ -231,3 +231,17 @@ def compact_step_sampled(f: Fractal, r: int, omegas: np.ndarray, fetch, rule: tu
     for i in range(8):
         count += np.where(mem[i], look(np.where(mem[i], nbr[i], omegas)), 0).astype(np.uint8)
     return apply_rule(look(omegas), count, rule)
+
+
+# ---------------------------------------------------------------- light-cone embedding (SURVEY §8c pin 11)
+def interior_cells(f: Fractal, g: int, margin: int) -> np.ndarray:
+    """Local cells j of a level-g sub-fractal whose expanded position λ_g(j) is more than
+    ``margin`` (Chebyshev) from every member cell on the border of its s^g x s^g box: a pattern
+    confined to them cannot reach or feel another sub-fractal within margin - 1 steps (one cell
+    per step), so it evolves as on the isolated level-g fractal."""
+    xs, ys = construction_table(f, g)
+    h = f.s ** g
+    border = (xs == 0) | (ys == 0) | (xs == h - 1) | (ys == h - 1)
+    bx, by = xs[border], ys[border]
+    d = np.min(np.maximum(np.abs(xs[:, None] - bx[None, :]), np.abs(ys[:, None] - by[None, :])), axis=1)
+    return np.nonzero(d > margin)[0]

@@ -251,3 +251,42 @@ def test_packed_r24_on_one_gpu_histogram_and_sampled():
     assert np.array_equal(bits(a), A.seed_at(SIERPINSKI, r, om, 42, 0.5))
     want = A.compact_step_sampled(SIERPINSKI, r, om, lambda q: A.seed_at(SIERPINSKI, r, q, 42, 0.5))
     assert np.array_equal(bits(b), want)
+
+
+def test_light_cone_r24_packed():
+    """The light-cone embedding (SURVEY §8c pin 11) at r=24 on the packed state: a level-5 pattern
+    planted at the last and at a random tile (Ω up to 2.8e11) evolves as the level-5 oracle run."""
+    r, g, T = 24, 5, 4
+    K = 3 ** g
+    inner = A.interior_cells(SIERPINSKI, g, T + 1)
+    p = mk("sierpinski-triangle", r, tile_level=7)
+    geo = p.geometry
+    a, b = p.new_packed(), p.new_packed()
+    rng = np.random.default_rng(24)
+
+    def index(om):
+        t = om // geo.tile_cells
+        j = om - t * geo.tile_cells
+        return ((t // 128) * geo.chunk_words + j) * 4 + (t // 32) % 4, t % 32
+
+    for t5 in (3 ** (r - g) - 1, int(rng.integers(0, 3 ** (r - g)))):
+        local = np.zeros(K, np.uint8)
+        local[rng.choice(inner, size=inner.size // 2, replace=False)] = 1
+        small = local.copy()
+        for _ in range(T):
+            small = A.compact_step(SIERPINSKI, g, small)
+        om = t5 * K + np.arange(K, dtype=np.int64)
+        widx, bit = index(om)
+        a.zero_()
+        live = local.astype(bool)
+        words = {}
+        for w, bt in zip(widx[live], bit[live]):
+            words[int(w)] = words.get(int(w), 0) | (1 << int(bt))
+        ws = np.array(sorted(words), dtype=np.int64)
+        vals = np.array([words[w] for w in ws], dtype=np.uint32).view(np.int32)
+        a[torch.from_numpy(ws).cuda()] = torch.from_numpy(vals).cuda()
+        fin = p.run_packed(a, b, T)
+        torch.cuda.synchronize()
+        got = ((fin[torch.from_numpy(widx).cuda()].to(torch.int64) >> torch.from_numpy(bit).cuda()) & 1)
+        assert np.array_equal(got.cpu().numpy().astype(np.uint8), small), t5
+        assert int(p.count_alive_packed(fin).item()) == int(small.sum()), t5

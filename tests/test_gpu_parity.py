@@ -382,3 +382,34 @@ def test_unbound_halo_is_rejected():
     p.seed(a, 1, 0.5)
     with pytest.raises(sq.SqueezeError):
         p.step(a, b)  # no halo bound
+
+
+# ---------------------------------------------------------------- light-cone embedding (SURVEY §8c pin 11)
+@pytest.mark.parametrize("r", [22])
+def test_light_cone_full_size_bytes(r):
+    """A random pattern on the interior of one level-5 sub-fractal at a random (and the last)
+    tile of the level-r fractal, everything else dead: after T steps the tile equals the level-5
+    oracle run and nothing else is alive (checks 64-bit addressing at any tile against small-r
+    truth; the oracle pin is tests/test_oracle_pins.py::test_light_cone_embedding)."""
+    g, T = 5, 4
+    K = 3 ** g
+    inner = A.interior_cells(SIERPINSKI, g, T + 1)
+    p = mk("sierpinski-triangle", r)
+    a, b = p.new_state(), p.new_state()
+    rng = np.random.default_rng(7)
+    for t in (3 ** (r - g) - 1, int(rng.integers(0, 3 ** (r - g)))):
+        local = np.zeros(K, np.uint8)
+        local[rng.choice(inner, size=inner.size // 2, replace=False)] = 1
+        small = local.copy()
+        for _ in range(T):
+            small = A.compact_step(SIERPINSKI, g, small)
+        a.zero_()
+        om = t * K + np.arange(K, dtype=np.int64)
+        idx = offsets_t(p, om)
+        a[idx] = torch.from_numpy(local).cuda()
+        fin = p.run(a, b, T)
+        torch.cuda.synchronize()
+        assert np.array_equal(fin[idx].cpu().numpy(), small), t
+        assert int(p.count_alive(fin).item()) == int(small.sum()), t
+    del a, b
+    torch.cuda.empty_cache()

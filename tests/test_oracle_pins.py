@@ -390,3 +390,27 @@ def test_mma_equals_nu():
         a, b, c = mma.encode(f, r, batch)
         assert mma.apply(a, b, c, len(batch)) == [maps.nu_map(f, r, w) for w in batch]
     assert mma.fp16_exact_max_level(SIERPINSKI) == 14  # 3^7 = 2187 > 2048 at μ = 15 (D14)
+
+
+# ------------------------------------------------------------------ light-cone embedding (SURVEY §8c pin 11)
+@pytest.mark.parametrize("f,r,g,T", [(SIERPINSKI, 8, 5, 4), (SIERPINSKI, 7, 4, 2), (CARPET, 5, 3, 1)])
+def test_light_cone_embedding(f, r, g, T):
+    """A pattern on the interior of ONE level-g sub-fractal of the level-r fractal (every other
+    cell dead) evolves for T steps exactly as on the isolated level-g fractal, and nothing outside
+    comes alive: locality (one cell per step) and the NBB replication (every level-g sub-fractal is
+    the same shape) fix it, independently of how λ/ν address the tile."""
+    rng = np.random.default_rng(r * 10 + g)
+    inner = automaton.interior_cells(f, g, T + 1)
+    assert inner.size > 0
+    K = f.k ** g
+    for t in (0, f.k ** (r - g) - 1, int(rng.integers(0, f.k ** (r - g)))):
+        local = np.zeros(K, np.uint8)
+        local[rng.choice(inner, size=max(1, inner.size // 2), replace=False)] = 1
+        small = local.copy()
+        big = np.zeros(f.k ** r, np.uint8)
+        big[t * K:(t + 1) * K] = local
+        for _ in range(T):
+            small = automaton.compact_step(f, g, small)
+            big = automaton.compact_step(f, r, big)
+        assert np.array_equal(big[t * K:(t + 1) * K], small)
+        assert int(big.sum()) == int(small.sum())
