@@ -413,3 +413,42 @@ def test_light_cone_full_size_bytes(r):
         assert int(p.count_alive(fin).item()) == int(small.sum()), t
     del a, b
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("nranks", [4])
+def test_sharded_r22_equals_unsharded(nranks):
+    """SURVEY pin 10(ii) at full size: r=22 split into P contiguous shards (halo gathered from the
+    unsharded state of the same step, what NCCL carries) equals the unsharded run byte for byte
+    after 2 steps; shard i's buffer is the unsharded buffer's tile range [tile_lo, tile_hi)."""
+    r, steps = 22, 2
+    f = sq.builtin_fractal("sierpinski-triangle")
+    full = mk("sierpinski-triangle", r)
+    S = [full.new_state() for _ in range(steps + 1)]  # unsharded states 0..steps (3 x 32.4 GB)
+    full.seed(S[0], 42, 0.5)
+    for s in range(steps):
+        full.step(S[s], S[s + 1])
+    torch.cuda.synchronize()
+    kp = full.geometry.tile_bytes
+    K = full.geometry.tile_cells
+    for i in range(nranks):  # one shard at a time
+        p = sq.Squeeze(f, r, rank=i, nranks=nranks, device=DEV)
+        nd = p.halo_needs()
+        rv = torch.zeros(max(1, len(nd)), dtype=torch.uint8, device="cuda")
+        p.halo_set_sends(np.zeros(0, np.uint64))
+        p.halo_bind(None, rv)
+        idx = offsets_t(full, nd.astype(np.int64)) if len(nd) else None
+        a, b = p.new_state(), p.new_state()
+        p.seed(a, 42, 0.5)
+        for s in range(steps):
+            if idx is not None:
+                rv[:len(nd)] = S[s][idx]
+            p.step(a, b)
+            a, b = b, a
+        torch.cuda.synchronize()
+        lo, hi = p.shard_range(i)
+        t0, t1 = lo // K, hi // K
+        assert torch.equal(a[:(t1 - t0) * kp], S[steps][t0 * kp:t1 * kp]), i
+        assert p.device_error() == 0
+        del a, b
+        p.close()
+        torch.cuda.empty_cache()
