@@ -439,6 +439,26 @@ def main():
             "note": "1 bit per cell, 128-tile bit-sliced chunks (squeeze_*_packed); algorithmic bytes = state "
                     "read + write; the tile adjacency rows add 4 B x link directions per tile; bit-exact with "
                     "the byte path (tests/test_gpu_packed.py)"}
+        if not args.no_e2e:  # end to end on the packed state: H2D of 3.9 GB instead of 32 GB
+            try:
+                hp = torch.empty(gq.packed_bytes // 4, dtype=torch.int32, pin_memory=True)
+            except RuntimeError:
+                hp = torch.empty(gq.packed_bytes // 4, dtype=torch.int32)
+            pq.seed_packed(pa, args.seed, args.density)
+            hp.copy_(pa[:gq.packed_bytes // 4])
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pq.run_host_packed(hp, pa, pb, K)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            pe_ms = e0.elapsed_time(e1)
+            extras["packed_state"]["e2e"] = {
+                "value": cells_per_s(gq.cells_total, K, pe_ms), "unit": "cells/s",
+                "h2d_bytes_per_step": gq.packed_bytes / K, "d2h_bytes_per_step": gq.packed_bytes / K,
+                "mode": f"squeeze_run_host_packed: H2D of the packed state, {K} steps, D2H, pinned host buffer",
+                "ms": pe_ms}
+            del hp
         del pa, pb
         if pq is not sq:
             pq.close()

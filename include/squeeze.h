@@ -247,6 +247,10 @@ squeeze_status squeeze_seed_packed(const void* ctx, uint32_t* d_packed, uint64_t
 squeeze_status squeeze_step_packed(void* ctx, const uint32_t* d_cur, uint32_t* d_next, squeeze_stream_t stream);
 /* `steps` packed steps ping-ponging d_a / d_b (final state in d_b if steps is odd). */
 squeeze_status squeeze_run_packed(void* ctx, uint32_t* d_a, uint32_t* d_b, uint64_t steps, squeeze_stream_t stream);
+/* End to end from host memory on the packed state (unsharded): H2D of h_packed (packed_bytes,
+ * ideally pinned), `steps` packed steps, D2H of the final state into h_packed, synchronised. */
+squeeze_status squeeze_run_host_packed(void* ctx, uint32_t* h_packed, uint32_t* d_a, uint32_t* d_b, uint64_t steps,
+                                       squeeze_stream_t stream);
 /* *d_out (device uint64) = number of alive cells in a packed buffer. */
 squeeze_status squeeze_count_alive_packed(const void* ctx, const uint32_t* d_packed, uint64_t* d_out,
                                           squeeze_stream_t stream);

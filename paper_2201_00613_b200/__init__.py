@@ -302,6 +302,12 @@ class Squeeze:
                    "run_packed")
         return b if steps % 2 else a
 
+    def run_host_packed(self, h_packed, a, b, steps: int, stream=None):
+        """End to end from host memory on the packed state (h_packed: CPU int32 tensor of
+        packed_bytes / 4 words, ideally pinned); the final state is written back into it."""
+        _lib.check(self.lib.squeeze_run_host_packed(self.ctx, _ptr(h_packed), _ptr(a), _ptr(b), steps,
+                                                    _stream(stream, a.device)), "run_host_packed")
+
     def count_alive_packed(self, packed, out=None, stream=None):
         import torch
         if out is None:

@@ -96,6 +96,7 @@ SIGNATURES = {
     "squeeze_seed_packed": ([vp, vp, ctypes.c_uint64, ctypes.c_uint64, vp], st),
     "squeeze_step_packed": ([vp, vp, vp, vp], st),
     "squeeze_run_packed": ([vp, vp, vp, ctypes.c_uint64, vp], st),
+    "squeeze_run_host_packed": ([vp, vp, vp, vp, ctypes.c_uint64, vp], st),
     "squeeze_count_alive_packed": ([vp, vp, vp, vp], st),
     "squeeze_heat_seed": ([vp, vp, ctypes.c_uint64, vp], st),
     "squeeze_heat_step": ([vp, vp, vp, ctypes.c_float, vp], st),

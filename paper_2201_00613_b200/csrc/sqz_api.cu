@@ -743,6 +743,22 @@ squeeze_status squeeze_run_host(void* ctx, uint8_t* h_state, uint8_t* d_a, uint8
   return cu(cudaStreamSynchronize(s));
 }
 
+squeeze_status squeeze_run_host_packed(void* ctx, uint32_t* h_packed, uint32_t* d_a, uint32_t* d_b, uint64_t steps,
+                                       squeeze_stream_t stream) {
+  if (!ctx || !h_packed) return SQZ_E_CONFIG;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_a);
+  if (st == SQZ_OK) st = check_state(c, d_b);
+  if (st != SQZ_OK) return st;
+  DevGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(d_a, h_packed, c->packed_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return SQZ_E_CUDA;
+  if ((st = squeeze_run_packed(ctx, d_a, d_b, steps, stream)) != SQZ_OK) return st;
+  const uint32_t* fin = (steps & 1) ? d_b : d_a;
+  if (cudaMemcpyAsync(h_packed, fin, c->packed_bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) return SQZ_E_CUDA;
+  return cu(cudaStreamSynchronize(s));
+}
+
 squeeze_status squeeze_count_alive(const void* ctx, const uint8_t* d_state, uint64_t* d_out, squeeze_stream_t stream) {
   if (!ctx || !d_out) return SQZ_E_CONFIG;
   const Ctx* c = static_cast<const Ctx*>(ctx);

@@ -290,3 +290,17 @@ def test_light_cone_r24_packed():
         got = ((fin[torch.from_numpy(widx).cuda()].to(torch.int64) >> torch.from_numpy(bit).cuda()) & 1)
         assert np.array_equal(got.cpu().numpy().astype(np.uint8), small), t5
         assert int(p.count_alive_packed(fin).item()) == int(small.sum()), t5
+
+
+def test_run_host_packed_round_trip():
+    r = 12
+    p = mk("sierpinski-triangle", r)
+    g = p.geometry
+    a, b = p.new_packed(), p.new_packed()
+    p.seed_packed(a, 5, 0.5)
+    h = a[:g.packed_bytes // 4].cpu().pin_memory()
+    p.run_host_packed(h, a, b, 3)
+    want = oracle_run("sierpinski-triangle", r, 5, 0.5, 3)[3]
+    dev = p.new_packed()
+    dev[:g.packed_bytes // 4] = h.cuda()
+    assert np.array_equal(cells(p, dev), want)
