@@ -524,7 +524,7 @@ def main():
             p24.close()
             torch.cuda.empty_cache()
         # --- second workload: heat diffusion on the compact fractal, float32 field
-        if args.heat_level:
+        if args.heat_level and args.fractal == "sierpinski-triangle":
             ph = pkg.Squeeze(f, args.heat_level, device=local)
             gh = ph.geometry
             ha, hb = ph.new_heat(), ph.new_heat()
@@ -622,66 +622,67 @@ def main():
         extras["map_ablation"] = abl
         del om_, mx, my, res
         torch.cuda.empty_cache()
-        # --- GPU expanded bounding-box baseline vs compact at r=16 (BASELINE configs[1])
-        r16 = 16
-        p16 = pkg.Squeeze(f, r16, device=local, **opts)
-        g0, g1 = p16.new_bb(), p16.new_bb()
-        p16.bb_seed(g0, args.seed, args.density)
-        c0, c1 = p16.new_state(), p16.new_state()
-        p16.seed(c0, args.seed, args.density)
-        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        if args.fractal == "sierpinski-triangle":  # BASELINE configs[1] (BB at r=16 fits for s=2 only)
+            # --- GPU expanded bounding-box baseline vs compact at r=16 (BASELINE configs[1])
+            r16 = 16
+            p16 = pkg.Squeeze(f, r16, device=local, **opts)
+            g0, g1 = p16.new_bb(), p16.new_bb()
+            p16.bb_seed(g0, args.seed, args.density)
+            c0, c1 = p16.new_state(), p16.new_state()
+            p16.seed(c0, args.seed, args.density)
+            flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
-        def timed(fn, n, flush_l2):
-            tot = 0.0
-            for i in range(n):
-                if flush_l2:
-                    flush.fill_(i & 0xFF)
-                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s0.record(stream)
-                fn(i)
-                s1.record(stream)
-                torch.cuda.synchronize()
-                tot += s0.elapsed_time(s1)
-            return tot / n
+            def timed(fn, n, flush_l2):
+                tot = 0.0
+                for i in range(n):
+                    if flush_l2:
+                        flush.fill_(i & 0xFF)
+                    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s0.record(stream)
+                    fn(i)
+                    s1.record(stream)
+                    torch.cuda.synchronize()
+                    tot += s0.elapsed_time(s1)
+                return tot / n
 
-        for i in range(3):
-            p16.bb_step(g0, g1)
-            p16.step(c0, c1)
-        bb_ms = timed(lambda i: p16.bb_step(g0 if i % 2 == 0 else g1, g1 if i % 2 == 0 else g0), 10, True)
-        cp_ms = timed(lambda i: p16.step(c0 if i % 2 == 0 else c1, c1 if i % 2 == 0 else c0), 50, True)
-        extras["bb_baseline"] = {
-            "level": r16, "bb_ms_per_step": bb_ms, "compact_ms_per_step": cp_ms, "speedup": bb_ms / cp_ms,
-            "bb_bytes": p16.bb_bytes() * 2, "compact_bytes": p16.geometry.state_bytes * 2,
-            "memory_ratio": (p16.geometry.n ** 2) / p16.geometry.cells_total,
-            "l2": "256 MiB buffer written before every timed step (flush)",
-            "paper_context": "paper: up to ~12x speedup (A100, rho<=8) and ~315x memory reduction at r=20"}
-        # the paper's three-way comparison (Figs. 10-11, Table 2) on B200 at r=16
-        p16.bb_seed(g1, args.seed, args.density)
-        lam_ms = timed(lambda i: p16.lambda_engine_step(g0 if i % 2 == 0 else g1, g1 if i % 2 == 0 else g0), 10, True)
-        rows = {"BB": {"ms": bb_ms, "bytes": p16.bb_bytes()}, "lambda": {"ms": lam_ms, "bytes": p16.bb_bytes()}}
-        for rho in (1, 2, 4, 8, 16, 32):
-            ba, bb2 = p16.new_blocks(rho), p16.new_blocks(rho)
-            p16.block_seed(rho, ba, args.seed, args.density)
-            p16.block_step(rho, ba, bb2)
-            ms_b = timed(lambda i: p16.block_step(rho, ba if i % 2 == 0 else bb2, bb2 if i % 2 == 0 else ba), 10, True)
-            rows[f"squeeze_rho{rho}"] = {"ms": ms_b, "bytes": p16.block_bytes(rho)}
-            del ba, bb2
-        rows["squeeze_tile_u8"] = {"ms": cp_ms, "bytes": p16.geometry.state_bytes}
-        pa16, pb16 = p16.new_packed(), p16.new_packed()
-        p16.seed_packed(pa16, args.seed, args.density)
-        p16.step_packed(pa16, pb16)
-        pk_ms = timed(lambda i: p16.step_packed(pa16 if i % 2 == 0 else pb16, pb16 if i % 2 == 0 else pa16), 50, True)
-        rows["squeeze_tile_packed"] = {"ms": pk_ms, "bytes": p16.geometry.packed_bytes}
-        del pa16, pb16
-        for v in rows.values():
-            v["speedup_vs_BB"] = bb_ms / v["ms"]
-            v["mrf_vs_BB_bytes"] = p16.bb_bytes() / v["bytes"]
-        extras["paper_comparison_r16"] = {
-            "note": "single-buffer bytes at 1 B/cell; the paper counts 4 B/cell (Table 2). Engines: BB (P:365), "
-                    "lambda(omega) (P:366), block-level Squeeze rho x rho (P:281-292), and this build's tile kernels",
-            "rows": rows}
-        del g0, g1, c0, c1, flush
-        torch.cuda.empty_cache()
+            for i in range(3):
+                p16.bb_step(g0, g1)
+                p16.step(c0, c1)
+            bb_ms = timed(lambda i: p16.bb_step(g0 if i % 2 == 0 else g1, g1 if i % 2 == 0 else g0), 10, True)
+            cp_ms = timed(lambda i: p16.step(c0 if i % 2 == 0 else c1, c1 if i % 2 == 0 else c0), 50, True)
+            extras["bb_baseline"] = {
+                "level": r16, "bb_ms_per_step": bb_ms, "compact_ms_per_step": cp_ms, "speedup": bb_ms / cp_ms,
+                "bb_bytes": p16.bb_bytes() * 2, "compact_bytes": p16.geometry.state_bytes * 2,
+                "memory_ratio": (p16.geometry.n ** 2) / p16.geometry.cells_total,
+                "l2": "256 MiB buffer written before every timed step (flush)",
+                "paper_context": "paper: up to ~12x speedup (A100, rho<=8) and ~315x memory reduction at r=20"}
+            # the paper's three-way comparison (Figs. 10-11, Table 2) on B200 at r=16
+            p16.bb_seed(g1, args.seed, args.density)
+            lam_ms = timed(lambda i: p16.lambda_engine_step(g0 if i % 2 == 0 else g1, g1 if i % 2 == 0 else g0), 10, True)
+            rows = {"BB": {"ms": bb_ms, "bytes": p16.bb_bytes()}, "lambda": {"ms": lam_ms, "bytes": p16.bb_bytes()}}
+            for rho in (1, 2, 4, 8, 16, 32):
+                ba, bb2 = p16.new_blocks(rho), p16.new_blocks(rho)
+                p16.block_seed(rho, ba, args.seed, args.density)
+                p16.block_step(rho, ba, bb2)
+                ms_b = timed(lambda i: p16.block_step(rho, ba if i % 2 == 0 else bb2, bb2 if i % 2 == 0 else ba), 10, True)
+                rows[f"squeeze_rho{rho}"] = {"ms": ms_b, "bytes": p16.block_bytes(rho)}
+                del ba, bb2
+            rows["squeeze_tile_u8"] = {"ms": cp_ms, "bytes": p16.geometry.state_bytes}
+            pa16, pb16 = p16.new_packed(), p16.new_packed()
+            p16.seed_packed(pa16, args.seed, args.density)
+            p16.step_packed(pa16, pb16)
+            pk_ms = timed(lambda i: p16.step_packed(pa16 if i % 2 == 0 else pb16, pb16 if i % 2 == 0 else pa16), 50, True)
+            rows["squeeze_tile_packed"] = {"ms": pk_ms, "bytes": p16.geometry.packed_bytes}
+            del pa16, pb16
+            for v in rows.values():
+                v["speedup_vs_BB"] = bb_ms / v["ms"]
+                v["mrf_vs_BB_bytes"] = p16.bb_bytes() / v["bytes"]
+            extras["paper_comparison_r16"] = {
+                "note": "single-buffer bytes at 1 B/cell; the paper counts 4 B/cell (Table 2). Engines: BB (P:365), "
+                        "lambda(omega) (P:366), block-level Squeeze rho x rho (P:281-292), and this build's tile kernels",
+                "rows": rows}
+            del g0, g1, c0, c1, flush
+            torch.cuda.empty_cache()
         extras["cpu_baseline"] = cpu_baseline(args)
 
     if rank == 0:
