@@ -44,16 +44,35 @@ def needs_rebuild() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compiles every source to an object in parallel (one nvcc per translation unit), then
+    links the shared library."""
     if not force and not needs_rebuild():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [nvcc_path(), *NVCC_FLAGS, "-shared", "-o", tmp,
-           *[os.path.join(CSRC, s) for s in SOURCES], "-lpthread"]
-    proc = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
-    log = proc.stdout + proc.stderr
+    import concurrent.futures as cf
+    import tempfile
+
+    nvcc = nvcc_path()
+    with tempfile.TemporaryDirectory(prefix="sqz_build_") as tmpd:
+        def compile_one(src):
+            obj = os.path.join(tmpd, src + ".o")
+            cmd = [nvcc, *NVCC_FLAGS, "-c", "-o", obj, os.path.join(CSRC, src)]
+            proc = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+            return obj, " ".join(cmd) + "\n" + proc.stdout + proc.stderr, proc.returncode
+
+        with cf.ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+            results = list(ex.map(compile_one, SOURCES))
+        log = "".join(r[1] for r in results)
+        rc = max(r[2] for r in results)
+        tmp = LIB + ".tmp"
+        if rc == 0:
+            cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp,
+                   *[r[0] for r in results], "-lpthread"]
+            proc = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+            log += " ".join(cmd) + "\n" + proc.stdout + proc.stderr
+            rc = proc.returncode
     with open(os.path.join(HERE, "build.log"), "w") as fh:
-        fh.write(" ".join(cmd) + "\n" + log)
-    if proc.returncode != 0:
+        fh.write(log)
+    if rc != 0:
         sys.stderr.write(log)
         raise RuntimeError("nvcc failed (see paper_2201_00613_b200/build.log)")
     if verbose:
