@@ -33,6 +33,7 @@ struct PackSmem {
   uint32_t* A0;   // kAdjSlots x ndirs x 128 adjacency words
   uint32_t* R;    // [4E][32] prefetched words holding out-of-chunk neighbour bits (next chunk)
   uint32_t* sl;   // [4E] link slot u = 4e + q: j2 << 10 | (direction * 128 + 32 q)
+  uint32_t* dp;   // [4 ndirs] direction pair v = 4d + q: first link << 16 | one past the last
   uint64_t* bar;  // [pstages] state copies landed, then [kAdjSlots] adjacency copies landed
   uint32_t ndirs, ns;
   __device__ __forceinline__ uint32_t* Z(uint32_t s) const { return Z0 + s * zw; }
@@ -57,6 +58,8 @@ __host__ __device__ inline size_t packed_layout(const TileParams& p, uint8_t* ba
   off += (size_t)4 * (prefetch_links(p) ? prefetch_links(p) : 1) * 32 * 4;
   if (s) s->sl = (uint32_t*)(base + off);
   off += align16((size_t)(p.E ? 4 * p.E : 1) * 4);
+  if (s) s->dp = (uint32_t*)(base + off);
+  off += align16((size_t)(p.ndirs ? 4 * p.ndirs : 1) * 4);
   if (s) s->bar = (uint64_t*)(base + off);
   off += (ns + kAdjSlots) * 8;
   return align16(off);
@@ -111,12 +114,16 @@ __device__ __forceinline__ void adj_load(const TileParams& p, const PackSmem& S,
 }
 
 // Link slot u = 4e + q: link e for the 32 tiles of lane group q (tiles 32q..32q+31 of the chunk).
-// Slots belong to warp u mod W, here and in the link phase of the next iteration (same thread:
-// program order suffices).  For a link whose neighbour tile is outside the chunk: a 4-byte
+// Two work splits.  SLOTS: slot u belongs to warp u mod W (few links per direction, e.g. the
+// Sierpinski triangle's 8 links).  PAIRS (BYDIR): the links of one direction d share each tile's
+// neighbour tile, so the work is split by pair v = 4d + q: the neighbour tile is read once per
+// pair, then each link of d costs one load, one ballot and one store (link-heavy fractals: the
+// carpet's 112 links per tile).  Either way a slot/pair belongs to the same warp here and in the
+// link phase of the next iteration (same thread: program order suffices).  For a link whose neighbour tile is outside the chunk: a 4-byte
 // cp.async of the packed word holding the neighbour bit.  `ntl` = the chunk's adjacency words
 // (neighbour tile + 1, from the coarse λ + ν at init: P:189 at tile level).  Commits one group.
 template <bool SHARDED>
-__device__ __forceinline__ void chunk_prefetch(const TileParams& p, const PackSmem& S, const PackChunk& pc,
+__device__ __forceinline__ void chunk_prefetch_slots(const TileParams& p, const PackSmem& S, const PackChunk& pc,
                                                const uint32_t* ntl, const uint32_t* __restrict__ cur32, int warp,
                                                int nwarps, int lane) {
   const uint32_t E = prefetch_links(p);
@@ -132,6 +139,37 @@ __device__ __forceinline__ void chunk_prefetch(const TileParams& p, const PackSm
     }
   }
   cp_async_commit();
+}
+
+template <bool SHARDED>
+__device__ __forceinline__ void chunk_prefetch_pairs(const TileParams& p, const PackSmem& S, const PackChunk& pc,
+                                               const uint32_t* ntl, const uint32_t* __restrict__ cur32, int warp,
+                                               int nwarps, int lane) {
+  if (prefetch_links(p)) {
+    for (uint32_t v = (uint32_t)warp; v < 4 * p.ndirs; v += (uint32_t)nwarps) {  // (direction, lane group)
+      const uint32_t q = v & 3u, d = v >> 2, span = S.dp[v];
+      const uint32_t a1 = ntl[d * kPackTiles + q * 32 + lane];
+      const uint32_t tl = a1 - 1u - (uint32_t)p.tile_lo;
+      if (a1 == 0 || a1 - 1u - pc.t0 < pc.nt) continue;
+      const bool local = !SHARDED || tl < (uint32_t)(p.tile_hi - p.tile_lo);
+      for (uint32_t e = span >> 16; e < (span & 0xFFFFu); ++e) {
+        const uint32_t j2 = S.sl[4 * e] >> 10, u = 4 * e + q;
+        if (local)
+          cp_async4(&S.R[u * 32 + lane], cur32 + ((uint64_t)(tl >> 7) * p.Kw + j2) * 4 + ((tl >> 5) & 3u));
+        else  // another shard's tile (sharded contexts): the bit from the halo, placed where the link reads it
+          S.R[u * 32 + lane] = halo_fetch(p.halo, (uint64_t)(a1 - 1u) * p.K + j2) << (tl & 31u);
+      }
+    }
+  }
+  cp_async_commit();
+}
+
+template <bool SHARDED, bool BYDIR>
+__device__ __forceinline__ void chunk_prefetch(const TileParams& p, const PackSmem& S, const PackChunk& pc,
+                                               const uint32_t* ntl, const uint32_t* __restrict__ cur32, int warp,
+                                               int nwarps, int lane) {
+  if (BYDIR) chunk_prefetch_pairs<SHARDED>(p, S, pc, ntl, cur32, warp, nwarps, lane);
+  else chunk_prefetch_slots<SHARDED>(p, S, pc, ntl, cur32, warp, nwarps, lane);
 }
 
 // Carry-save count of DMAX neighbour words and the rule, on one 32-bit lane of the word.
@@ -165,7 +203,7 @@ __device__ __forceinline__ uint32_t cell_rule(const uint32_t* x, uint32_t alive,
 // DMAX: neighbour slots per cell (5 for the Sierpinski triangle, else 8).  RB: j-blocks per warp
 // whose neighbour slots stay in registers for the whole launch (block jb = warp + i * W); later
 // blocks read their slots through L1.
-template <int DMAX, bool CONWAY, int RB, int MAXT, int MINB, bool SHARDED>
+template <int DMAX, bool CONWAY, int RB, int MAXT, int MINB, bool SHARDED, bool BYDIR>
 __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const uint4* __restrict__ cur,
                                                         uint4* __restrict__ next) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -192,6 +230,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
   for (uint32_t i = tid; i < NS * 4; i += blockDim.x) S.Z(i >> 2)[(Kw + E) * 4 + (i & 3)] = 0;  // zero slot
   for (uint32_t u = tid; u < 4 * E; u += blockDim.x)
     S.sl[u] = (p.link_j2[u >> 2] << 10) | (p.link_dir[u >> 2] * kPackTiles + 32 * (u & 3u));
+  for (uint32_t v = tid; v < 4 * p.ndirs; v += blockDim.x)
+    S.dp[v] = ((uint32_t)p.dir_start[v >> 2] << 16) | p.dir_start[(v >> 2) + 1];
   if (tid == 0) {
     for (uint32_t s = 0; s < NS + kAdjSlots; ++s) mbar_init(&S.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -206,7 +246,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
     for (uint32_t a = 0; a + 1 < kAdjSlots && c + a * G < nch; ++a) adj_load(p, S, pack_chunk(p, c + a * G), a);
   }
   mbar_wait(S.abar(0), 0);
-  chunk_prefetch<SHARDED>(p, S, pack_chunk(p, c), S.ntl(0), cur32, warp, nwarps, lane);
+  chunk_prefetch<SHARDED, BYDIR>(p, S, pack_chunk(p, c), S.ntl(0), cur32, warp, nwarps, lane);
 
   uint32_t it = 0, s = 0, sphase = 0;  // sphase bit s: parity of state stage s's next completion
   for (; c < nch; c += G, ++it, s = (s + 1 == NS) ? 0 : s + 1) {
@@ -220,6 +260,38 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
 
     // link words: bit i of u32 lane q of word Kw + e = cell j2 of the neighbour tile (link e)
     // of tile 32q + i
+    if (BYDIR) {
+    if ((uint32_t)warp < 4 * p.ndirs) {
+      mbar_wait(S.abar(a), (it / kAdjSlots) & 1);  // (already complete when the prefetch ran)
+      cp_async_wait_all();
+      const uint32_t rs = smem_u32(S.R) + lane * 4;
+      const uint32_t ntl_s = smem_u32(ntl) + lane * 4;
+      for (uint32_t v = (uint32_t)warp; v < 4 * p.ndirs; v += (uint32_t)nwarps) {  // (direction, lane group)
+        const uint32_t q = v & 3u, d = v >> 2, span = S.dp[v];
+        const uint32_t a1 = lds32(ntl_s + (d * kPackTiles + q * 32) * 4);
+        const uint32_t rel = a1 - 1u - pc.t0, tl = a1 - 1u - (uint32_t)p.tile_lo;
+        const bool in = rel < pc.nt;
+        const uint32_t present = a1 != 0 ? 1u : 0u;
+        const uint32_t sh = (in ? rel : tl) & 31u;
+        const uint32_t zrow = zs + (rel >> 5) * 4;
+        for (uint32_t e = span >> 16; e < (span & 0xFFFFu); ++e) {
+          const uint32_t j2 = S.sl[4 * e] >> 10, u = 4 * e + q;
+          uint32_t bit;
+          if (Epf) {  // branch-free: the word from this chunk's stage, or the prefetched one
+            bit = (lds32(in ? zrow + j2 * 16 : rs + u * 128) >> sh) & present;
+          } else {  // more links than the prefetch holds: synchronous gathers
+            bit = in           ? lds32(zrow + j2 * 16) >> sh
+                  : a1 == 0    ? 0u
+                  : !SHARDED || tl < nloc
+                      ? __ldg(cur32 + ((uint64_t)(tl >> 7) * Kw + j2) * 4 + ((tl >> 5) & 3u)) >> sh
+                      : halo_fetch(p.halo, (uint64_t)(a1 - 1u) * K + j2);  // another shard's tile
+          }
+          const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit & 1u);
+          if (lane == 0) Z[(Kw + e) * 4 + q] = bal;
+        }
+      }
+    }
+    } else {
     if ((uint32_t)warp < 4 * E) {
       mbar_wait(S.abar(a), (it / kAdjSlots) & 1);  // (already complete when the prefetch ran)
       cp_async_wait_all();
@@ -244,6 +316,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
         if (lane == 0) Z[(Kw + (u >> 2)) * 4 + (u & 3u)] = bal;
       }
     }
+    }
     __syncthreads();  // the one CTA barrier per chunk: state + link words in place, chunk it-1 done
     if (issuer) {
       if (c + (NS - 1) * G < nch) {
@@ -255,8 +328,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
     }
     if (c + G < nch) {  // out-of-chunk link gathers of the next chunk (its adjacency was issued long ago)
       const uint32_t a1 = (it + 1) & (kAdjSlots - 1);
-      if ((uint32_t)warp < 4 * Epf) mbar_wait(S.abar(a1), ((it + 1) / kAdjSlots) & 1);
-      chunk_prefetch<SHARDED>(p, S, pack_chunk(p, c + G), S.ntl(a1), cur32, warp, nwarps, lane);
+      if ((uint32_t)warp < (BYDIR ? 4 * p.ndirs : 4 * Epf) && Epf) mbar_wait(S.abar(a1), ((it + 1) / kAdjSlots) & 1);
+      chunk_prefetch<SHARDED, BYDIR>(p, S, pack_chunk(p, c + G), S.ntl(a1), cur32, warp, nwarps, lane);
     }
 
     // count + rule: lane = word j (128 cells), straight to HBM
@@ -429,7 +502,7 @@ __global__ void k_halo_pack_packed(const uint32_t* __restrict__ cur, const uint6
 using PackedFn = void (*)(TileParams, const uint4*, uint4*);
 
 // RB = j-blocks per warp with register-resident neighbour slots (ceil(nblk / W), capped).
-template <bool SH>
+template <bool SH, bool BD>
 static PackedFn pick_packed_t(const TileParams& p, int threads) {
   const bool conway = (p.birth == (1u << 3)) && (p.survive == ((1u << 2) | (1u << 3)));
   const uint32_t nblk = (uint32_t)((p.Kw + 31) / 32), W = (uint32_t)threads / 32;
@@ -437,26 +510,35 @@ static PackedFn pick_packed_t(const TileParams& p, int threads) {
   // small tiles: 3 blocks per warp, 3 CTAs per SM; large tiles (level 7 Sierpinski: 69 blocks):
   // all 9 blocks' slots in registers (108 registers), 2 CTAs per SM (tools/packed_timing.py)
   if (p.dmax <= 5) {
-    if (rb <= 3) return conway ? k_step_packed<5, true, 3, 256, 3, SH> : k_step_packed<5, false, 3, 256, 3, SH>;
-    return conway ? k_step_packed<5, true, 9, 256, 2, SH> : k_step_packed<5, false, 9, 256, 2, SH>;
+    if (rb <= 3) return conway ? k_step_packed<5, true, 3, 256, 3, SH, BD> : k_step_packed<5, false, 3, 256, 3, SH, BD>;
+    return conway ? k_step_packed<5, true, 9, 256, 2, SH, BD> : k_step_packed<5, false, 9, 256, 2, SH, BD>;
   }
-  if (rb <= 2) return conway ? k_step_packed<8, true, 2, 256, 3, SH> : k_step_packed<8, false, 2, 256, 3, SH>;
-  return conway ? k_step_packed<8, true, 6, 256, 2, SH> : k_step_packed<8, false, 6, 256, 2, SH>;
+  if (rb <= 2) return conway ? k_step_packed<8, true, 2, 256, 3, SH, BD> : k_step_packed<8, false, 2, 256, 3, SH, BD>;
+  return conway ? k_step_packed<8, true, 6, 256, 2, SH, BD> : k_step_packed<8, false, 6, 256, 2, SH, BD>;
+}
+
+// link work by (direction, lane group) pairs when directions carry several links each
+// (tools/packed_timing.py: carpet and empty bottles 20-23% faster, Sierpinski 6% slower)
+static bool links_by_direction(const TileParams& p) { return p.E >= 3 * p.ndirs; }
+
+template <bool SH>
+static PackedFn pick_packed_s(const TileParams& p, int threads) {
+  return links_by_direction(p) ? pick_packed_t<SH, true>(p, threads) : pick_packed_t<SH, false>(p, threads);
 }
 
 // SHARDED variants also read another shard's cells from the halo receive buffer.
 static PackedFn pick_packed(const TileParams& p, int threads) {
-  return p.halo.nneeds != 0 ? pick_packed_t<true>(p, threads) : pick_packed_t<false>(p, threads);
+  return p.halo.nneeds != 0 ? pick_packed_s<true>(p, threads) : pick_packed_s<false>(p, threads);
 }
 
 cudaError_t packed_prepare(const TileParams& p, size_t smem, int threads, int* occupancy) {
   cudaError_t e = cudaSuccess;
-  for (PackedFn fn : {pick_packed_t<false>(p, threads), pick_packed_t<true>(p, threads)}) {
+  for (PackedFn fn : {pick_packed_s<false>(p, threads), pick_packed_s<true>(p, threads)}) {
     e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   int blocks = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick_packed_t<false>(p, threads), threads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick_packed_s<false>(p, threads), threads, smem);
   if (e != cudaSuccess) return e;
   *occupancy = blocks;
   return blocks > 0 ? cudaSuccess : cudaErrorInvalidConfiguration;
