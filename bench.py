@@ -212,7 +212,7 @@ def cpu_baseline(args):
     try:
         import multiprocessing as mpc
         cores = len(os.sched_getaffinity(0))
-        big = min(sample * max(1, min(cores, 32)), f.k ** r)
+        big = min(sample * max(1, min(cores, 32)) // 4, f.k ** r)  # about 10 s of CPU work
         parts = [(lo, min(big, lo + -(-big // cores))) for lo in range(0, big, -(-big // cores))]
         with mpc.get_context("fork").Pool(len(parts)) as pool:
             pool.map(_oracle_part, [(args.fractal, r, lo, hi, args.seed, args.density) for lo, hi in parts[:1]])
