@@ -194,7 +194,8 @@ def run_sharded_packed_local(name, r, nranks, steps, g=0):
 
 @pytest.mark.parametrize("name,r,nranks,g", [("sierpinski-triangle", 10, 2, 3), ("sierpinski-triangle", 12, 3, 4),
                                              ("sierpinski-triangle", 13, 8, 5), ("sierpinski-carpet", 5, 4, 2),
-                                             ("empty-bottles", 6, 5, 2), ("sierpinski-triangle", 14, 2, 7)])
+                                             ("empty-bottles", 6, 5, 2), ("sierpinski-triangle", 14, 2, 7),
+                                             ("sierpinski-triangle", 4, 4, 1)])  # the last: 3 empty shards
 def test_sharded_packed_equals_oracle(name, r, nranks, g):
     got = run_sharded_packed_local(name, r, nranks, 5, g)
     assert np.array_equal(got, oracle_run(name, r, 42, 0.5, 5)[5])
