@@ -188,7 +188,8 @@ __device__ __forceinline__ uint32_t grab(uint32_t* ctr, int lane) { return grab(
 // gather of the word holding the neighbour cell.  The same warp consumes them in Phase B of
 // that chunk.  Always commits exactly one group.
 // Tile-padded byte layout: the gather fetches the aligned word holding the byte.
-__device__ __forceinline__ void chunk_neighbours(const TileParams& p, uint32_t* ntl, uint32_t* R, const ChunkInfo& c,
+__device__ __forceinline__ void chunk_neighbours(const TileParams& p, uint32_t* ntl, uint32_t* R, const uint32_t* lj2,
+                                                 const ChunkInfo& c,
                                                  const uint8_t* __restrict__ cur, int warp, int nwarps, int lane) {
   const uint64_t t = c.t0 + lane;
   const uint64_t t_end = c.t0 + c.nt;
@@ -198,10 +199,10 @@ __device__ __forceinline__ void chunk_neighbours(const TileParams& p, uint32_t* 
     const int64_t tn = (int64_t)a1 - 1;
     ntl[d * kChunkTiles + lane] = a1;  // tiles < 2^32 - 1 (checked on the host)
     if (tn >= 0 && ((uint64_t)tn < c.t0 || (uint64_t)tn >= t_end)) {
-      const uint32_t e1 = min((uint32_t)p.dir_start[d + 1], Epf);
-      for (uint32_t e = p.dir_start[d]; e < e1; ++e) {
+      const uint32_t e1 = min(lj2[p.E + d + 1], Epf);  // lj2: [E] link cells, then direction starts
+      for (uint32_t e = lj2[p.E + d]; e < e1; ++e) {
         uint32_t* dst = &R[e * kChunkTiles + lane];
-        const uint32_t j2 = p.link_j2[e];
+        const uint32_t j2 = lj2[e];
         if ((uint64_t)tn >= p.tile_lo && (uint64_t)tn < p.tile_hi) {
           const uint64_t off = ((uint64_t)tn - p.tile_lo) * p.Kp + j2;
           cp_async4(dst, cur + (off & ~3ull));

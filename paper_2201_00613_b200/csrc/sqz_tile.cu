@@ -36,6 +36,7 @@ struct TileSmem {
   uint32_t* R;     // [E][32] prefetched words holding out-of-chunk neighbour bytes — next chunk
   uint64_t* bar;   // [0,2) TMA loads landed, [2,4) all warps wrote the chunk's output
   uint32_t* ctr;   // [2] Phase-A and [2] count/write-back block counters, by chunk parity
+  uint32_t* lj2;   // [E] link e's cell in the neighbour tile, [E, E + ndirs + 1) direction starts
   __device__ __forceinline__ uint8_t* in(int b) const { return in0 + (size_t)b * cb; }
   __device__ __forceinline__ uint32_t* Z(int b) const { return Z0 + (size_t)b * zn; }
 };
@@ -63,6 +64,8 @@ __host__ __device__ inline size_t tile_layout(const TileParams& p, uint8_t* base
   off += 32;
   if (s) s->ctr = (uint32_t*)(base + off);
   off += 16;
+  if (s) s->lj2 = (uint32_t*)(base + off);
+  off += align16((size_t)(p.E + p.ndirs + 1) * 4);
   return align16(off);
 }
 
@@ -101,6 +104,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
   const uint32_t St = p.Kp;   // tile stride in shared memory
   const bool issuer = warp == lw && lane == 0;
 
+  // the link tables, read every chunk, from shared memory instead of global loads
+  for (uint32_t e = tid; e < p.E; e += blockDim.x) S.lj2[e] = p.link_j2[e];
+  for (uint32_t d = tid; d <= p.ndirs; d += blockDim.x) S.lj2[p.E + d] = p.dir_start[d];
   if (tid == 0) {
     S.Z(0)[p.zslot] = 0;
     S.Z(1)[p.zslot] = 0;
@@ -119,7 +125,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
   {  // prologue: chunk 0 loaded, neighbours + link prefetch of chunk 0
     const ChunkInfo c0 = chunk_info(p, chunk);
     if (issuer) chunk_load(p, c0, S.in(0), &S.bar[0], cur);
-    chunk_neighbours(p, S.ntl, S.R, c0, cur, warp, nwarps, lane);
+    chunk_neighbours(p, S.ntl, S.R, S.lj2, c0, cur, warp, nwarps, lane);
   }
 
   uint32_t it = 0;
@@ -150,9 +156,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
         const int64_t tn = (int64_t)S.ntl[d * kChunkTiles + lane] - 1;
         const uint64_t rel = (uint64_t)(tn - (int64_t)c.t0);
         const bool inside = tn >= 0 && rel < c.nt;
-        const uint32_t e1 = p.dir_start[d + 1];
-        for (uint32_t e = p.dir_start[d]; e < e1; ++e) {
-          const uint32_t j2 = p.link_j2[e];
+        const uint32_t e1 = S.lj2[p.E + d + 1];
+        for (uint32_t e = S.lj2[p.E + d]; e < e1; ++e) {
+          const uint32_t j2 = S.lj2[e];
           uint32_t v = 0;
           if (inside) v = inb[(uint32_t)rel * St + j2];
           else if (tn >= 0) {
@@ -178,7 +184,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     }
     __syncthreads();  // the one CTA barrier per chunk: all state and link words are in Zb
     // the next chunk's neighbour tiles + link prefetch overlap the count/write-back blocks
-    if (has_next) chunk_neighbours(p, S.ntl, S.R, chunk_info(p, chunk + G), cur, warp, nwarps, lane);
+    if (has_next) chunk_neighbours(p, S.ntl, S.R, S.lj2, chunk_info(p, chunk + G), cur, warp, nwarps, lane);
 
     // Phases C + D per j-block: lane L computes cell j0 + my_jj(L) of all 32 tiles (carry-save
     // count, rule), then the block is transposed back (lane = tile) and written in place.
