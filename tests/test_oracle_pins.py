@@ -414,3 +414,35 @@ def test_light_cone_embedding(f, r, g, T):
             big = automaton.compact_step(f, r, big)
         assert np.array_equal(big[t * K:(t + 1) * K], small)
         assert int(big.sum()) == int(small.sum())
+
+
+# ------------------------------------------------------------------ random NBB shapes
+@pytest.mark.parametrize("seed", range(8))
+def test_random_shapes_compact_equals_definition(seed):
+    """For random (s, k, τ): the construction table is a bijection onto the replication mask,
+    ν∘λ = id, and the λ/ν compact step (O6) equals the step on the embedding (O5) transported."""
+    rng = np.random.default_rng(1000 + seed)
+    s = int(rng.integers(2, 5))
+    k = int(rng.integers(1, s * s + 1))
+    cells = [(x, y) for y in range(s) for x in range(s)]
+    tau = tuple(cells[i] for i in rng.permutation(len(cells))[:k])
+    f = Fractal(f"rand{seed}", k, s, tau)
+    f.validate()
+    r = 0
+    while k ** (r + 1) <= 4096 and s ** (r + 1) <= 256:
+        r += 1
+    mask = construction.expanded_mask(f, r)
+    xs, ys = construction.construction_table(f, r)
+    assert int(mask.sum()) == k ** r
+    assert mask[ys, xs].all() and len(set(zip(xs.tolist(), ys.tolist()))) == k ** r
+    om = np.arange(k ** r, dtype=np.int64)
+    lx, ly = automaton.lambda_omega_np(f, r, om)
+    assert np.array_equal(lx, xs) and np.array_equal(ly, ys)
+    assert np.array_equal(automaton.nu_omega_np(f, r, xs, ys), om)
+    state, _ = automaton.seed_expanded(f, r, seed, 0.5)
+    cur = automaton.transport(f, r, state)
+    rule = (int(rng.integers(0, 512)), int(rng.integers(0, 512)))
+    for _ in range(3):
+        state = automaton.expanded_step(state, mask, rule)
+        cur = automaton.compact_step(f, r, cur, rule)
+        assert np.array_equal(cur, automaton.transport(f, r, state))
