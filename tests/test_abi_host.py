@@ -167,3 +167,18 @@ def test_shard_ranges_and_halo_plan(name, r, nranks):
         for rr in range(nranks):
             assert p.shard_range(rr) == product(name, r, rank=rr, nranks=nranks, tile_level=min(r, 3)).shard_range(rr)
     assert prev == V
+
+
+def test_missing_library_fails_loudly():
+    """No fallback: without the CUDA library every entry point raises (no CPU or PyTorch path)."""
+    import subprocess
+    import sys
+    code = ("import paper_2201_00613_b200 as pkg\n"
+            "try:\n"
+            "    pkg.Squeeze(pkg.Fractal('t', 3, 2, ((0, 0), (0, 1), (1, 1))), 4, device=0)\n"
+            "except pkg.SqueezeError as e:\n"
+            "    print('raised', e.status)\n")
+    env = dict(os.environ, SQZ_LIB="/nonexistent/libsqueeze.so")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert "raised -7" in out.stdout, out.stdout + out.stderr
