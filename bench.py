@@ -375,8 +375,8 @@ def main():
         e_ms = float(t[0])
         extras["e2e"] = {"value": cells_per_s(g.cells_total, K, e_ms), "unit": "cells/s",
                          "h2d_bytes_per_step": g.state_bytes * world / K, "d2h_bytes_per_step": g.state_bytes * world / K,
-                         "mode": f"ShardedSqueeze.run_host on every rank: H2D of the shard, {K} steps with NCCL "
-                                 f"halo exchange, D2H; max over ranks", "ms": e_ms}
+                         "mode": f"ShardedSqueeze.run_host on every rank: H2D of the shard, {K} steps with the "
+                                 f"{sh.transport} halo, D2H; max over ranks", "ms": e_ms}
         del h
     if rank == 0 and world == 1 and not args.no_extras:
         # repetitions of the K-step run (the first is the timed run above)

@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
   const int lw = nwarps - 1;  // the last warp issues TMA and the coarse λ
   const uint32_t St = p.Kp;   // tile stride in shared memory
   const bool issuer = warp == lw && lane == 0;
+  bool peer_sent = false;  // PEER: this lane stored halo cells into a peer buffer
 
   // the link tables, read every chunk, from shared memory instead of global loads
   for (uint32_t e = tid; e < p.E; e += blockDim.x) S.lj2[e] = p.link_j2[e];
@@ -142,6 +143,11 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
       }
     }
     if (tid == 0) S.ctr[buf ^ 1] = 0;  // next chunk's Phase-A counter (idle since the last barrier)
+    uint32_t pe0 = 0, pe1 = 0;  // PEER: this chunk's send range, loaded before the compute hides it
+    if (PEER && warp == lw) {
+      pe0 = p.peer_chunk_start[chunk];
+      pe1 = p.peer_chunk_start[chunk + 1];
+    }
     mbar_wait(&S.bar[buf], (it >> 1) & 1);
     uint8_t* inb = S.in(buf);
     uint32_t* Zb = S.Z(buf);
@@ -255,21 +261,25 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.bar[2 + buf]);
+    if (PEER && warp == lw && pe1 > pe0) {
+      // fused halo: the last warp stores this chunk's send cells straight into the peers' buffers
+      mbar_wait(&S.bar[2 + buf], (it >> 1) & 1);
+      for (uint32_t e = pe0 + (uint32_t)lane; e < pe1; e += 32) {
+        const uint32_t cell = p.peer_cell[e];
+        p.peer_recv[p.peer_of[e]][p.peer_pos[e]] = inb[(cell >> 16) * St + (cell & 0xFFFFu)];
+      }
+      peer_sent = true;
+      __syncwarp();
+    }
     if (issuer) {
       mbar_wait(&S.bar[2 + buf], (it >> 1) & 1);
-      if (PEER) {  // fused halo: this chunk's send cells go straight into the peers' buffers
-        const uint32_t e1 = p.peer_chunk_start[chunk + 1];
-        for (uint32_t e = p.peer_chunk_start[chunk]; e < e1; ++e) {
-          const uint32_t cell = p.peer_cell[e];
-          p.peer_recv[p.peer_of[e]][p.peer_pos[e]] = inb[(cell >> 16) * St + (cell & 0xFFFFu)];
-        }
-        __threadfence_system();
-      }
       chunk_store(p, c, inb, next);
     }
   }
   cp_async_wait_all();
   if (issuer) bulk_wait_all();
+  // one system-scope fence per storing thread, not per chunk (a MEMBAR.SYS costs microseconds)
+  if (PEER && peer_sent) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------------------
