@@ -1,8 +1,9 @@
 """Multi-PROCESS sharded run on one GPU: every rank is its own process with its own shard
 context on cuda:0, the halo travels through ``ShardedSqueeze`` / ``HaloExchange`` over a gloo
 group (host-staged; NCCL refuses two ranks on one device).  The union of the shards after
-T steps must equal the unsharded run byte for byte (itself pinned to the oracle).  This is
-the full product path of bench.py's N > 1 leg except the NCCL transport itself."""
+T steps must equal the unsharded run and the CPU oracle byte for byte.  This is the full
+product path of bench.py's N > 1 leg except the NCCL transport itself."""
+import functools
 import os
 import socket
 
@@ -13,6 +14,15 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
+
+
+@functools.lru_cache(maxsize=None)
+def _oracle_run(name, r, steps):
+    from oracle import automaton as A
+    from oracle.fractals import builtin
+
+    f = builtin(name)
+    return A.compact_run(f, r, A.seed_compact(f, r, 42, 0.5), steps)
 
 
 def _free_port():
@@ -68,3 +78,4 @@ def test_multiprocess_shards_equal_unsharded(name, r, world, steps, packed, tran
     fin = p.run(a, b, steps)
     torch.cuda.synchronize()
     assert np.array_equal(got, p.to_cells(fin).cpu().numpy())
+    assert np.array_equal(got, _oracle_run(name, r, steps))
