@@ -512,6 +512,9 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
             hn[j * 8 + k] = (uint16_t)slot;
           }
         c->heat_P = (uint32_t)hp.size();
+        // the same 128-bit quarter-warp bank-group spreading as the packed table (the slot order
+        // only changes the order of the float32 sum, inside the D16 bound)
+        optimize_slot_order(hn, c->tt.K, c->tt.max_degree <= 5 ? 5 : 8);
         if ((st = upload(&c->d_heat_nbr, hn.data(), hn.size())) != SQZ_OK) return fail(st);
         if ((st = upload(&c->d_heat_pairs, hp.data(), hp.size())) != SQZ_OK) return fail(st);
         if ((st = upload(&c->d_heat_j2, hj2.data(), hj2.size())) != SQZ_OK) return fail(st);
