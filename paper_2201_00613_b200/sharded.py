@@ -164,9 +164,12 @@ class ShardedSqueeze:
         self.primed = False  # the peer halo is pushed again from the new state
 
     def step(self, cur, nxt, naive: bool = False, ev0=None, ev1=None):
-        """One sharded step; ev0/ev1 (optional CUDA events) bracket the step kernel itself."""
+        """One sharded step; ev0/ev1 (optional CUDA events) bracket the step kernel itself.
+        Peer transport: `cur` must be the previous step's `nxt` (its halo was stored by that
+        step); `run` and `seed` re-push the halo from a new starting state."""
         if self.transport == "peer" and not naive:
             return self._step_peer(cur, nxt, ev0, ev1)
+        self._collective_halo()
         self.sq.halo_pack(cur)
         self.halo.exchange()
         if ev0 is not None:
@@ -174,6 +177,13 @@ class ShardedSqueeze:
         (self.sq.step_naive if naive else self.sq.step)(cur, nxt)
         if ev1 is not None:
             ev1.record()
+
+    def _collective_halo(self):
+        """A collective-halo step on a peer-transport shard: the context reads the exchange's
+        receive buffer again, and the next peer step re-pushes its halo."""
+        if self.transport == "peer":
+            self.sq.halo_bind(self.halo.send_buf, self.halo.recv_buf)
+            self.primed = False
 
     def _barrier(self):
         """Orders every rank's previous step before anyone's next one.  NCCL: a one-element
@@ -214,6 +224,7 @@ class ShardedSqueeze:
         self.sq.seed_packed(packed, seed, density)
 
     def step_packed(self, cur, nxt):
+        self._collective_halo()
         self.sq.halo_pack_packed(cur)
         self.halo.exchange()
         self.sq.step_packed(cur, nxt)

@@ -79,3 +79,37 @@ def test_multiprocess_shards_equal_unsharded(name, r, world, steps, packed, tran
     torch.cuda.synchronize()
     assert np.array_equal(got, p.to_cells(fin).cpu().numpy())
     assert np.array_equal(got, _oracle_run(name, r, steps))
+
+
+def _mixed_worker(rank, world, port, out):
+    """Peer transport with collective steps in between: peer, peer, literal (collective halo),
+    peer — the halo binding and the re-push must follow the transport of each step."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2201_00613_b200 as pkg
+        from paper_2201_00613_b200.sharded import ShardedSqueeze
+
+        torch.cuda.set_device(0)
+        sh = ShardedSqueeze(pkg.builtin_fractal("sierpinski-triangle"), 11, rank, world, 0, transport="peer")
+        a, b = sh.new_state(), sh.new_state()
+        sh.seed(a, 42, 0.5)
+        sh.step(a, b)
+        sh.step(b, a)
+        sh.step(a, b, naive=True)
+        sh.step(b, a)
+        torch.cuda.synchronize()
+        out[rank] = sh.sq.to_cells(a).cpu().numpy().copy()
+        assert sh.sq.device_error() == 0
+        sh.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_transport_mixed_with_collective_steps():
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.start_processes(_mixed_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
+    got = np.concatenate([out[0], out[1]])
+    assert np.array_equal(got, _oracle_run("sierpinski-triangle", 11, 4))
