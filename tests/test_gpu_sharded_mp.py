@@ -113,3 +113,65 @@ def test_peer_transport_mixed_with_collective_steps():
     mp.start_processes(_mixed_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
     got = np.concatenate([out[0], out[1]])
     assert np.array_equal(got, _oracle_run("sierpinski-triangle", 11, 4))
+
+
+def _digest(buf, n, piece=1 << 28):
+    """Position-weighted sums of bytes [0, n) of a device buffer, one per 256 MB piece: any single
+    differing byte changes its piece's sum (weights 1..65521)."""
+    out = []
+    for i in range(0, n, piece):
+        m = min(piece, n - i)
+        w = (torch.arange(m, device=buf.device, dtype=torch.int32) % 65521) + 1
+        out.append(int((buf[i:i + m].to(torch.int32) * w).sum(dtype=torch.int64).item()))
+    return out
+
+
+def _r22_peer_worker(rank, world, port, steps, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2201_00613_b200 as pkg
+        from paper_2201_00613_b200.sharded import ShardedSqueeze
+
+        torch.cuda.set_device(0)
+        sh = ShardedSqueeze(pkg.builtin_fractal("sierpinski-triangle"), 22, rank, world, 0, transport="peer")
+        a, b = sh.new_state(), sh.new_state()
+        sh.seed(a, 42, 0.5)
+        fin = sh.run(a, b, steps)
+        torch.cuda.synchronize()
+        g = sh.geometry
+        lo, hi = sh.sq.shard_range(rank)
+        t0, t1 = lo // g.tile_cells, hi // g.tile_cells
+        out[rank] = (t0, t1, _digest(fin, (t1 - t0) * g.tile_bytes), sh.sq.device_error())
+        del a, b, fin
+        sh.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_transport_r22_two_ranks_equals_unsharded():
+    """The fused peer-memory halo at the bench size: r=22 over 2 processes (peer transport, 3
+    steps, so the step kernel's own halo stores feed steps 2 and 3) equals the unsharded run
+    (itself pinned to the oracle) on every byte of each shard, compared through piecewise
+    position-weighted digests."""
+    import paper_2201_00613_b200 as pkg
+
+    steps = 3
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.start_processes(_r22_peer_worker, args=(2, _free_port(), steps, out), nprocs=2, join=True,
+                       start_method="spawn")
+    p = pkg.Squeeze(pkg.builtin_fractal("sierpinski-triangle"), 22, device=0)
+    a, b = p.new_state(), p.new_state()
+    p.seed(a, 42, 0.5)
+    fin = p.run(a, b, steps)
+    torch.cuda.synchronize()
+    kp = p.geometry.tile_bytes
+    for rank in range(2):
+        t0, t1, dig, err = out[rank]
+        assert err == 0
+        assert dig == _digest(fin[t0 * kp:], (t1 - t0) * kp), rank
+    del a, b, fin
+    p.close()
+    torch.cuda.empty_cache()
