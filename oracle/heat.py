@@ -109,14 +109,3 @@ def heat_compact_step_sampled(f: Fractal, r: int, omegas: np.ndarray, fetch, alp
     for i in range(8):
         flux += np.where(mem[i], look(np.where(mem[i], nbr[i], omegas)) - own, 0.0)
     return own + alpha * flux
-
-
-def fp32_step_bound(max_degree: int, alpha: float = ALPHA) -> float:
-    """Per-step bound, in units of eps32 x max|u|, on the deviation of a float32 evaluation of
-    the step from the exact one when the float32 side sums D = max_degree slots (absent
-    neighbours as the cell itself, which adds a zero term), forms s - D*u and applies one fused
-    multiply-add: (D - 1) * D (the sum) + D (D*u) + 2D (the difference), scaled by alpha, plus
-    the final rounding.  With alpha * D <= 1 the step is a convex combination (the maximum
-    principle), so the deviations of successive steps add: T steps -> T x this bound."""
-    d = max_degree
-    return alpha * ((d - 1) * d + d + 2 * d) + 1.0

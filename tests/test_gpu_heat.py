@@ -1,8 +1,9 @@
 """GPU parity of the heat-diffusion workload (reading D16) against the
 float64 CPU oracle (oracle/heat.py).
 
-Tolerance: the kernel evaluates each step in float32; ``heat.fp32_step_bound`` derives the
-per-step deviation (units of eps32 x max|u|) from its operation order, and because every step
+Tolerance: the kernel evaluates each step in float32; ``tests/heat_bound.fp32_step_bound(D)``
+derives the per-step deviation (units of eps32 x max|u|) from its operation order for the
+kernel's D neighbour slots (5 for the Sierpinski triangle, else 8), and because every step
 is a convex combination (α · max_degree <= 1) deviations of T steps add up to at most
 T x that bound.  The initial field is exact in float32 (24-bit values), so the seeds must
 match exactly.
@@ -13,6 +14,7 @@ import torch
 
 import paper_2201_00613_b200 as sq
 import sqz_inputs
+from heat_bound import fp32_step_bound, kernel_slots
 from oracle import heat
 from oracle.fractals import BUILTINS, SIERPINSKI
 
@@ -29,8 +31,9 @@ def cells(p, u):
     return p.heat_to_cells(u).double().cpu().numpy()
 
 
-def tol(steps, u0_max=1.0):
-    return steps * heat.fp32_step_bound(8) * EPS * u0_max
+def tol(steps, p, u0_max=1.0):
+    """T steps x the per-step bound for this context's slot count x max|u0| (u0 < 1)."""
+    return steps * fp32_step_bound(kernel_slots(p.geometry.max_degree)) * EPS * u0_max
 
 
 CASES = [("sierpinski-triangle", 0, 0), ("sierpinski-triangle", 2, 1), ("sierpinski-triangle", 8, 0),
@@ -51,7 +54,7 @@ def test_heat_seed_and_steps_vs_oracle(name, r, g):
     for t in range(steps):
         p.heat_step(a, b)
         want = heat.heat_compact_step(f, r, want)
-        np.testing.assert_allclose(cells(p, b), want, rtol=0, atol=tol(t + 1), err_msg=f"step {t + 1}")
+        np.testing.assert_allclose(cells(p, b), want, rtol=0, atol=tol(t + 1, p), err_msg=f"step {t + 1}")
         a, b = b, a
 
 
@@ -82,7 +85,7 @@ def test_heat_alpha(alpha):
     fin = p.heat_run(a, b, 4, alpha)
     want = heat.heat_compact_run(SIERPINSKI, r, heat.seed_heat_compact(SIERPINSKI, r, 8), 4,
                                  float(np.float32(alpha)))
-    np.testing.assert_allclose(cells(p, fin), want, rtol=0, atol=tol(4))
+    np.testing.assert_allclose(cells(p, fin), want, rtol=0, atol=tol(4, p))
 
 
 def test_heat_conservation_and_sum():
@@ -95,7 +98,7 @@ def test_heat_conservation_and_sum():
     fin = p.heat_run(a, b, 10)
     s1 = p.heat_sum(fin).item()
     n = 3 ** r
-    assert abs(s1 - s0) <= n * tol(10)
+    assert abs(s1 - s0) <= n * tol(10, p)
 
 
 def test_heat_rejects_aliasing():
@@ -125,4 +128,4 @@ def test_heat_full_size_sampled():
 
     assert np.array_equal(fetch(a, om), heat.seed_heat_at(SIERPINSKI, r, om, 42))
     want = heat.heat_compact_step_sampled(SIERPINSKI, r, om, lambda q: fetch(a, q))
-    np.testing.assert_allclose(fetch(b, om), want, rtol=0, atol=tol(1))
+    np.testing.assert_allclose(fetch(b, om), want, rtol=0, atol=tol(1, p))

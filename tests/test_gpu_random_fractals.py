@@ -9,6 +9,7 @@ import torch
 
 import paper_2201_00613_b200 as sq
 from oracle import automaton as A
+from heat_bound import fp32_step_bound, kernel_slots
 from oracle import heat
 from oracle.fractals import Fractal
 
@@ -86,4 +87,4 @@ def test_random_fractal_parity(seed, s, k):
         u = heat.heat_compact_step(f, r, u)
     torch.cuda.synchronize()
     got_u = p.heat_to_cells(fin).double().cpu().numpy()
-    np.testing.assert_allclose(got_u, u, rtol=0, atol=3 * heat.fp32_step_bound(8) * 2.0 ** -24)
+    np.testing.assert_allclose(got_u, u, rtol=0, atol=3 * fp32_step_bound(kernel_slots(p.geometry.max_degree)) * 2.0 ** -24)

@@ -14,6 +14,7 @@ import pytest
 import scipy.ndimage
 
 import sqz_inputs
+from heat_bound import fp32_step_bound
 from oracle import automaton, construction, heat
 from oracle.fractals import BUILTINS, CARPET, EMPTY_BOTTLES, FULL_SQUARE, SIERPINSKI, VICSEK
 
@@ -119,23 +120,27 @@ def test_initial_field_is_float32_exact():
     assert np.all((u * (1 << sqz_inputs.HEAT_BITS)) == np.floor(u * (1 << sqz_inputs.HEAT_BITS)))
 
 
-@pytest.mark.parametrize("f,r", [(SIERPINSKI, 6), (CARPET, 3)])
-def test_fp32_bound_holds_for_a_float32_evaluation(f, r):
-    """A float32 evaluation in the order the bound assumes (D slots, absent ones as the cell
-    itself, s - D*u, one fused multiply-add emulated in float64 then rounded) stays within
-    T x fp32_step_bound x eps32 x max|u0| of the float64 oracle."""
-    D = 8
+@pytest.mark.parametrize("f,r,D", [(SIERPINSKI, 6, 5), (SIERPINSKI, 6, 8), (CARPET, 3, 8)])
+def test_fp32_bound_holds_for_a_float32_evaluation(f, r, D):
+    """A float32 evaluation in the order the bound assumes (D slots: the member neighbours, then
+    the cell itself for the rest, s - D*u, one fused multiply-add emulated in float64 then
+    rounded) stays within T x fp32_step_bound(D) x eps32 x max|u0| of the float64 oracle.
+    D = 5 is the Sierpinski kernel's slot count (never more than 5 member neighbours, pin 7)."""
     u64 = heat.seed_heat_compact(f, r, 6)
     u32 = u64.astype(np.float32)
     om = np.arange(f.k ** r)
     nbr, mem = automaton.compact_neighbours(f, r, om)
+    assert int(mem.sum(axis=0).max()) <= D
     T = 12
     for _ in range(T):
         s = np.zeros(om.size, dtype=np.float32)
         for i in range(8):
-            s = (s + np.where(mem[i], u32[nbr[i]], u32)).astype(np.float32)
+            s = (s + np.where(mem[i], u32[nbr[i]], np.float32(0))).astype(np.float32)
+        pad = D - mem.sum(axis=0)
+        for k in range(D):
+            s = np.where(pad > k, (s + u32).astype(np.float32), s)
         d = (s - np.float32(D) * u32).astype(np.float32)
         u32 = (u32.astype(np.float64) + heat.ALPHA * d.astype(np.float64)).astype(np.float32)
         u64 = heat.heat_compact_step(f, r, u64)
-    bound = T * heat.fp32_step_bound(D) * 2.0 ** -24
+    bound = T * fp32_step_bound(D) * 2.0 ** -24
     assert np.max(np.abs(u32 - u64)) <= bound

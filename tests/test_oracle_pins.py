@@ -319,6 +319,63 @@ def test_seed_density_extremes_and_determinism():
         int(sqz_inputs.alive_bits(np.array([3]), np.array([5]), 42, sqz_inputs.density_threshold(0.5))[0])
 
 
+@pytest.mark.parametrize("f,rmax", SMALL)
+def test_seed_at_equals_seed_compact(f, rmax):
+    """``seed_at`` (D9 at λ(Ω) through the vectorised closed-form maps, the expected value of
+    every full-size GPU seed check) equals ``seed_compact`` (D9 at the O2 construction table,
+    which ``test_compact_equals_expanded_definition`` ties to the expanded O4 draw) at EVERY Ω.
+    D9 is not symmetric in (X, Y), so an x/y swap in either helper fails here."""
+    for r in range(rmax + 1):
+        om = np.arange(f.k ** r, dtype=np.int64)
+        for seed, density in ((42, 0.5), (7, 0.3)):
+            assert np.array_equal(automaton.seed_at(f, r, om, seed, density),
+                                  automaton.seed_compact(f, r, seed, density)), (f.name, r, seed)
+    st, _ = automaton.seed_expanded(SIERPINSKI, 5, 3, 0.5)
+    assert not np.array_equal(st, st.T)  # the draw really tells x from y
+
+
+@pytest.mark.parametrize("f,r,g", [(SIERPINSKI, 22, 11), (SIERPINSKI, 24, 12), (CARPET, 10, 5),
+                                   (EMPTY_BOTTLES, 11, 6)])
+def test_seed_at_large_level_by_block_decomposition(f, r, g):
+    """At the full-size levels (no O2 table of k^r entries fits) ``seed_at`` is pinned by the O2
+    recursion unrolled g times: C_r[t·k^g + j] = s^g·C_{r-g}[t] + C_g[j] (the low g digits of Ω
+    address the level-g sub-fractal), both tables built by array recursion only."""
+    xs_hi, ys_hi = construction.construction_table(f, r - g)
+    xs_lo, ys_lo = construction.construction_table(f, g)
+    om = np.unique(sqz_inputs.random_indices(20000, f.k ** r, seed=11).astype(np.int64))
+    om = np.concatenate([om, [0, f.k ** r - 1]])
+    t, j = om // f.k ** g, om % f.k ** g
+    X = f.s ** g * xs_hi[t] + xs_lo[j]
+    Y = f.s ** g * ys_hi[t] + ys_lo[j]
+    x, y = automaton.lambda_omega_np(f, r, om)
+    assert np.array_equal(x, X) and np.array_equal(y, Y)
+    q = sqz_inputs.density_threshold(0.5)
+    assert np.array_equal(automaton.seed_at(f, r, om, 42, 0.5), sqz_inputs.alive_bits(X, Y, 42, q))
+
+
+@pytest.mark.parametrize("f,rmax", SMALL)
+def test_inverse_table_inverts_construction_and_marks_holes(f, rmax):
+    """``inverse_table`` (the expected value of the exhaustive ν map tests) against the pinned
+    O1/O2 constructions: E[C_r[Ω]] = Ω for every Ω, and E = -1 exactly on the holes of the O1
+    replication mask (indexed [y, x] like the mask)."""
+    for r in range(rmax + 1):
+        e = construction.inverse_table(f, r)
+        xs, ys = construction.construction_table(f, r)
+        assert np.array_equal(e[ys, xs], np.arange(f.k ** r))
+        mask = construction.expanded_mask(f, r)
+        assert np.array_equal(e == -1, ~mask)
+        assert int((e >= 0).sum()) == f.k ** r
+
+
+def test_inverse_table_orientation_is_pascal():
+    """Independent of O1/O2: E[y, x] >= 0 iff C(y, x) is odd (Lucas, P:224 orientation)."""
+    r = 6
+    e = construction.inverse_table(SIERPINSKI, r)
+    for y in range(2 ** r):
+        for x in range(2 ** r):
+            assert (e[y, x] >= 0) == (x <= y and math.comb(y, x) % 2 == 1), (x, y)
+
+
 def test_mix_known_value():
     """splitmix64 finaliser of 0 is 0; the reference splitmix64 stream from state 0 starts
     with 0xE220A8397B1DCDAF = mix(0x9E3779B97F4A7C15) (textbook generator output)."""
