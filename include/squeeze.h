@@ -179,15 +179,18 @@ squeeze_status squeeze_step_naive(void* ctx, const uint8_t* d_cur, uint8_t* d_ne
  * captures the two-step ping-pong once into a CUDA graph and replays it. */
 squeeze_status squeeze_run(void* ctx, uint8_t* d_a, uint8_t* d_b, uint64_t steps, int use_graph,
                            squeeze_stream_t stream);
-/* End to end from HOST memory: copies h_state (this shard's tile-padded state, state_bytes long,
- * ideally pinned) to d_a, runs `steps` steps, copies the final state back into h_state,
- * and synchronises `stream`.  d_a, d_b are caller-owned device scratch buffers. */
+/* End to end from HOST memory: copies h_state (the tile-padded state, state_bytes long, ideally
+ * pinned) to d_a, runs `steps` steps, copies the final state back into h_state, and synchronises
+ * `stream`.  d_a, d_b are caller-owned device scratch buffers.  Unsharded contexts only:
+ * SQZ_E_CONFIG (before any copy is enqueued) for a sharded context or aliased d_a == d_b.  The
+ * library cannot see the host buffer's length: the caller guarantees state_bytes. */
 squeeze_status squeeze_run_host(void* ctx, uint8_t* h_state, uint8_t* d_a, uint8_t* d_b, uint64_t steps,
                                 squeeze_stream_t stream);
 /* *d_out (device uint64) = number of alive cells of this shard. */
 squeeze_status squeeze_count_alive(const void* ctx, const uint8_t* d_state, uint64_t* d_out,
                                    squeeze_stream_t stream);
-/* Copy of the device-side error flag (synchronises the device): SQZ_OK or SQZ_E_HALO. */
+/* Reads AND CLEARS the device-side error flag (synchronises the device): SQZ_E_HALO once for
+ * every run of steps in which a kernel missed a halo cell, then SQZ_OK again. */
 squeeze_status squeeze_device_error(const void* ctx);
 
 /* ---- halo exchange plan for sharded contexts (data moved by the caller, e.g. NCCL) ---- */
@@ -209,9 +212,11 @@ squeeze_status squeeze_halo_pack(const void* ctx, const uint8_t* d_cur, squeeze_
  * (e.g. a barrier after each step) and alternates two receive buffers by step parity.
  * squeeze_ipc_handle / _open / _close: cudaIpc{Get,Open,Close}MemHandle (64-byte handles).
  * squeeze_halo_peer_plan: destination of every send (squeeze_halo_set_sends order): peer slot
- *   send_peer[i] and byte position send_pos[i] in that peer's receive buffer.
+ *   send_peer[i] (the destination RANK: < nranks and != this rank, else SQZ_E_CONFIG) and byte
+ *   position send_pos[i] in that peer's receive buffer (the caller's plan guarantees it is below
+ *   the receiver's squeeze_halo_needs count).  squeeze_halo_set_sends drops an existing peer plan.
  * squeeze_halo_peer_bind: device pointers (IPC-opened) of the peers' receive buffers for one
- *   parity, indexed by peer slot.  squeeze_halo_peer_select: parity the next squeeze_step writes
+ *   parity, indexed by peer slot: npeers must be 0 (unbind) or nranks (SQZ_E_CONFIG otherwise).  squeeze_halo_peer_select: parity the next squeeze_step writes
  *   (-1 = off, the default).  Byte state only (squeeze_step). */
 squeeze_status squeeze_ipc_handle(const void* d_ptr, uint8_t* handle);
 squeeze_status squeeze_ipc_open(const uint8_t* handle, int device, void** d_ptr);

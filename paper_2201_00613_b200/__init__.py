@@ -85,6 +85,13 @@ def ipc_close(ptr: int) -> None:
     _lib.check(_lib.load().squeeze_ipc_close(ptr), "ipc_close")
 
 
+E_CONFIG = -6  # SQZ_E_CONFIG (include/squeeze.h)
+
+
+def _bad(what: str, why: str):
+    return SqueezeError(E_CONFIG, f"{what}: {why}")
+
+
 def _stream(stream, device):
     import torch
     if stream is None:
@@ -127,6 +134,49 @@ class Squeeze:
             self.close()
         except Exception:
             pass
+
+    # ------------------------------------------------------------------ argument checks
+    # The C ABI sees raw pointers only, so the binding checks what it cannot: tensor type, device,
+    # contiguity, dtype and size.  A failed check raises SqueezeError(SQZ_E_CONFIG) before any call.
+    def _dev(self, t, what, dtypes, nbytes=0, numel=None):
+        import torch
+        if not isinstance(t, torch.Tensor):
+            raise _bad(what, f"expected a torch tensor, got {type(t).__name__}")
+        if t.device.type != "cuda" or (self.device is not None and t.device.index != int(self.device)):
+            raise _bad(what, f"tensor on {t.device}, context on cuda:{self.device}")
+        if not t.is_contiguous():
+            raise _bad(what, "tensor must be contiguous")
+        if dtypes and t.dtype not in dtypes:
+            raise _bad(what, f"dtype {t.dtype}, expected one of {[str(d) for d in dtypes]}")
+        if t.numel() * t.element_size() < nbytes:
+            raise _bad(what, f"{t.numel() * t.element_size()} bytes < required {nbytes}")
+        if numel is not None and t.numel() != numel:
+            raise _bad(what, f"{t.numel()} elements, expected {numel}")
+        return t
+
+    def _host(self, t, what, dtypes, nbytes):
+        import torch
+        if not isinstance(t, torch.Tensor) or t.device.type != "cpu":
+            raise _bad(what, "expected a CPU tensor")
+        if not t.is_contiguous():
+            raise _bad(what, "tensor must be contiguous")
+        if dtypes and t.dtype not in dtypes:
+            raise _bad(what, f"dtype {t.dtype}, expected one of {[str(d) for d in dtypes]}")
+        if t.numel() * t.element_size() < nbytes:
+            raise _bad(what, f"{t.numel() * t.element_size()} bytes < required {nbytes}")
+        return t
+
+    def _state(self, t, what):
+        import torch
+        return self._dev(t, what, (torch.uint8,), self.geometry.state_bytes)
+
+    def _packed(self, t, what):
+        import torch
+        return self._dev(t, what, (torch.int32, torch.uint32), self.geometry.packed_bytes)
+
+    def _heat(self, t, what):
+        import torch
+        return self._dev(t, what, (torch.float32,), self.geometry.heat_bytes)
 
     # ------------------------------------------------------------------ host helpers
     def lambda_host(self, omega: int) -> tuple:
@@ -191,7 +241,7 @@ class Squeeze:
 
     def map_lambda(self, omega, stream=None):
         import torch
-        omega = omega.contiguous()
+        self._dev(omega, "map_lambda omega", (torch.int64,))
         x = torch.empty(omega.numel(), dtype=torch.int32, device=omega.device)
         y = torch.empty_like(x)
         _lib.check(self.lib.squeeze_map_lambda(self.ctx, _ptr(omega), _ptr(x), _ptr(y), omega.numel(),
@@ -200,8 +250,8 @@ class Squeeze:
 
     def map_nu(self, x, y, stream=None):
         import torch
-        x = x.contiguous()
-        y = y.contiguous()
+        self._dev(x, "map_nu x", (torch.int32, torch.uint32))
+        self._dev(y, "map_nu y", (torch.int32, torch.uint32), numel=x.numel())
         om = torch.empty(x.numel(), dtype=torch.int64, device=x.device)
         _lib.check(self.lib.squeeze_map_nu(self.ctx, _ptr(x), _ptr(y), _ptr(om), x.numel(),
                                            _stream(stream, x.device)), "map_nu")
@@ -210,39 +260,52 @@ class Squeeze:
     def map_nu_mma(self, x, y, stream=None):
         """ν through the integer tensor-core product (NEXT-3 ablation); same output as map_nu."""
         import torch
-        x = x.contiguous()
-        y = y.contiguous()
+        self._dev(x, "map_nu_mma x", (torch.int32, torch.uint32))
+        self._dev(y, "map_nu_mma y", (torch.int32, torch.uint32), numel=x.numel())
         om = torch.empty(x.numel(), dtype=torch.int64, device=x.device)
         _lib.check(self.lib.squeeze_map_nu_mma(self.ctx, _ptr(x), _ptr(y), _ptr(om), x.numel(),
                                                _stream(stream, x.device)), "map_nu_mma")
         return om
 
     def seed(self, state, seed: int = 42, density: float = 0.5, stream=None):
+        self._state(state, "seed")
         _lib.check(self.lib.squeeze_seed(self.ctx, _ptr(state), seed, density_q(density),
                                          _stream(stream, state.device)), "seed")
 
     def step(self, cur, nxt, stream=None):
+        self._state(cur, "step cur")
+        self._state(nxt, "step next")
         _lib.check(self.lib.squeeze_step(self.ctx, _ptr(cur), _ptr(nxt), _stream(stream, cur.device)), "step")
 
     def step_naive(self, cur, nxt, stream=None):
+        self._state(cur, "step_naive cur")
+        self._state(nxt, "step_naive next")
         _lib.check(self.lib.squeeze_step_naive(self.ctx, _ptr(cur), _ptr(nxt), _stream(stream, cur.device)),
                    "step_naive")
 
     def run(self, a, b, steps: int, use_graph: bool = False, stream=None):
         """Returns the tensor holding the final state (b if steps is odd, else a)."""
+        self._state(a, "run a")
+        self._state(b, "run b")
         _lib.check(self.lib.squeeze_run(self.ctx, _ptr(a), _ptr(b), steps, int(use_graph),
                                         _stream(stream, a.device)), "run")
         return b if steps % 2 else a
 
     def run_host(self, h_state, a, b, steps: int, stream=None):
         """End to end from host memory (h_state: CPU uint8 tensor, ideally pinned)."""
+        import torch
+        self._host(h_state, "run_host h_state", (torch.uint8,), self.geometry.state_bytes)
+        self._state(a, "run_host a")
+        self._state(b, "run_host b")
         _lib.check(self.lib.squeeze_run_host(self.ctx, _ptr(h_state), _ptr(a), _ptr(b), steps,
                                              _stream(stream, a.device)), "run_host")
 
     def count_alive(self, state, out=None, stream=None):
         import torch
+        self._state(state, "count_alive")
         if out is None:
             out = torch.zeros(1, dtype=torch.int64, device=state.device)
+        self._dev(out, "count_alive out", (torch.int64,), 8)
         _lib.check(self.lib.squeeze_count_alive(self.ctx, _ptr(state), _ptr(out), _stream(stream, state.device)),
                    "count_alive")
         return out
@@ -267,10 +330,12 @@ class Squeeze:
         _lib.check(self.lib.squeeze_halo_peer_select(self.ctx, parity), "halo_peer_select")
 
     def halo_peer_push(self, cur, parity: int, stream=None) -> None:
+        self._state(cur, "halo_peer_push")
         _lib.check(self.lib.squeeze_halo_peer_push(self.ctx, _ptr(cur), parity, _stream(stream, cur.device)),
                    "halo_peer_push")
 
     def halo_pack(self, cur, stream=None) -> None:
+        self._state(cur, "halo_pack")
         _lib.check(self.lib.squeeze_halo_pack(self.ctx, _ptr(cur), _stream(stream, cur.device)), "halo_pack")
 
     # ------------------------------------------------------------------ packed state (NEXT-1)
@@ -279,25 +344,35 @@ class Squeeze:
         return torch.empty(max(16, self.geometry.packed_bytes) // 4, dtype=torch.int32, device=f"cuda:{self.device}")
 
     def halo_pack_packed(self, cur, stream=None) -> None:
+        self._packed(cur, "halo_pack_packed")
         _lib.check(self.lib.squeeze_halo_pack_packed(self.ctx, _ptr(cur), _stream(stream, cur.device)),
                    "halo_pack_packed")
 
     def pack(self, state, packed, stream=None):
+        self._state(state, "pack state")
+        self._packed(packed, "pack packed")
         _lib.check(self.lib.squeeze_pack(self.ctx, _ptr(state), _ptr(packed), _stream(stream, state.device)), "pack")
 
     def unpack(self, packed, state, stream=None):
+        self._packed(packed, "unpack packed")
+        self._state(state, "unpack state")
         _lib.check(self.lib.squeeze_unpack(self.ctx, _ptr(packed), _ptr(state), _stream(stream, state.device)),
                    "unpack")
 
     def seed_packed(self, packed, seed: int = 42, density: float = 0.5, stream=None):
+        self._packed(packed, "seed_packed")
         _lib.check(self.lib.squeeze_seed_packed(self.ctx, _ptr(packed), seed, density_q(density),
                                                 _stream(stream, packed.device)), "seed_packed")
 
     def step_packed(self, cur, nxt, stream=None):
+        self._packed(cur, "step_packed cur")
+        self._packed(nxt, "step_packed next")
         _lib.check(self.lib.squeeze_step_packed(self.ctx, _ptr(cur), _ptr(nxt), _stream(stream, cur.device)),
                    "step_packed")
 
     def run_packed(self, a, b, steps: int, stream=None):
+        self._packed(a, "run_packed a")
+        self._packed(b, "run_packed b")
         _lib.check(self.lib.squeeze_run_packed(self.ctx, _ptr(a), _ptr(b), steps, _stream(stream, a.device)),
                    "run_packed")
         return b if steps % 2 else a
@@ -305,13 +380,19 @@ class Squeeze:
     def run_host_packed(self, h_packed, a, b, steps: int, stream=None):
         """End to end from host memory on the packed state (h_packed: CPU int32 tensor of
         packed_bytes / 4 words, ideally pinned); the final state is written back into it."""
+        import torch
+        self._host(h_packed, "run_host_packed h_packed", (torch.int32, torch.uint32), self.geometry.packed_bytes)
+        self._packed(a, "run_host_packed a")
+        self._packed(b, "run_host_packed b")
         _lib.check(self.lib.squeeze_run_host_packed(self.ctx, _ptr(h_packed), _ptr(a), _ptr(b), steps,
                                                     _stream(stream, a.device)), "run_host_packed")
 
     def count_alive_packed(self, packed, out=None, stream=None):
         import torch
+        self._packed(packed, "count_alive_packed")
         if out is None:
             out = torch.zeros(1, dtype=torch.int64, device=packed.device)
+        self._dev(out, "count_alive_packed out", (torch.int64,), 8)
         _lib.check(self.lib.squeeze_count_alive_packed(self.ctx, _ptr(packed), _ptr(out),
                                                        _stream(stream, packed.device)), "count_alive_packed")
         return out
@@ -332,21 +413,28 @@ class Squeeze:
         return torch.zeros(max(4, self.geometry.heat_bytes // 4), dtype=torch.float32, device=f"cuda:{self.device}")
 
     def heat_seed(self, u, seed: int = 42, stream=None):
+        self._heat(u, "heat_seed")
         _lib.check(self.lib.squeeze_heat_seed(self.ctx, _ptr(u), seed, _stream(stream, u.device)), "heat_seed")
 
     def heat_step(self, cur, nxt, alpha: float = 0.125, stream=None):
+        self._heat(cur, "heat_step cur")
+        self._heat(nxt, "heat_step next")
         _lib.check(self.lib.squeeze_heat_step(self.ctx, _ptr(cur), _ptr(nxt), alpha, _stream(stream, cur.device)),
                    "heat_step")
 
     def heat_run(self, a, b, steps: int, alpha: float = 0.125, stream=None):
+        self._heat(a, "heat_run a")
+        self._heat(b, "heat_run b")
         _lib.check(self.lib.squeeze_heat_run(self.ctx, _ptr(a), _ptr(b), steps, alpha, _stream(stream, a.device)),
                    "heat_run")
         return b if steps % 2 else a
 
     def heat_sum(self, u, out=None, stream=None):
         import torch
+        self._heat(u, "heat_sum")
         if out is None:
             out = torch.zeros(1, dtype=torch.float64, device=u.device)
+        self._dev(out, "heat_sum out", (torch.float64,), 8)
         _lib.check(self.lib.squeeze_heat_sum(self.ctx, _ptr(u), _ptr(out), _stream(stream, u.device)), "heat_sum")
         return out
 
@@ -360,6 +448,9 @@ class Squeeze:
     # ------------------------------------------------------------------ paper comparison engines (NEXT-2)
     def lambda_engine_step(self, cur_grid, next_grid, stream=None):
         """λ(ω) engine: compact thread grid over an expanded BB-layout grid."""
+        import torch
+        self._dev(cur_grid, "lambda_engine_step cur", (torch.uint8,), self.bb_bytes())
+        self._dev(next_grid, "lambda_engine_step next", (torch.uint8,), self.bb_bytes())
         _lib.check(self.lib.squeeze_lambda_engine_step(self.ctx, _ptr(cur_grid), _ptr(next_grid),
                                                        _stream(stream, cur_grid.device)), "lambda_engine_step")
 
@@ -373,11 +464,16 @@ class Squeeze:
         return torch.empty(max(16, self.block_bytes(rho)), dtype=torch.uint8, device=f"cuda:{self.device}")
 
     def block_seed(self, rho: int, blocks, seed: int = 42, density: float = 0.5, stream=None):
+        import torch
+        self._dev(blocks, "block_seed", (torch.uint8,), self.block_bytes(rho))
         _lib.check(self.lib.squeeze_block_seed(self.ctx, rho, _ptr(blocks), seed, density_q(density),
                                                _stream(stream, blocks.device)), "block_seed")
 
     def block_step(self, rho: int, cur, nxt, stream=None):
         """Block-level Squeeze with rho x rho expanded micro-embeddings per block."""
+        import torch
+        self._dev(cur, "block_step cur", (torch.uint8,), self.block_bytes(rho))
+        self._dev(nxt, "block_step next", (torch.uint8,), self.block_bytes(rho))
         _lib.check(self.lib.squeeze_block_step(self.ctx, rho, _ptr(cur), _ptr(nxt), _stream(stream, cur.device)),
                    "block_step")
 
@@ -392,13 +488,21 @@ class Squeeze:
         return torch.empty(self.bb_bytes(), dtype=torch.uint8, device=f"cuda:{self.device}")
 
     def bb_seed(self, grid, seed: int = 42, density: float = 0.5, stream=None):
+        import torch
+        self._dev(grid, "bb_seed", (torch.uint8,), self.bb_bytes())
         _lib.check(self.lib.squeeze_bb_seed(self.ctx, _ptr(grid), seed, density_q(density),
                                             _stream(stream, grid.device)), "bb_seed")
 
     def bb_step(self, cur, nxt, stream=None):
+        import torch
+        self._dev(cur, "bb_step cur", (torch.uint8,), self.bb_bytes())
+        self._dev(nxt, "bb_step next", (torch.uint8,), self.bb_bytes())
         _lib.check(self.lib.squeeze_bb_step(self.ctx, _ptr(cur), _ptr(nxt), _stream(stream, cur.device)),
                    "bb_step")
 
     def bb_to_compact(self, grid, state, stream=None):
+        import torch
+        self._dev(grid, "bb_to_compact grid", (torch.uint8,), self.bb_bytes())
+        self._state(state, "bb_to_compact state")
         _lib.check(self.lib.squeeze_bb_to_compact(self.ctx, _ptr(grid), _ptr(state),
                                                   _stream(stream, grid.device)), "bb_to_compact")

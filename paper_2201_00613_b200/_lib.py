@@ -133,8 +133,11 @@ def load() -> ctypes.CDLL:
 
 
 def _strerror(status: int) -> str:
+    # Never load() from here: a failing load raises SqueezeError, whose message comes from here.
+    if _LIB is None:
+        return "libsqueeze.so not loaded"
     try:
-        return load().squeeze_strerror(status).decode()
+        return _LIB.squeeze_strerror(status).decode()
     except Exception:  # pragma: no cover
         return "squeeze error"
 

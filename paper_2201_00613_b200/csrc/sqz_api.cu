@@ -86,6 +86,7 @@ struct Ctx {
   uint32_t* d_send_peer = nullptr;  // the same destinations in send order (squeeze_halo_peer_push)
   uint64_t* d_send_pos = nullptr;
   int peer_parity = -1;  // -1: fused stores off
+  uint32_t peer_slots[2] = {0, 0};  // entries of the bound peer pointer arrays (== nranks)
   int* d_err = nullptr;
   uint8_t* d_send = nullptr;
   const uint8_t* d_recv = nullptr;
@@ -737,6 +738,7 @@ squeeze_status squeeze_run_host(void* ctx, uint8_t* h_state, uint8_t* d_a, uint8
   squeeze_status st = check_state(c, d_a);
   if (st == SQZ_OK) st = check_state(c, d_b);
   if (st != SQZ_OK) return st;
+  if (c->nranks > 1 || d_a == d_b) return SQZ_E_CONFIG;  // before any transfer is enqueued
   DevGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   if (cudaMemcpyAsync(d_a, h_state, c->state_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return SQZ_E_CUDA;
@@ -753,6 +755,7 @@ squeeze_status squeeze_run_host_packed(void* ctx, uint32_t* h_packed, uint32_t* 
   squeeze_status st = check_state(c, d_a);
   if (st == SQZ_OK) st = check_state(c, d_b);
   if (st != SQZ_OK) return st;
+  if (c->nranks > 1 || d_a == d_b) return SQZ_E_CONFIG;  // before any transfer is enqueued
   DevGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   if (cudaMemcpyAsync(d_a, h_packed, c->packed_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return SQZ_E_CUDA;
@@ -779,6 +782,8 @@ squeeze_status squeeze_device_error(const void* ctx) {
   int flag = 0;
   if (cudaDeviceSynchronize() != cudaSuccess) return SQZ_E_CUDA;
   if (cudaMemcpy(&flag, c->d_err, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return SQZ_E_CUDA;
+  // read-and-reset: a miss is reported once, by the first call after the step that missed
+  if (flag && cudaMemset(c->d_err, 0, sizeof(int)) != cudaSuccess) return SQZ_E_CUDA;
   return flag ? SQZ_E_HALO : SQZ_OK;
 }
 
@@ -797,6 +802,22 @@ squeeze_status squeeze_halo_set_sends(void* ctx, const uint64_t* omegas, uint64_
     for (uint64_t i = 0; i < count; ++i)
       if (omegas[i] < c->sr.omega_lo || omegas[i] >= c->sr.omega_hi) return SQZ_E_CONFIG;
     c->sends.assign(omegas, omegas + count);
+    if (c->device >= 0) {  // a peer plan indexes the old send list: drop it (re-plan after this call)
+      DevGuard g(c->device);
+      for (auto** q : {&c->d_peer_chunk_start, &c->d_peer_cell, &c->d_peer_of, &c->d_send_peer}) {
+        cudaFree(*q);
+        *q = nullptr;
+      }
+      for (auto** q : {&c->d_peer_pos, &c->d_send_pos}) {
+        cudaFree(*q);
+        *q = nullptr;
+      }
+      c->peer_parity = -1;
+      if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+      }
+    }
     c->send_offsets.resize(count);
     c->send_bits.resize(count);
     for (uint64_t i = 0; i < count; ++i) {  // tile-padded byte offsets / packed bits of the cells to send
@@ -872,7 +893,7 @@ squeeze_status squeeze_halo_peer_push(const void* ctx, const uint8_t* d_cur, int
   squeeze_status st = check_state(c, d_cur);
   if (st != SQZ_OK) return st;
   if (c->sends.empty()) return SQZ_OK;
-  if (!c->d_peer_recv[parity] || !c->d_peer_chunk_start) return SQZ_E_CONFIG;
+  if (!c->d_peer_recv[parity] || !c->d_peer_chunk_start || c->peer_slots[parity] != c->nranks) return SQZ_E_CONFIG;
   DevGuard g(c->device);
   return cu(launch_halo_peer_push(d_cur, c->d_sends, c->d_send_peer, c->d_send_pos, c->sends.size(),
                                   c->d_peer_recv[parity], (cudaStream_t)stream));
@@ -885,6 +906,10 @@ squeeze_status squeeze_halo_peer_plan(void* ctx, const uint32_t* send_peer, cons
     if (c->device < 0) return SQZ_E_NO_DEVICE;
     const uint64_t n = c->sends.size();
     if (n && (!send_peer || !send_pos)) return SQZ_E_CONFIG;
+    // every destination is another rank of this context (peer slot = rank; the step kernel stores
+    // through peer_recv[slot], so an out-of-range slot would write through a wild pointer)
+    for (uint64_t i = 0; i < n; ++i)
+      if (send_peer[i] >= c->nranks || send_peer[i] == c->rank) return SQZ_E_CONFIG;
     // CSR over the tile kernel's 32-tile chunks; cell = tile in chunk << 16 | j
     const uint64_t nch = (c->sr.tile_hi - c->sr.tile_lo + kChunkTiles - 1) / kChunkTiles;
     std::vector<uint32_t> start(nch + 1, 0), cell(n), of(n);
@@ -930,9 +955,12 @@ squeeze_status squeeze_halo_peer_bind(void* ctx, uint32_t parity, uint32_t npeer
   if (!ctx || parity > 1 || (npeers && !peer_recv)) return SQZ_E_CONFIG;
   Ctx* c = static_cast<Ctx*>(ctx);
   if (c->device < 0) return SQZ_E_NO_DEVICE;
+  // one pointer per rank (slot = rank); the own slot is never stored through
+  if (npeers != 0 && npeers != c->nranks) return SQZ_E_CONFIG;
   DevGuard g(c->device);
   cudaFree(c->d_peer_recv[parity]);
   c->d_peer_recv[parity] = nullptr;
+  c->peer_slots[parity] = npeers;
   if (npeers == 0) return SQZ_OK;
   return upload(&c->d_peer_recv[parity], reinterpret_cast<uint8_t* const*>(peer_recv), npeers);
 }
@@ -942,6 +970,7 @@ squeeze_status squeeze_halo_peer_select(void* ctx, int parity) {
   Ctx* c = static_cast<Ctx*>(ctx);
   if (parity >= 0 && (!c->d_peer_chunk_start || (!c->d_peer_recv[parity] && !c->sends.empty())))
     return SQZ_E_CONFIG;
+  if (parity >= 0 && !c->sends.empty() && c->peer_slots[parity] != c->nranks) return SQZ_E_CONFIG;
   c->peer_parity = parity;
   if (c->graph) {  // a captured run would replay the old parameters
     cudaGraphExecDestroy(c->graph);

@@ -177,8 +177,34 @@ def test_missing_library_fails_loudly():
             "try:\n"
             "    pkg.Squeeze(pkg.Fractal('t', 3, 2, ((0, 0), (0, 1), (1, 1))), 4, device=0)\n"
             "except pkg.SqueezeError as e:\n"
-            "    print('raised', e.status)\n")
+            "    print('raised', e.status, e)\n")
     env = dict(os.environ, SQZ_LIB="/nonexistent/libsqueeze.so")
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert "raised -7" in out.stdout, out.stdout + out.stderr
+    assert "not loaded" in out.stdout + out.stderr or "missing" in out.stdout + out.stderr
+    assert "RecursionError" not in out.stderr
+
+
+def test_binding_rejects_bad_tensors_before_the_call():
+    """The C ABI sees raw pointers only, so the binding checks tensor type, device, contiguity,
+    dtype and size and raises SqueezeError(SQZ_E_CONFIG) without calling the library (ADVICE:
+    an int32 Ω array would make the map kernel read 8 bytes per 4-byte element)."""
+    import torch
+    import paper_2201_00613_b200 as pkg
+    p = product("sierpinski-triangle", 6)  # host-only context (device=None)
+    p.device = 0  # pretend the context is on cuda:0: every CPU tensor must be rejected by the binding
+    cpu_state = torch.zeros(p.geometry.state_bytes, dtype=torch.uint8)
+    for call in (lambda: p.step(cpu_state, cpu_state), lambda: p.seed(cpu_state),
+                 lambda: p.map_lambda(torch.zeros(4, dtype=torch.int32)),
+                 lambda: p.map_nu(torch.zeros(4, dtype=torch.int32), torch.zeros(3, dtype=torch.int32)),
+                 lambda: p.step_packed(torch.zeros(4, dtype=torch.int32), torch.zeros(4, dtype=torch.int32)),
+                 lambda: p.heat_step(torch.zeros(4), torch.zeros(4)), lambda: p.count_alive(cpu_state)):
+        with pytest.raises(pkg.SqueezeError) as ei:
+            call()
+        assert ei.value.status == -6
+    with pytest.raises(pkg.SqueezeError) as ei:  # short host buffer for the end-to-end run
+        p.run_host(torch.zeros(p.geometry.state_bytes - 1, dtype=torch.uint8), None, None, 1)
+    assert ei.value.status == -6 and "bytes" in str(ei.value)
+    with pytest.raises(pkg.SqueezeError):  # wrong host dtype
+        p.run_host(torch.zeros(p.geometry.state_bytes, dtype=torch.float32), None, None, 1)
