@@ -454,28 +454,3 @@ def test_sharded_r22_equals_unsharded(nranks):
         del a, b
         p.close()
         torch.cuda.empty_cache()
-
-
-def _oracle_first_step_part(job):
-    lo, hi, r, seed, density = job
-    om = np.arange(lo, hi, dtype=np.int64)
-    return A.compact_step_sampled(SIERPINSKI, r, om, lambda q: A.seed_at(SIERPINSKI, r, q, seed, density))
-
-
-def test_full_state_r16_first_step_vs_oracle():
-    """SURVEY pin 10(iv): the WHOLE r=16 state (4.3e7 cells) after one step equals the oracle's
-    O6 step of the D9 seed, computed on every host core (fork pool over contiguous Ω ranges)."""
-    import multiprocessing as mpc
-    r, seed, density = 16, 42, 0.5
-    p = mk("sierpinski-triangle", r)
-    a, b = p.new_state(), p.new_state()
-    p.seed(a, seed, density)
-    p.step(a, b)
-    got = host(p, b)
-    total = 3 ** r
-    workers = max(1, min(32, len(os.sched_getaffinity(0))))
-    step = -(-total // (workers * 4))
-    jobs = [(lo, min(total, lo + step), r, seed, density) for lo in range(0, total, step)]
-    with mpc.get_context("fork").Pool(workers) as pool:
-        want = np.concatenate(pool.map(_oracle_first_step_part, jobs))
-    assert np.array_equal(got, want)

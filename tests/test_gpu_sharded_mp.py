@@ -115,18 +115,14 @@ def test_peer_transport_mixed_with_collective_steps():
     assert np.array_equal(got, _oracle_run("sierpinski-triangle", 11, 4))
 
 
-def _digest(buf, n, piece=1 << 28):
-    """Position-weighted sums of bytes [0, n) of a device buffer, one per 256 MB piece: any single
-    differing byte changes its piece's sum (weights 1..65521)."""
-    out = []
-    for i in range(0, n, piece):
-        m = min(piece, n - i)
-        w = (torch.arange(m, device=buf.device, dtype=torch.int32) % 65521) + 1
-        out.append(int((buf[i:i + m].to(torch.int32) * w).sum(dtype=torch.int64).item()))
-    return out
+class _DevBytes:
+    """A raw device allocation (CUDA IPC-opened) seen by torch through __cuda_array_interface__."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (ptr, False), "version": 3}
 
 
-def _r22_peer_worker(rank, world, port, steps, out):
+def _r22_peer_worker(rank, world, port, steps, ref_handle, ref_bytes, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -143,7 +139,20 @@ def _r22_peer_worker(rank, world, port, steps, out):
         g = sh.geometry
         lo, hi = sh.sq.shard_range(rank)
         t0, t1 = lo // g.tile_cells, hi // g.tile_cells
-        out[rank] = (t0, t1, _digest(fin, (t1 - t0) * g.tile_bytes), sh.sq.device_error())
+        kp = g.tile_bytes
+        # the unsharded run's final state, mapped from the parent: every byte, piece by piece
+        ptr = pkg.ipc_open(ref_handle, 0)
+        ref = torch.as_tensor(_DevBytes(ptr, ref_bytes), device="cuda")
+        n, piece, bad = (t1 - t0) * kp, 1 << 30, -1
+        for i in range(0, n, piece):
+            m = min(piece, n - i)
+            if not torch.equal(fin[i:i + m], ref[t0 * kp + i:t0 * kp + i + m]):
+                bad = i + int(torch.nonzero(fin[i:i + m] != ref[t0 * kp + i:t0 * kp + i + m])[0].item())
+                break
+        torch.cuda.synchronize()
+        del ref
+        pkg.ipc_close(ptr)
+        out[rank] = (n, bad, sh.sq.device_error())
         del a, b, fin
         sh.close()
     finally:
@@ -153,25 +162,31 @@ def _r22_peer_worker(rank, world, port, steps, out):
 def test_peer_transport_r22_two_ranks_equals_unsharded():
     """The fused peer-memory halo at the bench size: r=22 over 2 processes (peer transport, 3
     steps, so the step kernel's own halo stores feed steps 2 and 3) equals the unsharded run
-    (itself pinned to the oracle) on every byte of each shard, compared through piecewise
-    position-weighted digests."""
+    (itself pinned to the oracle) on EVERY byte of each shard: the parent's final state is mapped
+    into each rank (CUDA IPC) and compared exactly, 1 GB piece by piece."""
     import paper_2201_00613_b200 as pkg
 
     steps = 3
-    ctx = mp.get_context("spawn")
-    out = ctx.Manager().dict()
-    mp.start_processes(_r22_peer_worker, args=(2, _free_port(), steps, out), nprocs=2, join=True,
-                       start_method="spawn")
     p = pkg.Squeeze(pkg.builtin_fractal("sierpinski-triangle"), 22, device=0)
     a, b = p.new_state(), p.new_state()
     p.seed(a, 42, 0.5)
     fin = p.run(a, b, steps)
+    nbytes = p.geometry.state_bytes
+    ref_ptr = pkg.ipc_alloc(nbytes, 0)
+    ref = torch.as_tensor(_DevBytes(ref_ptr, nbytes), device="cuda")
+    ref.copy_(fin[:nbytes])
     torch.cuda.synchronize()
-    kp = p.geometry.tile_bytes
-    for rank in range(2):
-        t0, t1, dig, err = out[rank]
-        assert err == 0
-        assert dig == _digest(fin[t0 * kp:], (t1 - t0) * kp), rank
-    del a, b, fin
+    del a, b, fin, ref
     p.close()
     torch.cuda.empty_cache()
+    try:
+        ctx = mp.get_context("spawn")
+        out = ctx.Manager().dict()
+        mp.start_processes(_r22_peer_worker, args=(2, _free_port(), steps, pkg.ipc_handle(ref_ptr), nbytes, out),
+                           nprocs=2, join=True, start_method="spawn")
+    finally:
+        pkg.ipc_free(ref_ptr)
+    for rank in range(2):
+        n, bad, err = out[rank]
+        assert err == 0
+        assert n > 0 and bad == -1, (rank, bad)
