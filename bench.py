@@ -58,6 +58,7 @@ def parse_args():
     ap.add_argument("--reps", type=int, default=5, help="repetitions of the K-step run reported (mean, stderr)")
     ap.add_argument("--cpu-sample", type=int, default=1 << 21, help="cells in the cpu_baseline sample")
     ap.add_argument("--ref-sample", type=int, default=1 << 16, help="cells per --impl reference step")
+    ap.add_argument("--comm-timeout", type=int, default=600, help="N > 1: process-group timeout (s)")
     return ap.parse_args()
 
 
@@ -145,6 +146,29 @@ def ncu_traffic(workload_key: str):
 
 def cells_per_s(cells, steps, ms):
     return cells * steps / (ms / 1e3)
+
+
+def gather_rows(world, row):
+    """Every rank's timing row on every rank (all_gather_object over the default group)."""
+    if world == 1:
+        return [row]
+    import torch.distributed as dist
+    rows = [None] * world
+    dist.all_gather_object(rows, row)
+    return rows
+
+
+def multi_rank_fields(rows, peak):
+    """N > 1: the roofline of the SLOWEST rank's step kernel (its own algorithmic bytes over its
+    own average launch time) and the per-rank split of a step into kernel time and the rest
+    (halo transport + cross-rank ordering).  Rows: rank, cells, alg_bytes, kernel_ms, step_ms."""
+    slow = max(rows, key=lambda r: r["kernel_ms"])
+    achieved = slow["alg_bytes"] / (slow["kernel_ms"] / 1e3) / 1e9
+    per_rank = [{"rank": r["rank"], "cells": r["cells"], "kernel_ms": r["kernel_ms"], "step_ms": r["step_ms"],
+                 "halo_and_ordering_ms": max(0.0, r["step_ms"] - r["kernel_ms"]),
+                 "hbm_frac": r["alg_bytes"] / (r["kernel_ms"] / 1e3) / 1e9 / peak} for r in rows]
+    return {"achieved": achieved, "frac": achieved / peak, "avg_launch_ms": slow["kernel_ms"],
+            "algorithmic_bytes_per_launch": slow["alg_bytes"], "slowest_rank": slow["rank"]}, per_rank
 
 
 # ------------------------------------------------------------------------------ reference arm
@@ -263,11 +287,23 @@ def main():
     if os.environ.get("SQZ_SHARE_GPU") == "1":
         local = 0
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
+        import datetime
+        t_init = time.perf_counter()
+        tmo = datetime.timedelta(seconds=args.comm_timeout)  # a hung peer aborts the job (reading D17)
         if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"), timeout=tmo)
+            dist.barrier()  # the communicator exists after the first collective
         else:
-            dist.init_process_group(backend)
+            dist.init_process_group(backend, timeout=tmo)
+        t_init = time.perf_counter() - t_init
+        ver = ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else None
+        comm = {"backend": backend, "init_s": t_init, "nccl_version": ver, "timeout_s": args.comm_timeout,
+                "shared_gpu": os.environ.get("SQZ_SHARE_GPU") == "1"}
+        print(f"[rank {rank}] process group {backend} up in {t_init:.2f} s"
+              + (f" (NCCL {ver}, device cuda:{local})" if ver else f" (device cuda:{local})"), file=sys.stderr,
+              flush=True)
     red_dev = "cuda" if backend == "nccl" else "cpu"
     f = pkg.builtin_fractal(args.fractal)
     opts = dict(tile_level=args.tile_level, block_threads=args.block_threads, ctas_per_sm=args.ctas_per_sm)
@@ -329,29 +365,32 @@ def main():
         if world > 1:
             dist.barrier()
     clocks = clk.summary()
-    ms = ev_all[0].elapsed_time(ev_all[1])
+    ms_own = ev_all[0].elapsed_time(ev_all[1])
     kern_ms = [e0.elapsed_time(e1) for e0, e1 in ev_k]
     kern_avg = sum(kern_ms) / K
-    if world > 1:
-        t = torch.tensor([ms, kern_avg], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, kern_avg_max = float(t[0]), float(t[1])
-    else:
-        kern_avg_max = kern_avg
-    if sq.device_error() != 0:
+    if sh is not None:
+        sh.check(args.comm_timeout)  # deadline + device halo-miss flag (reading D17)
+    elif sq.device_error() != 0:
         raise RuntimeError("device error flag set (halo miss)")
-    value = cells_per_s(g.cells_total, K, ms)
     peak, peak_src = measured_hbm_peak()
     # 1 B read + 1 B written per compact cell (uint8, D10); packed: the 1-bit words read + written
     alg_bytes = 2 * g.packed_bytes if packed else 2 * g.local_cells
-    achieved = alg_bytes / (kern_avg / 1e3) / 1e9
+    rows = gather_rows(world, {"rank": rank, "cells": g.local_cells, "alg_bytes": alg_bytes, "kernel_ms": kern_avg,
+                               "step_ms": ms_own / K})
+    ms = max(r["step_ms"] for r in rows) * K  # the slowest rank's device time (max over ranks)
+    value = cells_per_s(g.cells_total, K, ms)
     wl_key = f"{args.fractal}-r{args.level}-n{world}"
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+    roofline = {"bound": "hbm", "peak": peak, "unit": "GB/s",
                 "traffic": None if packed else ncu_traffic(wl_key),
-                "kernel": "sqz::k_step_packed" if packed else "sqz::k_step_tile",
-                "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": kern_avg, "peak_source": peak_src,
+                "kernel": "sqz::k_step_packed" if packed else "sqz::k_step_tile", "peak_source": peak_src,
                 "pipes_pct_active": None if packed else ncu_pipes(wl_key)}
+    slow, per_rank = multi_rank_fields(rows, peak)
+    roofline.update(slow)
+    achieved = roofline["achieved"]
     extras = {}
+    if world > 1:
+        extras["per_rank"] = per_rank
+        extras["comm"] = comm
     pack_launch = sh is not None and sh.halo.sends.size and (packed or sh.transport != "peer")
     launches = K * (1 + (1 if pack_launch else 0))
 
@@ -706,9 +745,13 @@ def main():
             "gpu_launches": launches,
             "hbm_fraction_kernel": achieved / peak,
         }
+        if world > 1 and comm and comm["shared_gpu"]:
+            line["shared_gpu"] = True  # every rank on cuda:0: a check of the multi-rank path, not a number
+            line["distinct_gpus"] = 1
         line.update(extras)
         if "cpu_baseline" not in line:
-            line["cpu_baseline"] = None
+            line["cpu_baseline"] = {"value": None, "unit": "cells/s", "cores": None, "kind": "oracle",
+                                    "sample": "measured on rank 0 at N=1 only (bench contract); see the N=1 line"}
         if "e2e" not in line:
             line["e2e"] = None
         print(json.dumps(line), flush=True)

@@ -20,7 +20,12 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import B3S23, Fractal, Squeeze
+from . import B3S23, Fractal, Squeeze, SqueezeError
+
+
+class HaloTimeout(RuntimeError):
+    """A sharded step did not complete within the caller's deadline (a peer stalled or the
+    collective hung); the caller aborts the process group (reading D17)."""
 
 
 class HaloExchange:
@@ -158,6 +163,23 @@ class ShardedSqueeze:
 
     def new_state(self):
         return self.sq.new_state()
+
+    def check(self, timeout_s: float = 300.0) -> None:
+        """The failure path of a sharded run (D17): wait for this rank's
+        stream with a deadline instead of blocking forever on a stalled peer (HaloTimeout), then
+        surface a device-side halo miss (SqueezeError SQZ_E_HALO, read-and-reset).  Asynchronous
+        NCCL errors surface through torch's NCCL watchdog (the process group's timeout aborts the
+        communicator) and are re-raised by the next collective."""
+        import time
+        stream = torch.cuda.current_stream(self.device)
+        t_end = time.monotonic() + timeout_s
+        while not stream.query():
+            if time.monotonic() > t_end:
+                raise HaloTimeout(f"rank {self.rank}: sharded steps not done after {timeout_s:.0f} s")
+            time.sleep(0.001)
+        st = self.sq.device_error()
+        if st != 0:
+            raise SqueezeError(st, f"rank {self.rank}: sharded step")
 
     def seed(self, state, seed=42, density=0.5):
         self.sq.seed(state, seed, density)
