@@ -58,6 +58,7 @@ def parse_args():
     ap.add_argument("--reps", type=int, default=5, help="repetitions of the K-step run reported (mean, stderr)")
     ap.add_argument("--cpu-sample", type=int, default=1 << 21, help="cells in the cpu_baseline sample")
     ap.add_argument("--ref-sample", type=int, default=1 << 16, help="cells per --impl reference step")
+    ap.add_argument("--bb-runs", type=int, default=3, help="runs x 1000 iterations of the r=16 BB protocol")
     ap.add_argument("--comm-timeout", type=int, default=600, help="N > 1: process-group timeout (s)")
     return ap.parse_args()
 
@@ -419,17 +420,18 @@ def main():
         del h
     if rank == 0 and world == 1 and not args.no_extras:
         # repetitions of the K-step run (the first is the timed run above)
-        reps = [ms / K]
-        for _ in range(args.reps - 1):
+        reps = []
+        KR = max(K, 100)  # 100 steps x 5 repetitions (on top of the timed run above)
+        for _ in range(args.reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            for i in range(K):
+            for i in range(KR):
                 step(bufs[i % 2], bufs[(i + 1) % 2])
             e1.record(stream)
             torch.cuda.synchronize()
-            reps.append(e0.elapsed_time(e1) / K)
+            reps.append(e0.elapsed_time(e1) / KR)
         mean = statistics.fmean(reps)
-        extras["repetitions"] = {"n": len(reps), "steps_each": K, "ms_per_step_mean": mean,
+        extras["repetitions"] = {"n": len(reps), "steps_each": KR, "ms_per_step_mean": mean,
                                  "ms_per_step_stderr": (statistics.stdev(reps) / len(reps) ** 0.5) if len(reps) > 1
                                  else None, "ms_per_step": reps}
         del bufs
@@ -616,20 +618,26 @@ def main():
                 for i in range(3):
                     fn(fa if i % 2 == 0 else fb, fb if i % 2 == 0 else fa)
                 torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                for i in range(20):
-                    fn(fa if i % 2 == 0 else fb, fb if i % 2 == 0 else fa)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                fms = e0.elapsed_time(e1) / 20
-                row[mode] = {"ms_per_step": fms, "cells_per_s": cells_per_s(gf.cells_total, 1, fms),
-                             "hbm_frac": nbytes / (fms / 1e3) / 1e9 / peak}
+                reps_ms = []  # 100 steps x 5 repetitions
+                for _ in range(5):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    for i in range(100):
+                        fn(fa if i % 2 == 0 else fb, fb if i % 2 == 0 else fa)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    reps_ms.append(e0.elapsed_time(e1) / 100)
+                fms = statistics.fmean(reps_ms)
+                row[mode] = {"ms_per_step": fms, "ms_per_step_stderr": statistics.stdev(reps_ms) / 5 ** 0.5,
+                             "cells_per_s": cells_per_s(gf.cells_total, 1, fms),
+                             "hbm_frac": nbytes / (fms / 1e3) / 1e9 / peak, "steps": 100, "repetitions": 5}
                 del fa, fb
             pf.close()
             fr_rows[fname] = row
         extras["fractal_configs"] = {"note": "BASELINE configs[3]: carpet (D11 row-major minus centre) and empty "
-                                             "bottles (D11 assumed silhouette), 20 steps each, B3/S23",
+                                             "bottles (D11 assumed silhouette), 100 steps x 5 repetitions each (SURVEY §8d C4), "
+                                             "B3/S23; hbm_frac on the algorithmic bytes (2 B/cell bytes, "
+                                             "2 x packed_bytes packed)",
                                      "rows": fr_rows}
         torch.cuda.empty_cache()
         # --- NEXT-3 ablation: batched ν map, LUT kernel vs integer tensor-core product
@@ -689,8 +697,34 @@ def main():
                 p16.step(c0, c1)
             bb_ms = timed(lambda i: p16.bb_step(g0 if i % 2 == 0 else g1, g1 if i % 2 == 0 else g0), 10, True)
             cp_ms = timed(lambda i: p16.step(c0 if i % 2 == 0 else c1, c1 if i % 2 == 0 else c0), 50, True)
+
+            def protocol(fn, runs, iters):
+                """The paper's protocol: runs x iterations back to back, mean time per step."""
+                per = []
+                for _ in range(runs):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    fn(iters)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    per.append(e0.elapsed_time(e1) / iters)
+                return {"runs": runs, "iterations": iters, "ms_per_step_mean": statistics.fmean(per),
+                        "ms_per_step_stderr": statistics.stdev(per) / len(per) ** 0.5 if len(per) > 1 else None}
+
+            def bb_iters(n):
+                for i in range(n):
+                    p16.bb_step(g0 if i % 2 == 0 else g1, g1 if i % 2 == 0 else g0)
+
+            pc = protocol(lambda n: p16.run(c0, c1, n, use_graph=True), 100, 1000)
+            pb = protocol(bb_iters, args.bb_runs, 1000)
             extras["bb_baseline"] = {
                 "level": r16, "bb_ms_per_step": bb_ms, "compact_ms_per_step": cp_ms, "speedup": bb_ms / cp_ms,
+                "paper_protocol": {"compact": pc, "bb": pb,
+                                   "speedup": pb["ms_per_step_mean"] / pc["ms_per_step_mean"],
+                                   "note": "P:377: mean over runs of 1000 back-to-back iterations (compact: 100 "
+                                           "runs, squeeze_run with the CUDA graph; BB: --bb-runs runs, each 1000 "
+                                           "iterations); the r=16 compact state (87 MB) stays L2-resident here, "
+                                           "as in the paper's protocol"},
                 "bb_bytes": p16.bb_bytes() * 2, "compact_bytes": p16.geometry.state_bytes * 2,
                 "memory_ratio": (p16.geometry.n ** 2) / p16.geometry.cells_total,
                 "l2": "256 MiB buffer written before every timed step (flush)",

@@ -112,6 +112,12 @@ typedef struct {
   uint64_t heat_bytes;   /* bytes of a HEAT field buffer (squeeze_heat_*) */
   uint32_t heat_chunk_tiles; /* tiles per chunk of the heat layout (4: one float4 word per cell) */
   uint32_t heat_pairs;   /* remote (own cell, neighbour) pairs per tile of the heat kernel */
+  uint32_t byte_kernel;  /* squeeze_step's kernel: 0 = chunk-staged (k_step_tile), 1 = streaming
+                          * large-tile step (k_step_stream, when a 32-tile chunk does not fit shared
+                          * memory twice); both compute the same step on the same layout */
+  uint32_t packed_ok;    /* 1 if the packed step fits at this tile level (else its calls return
+                          * SQZ_E_INVALID_LEVEL) */
+  uint32_t heat_ok;      /* 1 if the heat step fits at this tile level (likewise) */
 } squeeze_geometry_t;
 
 const char* squeeze_strerror(squeeze_status st);

@@ -49,7 +49,8 @@ class GeometryC(ctypes.Structure):
                 ("tile_cells", ctypes.c_uint64), ("num_tiles", ctypes.c_uint64), ("chunk_tiles", ctypes.c_uint32),
                 ("remote_links", ctypes.c_uint32), ("max_degree", ctypes.c_uint32), ("tile_bytes", ctypes.c_uint32),
                 ("packed_bytes", ctypes.c_uint64), ("chunk_words", ctypes.c_uint32), ("packed_tiles", ctypes.c_uint32),
-                ("heat_bytes", ctypes.c_uint64), ("heat_chunk_tiles", ctypes.c_uint32), ("heat_pairs", ctypes.c_uint32)]
+                ("heat_bytes", ctypes.c_uint64), ("heat_chunk_tiles", ctypes.c_uint32), ("heat_pairs", ctypes.c_uint32),
+                ("byte_kernel", ctypes.c_uint32), ("packed_ok", ctypes.c_uint32), ("heat_ok", ctypes.c_uint32)]
 
 
 vp = ctypes.c_void_p
@@ -170,6 +171,9 @@ class Geometry:
     heat_bytes: int
     heat_chunk_tiles: int
     heat_pairs: int
+    byte_kernel: int
+    packed_ok: int
+    heat_ok: int
 
     @property
     def local_cells(self) -> int:

@@ -92,6 +92,10 @@ struct Ctx {
   const uint8_t* d_recv = nullptr;
   int tile_threads = 0, tile_grid = 0;
   size_t tile_smem = 0;
+  // large tiles (a 32-tile chunk does not fit shared memory twice): the streaming byte step
+  bool stream = false;
+  int stream_minb = 1, stream_grid = 0;
+  uint32_t stream_sin = 0, stream_sout = 0;
   std::map<uint32_t, BlockLevel> blocks;  // by m = log_s rho
   // CUDA graph of the two-step ping-pong
   cudaGraphExec_t graph = nullptr;
@@ -239,6 +243,8 @@ TileParams tile_params(const Ctx* c) {
   p.adj = c->d_adj;
   p.adj_stride = adj_stride(c);
   p.pstages = c->packed_stages;
+  p.sin = c->stream_sin;
+  p.sout = c->stream_sout;
   if (c->peer_parity >= 0 && c->d_peer_chunk_start) {
     p.peer_recv = c->d_peer_recv[c->peer_parity];
     p.peer_chunk_start = c->d_peer_chunk_start;
@@ -264,6 +270,7 @@ HeatParams heat_params(const Ctx* c, float alpha) {
 squeeze_status do_heat_step(Ctx* c, const float* cur, float* next, float alpha, cudaStream_t st) {
   if (c->nranks > 1) return SQZ_E_CONFIG;
   if (c->NT >= 0xFFFFFFFFull) return SQZ_E_OVERFLOW;
+  if (c->heat_grid == 0) return SQZ_E_INVALID_LEVEL;  // the heat unit does not fit at this tile level
   return cu(launch_heat_step(heat_params(c, alpha), tile_params(c), cur, next, c->heat_grid, st));
 }
 
@@ -271,6 +278,10 @@ squeeze_status do_step(Ctx* c, const uint8_t* cur, uint8_t* next, cudaStream_t s
   if (c->nranks > 1 && !c->needs.empty() && c->d_recv == nullptr) return SQZ_E_CONFIG;
   if (c->NT >= 0xFFFFFFFFull) return SQZ_E_OVERFLOW;  // the tile kernel keeps tile indices in 32 bits
   TileParams p = tile_params(c);
+  if (c->stream) {
+    int grid = (int)std::min<uint64_t>((uint64_t)c->stream_grid, p.nchunks ? p.nchunks : 1);
+    return cu(launch_step_stream(p, cur, next, grid, c->stream_minb, c->tile_smem, st));
+  }
   int grid = (int)std::min<uint64_t>((uint64_t)c->tile_grid, p.nchunks ? p.nchunks : 1);
   return cu(launch_step_tile(p, cur, next, grid, c->tile_threads, c->tile_smem, st));
 }
@@ -278,6 +289,7 @@ squeeze_status do_step(Ctx* c, const uint8_t* cur, uint8_t* next, cudaStream_t s
 squeeze_status do_step_packed(Ctx* c, const uint32_t* cur, uint32_t* next, cudaStream_t st) {
   if (c->nranks > 1 && !c->needs.empty() && c->d_recv == nullptr) return SQZ_E_CONFIG;
   if (c->NT >= 0xFFFFFFFFull) return SQZ_E_OVERFLOW;
+  if (c->packed_grid == 0) return SQZ_E_INVALID_LEVEL;  // the packed chunk does not fit at this tile level
   TileParams p = tile_params(c);
   p.nbr = c->d_nbr_packed;
   const uint64_t pch = (p.tile_hi - p.tile_lo + kPackTiles - 1) / kPackTiles;
@@ -399,6 +411,16 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
     if (g > r) return fail(SQZ_E_INVALID_LEVEL);
     rc = build_tile_tables(c->f, g, c->tt);
     if (rc != SQZ_OK) return fail((squeeze_status)rc);
+    // link-heavy fractals (more than 2% of a tile's cells are boundary links, e.g. the carpet's
+    // full tile edges) take the next tile level when it has at most 4096 cells: links grow
+    // with the tile perimeter, cells with k^g (SURVEY §7 hard part 3; the streaming byte step)
+    if (!c->opts.tile_level && g < r && (uint64_t)c->tt.E * 50 > c->tt.K && c->tt.K * c->f.k <= 4096) {
+      TileTables up;
+      if (build_tile_tables(c->f, g + 1, up) == SQZ_OK) {
+        c->tt = std::move(up);
+        g = g + 1;
+      }
+    }
     build_level_maps(c->f, r, c->full);
     build_level_maps(c->f, r - g, c->coarse);
     checked_pow(c->f.k, r - g, ~0ull, c->NT);
@@ -459,10 +481,21 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       if (threads % 32 || threads > 1024) return fail(SQZ_E_CONFIG);
       c->tile_threads = (int)threads;
       int occ = 0;
-      if (tile_prepare(p, c->tile_smem, c->tile_threads, &occ) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
-      if (c->opts.ctas_per_sm) occ = std::min<int>(occ, (int)c->opts.ctas_per_sm);
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+      // two double-buffered 32-tile chunks per SM, else the streaming step (sqz_stream.cu)
+      c->stream = 2 * c->tile_smem > 227 * 1024 || tile_prepare(p, c->tile_smem, c->tile_threads, &occ) != cudaSuccess;
+      if (c->stream) {
+        cudaGetLastError();  // a refused attribute of the chunk-staged kernel is not an error of the context
+        if (c->tt.K > 0xFFFFu || !stream_plan(p, c->nranks > 1, &c->stream_minb)) return fail(SQZ_E_INVALID_LEVEL);
+        c->stream_sin = p.sin;
+        c->stream_sout = p.sout;
+        c->tile_smem = stream_smem_bytes(p, c->nranks > 1);
+        c->tile_threads = stream_threads();
+        if (stream_prepare(p, c->tile_smem, c->stream_minb, &occ) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
+        c->stream_grid = sms * std::max(1, occ);
+      }
+      if (c->opts.ctas_per_sm) occ = std::min<int>(occ, (int)c->opts.ctas_per_sm);
       c->tile_grid = sms * std::max(1, occ);
       p.Kw = c->Kw;
       // packed step: 8 warps (tools/packed_timing.py: 8 warps with every block's slots in
@@ -478,8 +511,13 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       c->packed_stages = p.pstages;
       c->packed_smem = packed_smem_bytes(p);
       int pocc = 0;
-      if (packed_prepare(p, c->packed_smem, c->packed_threads, &pocc) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
-      c->packed_grid = sms * std::max(1, pocc);
+      // a chunk of 128 tiles that does not fit shared memory leaves the packed step unavailable at
+      // this tile level (its entry points return SQZ_E_INVALID_LEVEL), not the context
+      if (c->packed_smem <= 227 * 1024 && packed_prepare(p, c->packed_smem, c->packed_threads, &pocc) == cudaSuccess)
+        c->packed_grid = sms * std::max(1, pocc);
+      else
+        c->packed_grid = 0;
+      cudaGetLastError();  // (clears a refused shared-memory attribute)
       // ν tensor-core ablation: H_ν as int16 and the per-level weight bytes of k^(μ-1)
       if (c->f.s * c->f.s <= kMmaMaxS2 && c->f.k <= 256 && r <= 32) {
         std::vector<int16_t> hh(c->f.hnu.begin(), c->f.hnu.end());
@@ -527,8 +565,8 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
         }  // (at least 2 stages: a unit's successor is filled while the unit is computed)
         h.stages = c->heat_stages;
         int hocc = 0;
-        if (heat_prepare(h, q, &hocc) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
-        c->heat_grid = sms * std::max(1, hocc);
+        c->heat_grid = heat_prepare(h, q, &hocc) == cudaSuccess ? sms * std::max(1, hocc) : 0;
+        cudaGetLastError();
       }
       // tile adjacency: the coarse λ and one coarse ν per link direction of every local tile,
       // evaluated once here instead of every step
@@ -579,6 +617,9 @@ squeeze_status squeeze_geometry(const void* ctx, squeeze_geometry_t* out) {
   out->heat_bytes = c->heat_bytes;
   out->heat_chunk_tiles = 4;
   out->heat_pairs = c->heat_P;
+  out->byte_kernel = c->stream ? 1u : 0u;
+  out->packed_ok = c->packed_grid > 0 ? 1u : 0u;
+  out->heat_ok = c->heat_grid > 0 ? 1u : 0u;
   return SQZ_OK;
 }
 

@@ -189,11 +189,10 @@ __device__ __forceinline__ uint32_t grab(uint32_t* ctr, int lane) { return grab(
 // that chunk.  Always commits exactly one group.
 // Tile-padded byte layout: the gather fetches the aligned word holding the byte.
 __device__ __forceinline__ void chunk_neighbours(const TileParams& p, uint32_t* ntl, uint32_t* R, const uint32_t* lj2,
-                                                 const ChunkInfo& c,
-                                                 const uint8_t* __restrict__ cur, int warp, int nwarps, int lane) {
+                                                 const ChunkInfo& c, const uint8_t* __restrict__ cur, int warp,
+                                                 int nwarps, int lane, uint32_t Epf) {
   const uint64_t t = c.t0 + lane;
   const uint64_t t_end = c.t0 + c.nt;
-  const uint32_t Epf = prefetch_links(p);
   for (int d = warp; d < (int)p.ndirs; d += nwarps) {
     const uint32_t a1 = (t < p.tile_hi) ? __ldg(p.adj + d * p.adj_stride + (t - p.tile_lo)) : 0u;
     const int64_t tn = (int64_t)a1 - 1;
@@ -213,6 +212,12 @@ __device__ __forceinline__ void chunk_neighbours(const TileParams& p, uint32_t* 
     }
   }
   cp_async_commit();
+}
+
+__device__ __forceinline__ void chunk_neighbours(const TileParams& p, uint32_t* ntl, uint32_t* R, const uint32_t* lj2,
+                                                 const ChunkInfo& c, const uint8_t* __restrict__ cur, int warp,
+                                                 int nwarps, int lane) {
+  chunk_neighbours(p, ntl, R, lj2, c, cur, warp, nwarps, lane, prefetch_links(p));
 }
 
 }  // namespace sqz

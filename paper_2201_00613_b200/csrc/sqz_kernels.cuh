@@ -58,6 +58,7 @@ struct TileParams {
   const uint32_t* adj;
   uint64_t adj_stride;  // a multiple of kPackTiles
   uint32_t pstages;     // pipeline stages of the packed step
+  uint32_t sin, sout;   // slice-ring depths of the large-tile byte step (sqz_stream.cu)
 };
 
 // ν as an integer tensor-core product (sqz_mma.cu, SURVEY NEXT-3 ablation).
@@ -85,6 +86,13 @@ cudaError_t launch_block_step(const LevelMaps& coarse, uint32_t rho, const uint8
 cudaError_t launch_block_seed(const LevelMaps& coarse, uint32_t rho, const uint8_t* micro, uint8_t* blocks,
                               uint64_t seed, uint64_t q, cudaStream_t st);
 cudaError_t launch_tile_adjacency(const TileParams& p, uint32_t* adj, cudaStream_t st);
+// Large-tile byte step (sqz_stream.cu): plan (ring depths, CTAs per SM), prepare, launch.
+size_t stream_smem_bytes(const TileParams& p, bool peer);
+bool stream_plan(TileParams& p, bool peer, int* minb);
+int stream_threads();
+cudaError_t stream_prepare(const TileParams& p, size_t smem, int minb, int* occupancy);
+cudaError_t launch_step_stream(const TileParams& p, const uint8_t* cur, uint8_t* next, int grid, int minb,
+                               size_t smem, cudaStream_t st);
 size_t packed_smem_bytes(const TileParams& p);
 cudaError_t packed_prepare(const TileParams& p, size_t smem, int threads, int* occupancy);
 cudaError_t launch_step_packed(const TileParams& p, const uint32_t* cur, uint32_t* next, int grid, int threads,

@@ -1,0 +1,352 @@
+// sqz_stream.cu — the byte-state step for LARGE tiles.
+//
+// Link-heavy fractals (the carpet's full tile edges: 112 outside cells per 512-cell tile
+// at tile level 3) need larger tiles: at level 4 the carpet's links fall to 328 per 4096 cells
+// (SURVEY §7 hard part 3).  A 32-tile chunk of such tiles (131 KB) no longer fits shared memory
+// twice, so this kernel keeps the chunk only in its bit-sliced form Z (4 B per cell position, bit
+// i = tile i, the same form k_step_tile builds) and STREAMS the bytes through two small rings:
+//
+//   producer warp:   slice q of the chunk (cells [512q, 512q+512) of its 32 tiles) -> in-ring slot
+//                    (32 one-dimensional bulk copies, one per tile, on the slot's mbarrier)
+//   consumer warps:  Phase A  slice -> Z (lane = tile: pack 32 bytes, 32x32 warp transpose)
+//                    Phase B  boundary-link words from Z (neighbour tile in the chunk) or from the
+//                             4-byte gathers issued one chunk ahead (outside the chunk)
+//                    Phase C+D count + rule per j-block, transpose back -> out-ring slot; consumer
+//                             warp 0 bulk-stores each finished slice (32 copies, one per tile)
+//
+// Consumer warp w owns j-block w of every slice (16 warps x 32 cells = 512), so its neighbour
+// table rows stay in registers; three named barriers per chunk (Z complete, links complete, Z
+// free).  The neighbour structure is the one of k_step_tile (P:57, P:189 at tile level).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "sqz_bits.cuh"
+
+namespace sqz {
+
+constexpr uint32_t kStreamSW = 512;   // cells (bytes) per slice and tile
+constexpr uint32_t kStreamSWp = 528;  // slot stride per tile: an odd multiple of 16 >= SW + 16
+constexpr int kStreamNW = 16;         // consumer warps: one j-block of each slice apiece
+constexpr int kStreamThreads = 32 * (kStreamNW + 1);
+constexpr uint32_t kStreamMaxLinks = 1024;
+
+struct StreamSmem {
+  uint8_t* in0;     // nin slots of 32 x SWp bytes
+  uint8_t* out0;    // nout slots of 32 x SWp bytes
+  uint32_t* Z;      // [K state words | E link words | zero word]
+  uint32_t* Wn;     // PEER: the chunk's new state words (bit i = tile i), K words
+  uint32_t* ntl;    // [ndirs][32] neighbour tile + 1 of each lane's tile (next chunk)
+  uint32_t* R;      // [E][32] prefetched words holding out-of-chunk neighbour bytes (next chunk)
+  uint32_t* lj2;    // [E] link cells, then ndirs + 1 direction starts
+  uint64_t* bar;    // infull[nin], inempty[nin], outfull[nout], outempty[nout]
+};
+
+__host__ __device__ inline size_t stream_layout(const TileParams& p, bool peer, uint8_t* base, StreamSmem* s) {
+  const size_t slot = (size_t)kChunkTiles * kStreamSWp;
+  size_t off = 0;
+  if (s) s->in0 = base + off;
+  off += p.sin * slot;
+  if (s) s->out0 = base + off;
+  off += p.sout * slot;
+  if (s) s->Z = (uint32_t*)(base + off);
+  off += align16((size_t)(p.K + p.E + 1) * 4);
+  if (s) s->Wn = (uint32_t*)(base + off);
+  off += peer ? align16((size_t)p.K * 4) : 0;
+  if (s) s->ntl = (uint32_t*)(base + off);
+  off += (size_t)(p.ndirs ? p.ndirs : 1) * kChunkTiles * 4;
+  if (s) s->R = (uint32_t*)(base + off);
+  off += (size_t)(p.E ? p.E : 1) * kChunkTiles * 4;
+  if (s) s->lj2 = (uint32_t*)(base + off);
+  off += align16((size_t)(p.E + p.ndirs + 1) * 4);
+  if (s) s->bar = (uint64_t*)(base + off);
+  off += (size_t)2 * (p.sin + p.sout) * 8;
+  return align16(off);
+}
+
+size_t stream_smem_bytes(const TileParams& p, bool peer) { return stream_layout(p, peer, nullptr, nullptr); }
+
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;" ::"r"(kStreamNW * 32) : "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+// 17 warps: 120 registers at one CTA per SM, 56 at two (the register file is 64K per SM)
+template <int MINB>
+struct StreamRegs {
+  static constexpr int n = MINB >= 2 ? 56 : 120;
+};
+
+template <int DMAX, bool CONWAY, int RB, int MINB, int NOUT, bool PEER>
+__global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, const uint8_t* __restrict__ cur,
+                                                              uint8_t* __restrict__ next) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  StreamSmem S;
+  stream_layout(p, PEER, smem_raw, &S);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t K = (uint32_t)p.K, Kp = p.Kp, E = p.E, NIN = p.sin;
+  const uint32_t KP32 = (K + 31) & ~31u, nblk = KP32 / 32;
+  const uint32_t nsl = (KP32 + kStreamSW - 1) / kStreamSW;
+  uint64_t* infull = S.bar;
+  uint64_t* inempty = S.bar + NIN;
+  uint64_t* outfull = S.bar + 2 * NIN;
+  uint64_t* outempty = S.bar + 2 * NIN + NOUT;
+
+  for (uint32_t e = tid; e < E; e += blockDim.x) S.lj2[e] = p.link_j2[e];
+  for (uint32_t d = tid; d <= p.ndirs; d += blockDim.x) S.lj2[E + d] = p.dir_start[d];
+  if (tid == 0) {
+    S.Z[p.zslot] = 0;
+    for (uint32_t i = 0; i < NIN; ++i) {
+      mbar_init(&infull[i], 1);
+      mbar_init(&inempty[i], kStreamNW);
+    }
+    for (uint32_t i = 0; i < NOUT; ++i) {
+      mbar_init(&outfull[i], kStreamNW);
+      mbar_init(&outempty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if ((uint64_t)blockIdx.x >= p.nchunks) return;
+  const uint64_t G = gridDim.x;
+  const uint32_t in_base = smem_u32(S.in0), out_base = smem_u32(S.out0);
+  const uint32_t slot_bytes = kChunkTiles * kStreamSWp;
+
+  if (warp == 0) {  // ------------------------------------------------ producer: slices in
+    uint32_t seq = 0;
+    for (uint64_t chunk = blockIdx.x; chunk < p.nchunks; chunk += G) {
+      const ChunkInfo c = chunk_info(p, chunk);
+      const uint8_t* src = cur + (c.t0 - p.tile_lo + lane) * Kp;
+      for (uint32_t q = 0; q < nsl; ++q, ++seq) {
+        const uint32_t slot = seq % NIN, u = seq / NIN;
+        if (u > 0) mbar_wait(&inempty[slot], (u - 1) & 1);
+        const uint32_t bytes = (q + 1 == nsl) ? Kp - q * kStreamSW : kStreamSW;
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&infull[slot])),
+                       "r"(c.nt * bytes)
+                       : "memory");
+        __syncwarp();
+        if ((uint32_t)lane < c.nt)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  in_base + slot * slot_bytes + lane * kStreamSWp),
+              "l"(src + q * kStreamSW), "r"(bytes), "r"(smem_u32(&infull[slot]))
+              : "memory");
+      }
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------------- consumers
+  const int cw = warp - 1;
+  const uint32_t my_jj = 4 * (lane & 7) + (lane >> 3);  // cell offset this lane holds after a transpose
+  const Transposer tr(lane);
+  uint4 rows[RB];  // neighbour-table rows of this warp's j-blocks (block cw of slices 0..RB-1)
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    const uint32_t j = ((uint32_t)i * kStreamNW + (uint32_t)cw) * 32 + my_jj;
+    rows[i] = j < K ? __ldg(reinterpret_cast<const uint4*>(p.nbr) + j) : make_uint4(0, 0, 0, 0);
+  }
+  const uint32_t z_s = smem_u32(S.Z);
+  bool peer_sent = false;
+  chunk_neighbours(p, S.ntl, S.R, S.lj2, chunk_info(p, blockIdx.x), cur, cw, kStreamNW, lane, E);
+
+  uint32_t seq = 0;
+  for (uint64_t chunk = blockIdx.x; chunk < p.nchunks; chunk += G, seq += nsl) {
+    const ChunkInfo c = chunk_info(p, chunk);
+    uint32_t pe0 = 0, pe1 = 0;
+    if (PEER && cw == kStreamNW - 1) {
+      pe0 = p.peer_chunk_start[chunk];
+      pe1 = p.peer_chunk_start[chunk + 1];
+    }
+    // Phase A: slice q, j-block q * NW + cw -> Z
+    for (uint32_t q = 0; q < nsl; ++q) {
+      const uint32_t s = seq + q, slot = s % NIN;
+      mbar_wait(&infull[slot], (s / NIN) & 1);
+      const uint32_t jb = q * kStreamNW + (uint32_t)cw;
+      if (jb < nblk) {
+        const uint32_t a = in_base + slot * slot_bytes + (uint32_t)lane * kStreamSWp + (uint32_t)cw * 32;
+        const uint32_t x = tr(pack01(lds128(a), lds128(a + 16)));
+        const uint32_t j = jb * 32 + my_jj;
+        if (j < K) sts32(z_s + 4 * j, x);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&inempty[slot]);
+    }
+    consumers_sync();  // Z holds every state word of the chunk
+
+    // Phase B: link words; warp w owns directions w, w + NW, ... (it prefetched them last chunk)
+    cp_async_wait_all();
+    for (int d = cw; d < (int)p.ndirs; d += kStreamNW) {
+      const int64_t tn = (int64_t)S.ntl[d * kChunkTiles + lane] - 1;
+      const uint64_t rel = (uint64_t)(tn - (int64_t)c.t0);
+      const bool inside = tn >= 0 && rel < c.nt;
+      const uint32_t e1 = S.lj2[E + d + 1];
+      for (uint32_t e = S.lj2[E + d]; e < e1; ++e) {
+        const uint32_t j2 = S.lj2[e];
+        uint32_t v = 0;
+        if (inside) v = (lds32(z_s + 4 * j2) >> (uint32_t)rel) & 1u;
+        else if (tn >= 0) v = (S.R[e * kChunkTiles + lane] >> (8 * (j2 & 3u))) & 0xFFu;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
+        if (lane == 0) S.Z[K + e] = bal;
+      }
+    }
+    consumers_sync();  // link words published
+    if (chunk + G < p.nchunks) chunk_neighbours(p, S.ntl, S.R, S.lj2, chunk_info(p, chunk + G), cur, cw, kStreamNW, lane, E);
+
+    // Phase C+D: slice q -> out-ring slot, warp 0 of the consumers bulk-stores it
+    const uint32_t live_lanes = c.nt >= 32 ? 0xFFFFFFFFu : ((1u << c.nt) - 1u);
+    auto slice_out = [&](uint32_t q, const uint4& row) {
+      const uint32_t s = seq + q, oslot = s % NOUT, u = s / NOUT;
+      if (u > 0) mbar_wait(&outempty[oslot], (u - 1) & 1);
+      const uint32_t jb = q * kStreamNW + (uint32_t)cw;
+      if (jb < nblk) {
+        const uint32_t j = jb * 32 + my_jj;
+        uint32_t nw = 0;
+        if (j < K) {
+          uint32_t x[8];
+          x[0] = lds32(z_s + (row.x & 0xFFFFu));
+          x[1] = lds32(z_s + (row.x >> 16));
+          x[2] = lds32(z_s + (row.y & 0xFFFFu));
+          x[3] = lds32(z_s + (row.y >> 16));
+          x[4] = lds32(z_s + (row.z & 0xFFFFu));
+          if (DMAX > 5) {
+            x[5] = lds32(z_s + (row.z >> 16));
+            x[6] = lds32(z_s + (row.w & 0xFFFFu));
+            x[7] = lds32(z_s + (row.w >> 16));
+          }
+          uint32_t c0, c1, c2, c3;
+          if (DMAX <= 5) {
+            const uint32_t s1 = x[0] ^ x[1] ^ x[2], k1 = maj3(x[0], x[1], x[2]);
+            const uint32_t s2 = s1 ^ x[3] ^ x[4], k2 = maj3(s1, x[3], x[4]);
+            c0 = s2;
+            c1 = k1 ^ k2;
+            c2 = k1 & k2;
+            c3 = 0;
+          } else {
+            const uint32_t sa = x[0] ^ x[1] ^ x[2], ka = maj3(x[0], x[1], x[2]);
+            const uint32_t sb = x[3] ^ x[4] ^ x[5], kb = maj3(x[3], x[4], x[5]);
+            const uint32_t sc = sa ^ sb ^ x[6], kc = maj3(sa, sb, x[6]);
+            c0 = sc ^ x[7];
+            const uint32_t kd = sc & x[7];
+            const uint32_t se = ka ^ kb ^ kc, ke = maj3(ka, kb, kc);
+            c1 = se ^ kd;
+            const uint32_t kf = se & kd;
+            c2 = ke ^ kf;
+            c3 = ke & kf;
+          }
+          const uint32_t alive = lds32(z_s + 4 * j);
+          if (CONWAY) nw = c1 & ~c2 & ~c3 & (c0 | alive);  // B3/S23
+          else nw = (alive & rule_bits(p.survive, c0, c1, c2, c3)) | (~alive & rule_bits(p.birth, c0, c1, c2, c3));
+          nw &= live_lanes;
+          if (PEER) S.Wn[j] = nw;
+        }
+        const uint32_t xb = tr(nw);  // bit 8p+m = cell jb*32 + 4m + p of this lane's tile (0 past K)
+        const uint32_t o = out_base + oslot * slot_bytes + (uint32_t)lane * kStreamSWp + (uint32_t)cw * 32;
+        const uint32_t m = 0x01010101u;
+        sts128(o, xb & m, (xb >> 1) & m, (xb >> 2) & m, (xb >> 3) & m);
+        sts128(o + 16, (xb >> 4) & m, (xb >> 5) & m, (xb >> 6) & m, (xb >> 7) & m);
+        if (jb + 1 == nblk && Kp > KP32) sts128(o + 32, 0u, 0u, 0u, 0u);  // the tile's 16 zero padding bytes
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&outfull[oslot]);
+      if (cw == 0) {  // the storer: slice q of the chunk's 32 tiles, one bulk copy per tile
+        mbar_wait(&outfull[oslot], u & 1);
+        const uint32_t bytes = (q + 1 == nsl) ? Kp - q * kStreamSW : kStreamSW;
+        if ((uint32_t)lane < c.nt)
+          tma_store_1d(next + (c.t0 - p.tile_lo + lane) * Kp + q * kStreamSW,
+                       S.out0 + oslot * slot_bytes + lane * kStreamSWp, bytes);
+        bulk_wait_read<NOUT - 1>();  // the slot of slice s + 1 has been read out (its use s + 1 - NOUT)
+        __syncwarp();
+        if (lane == 0 && s + 1 >= NOUT) mbar_arrive(&outempty[(s + 1) % NOUT]);
+      }
+    };
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+      if ((uint32_t)i < nsl) slice_out((uint32_t)i, rows[i]);
+    for (uint32_t q = RB; q < nsl; ++q) {
+      const uint32_t j = (q * kStreamNW + (uint32_t)cw) * 32 + my_jj;
+      slice_out(q, j < K ? __ldg(reinterpret_cast<const uint4*>(p.nbr) + j) : make_uint4(0, 0, 0, 0));
+    }
+    consumers_sync();  // Z (and Wn) no longer read: the next chunk may overwrite them
+    if (PEER && cw == kStreamNW - 1 && pe1 > pe0) {
+      // fused halo: the chunk's send cells, from the new state words, straight into the peers' buffers
+      for (uint32_t e = pe0 + (uint32_t)lane; e < pe1; e += 32) {
+        const uint32_t cell = p.peer_cell[e];
+        p.peer_recv[p.peer_of[e]][p.peer_pos[e]] = (uint8_t)((S.Wn[cell & 0xFFFFu] >> (cell >> 16)) & 1u);
+      }
+      peer_sent = true;
+    }
+  }
+  cp_async_wait_all();
+  if (cw == 0) bulk_wait_all();
+  if (PEER && peer_sent) __threadfence_system();
+}
+
+using StreamFn = void (*)(TileParams, const uint8_t*, uint8_t*);
+
+template <bool PEER, int RB, int MINB>
+static StreamFn pick_stream_r(const TileParams& p) {
+  const bool conway = (p.birth == (1u << 3)) && (p.survive == ((1u << 2) | (1u << 3)));
+  if (p.sout == 3) {
+    if (p.dmax <= 5) return conway ? k_step_stream<5, true, RB, MINB, 3, PEER> : k_step_stream<5, false, RB, MINB, 3, PEER>;
+    return conway ? k_step_stream<8, true, RB, MINB, 3, PEER> : k_step_stream<8, false, RB, MINB, 3, PEER>;
+  }
+  if (p.dmax <= 5) return conway ? k_step_stream<5, true, RB, MINB, 2, PEER> : k_step_stream<5, false, RB, MINB, 2, PEER>;
+  return conway ? k_step_stream<8, true, RB, MINB, 2, PEER> : k_step_stream<8, false, RB, MINB, 2, PEER>;
+}
+
+// RB = slices whose neighbour rows stay in registers: 8 at one CTA per SM (carpet level 4: all 8
+// slices), 2 at two CTAs per SM (56 registers).
+template <bool PEER>
+static StreamFn pick_stream_t(const TileParams& p, int minb) {
+  return minb >= 2 ? pick_stream_r<PEER, 2, 2>(p) : pick_stream_r<PEER, 8, 1>(p);
+}
+
+// The ring depths (p.sin, p.sout) and CTAs per SM for these tables: two CTAs per SM when three
+// input and two output slots fit twice, else one CTA with the deepest input ring that fits.
+bool stream_plan(TileParams& p, bool peer, int* minb) {
+  if (p.E > kStreamMaxLinks) return false;
+  const size_t cap = 227 * 1024;
+  p.sin = 3;
+  p.sout = 2;
+  const char* force = getenv("SQZ_STREAM_CTAS");  // tuning knob: 1 or 2 CTAs per SM
+  if ((!force || atoi(force) >= 2) && 2 * stream_smem_bytes(p, peer) <= cap) {
+    *minb = 2;
+    return true;
+  }
+  *minb = 1;
+  for (p.sin = 6; p.sin >= 2; --p.sin)
+    if (stream_smem_bytes(p, peer) <= cap) return true;
+  return false;
+}
+
+int stream_threads() { return kStreamThreads; }
+
+cudaError_t stream_prepare(const TileParams& p, size_t smem, int minb, int* occupancy) {
+  for (StreamFn fn : {pick_stream_t<false>(p, minb), pick_stream_t<true>(p, minb)}) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  int blocks = 0;
+  cudaError_t e =
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pick_stream_t<false>(p, minb), kStreamThreads, smem);
+  if (e != cudaSuccess) return e;
+  *occupancy = blocks;
+  return blocks > 0 ? cudaSuccess : cudaErrorInvalidConfiguration;
+}
+
+cudaError_t launch_step_stream(const TileParams& p, const uint8_t* cur, uint8_t* next, int grid, int minb,
+                               size_t smem, cudaStream_t st) {
+  if (p.nchunks == 0) return cudaSuccess;
+  StreamFn fn = p.peer_recv ? pick_stream_t<true>(p, minb) : pick_stream_t<false>(p, minb);
+  fn<<<grid, kStreamThreads, smem, st>>>(p, cur, next);
+  return cudaGetLastError();
+}
+
+}  // namespace sqz
