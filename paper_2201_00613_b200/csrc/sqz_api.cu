@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -492,7 +493,12 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
         c->stream_sout = p.sout;
         c->tile_smem = stream_smem_bytes(p, c->nranks > 1);
         c->tile_threads = stream_threads();
-        if (stream_prepare(p, c->tile_smem, c->stream_minb, &occ) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
+        const cudaError_t se = stream_prepare(p, c->tile_smem, c->stream_minb, &occ);
+        if (getenv("SQZ_DEBUG"))
+          fprintf(stderr, "sqz: streaming step K=%llu E=%u rings %u/%u smem %zu minb %d occupancy %d (%s)\n",
+                  (unsigned long long)c->tt.K, c->tt.E, p.sin, p.sout, c->tile_smem, c->stream_minb, occ,
+                  cudaGetErrorString(se));
+        if (se != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
         c->stream_grid = sms * std::max(1, occ);
       }
       if (c->opts.ctas_per_sm) occ = std::min<int>(occ, (int)c->opts.ctas_per_sm);

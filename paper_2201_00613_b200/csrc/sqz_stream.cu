@@ -6,7 +6,7 @@
 // twice, so this kernel keeps the chunk only in its bit-sliced form Z (4 B per cell position, bit
 // i = tile i, the same form k_step_tile builds) and STREAMS the bytes through two small rings:
 //
-//   producer warp:   slice q of the chunk (cells [512q, 512q+512) of its 32 tiles) -> in-ring slot
+//   producer warp:   slice q of the chunk (cells [480q, 480q+480) of its 32 tiles) -> in-ring slot
 //                    (32 one-dimensional bulk copies, one per tile, on the slot's mbarrier)
 //   consumer warps:  Phase A  slice -> Z (lane = tile: pack 32 bytes, 32x32 warp transpose)
 //                    Phase B  boundary-link words from Z (neighbour tile in the chunk) or from the
@@ -14,7 +14,7 @@
 //                    Phase C+D count + rule per j-block, transpose back -> out-ring slot; consumer
 //                             warp 0 bulk-stores each finished slice (32 copies, one per tile)
 //
-// Consumer warp w owns j-block w of every slice (16 warps x 32 cells = 512), so its neighbour
+// Consumer warp w owns j-block w of every slice (15 warps x 32 cells = 480), so its neighbour
 // table rows stay in registers; three named barriers per chunk (Z complete, links complete, Z
 // free).  The neighbour structure is the one of k_step_tile (P:57, P:189 at tile level).
 #include <cuda_runtime.h>
@@ -25,9 +25,9 @@
 
 namespace sqz {
 
-constexpr uint32_t kStreamSW = 512;   // cells (bytes) per slice and tile
-constexpr uint32_t kStreamSWp = 528;  // slot stride per tile: an odd multiple of 16 >= SW + 16
-constexpr int kStreamNW = 16;         // consumer warps: one j-block of each slice apiece
+constexpr uint32_t kStreamSW = 480;   // cells (bytes) per slice and tile: one j-block per consumer warp
+constexpr uint32_t kStreamSWp = 496;  // slot stride per tile: an odd multiple of 16 >= SW + 16
+constexpr int kStreamNW = 15;         // consumer warps: one j-block of each slice apiece
 constexpr int kStreamThreads = 32 * (kStreamNW + 1);
 constexpr uint32_t kStreamMaxLinks = 1024;
 
@@ -75,10 +75,11 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 
-// 17 warps: 120 registers at one CTA per SM, 56 at two (the register file is 64K per SM)
+// 16 warps: 128 registers at one CTA per SM, 64 at two (16K registers per SM sub-partition,
+// which holds every fourth warp)
 template <int MINB>
 struct StreamRegs {
-  static constexpr int n = MINB >= 2 ? 56 : 120;
+  static constexpr int n = MINB >= 2 ? 64 : 128;
 };
 
 template <int DMAX, bool CONWAY, int RB, int MINB, int NOUT, bool PEER>
@@ -301,8 +302,8 @@ static StreamFn pick_stream_r(const TileParams& p) {
   return conway ? k_step_stream<8, true, RB, MINB, 2, PEER> : k_step_stream<8, false, RB, MINB, 2, PEER>;
 }
 
-// RB = slices whose neighbour rows stay in registers: 8 at one CTA per SM (carpet level 4: all 8
-// slices), 2 at two CTAs per SM (56 registers).
+// RB = slices whose neighbour rows stay in registers: 8 at one CTA per SM (carpet level 4: 8 of
+// its 9 slices), 2 at two CTAs per SM (64 registers).
 template <bool PEER>
 static StreamFn pick_stream_t(const TileParams& p, int minb) {
   return minb >= 2 ? pick_stream_r<PEER, 2, 2>(p) : pick_stream_r<PEER, 8, 1>(p);
