@@ -17,7 +17,9 @@
 // Consumer warp w owns j-block w of every slice (15 warps x 32 cells = 480), so its neighbour
 // table rows stay in registers; three named barriers per chunk (Z complete, links complete, Z
 // free).  The neighbour structure is the one of k_step_tile (P:57, P:189 at tile level).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <stdint.h>
 #include <stdlib.h>
 
@@ -26,24 +28,27 @@
 namespace sqz {
 
 constexpr uint32_t kStreamSW = 480;   // cells (bytes) per slice and tile: one j-block per consumer warp
-constexpr uint32_t kStreamSWp = 496;  // slot stride per tile: an odd multiple of 16 >= SW + 16
+constexpr uint32_t kStreamBox = 240;  // TMA box width: a slice is two [32 tiles x 240 B] boxes; the
+                                      // 240-byte row pitch (an odd multiple of 16) keeps the lanes'
+                                      // 128-bit accesses (lane = tile) bank-conflict-free
+constexpr uint32_t kStreamSlot = 2 * kChunkTiles * kStreamBox;  // bytes per ring slot
 constexpr int kStreamNW = 15;         // consumer warps: one j-block of each slice apiece
 constexpr int kStreamThreads = 32 * (kStreamNW + 1);
 constexpr uint32_t kStreamMaxLinks = 1024;
 
 struct StreamSmem {
-  uint8_t* in0;     // nin slots of 32 x SWp bytes
-  uint8_t* out0;    // nout slots of 32 x SWp bytes
+  uint8_t* in0;     // nin slots of two [32][240] boxes
+  uint8_t* out0;    // nout slots of two [32][240] boxes
   uint32_t* Z;      // [K state words | E link words | zero word]
   uint32_t* Wn;     // PEER: the chunk's new state words (bit i = tile i), K words
-  uint32_t* ntl;    // [ndirs][32] neighbour tile + 1 of each lane's tile (next chunk)
-  uint32_t* R;      // [E][32] prefetched words holding out-of-chunk neighbour bytes (next chunk)
-  uint32_t* lj2;    // [E] link cells, then ndirs + 1 direction starts
+  uint32_t* ntl;    // [2][ndirs][32] neighbour tile + 1 of each lane's tile, by chunk parity
+  uint32_t* R;      // [E][32] words holding the out-of-chunk neighbour byte of each link (this chunk)
+  uint32_t* lj2;    // [E] link e: its cell in the neighbour tile | direction << 16
   uint64_t* bar;    // infull[nin], inempty[nin], outfull[nout], outempty[nout]
 };
 
 __host__ __device__ inline size_t stream_layout(const TileParams& p, bool peer, uint8_t* base, StreamSmem* s) {
-  const size_t slot = (size_t)kChunkTiles * kStreamSWp;
+  const size_t slot = kStreamSlot;
   size_t off = 0;
   if (s) s->in0 = base + off;
   off += p.sin * slot;
@@ -54,11 +59,11 @@ __host__ __device__ inline size_t stream_layout(const TileParams& p, bool peer, 
   if (s) s->Wn = (uint32_t*)(base + off);
   off += peer ? align16((size_t)p.K * 4) : 0;
   if (s) s->ntl = (uint32_t*)(base + off);
-  off += (size_t)(p.ndirs ? p.ndirs : 1) * kChunkTiles * 4;
+  off += (size_t)2 * (p.ndirs ? p.ndirs : 1) * kChunkTiles * 4;
   if (s) s->R = (uint32_t*)(base + off);
   off += (size_t)(p.E ? p.E : 1) * kChunkTiles * 4;
   if (s) s->lj2 = (uint32_t*)(base + off);
-  off += align16((size_t)(p.E + p.ndirs + 1) * 4);
+  off += align16((size_t)(p.E ? p.E : 1) * 4);
   if (s) s->bar = (uint64_t*)(base + off);
   off += (size_t)2 * (p.sin + p.sout) * 8;
   return align16(off);
@@ -75,6 +80,24 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 
+// Non-blocking: has the phase of `parity` completed?  (lane 0 tests, the warp agrees)
+__device__ __forceinline__ bool mbar_test_warp(uint64_t* bar, uint32_t parity, int lane) {
+  uint32_t done = 0;
+  if (lane == 0)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  return __shfl_sync(0xFFFFFFFFu, done, 0) != 0;
+}
+
+// Shared-memory offset of byte x (a multiple of 16, < 480) of a tile's slice row, relative to the
+// row's start in box 0: the row continues in box 1 after 240 bytes.
+__device__ __forceinline__ uint32_t box_off(uint32_t x) {
+  return x < kStreamBox ? x : x - kStreamBox + kStreamSlot / 2;
+}
+
 // 16 warps: 128 registers at one CTA per SM, 64 at two (16K registers per SM sub-partition,
 // which holds every fourth warp)
 template <int MINB>
@@ -82,9 +105,35 @@ struct StreamRegs {
   static constexpr int n = MINB >= 2 ? 64 : 128;
 };
 
+// Adjacency words of chunk c (neighbour tile + 1 per link direction and lane tile, built at init)
+// -> ntl buffer, by cp.async; warps by direction.  Rows are padded to whole 128-tile chunks.
+__device__ __forceinline__ void adj_prefetch(const TileParams& p, uint32_t* ntl, const ChunkInfo& c, int cw, int lane) {
+  for (uint32_t d = (uint32_t)cw; d < p.ndirs; d += kStreamNW)
+    cp_async4(&ntl[d * kChunkTiles + lane], p.adj + d * p.adj_stride + (c.t0 - p.tile_lo + lane));
+  cp_async_commit();
+}
+
+// For every link e (spread over the consumer warps) whose neighbour tile lies outside chunk c: the
+// word holding the neighbour byte, by a 4-byte cp.async (or from the halo for another shard's tile).
+__device__ __forceinline__ void link_prefetch(const TileParams& p, const StreamSmem& S, const uint32_t* ntl,
+                                              const ChunkInfo& c, const uint8_t* __restrict__ cur, int cw, int lane) {
+  for (uint32_t e = (uint32_t)cw; e < p.E; e += kStreamNW) {
+    const uint32_t le = S.lj2[e], j2 = le & 0xFFFFu, d = le >> 16;
+    const int64_t tn = (int64_t)ntl[d * kChunkTiles + lane] - 1;
+    if (tn < 0 || ((uint64_t)tn >= c.t0 && (uint64_t)tn < c.t0 + c.nt)) continue;
+    uint32_t* dst = &S.R[e * kChunkTiles + lane];
+    if ((uint64_t)tn >= p.tile_lo && (uint64_t)tn < p.tile_hi)
+      cp_async4(dst, cur + ((((uint64_t)tn - p.tile_lo) * p.Kp + j2) & ~3ull));
+    else
+      *dst = fetch_cell(cur, (uint64_t)tn * p.K + j2, p.halo) << (8 * (j2 & 3u));  // halo: rare, synchronous
+  }
+  cp_async_commit();
+}
+
 template <int DMAX, bool CONWAY, int RB, int MINB, int NOUT, bool PEER>
 __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, const uint8_t* __restrict__ cur,
-                                                              uint8_t* __restrict__ next) {
+                                                              const __grid_constant__ CUtensorMap tm_in,
+                                                              const __grid_constant__ CUtensorMap tm_out) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   StreamSmem S;
   stream_layout(p, PEER, smem_raw, &S);
@@ -97,8 +146,7 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
   uint64_t* outfull = S.bar + 2 * NIN;
   uint64_t* outempty = S.bar + 2 * NIN + NOUT;
 
-  for (uint32_t e = tid; e < E; e += blockDim.x) S.lj2[e] = p.link_j2[e];
-  for (uint32_t d = tid; d <= p.ndirs; d += blockDim.x) S.lj2[E + d] = p.dir_start[d];
+  for (uint32_t e = tid; e < E; e += blockDim.x) S.lj2[e] = p.link_j2[e] | ((uint32_t)p.link_dir[e] << 16);
   if (tid == 0) {
     S.Z[p.zslot] = 0;
     for (uint32_t i = 0; i < NIN; ++i) {
@@ -115,30 +163,62 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
   if ((uint64_t)blockIdx.x >= p.nchunks) return;
   const uint64_t G = gridDim.x;
   const uint32_t in_base = smem_u32(S.in0), out_base = smem_u32(S.out0);
-  const uint32_t slot_bytes = kChunkTiles * kStreamSWp;
+  const uint32_t slot_bytes = kStreamSlot;
 
-  if (warp == 0) {  // ------------------------------------------------ producer: slices in
-    uint32_t seq = 0;
-    for (uint64_t chunk = blockIdx.x; chunk < p.nchunks; chunk += G) {
-      const ChunkInfo c = chunk_info(p, chunk);
-      const uint8_t* src = cur + (c.t0 - p.tile_lo + lane) * Kp;
-      for (uint32_t q = 0; q < nsl; ++q, ++seq) {
-        const uint32_t slot = seq % NIN, u = seq / NIN;
-        if (u > 0) mbar_wait(&inempty[slot], (u - 1) & 1);
-        const uint32_t bytes = (q + 1 == nsl) ? Kp - q * kStreamSW : kStreamSW;
-        if (lane == 0)
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&infull[slot])),
-                       "r"(c.nt * bytes)
-                       : "memory");
-        __syncwarp();
-        if ((uint32_t)lane < c.nt)
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  in_base + slot * slot_bytes + lane * kStreamSWp),
-              "l"(src + q * kStreamSW), "r"(bytes), "r"(smem_u32(&infull[slot]))
-              : "memory");
+  if (warp == 0) {  // ------------------------------- the copy warp: slices in and out, never blocking
+    const uint32_t total = (uint32_t)((p.nchunks - blockIdx.x + G - 1) / G) * nsl;
+    uint32_t ld = 0, st = 0, ld_q = 0, st_q = 0;
+    uint64_t ld_c = blockIdx.x, st_c = blockIdx.x;
+    while (st < total) {
+      bool did = false;
+      if (ld < total) {
+        const uint32_t slot = ld % NIN, u = ld / NIN;
+        if (u == 0 || mbar_test_warp(&inempty[slot], (u - 1) & 1, lane)) {
+          if (lane == 0) {  // two 2D boxes [32 tiles x 240 B] (rows past the shard, columns past Kp: zero)
+            const uint32_t bar = smem_u32(&infull[slot]);
+            const int32_t row = (int32_t)(ld_c * kChunkTiles), x0 = (int32_t)(ld_q * kStreamSW);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kStreamSlot)
+                         : "memory");
+            for (int h = 0; h < 2; ++h)
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                  "[%4];" ::"r"(in_base + slot * slot_bytes + h * (kStreamSlot / 2)),
+                  "l"(&tm_in), "r"(x0 + h * (int32_t)kStreamBox), "r"(row), "r"(bar)
+                  : "memory");
+          }
+          __syncwarp();
+          ++ld;
+          if (++ld_q == nsl) {
+            ld_q = 0;
+            ld_c += G;
+          }
+          did = true;
+        }
       }
+      const uint32_t oslot = st % NOUT;
+      if (mbar_test_warp(&outfull[oslot], (st / NOUT) & 1, lane)) {
+        if (lane == 0) {  // two 2D boxes; rows past the shard and columns past Kp are not written
+          const int32_t row = (int32_t)(st_c * kChunkTiles), x0 = (int32_t)(st_q * kStreamSW);
+          for (int h = 0; h < 2; ++h)
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&tm_out),
+                         "r"(x0 + h * (int32_t)kStreamBox), "r"(row),
+                         "r"(out_base + oslot * slot_bytes + h * (kStreamSlot / 2))
+                         : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          bulk_wait_read<NOUT - 1>();  // slice st + 1 - NOUT has been read out: its slot may be refilled
+          if (st + 1 >= NOUT) mbar_arrive(&outempty[(st + 1) % NOUT]);
+        }
+        __syncwarp();
+        ++st;
+        if (++st_q == nsl) {
+          st_q = 0;
+          st_c += G;
+        }
+        did = true;
+      }
+      if (!did) __nanosleep(20);
     }
+    bulk_wait_all();
     return;
   }
 
@@ -153,12 +233,20 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
     rows[i] = j < K ? __ldg(reinterpret_cast<const uint4*>(p.nbr) + j) : make_uint4(0, 0, 0, 0);
   }
   const uint32_t z_s = smem_u32(S.Z);
+  const uint32_t ntl_words = (p.ndirs ? p.ndirs : 1) * kChunkTiles;
   bool peer_sent = false;
-  chunk_neighbours(p, S.ntl, S.R, S.lj2, chunk_info(p, blockIdx.x), cur, cw, kStreamNW, lane, E);
+  {  // prologue: adjacency of the first two chunks, the first chunk's link gathers
+    adj_prefetch(p, S.ntl, chunk_info(p, blockIdx.x), cw, lane);
+    if (blockIdx.x + G < p.nchunks) adj_prefetch(p, S.ntl + ntl_words, chunk_info(p, blockIdx.x + G), cw, lane);
+    cp_async_wait_all();
+    consumers_sync();
+    link_prefetch(p, S, S.ntl, chunk_info(p, blockIdx.x), cur, cw, lane);
+  }
 
-  uint32_t seq = 0;
-  for (uint64_t chunk = blockIdx.x; chunk < p.nchunks; chunk += G, seq += nsl) {
+  uint32_t seq = 0, it = 0;
+  for (uint64_t chunk = blockIdx.x; chunk < p.nchunks; chunk += G, seq += nsl, ++it) {
     const ChunkInfo c = chunk_info(p, chunk);
+    uint32_t* ntl = S.ntl + (it & 1) * ntl_words;
     uint32_t pe0 = 0, pe1 = 0;
     if (PEER && cw == kStreamNW - 1) {
       pe0 = p.peer_chunk_start[chunk];
@@ -170,36 +258,33 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
       mbar_wait(&infull[slot], (s / NIN) & 1);
       const uint32_t jb = q * kStreamNW + (uint32_t)cw;
       if (jb < nblk) {
-        const uint32_t a = in_base + slot * slot_bytes + (uint32_t)lane * kStreamSWp + (uint32_t)cw * 32;
-        const uint32_t x = tr(pack01(lds128(a), lds128(a + 16)));
+        const uint32_t a = in_base + slot * slot_bytes + (uint32_t)lane * kStreamBox;
+        const uint32_t x = tr(pack01(lds128(a + box_off(cw * 32)), lds128(a + box_off(cw * 32 + 16))));
         const uint32_t j = jb * 32 + my_jj;
         if (j < K) sts32(z_s + 4 * j, x);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&inempty[slot]);
     }
-    consumers_sync();  // Z holds every state word of the chunk
+    cp_async_wait_all();  // this chunk's link gathers and the next chunk's adjacency (own copies)
+    consumers_sync();     // Z, R and both adjacency buffers visible to every consumer warp
 
-    // Phase B: link words; warp w owns directions w, w + NW, ... (it prefetched them last chunk)
-    cp_async_wait_all();
-    for (int d = cw; d < (int)p.ndirs; d += kStreamNW) {
-      const int64_t tn = (int64_t)S.ntl[d * kChunkTiles + lane] - 1;
+    // Phase B: link words, links spread over the warps
+    for (uint32_t e = (uint32_t)cw; e < E; e += kStreamNW) {
+      const uint32_t le = S.lj2[e], j2 = le & 0xFFFFu, d = le >> 16;
+      const int64_t tn = (int64_t)ntl[d * kChunkTiles + lane] - 1;
       const uint64_t rel = (uint64_t)(tn - (int64_t)c.t0);
-      const bool inside = tn >= 0 && rel < c.nt;
-      const uint32_t e1 = S.lj2[E + d + 1];
-      for (uint32_t e = S.lj2[E + d]; e < e1; ++e) {
-        const uint32_t j2 = S.lj2[e];
-        uint32_t v = 0;
-        if (inside) v = (lds32(z_s + 4 * j2) >> (uint32_t)rel) & 1u;
-        else if (tn >= 0) v = (S.R[e * kChunkTiles + lane] >> (8 * (j2 & 3u))) & 0xFFu;
-        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
-        if (lane == 0) S.Z[K + e] = bal;
-      }
+      uint32_t v = 0;
+      if (tn >= 0 && rel < c.nt) v = (lds32(z_s + 4 * j2) >> (uint32_t)rel) & 1u;
+      else if (tn >= 0) v = (S.R[e * kChunkTiles + lane] >> (8 * (j2 & 3u))) & 0xFFu;
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
+      if (lane == 0) S.Z[K + e] = bal;
     }
-    consumers_sync();  // link words published
-    if (chunk + G < p.nchunks) chunk_neighbours(p, S.ntl, S.R, S.lj2, chunk_info(p, chunk + G), cur, cw, kStreamNW, lane, E);
+    consumers_sync();  // link words published; R and this chunk's adjacency buffer are free
+    if (chunk + 2 * G < p.nchunks) adj_prefetch(p, ntl, chunk_info(p, chunk + 2 * G), cw, lane);
+    if (chunk + G < p.nchunks) link_prefetch(p, S, S.ntl + ((it + 1) & 1) * ntl_words, chunk_info(p, chunk + G), cur, cw, lane);
 
-    // Phase C+D: slice q -> out-ring slot, warp 0 of the consumers bulk-stores it
+    // Phase C+D: slice q -> out-ring slot (the copy warp stores it)
     const uint32_t live_lanes = c.nt >= 32 ? 0xFFFFFFFFu : ((1u << c.nt) - 1u);
     auto slice_out = [&](uint32_t q, const uint4& row) {
       const uint32_t s = seq + q, oslot = s % NOUT, u = s / NOUT;
@@ -247,25 +332,15 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
           if (PEER) S.Wn[j] = nw;
         }
         const uint32_t xb = tr(nw);  // bit 8p+m = cell jb*32 + 4m + p of this lane's tile (0 past K)
-        const uint32_t o = out_base + oslot * slot_bytes + (uint32_t)lane * kStreamSWp + (uint32_t)cw * 32;
+        const uint32_t o = out_base + oslot * slot_bytes + (uint32_t)lane * kStreamBox;
         const uint32_t m = 0x01010101u;
-        sts128(o, xb & m, (xb >> 1) & m, (xb >> 2) & m, (xb >> 3) & m);
-        sts128(o + 16, (xb >> 4) & m, (xb >> 5) & m, (xb >> 6) & m, (xb >> 7) & m);
-        if (jb + 1 == nblk && Kp > KP32) sts128(o + 32, 0u, 0u, 0u, 0u);  // the tile's 16 zero padding bytes
+        sts128(o + box_off(cw * 32), xb & m, (xb >> 1) & m, (xb >> 2) & m, (xb >> 3) & m);
+        sts128(o + box_off(cw * 32 + 16), (xb >> 4) & m, (xb >> 5) & m, (xb >> 6) & m, (xb >> 7) & m);
+        if (jb + 1 == nblk && Kp > KP32) sts128(o + box_off(cw * 32 + 32), 0u, 0u, 0u, 0u);  // 16 zero padding bytes
       }
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&outfull[oslot]);
-      if (cw == 0) {  // the storer: slice q of the chunk's 32 tiles, one bulk copy per tile
-        mbar_wait(&outfull[oslot], u & 1);
-        const uint32_t bytes = (q + 1 == nsl) ? Kp - q * kStreamSW : kStreamSW;
-        if ((uint32_t)lane < c.nt)
-          tma_store_1d(next + (c.t0 - p.tile_lo + lane) * Kp + q * kStreamSW,
-                       S.out0 + oslot * slot_bytes + lane * kStreamSWp, bytes);
-        bulk_wait_read<NOUT - 1>();  // the slot of slice s + 1 has been read out (its use s + 1 - NOUT)
-        __syncwarp();
-        if (lane == 0 && s + 1 >= NOUT) mbar_arrive(&outempty[(s + 1) % NOUT]);
-      }
     };
 #pragma unroll
     for (int i = 0; i < RB; ++i)
@@ -285,16 +360,15 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
     }
   }
   cp_async_wait_all();
-  if (cw == 0) bulk_wait_all();
   if (PEER && peer_sent) __threadfence_system();
 }
 
-using StreamFn = void (*)(TileParams, const uint8_t*, uint8_t*);
+using StreamFn = void (*)(TileParams, const uint8_t*, const CUtensorMap, const CUtensorMap);
 
 template <bool PEER, int RB, int MINB>
 static StreamFn pick_stream_r(const TileParams& p) {
   const bool conway = (p.birth == (1u << 3)) && (p.survive == ((1u << 2) | (1u << 3)));
-  if (p.sout == 3) {
+  if (p.sout >= 3) {
     if (p.dmax <= 5) return conway ? k_step_stream<5, true, RB, MINB, 3, PEER> : k_step_stream<5, false, RB, MINB, 3, PEER>;
     return conway ? k_step_stream<8, true, RB, MINB, 3, PEER> : k_step_stream<8, false, RB, MINB, 3, PEER>;
   }
@@ -309,20 +383,25 @@ static StreamFn pick_stream_t(const TileParams& p, int minb) {
   return minb >= 2 ? pick_stream_r<PEER, 2, 2>(p) : pick_stream_r<PEER, 8, 1>(p);
 }
 
-// The ring depths (p.sin, p.sout) and CTAs per SM for these tables: two CTAs per SM when three
-// input and two output slots fit twice, else one CTA with the deepest input ring that fits.
+// The ring depths (p.sin, p.sout) and CTAs per SM for these tables: two CTAs per SM when both fit
+// with at least three input slots, else one CTA with the deepest input ring that fits.
 bool stream_plan(TileParams& p, bool peer, int* minb) {
   if (p.E > kStreamMaxLinks) return false;
   const size_t cap = 227 * 1024;
-  p.sin = 3;
-  p.sout = 2;
   const char* force = getenv("SQZ_STREAM_CTAS");  // tuning knob: 1 or 2 CTAs per SM
-  if ((!force || atoi(force) >= 2) && 2 * stream_smem_bytes(p, peer) <= cap) {
-    *minb = 2;
-    return true;
+  if (!force || atoi(force) >= 2) {
+    for (uint32_t out = 3; out >= 2; --out) {
+      p.sout = out;
+      p.sin = out + 1;
+      if (2 * stream_smem_bytes(p, peer) <= cap) {
+        *minb = 2;
+        return true;
+      }
+    }
   }
   *minb = 1;
-  for (p.sin = 6; p.sin >= 2; --p.sin)
+  p.sout = 3;
+  for (p.sin = 8; p.sin >= 2; --p.sin)
     if (stream_smem_bytes(p, peer) <= cap) return true;
   return false;
 }
@@ -342,11 +421,37 @@ cudaError_t stream_prepare(const TileParams& p, size_t smem, int minb, int* occu
   return blocks > 0 ? cudaSuccess : cudaErrorInvalidConfiguration;
 }
 
+// 2D tensor map of a tile-padded state buffer: dim 0 = the Kp bytes of a tile, dim 1 = the shard's
+// tiles (row pitch Kp, a multiple of 16); boxes of [32 tiles x 240 B]; out-of-range reads are zero.
+static cudaError_t state_tensor_map(CUtensorMap* tm, const TileParams& p, const void* base) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return cudaErrorNotSupported;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {p.Kp, p.tile_hi - p.tile_lo};
+  const cuuint64_t strides[1] = {p.Kp};
+  const cuuint32_t box[2] = {kStreamBox, kChunkTiles};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 cudaError_t launch_step_stream(const TileParams& p, const uint8_t* cur, uint8_t* next, int grid, int minb,
                                size_t smem, cudaStream_t st) {
   if (p.nchunks == 0) return cudaSuccess;
+  alignas(64) CUtensorMap tin, tout;
+  cudaError_t e = state_tensor_map(&tin, p, cur);
+  if (e == cudaSuccess) e = state_tensor_map(&tout, p, next);
+  if (e != cudaSuccess) return e;
   StreamFn fn = p.peer_recv ? pick_stream_t<true>(p, minb) : pick_stream_t<false>(p, minb);
-  fn<<<grid, kStreamThreads, smem, st>>>(p, cur, next);
+  fn<<<grid, kStreamThreads, smem, st>>>(p, cur, tin, tout);
   return cudaGetLastError();
 }
 
