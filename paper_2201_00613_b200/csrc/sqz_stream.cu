@@ -80,18 +80,6 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 
-// Non-blocking: has the phase of `parity` completed?  (lane 0 tests, the warp agrees)
-__device__ __forceinline__ bool mbar_test_warp(uint64_t* bar, uint32_t parity, int lane) {
-  uint32_t done = 0;
-  if (lane == 0)
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  return __shfl_sync(0xFFFFFFFFu, done, 0) != 0;
-}
-
 // Shared-memory offset of byte x (a multiple of 16, < 480) of a tile's slice row, relative to the
 // row's start in box 0: the row continues in box 1 after 240 bytes.
 __device__ __forceinline__ uint32_t box_off(uint32_t x) {
@@ -117,10 +105,20 @@ __device__ __forceinline__ void adj_prefetch(const TileParams& p, uint32_t* ntl,
 // word holding the neighbour byte, by a 4-byte cp.async (or from the halo for another shard's tile).
 __device__ __forceinline__ void link_prefetch(const TileParams& p, const StreamSmem& S, const uint32_t* ntl,
                                               const ChunkInfo& c, const uint8_t* __restrict__ cur, int cw, int lane) {
-  for (uint32_t e = (uint32_t)cw; e < p.E; e += kStreamNW) {
+  // warp cw: the contiguous link range [E cw / NW, E (cw+1) / NW) (links are sorted by direction, so
+  // the neighbour tile is looked up once per direction)
+  const uint32_t e1 = p.E * (uint32_t)(cw + 1) / kStreamNW;
+  uint32_t dprev = ~0u;
+  int64_t tn = -1;
+  bool out = false;
+  for (uint32_t e = p.E * (uint32_t)cw / kStreamNW; e < e1; ++e) {
     const uint32_t le = S.lj2[e], j2 = le & 0xFFFFu, d = le >> 16;
-    const int64_t tn = (int64_t)ntl[d * kChunkTiles + lane] - 1;
-    if (tn < 0 || ((uint64_t)tn >= c.t0 && (uint64_t)tn < c.t0 + c.nt)) continue;
+    if (d != dprev) {
+      dprev = d;
+      tn = (int64_t)ntl[d * kChunkTiles + lane] - 1;
+      out = tn >= 0 && ((uint64_t)tn < c.t0 || (uint64_t)tn >= c.t0 + c.nt);
+    }
+    if (!out) continue;
     uint32_t* dst = &S.R[e * kChunkTiles + lane];
     if ((uint64_t)tn >= p.tile_lo && (uint64_t)tn < p.tile_hi)
       cp_async4(dst, cur + ((((uint64_t)tn - p.tile_lo) * p.Kp + j2) & ~3ull));
@@ -165,60 +163,47 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
   const uint32_t in_base = smem_u32(S.in0), out_base = smem_u32(S.out0);
   const uint32_t slot_bytes = kStreamSlot;
 
-  if (warp == 0) {  // ------------------------------- the copy warp: slices in and out, never blocking
-    const uint32_t total = (uint32_t)((p.nchunks - blockIdx.x + G - 1) / G) * nsl;
-    uint32_t ld = 0, st = 0, ld_q = 0, st_q = 0;
-    uint64_t ld_c = blockIdx.x, st_c = blockIdx.x;
-    while (st < total) {
-      bool did = false;
-      if (ld < total) {
-        const uint32_t slot = ld % NIN, u = ld / NIN;
-        if (u == 0 || mbar_test_warp(&inempty[slot], (u - 1) & 1, lane)) {
-          if (lane == 0) {  // two 2D boxes [32 tiles x 240 B] (rows past the shard, columns past Kp: zero)
-            const uint32_t bar = smem_u32(&infull[slot]);
-            const int32_t row = (int32_t)(ld_c * kChunkTiles), x0 = (int32_t)(ld_q * kStreamSW);
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kStreamSlot)
-                         : "memory");
-            for (int h = 0; h < 2; ++h)
-              asm volatile(
-                  "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-                  "[%4];" ::"r"(in_base + slot * slot_bytes + h * (kStreamSlot / 2)),
-                  "l"(&tm_in), "r"(x0 + h * (int32_t)kStreamBox), "r"(row), "r"(bar)
-                  : "memory");
-          }
-          __syncwarp();
-          ++ld;
-          if (++ld_q == nsl) {
-            ld_q = 0;
-            ld_c += G;
-          }
-          did = true;
+  if (warp == 0) {  // ------------------------------------------- the copy warp (one thread): slices in and out
+    if (lane == 0) {
+      const uint32_t total = (uint32_t)((p.nchunks - blockIdx.x + G - 1) / G) * nsl;
+      auto load = [&](uint32_t s) {  // slice s of this CTA: two 2D boxes [32 tiles x 240 B] (rows past the
+        const uint32_t slot = s % NIN, q = s % nsl;  // shard and columns past Kp read as zero)
+        const uint64_t chunk = blockIdx.x + (uint64_t)(s / nsl) * G;
+        const uint32_t bar = smem_u32(&infull[slot]);
+        const int32_t row = (int32_t)(chunk * kChunkTiles), x0 = (int32_t)(q * kStreamSW);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kStreamSlot) : "memory");
+        for (int h = 0; h < 2; ++h)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+              "[%4];" ::"r"(in_base + slot * slot_bytes + h * (kStreamSlot / 2)),
+              "l"(&tm_in), "r"(x0 + h * (int32_t)kStreamBox), "r"(row), "r"(bar)
+              : "memory");
+      };
+      uint32_t ld = 0;
+      for (; ld < NIN && ld < total; ++ld) load(ld);
+      // the consumers' order: Phase A frees the chunk's input slots one slice at a time (each freed
+      // slot takes the slice NIN ahead), then C+D fills its output slices in order
+      for (uint32_t s0 = 0; s0 < total; s0 += nsl) {
+        for (uint32_t s = s0; s < s0 + nsl && ld < total; ++s, ++ld) {
+          mbar_wait(&inempty[s % NIN], (s / NIN) & 1);
+          load(ld);
         }
-      }
-      const uint32_t oslot = st % NOUT;
-      if (mbar_test_warp(&outfull[oslot], (st / NOUT) & 1, lane)) {
-        if (lane == 0) {  // two 2D boxes; rows past the shard and columns past Kp are not written
-          const int32_t row = (int32_t)(st_c * kChunkTiles), x0 = (int32_t)(st_q * kStreamSW);
-          for (int h = 0; h < 2; ++h)
+        for (uint32_t s = s0; s < s0 + nsl; ++s) {
+          const uint32_t oslot = s % NOUT, q = s % nsl;
+          mbar_wait(&outfull[oslot], (s / NOUT) & 1);
+          const int32_t row = (int32_t)((blockIdx.x + (uint64_t)(s / nsl) * G) * kChunkTiles);
+          for (int h = 0; h < 2; ++h)  // rows past the shard and columns past Kp are not written
             asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&tm_out),
-                         "r"(x0 + h * (int32_t)kStreamBox), "r"(row),
+                         "r"((int32_t)(q * kStreamSW) + h * (int32_t)kStreamBox), "r"(row),
                          "r"(out_base + oslot * slot_bytes + h * (kStreamSlot / 2))
                          : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          bulk_wait_read<NOUT - 1>();  // slice st + 1 - NOUT has been read out: its slot may be refilled
-          if (st + 1 >= NOUT) mbar_arrive(&outempty[(st + 1) % NOUT]);
+          bulk_wait_read<NOUT - 1>();  // slice s + 1 - NOUT has been read out: its slot may be refilled
+          if (s + 1 >= NOUT) mbar_arrive(&outempty[(s + 1) % NOUT]);
         }
-        __syncwarp();
-        ++st;
-        if (++st_q == nsl) {
-          st_q = 0;
-          st_c += G;
-        }
-        did = true;
       }
-      if (!did) __nanosleep(20);
+      bulk_wait_all();
     }
-    bulk_wait_all();
     return;
   }
 
@@ -269,16 +254,26 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
     cp_async_wait_all();  // this chunk's link gathers and the next chunk's adjacency (own copies)
     consumers_sync();     // Z, R and both adjacency buffers visible to every consumer warp
 
-    // Phase B: link words, links spread over the warps
-    for (uint32_t e = (uint32_t)cw; e < E; e += kStreamNW) {
+    // Phase B: link words, links spread over the warps (contiguous ranges)
+    {
+    const uint32_t e1 = E * (uint32_t)(cw + 1) / kStreamNW;  // this warp's contiguous link range
+    uint32_t dprev = ~0u, rel = 0;
+    bool inside = false, present = false;
+    for (uint32_t e = E * (uint32_t)cw / kStreamNW; e < e1; ++e) {
       const uint32_t le = S.lj2[e], j2 = le & 0xFFFFu, d = le >> 16;
-      const int64_t tn = (int64_t)ntl[d * kChunkTiles + lane] - 1;
-      const uint64_t rel = (uint64_t)(tn - (int64_t)c.t0);
+      if (d != dprev) {  // the neighbour tile of this lane's tile in direction d
+        dprev = d;
+        const int64_t tn = (int64_t)ntl[d * kChunkTiles + lane] - 1;
+        present = tn >= 0;
+        rel = (uint32_t)(tn - (int64_t)c.t0);
+        inside = present && (uint64_t)(tn - (int64_t)c.t0) < c.nt;
+      }
       uint32_t v = 0;
-      if (tn >= 0 && rel < c.nt) v = (lds32(z_s + 4 * j2) >> (uint32_t)rel) & 1u;
-      else if (tn >= 0) v = (S.R[e * kChunkTiles + lane] >> (8 * (j2 & 3u))) & 0xFFu;
+      if (inside) v = (lds32(z_s + 4 * j2) >> rel) & 1u;
+      else if (present) v = (S.R[e * kChunkTiles + lane] >> (8 * (j2 & 3u))) & 0xFFu;
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
       if (lane == 0) S.Z[K + e] = bal;
+    }
     }
     consumers_sync();  // link words published; R and this chunk's adjacency buffer are free
     if (chunk + 2 * G < p.nchunks) adj_prefetch(p, ntl, chunk_info(p, chunk + 2 * G), cw, lane);
