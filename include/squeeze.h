@@ -192,6 +192,15 @@ squeeze_status squeeze_run(void* ctx, uint8_t* d_a, uint8_t* d_b, uint64_t steps
  * library cannot see the host buffer's length: the caller guarantees state_bytes. */
 squeeze_status squeeze_run_host(void* ctx, uint8_t* h_state, uint8_t* d_a, uint8_t* d_b, uint64_t steps,
                                 squeeze_stream_t stream);
+/* End to end from host memory with the state crossing PCIe at 1 BIT per cell: h_packed holds the
+ * state in the packed layout (packed_bytes, see the packed section below; squeeze_pack/_unpack
+ * convert on the device), d_packed is a caller-owned device buffer of packed_bytes.  H2D of
+ * h_packed, unpack into d_a, `steps` byte-state steps (the CUDA-graph ping-pong of squeeze_run),
+ * pack of the final state, D2H into h_packed, synchronise.  The state is binary, so this moves 8x
+ * fewer bytes over PCIe than squeeze_run_host for the same result.  Unsharded contexts only
+ * (SQZ_E_CONFIG before any copy otherwise). */
+squeeze_status squeeze_run_host_bits(void* ctx, uint32_t* h_packed, uint8_t* d_a, uint8_t* d_b, uint32_t* d_packed,
+                                    uint64_t steps, squeeze_stream_t stream);
 /* *d_out (device uint64) = number of alive cells of this shard. */
 squeeze_status squeeze_count_alive(const void* ctx, const uint8_t* d_state, uint64_t* d_out,
                                    squeeze_stream_t stream);

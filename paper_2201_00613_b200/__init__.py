@@ -300,6 +300,18 @@ class Squeeze:
         _lib.check(self.lib.squeeze_run_host(self.ctx, _ptr(h_state), _ptr(a), _ptr(b), steps,
                                              _stream(stream, a.device)), "run_host")
 
+    def run_host_bits(self, h_packed, a, b, d_packed, steps: int, stream=None):
+        """End to end from host memory, the state crossing PCIe at 1 bit per cell: h_packed (CPU int32
+        tensor of packed_bytes / 4 words in the packed layout, ideally pinned) -> d_packed -> unpack into
+        a -> `steps` byte-state steps -> pack -> back into h_packed."""
+        import torch
+        self._host(h_packed, "run_host_bits h_packed", (torch.int32, torch.uint32), self.geometry.packed_bytes)
+        self._state(a, "run_host_bits a")
+        self._state(b, "run_host_bits b")
+        self._packed(d_packed, "run_host_bits d_packed")
+        _lib.check(self.lib.squeeze_run_host_bits(self.ctx, _ptr(h_packed), _ptr(a), _ptr(b), _ptr(d_packed), steps,
+                                                  _stream(stream, a.device)), "run_host_bits")
+
     def count_alive(self, state, out=None, stream=None):
         import torch
         self._state(state, "count_alive")

@@ -76,6 +76,7 @@ SIGNATURES = {
     "squeeze_step_naive": ([vp, vp, vp, vp], st),
     "squeeze_run": ([vp, vp, vp, ctypes.c_uint64, ctypes.c_int, vp], st),
     "squeeze_run_host": ([vp, vp, vp, vp, ctypes.c_uint64, vp], st),
+    "squeeze_run_host_bits": ([vp, vp, vp, vp, vp, ctypes.c_uint64, vp], st),
     "squeeze_count_alive": ([vp, vp, vp, vp], st),
     "squeeze_device_error": ([vp], st),
     "squeeze_halo_needs": ([vp, u64p, ctypes.c_uint64, u64p], st),

@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsqueeze.so")
-SOURCES = ["sqz_api.cu", "sqz_kernels.cu", "sqz_tile.cu", "sqz_stream.cu", "sqz_packed.cu", "sqz_engines.cu", "sqz_heat.cu", "sqz_mma.cu", "sqz_host.cpp"]
+SOURCES = ["sqz_api.cu", "sqz_kernels.cu", "sqz_tile.cu", "sqz_stream.cu", "sqz_packed.cu", "sqz_engines.cu", "sqz_bb.cu", "sqz_heat.cu", "sqz_mma.cu", "sqz_host.cpp"]
 HEADERS = ["sqz_common.h", "sqz_host.h", "sqz_kernels.cuh", "sqz_device.cuh", "sqz_bits.cuh", "sqz_heat.cuh"]
 
 NVCC_FLAGS = [

@@ -795,6 +795,27 @@ squeeze_status squeeze_run_host(void* ctx, uint8_t* h_state, uint8_t* d_a, uint8
   return cu(cudaStreamSynchronize(s));
 }
 
+squeeze_status squeeze_run_host_bits(void* ctx, uint32_t* h_packed, uint8_t* d_a, uint8_t* d_b, uint32_t* d_packed,
+                                    uint64_t steps, squeeze_stream_t stream) {
+  if (!ctx || !h_packed) return SQZ_E_CONFIG;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  squeeze_status st = check_state(c, d_a);
+  if (st == SQZ_OK) st = check_state(c, d_b);
+  if (st == SQZ_OK) st = check_state(c, d_packed);
+  if (st != SQZ_OK) return st;
+  if (c->nranks > 1 || d_a == d_b) return SQZ_E_CONFIG;  // before any transfer is enqueued
+  DevGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  // the state crosses PCIe at 1 bit per cell (the packed layout); the step runs on bytes
+  if (cudaMemcpyAsync(d_packed, h_packed, c->packed_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return SQZ_E_CUDA;
+  if ((st = cu(launch_unpack(tile_params(c), d_packed, d_a, s))) != SQZ_OK) return st;
+  if ((st = squeeze_run(ctx, d_a, d_b, steps, 1, stream)) != SQZ_OK) return st;
+  const uint8_t* fin = (steps & 1) ? d_b : d_a;
+  if ((st = cu(launch_pack(tile_params(c), fin, d_packed, s))) != SQZ_OK) return st;
+  if (cudaMemcpyAsync(h_packed, d_packed, c->packed_bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) return SQZ_E_CUDA;
+  return cu(cudaStreamSynchronize(s));
+}
+
 squeeze_status squeeze_run_host_packed(void* ctx, uint32_t* h_packed, uint32_t* d_a, uint32_t* d_b, uint64_t steps,
                                        squeeze_stream_t stream) {
   if (!ctx || !h_packed) return SQZ_E_CONFIG;

@@ -197,69 +197,8 @@ __global__ void k_bb_seed(LevelMaps gm, uint8_t* __restrict__ grid, uint64_t n, 
   }
 }
 
-__device__ __forceinline__ uint32_t alive_bytes(uint32_t v) { return v & ~(v >> 1) & 0x01010101u; }
 
-// 16 cells of one row per thread; n % 16 == 0.
-__global__ void k_bb_step16(const uint8_t* __restrict__ cur, uint8_t* __restrict__ next, uint64_t n, uint32_t birth,
-                            uint32_t survive) {
-  uint64_t per_row = n / 16;
-  uint64_t total = per_row * n;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t y = i / per_row, x0 = (i - y * per_row) * 16;
-    uint32_t A[3][6];  // rows y-1, y, y+1: [0] = left byte, [1..4] = words, [5] = right byte
-    uint32_t mid_raw[4];
-#pragma unroll
-    for (int rr = 0; rr < 3; ++rr) {
-      int64_t yy = (int64_t)y + rr - 1;
-      if (yy < 0 || yy >= (int64_t)n) {
-#pragma unroll
-        for (int q = 0; q < 6; ++q) A[rr][q] = 0;
-        if (rr == 1) mid_raw[0] = mid_raw[1] = mid_raw[2] = mid_raw[3] = 0;
-        continue;
-      }
-      const uint8_t* row = cur + (uint64_t)yy * n;
-      uint4 v = __ldg(reinterpret_cast<const uint4*>(row + x0));
-      if (rr == 1) {
-        mid_raw[0] = v.x; mid_raw[1] = v.y; mid_raw[2] = v.z; mid_raw[3] = v.w;
-      }
-      A[rr][1] = alive_bytes(v.x);
-      A[rr][2] = alive_bytes(v.y);
-      A[rr][3] = alive_bytes(v.z);
-      A[rr][4] = alive_bytes(v.w);
-      uint32_t l = x0 > 0 ? __ldg(row + x0 - 1) : 0u;
-      uint32_t r = x0 + 16 < n ? __ldg(row + x0 + 16) : 0u;
-      A[rr][0] = (l == 1u) ? 1u : 0u;
-      A[rr][5] = (r == 1u) ? 1u : 0u;
-    }
-    uint32_t out[4];
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      uint32_t cnt = 0;
-#pragma unroll
-      for (int rr = 0; rr < 3; ++rr) {
-        uint32_t c = A[rr][w + 1];
-        uint32_t prev_top = (w == 0) ? A[rr][0] : (A[rr][w] >> 24);
-        uint32_t next_low = (w == 3) ? A[rr][5] : (A[rr][w + 2] & 0xFFu);
-        uint32_t left = (c << 8) | prev_top;
-        uint32_t right = (c >> 8) | (next_low << 24);
-        cnt += left + right + (rr == 1 ? 0u : c);
-      }
-      uint32_t raw = mid_raw[w];
-      uint32_t o = 0;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        uint32_t v = (raw >> (8 * b)) & 0xFFu;
-        uint32_t c = (cnt >> (8 * b)) & 0xFFu;
-        uint32_t nb = (v == 2u) ? 2u : rule_byte(v, c, birth, survive);
-        o |= nb << (8 * b);
-      }
-      out[w] = o;
-    }
-    *reinterpret_cast<uint4*>(next + y * n + x0) = make_uint4(out[0], out[1], out[2], out[3]);
-  }
-}
-
-// generic per-cell BB step (n < 16 or n % 16 != 0)
+// generic per-cell BB step (n % 32 != 0, e.g. s = 3 fractals); powers of two take sqz_bb.cu
 __global__ void k_bb_step1(const uint8_t* __restrict__ cur, uint8_t* __restrict__ next, uint64_t n, uint32_t birth,
                            uint32_t survive) {
   uint64_t total = n * n;
@@ -411,11 +350,8 @@ cudaError_t launch_bb_seed(const LevelMaps& m, uint8_t* grid, uint64_t seed, uin
 
 cudaError_t launch_bb_step(const uint8_t* cur, uint8_t* next, uint64_t n, uint32_t birth, uint32_t survive,
                            cudaStream_t st) {
-  if (n % 16 == 0) {
-    k_bb_step16<<<grid_for(n * n / 16, 256), 256, 0, st>>>(cur, next, n, birth, survive);
-  } else {
-    k_bb_step1<<<grid_for(n * n, 256), 256, 0, st>>>(cur, next, n, birth, survive);
-  }
+  if (bb_bits_ok(n)) return launch_bb_step_bits(cur, next, n, birth, survive, st);
+  k_bb_step1<<<grid_for(n * n, 256), 256, 0, st>>>(cur, next, n, birth, survive);
   return cudaGetLastError();
 }
 

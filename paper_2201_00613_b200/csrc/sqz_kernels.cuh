@@ -123,6 +123,10 @@ cudaError_t launch_halo_pack(const uint8_t* cur, const uint64_t* send_offsets, u
 cudaError_t launch_bb_seed(const LevelMaps& m, uint8_t* grid, uint64_t seed, uint64_t q, cudaStream_t st);
 cudaError_t launch_bb_step(const uint8_t* cur, uint8_t* next, uint64_t n, uint32_t birth, uint32_t survive,
                            cudaStream_t st);
+// bit-sliced BB step (sqz_bb.cu) for n % 32 == 0
+bool bb_bits_ok(uint64_t n);
+cudaError_t launch_bb_step_bits(const uint8_t* cur, uint8_t* next, uint64_t n, uint32_t birth, uint32_t survive,
+                                cudaStream_t st);
 cudaError_t launch_bb_to_compact(const LevelMaps& m, const PadLayout& L, const uint8_t* grid, uint8_t* state,
                                  cudaStream_t st);
 

@@ -254,7 +254,8 @@ def test_tile_equals_naive_multistep_r16():
 
 # ------------------------------------------------------------------ BB baseline
 @pytest.mark.parametrize("name,r", [("sierpinski-triangle", 6), ("sierpinski-triangle", 9), ("sierpinski-carpet", 3),
-                                    ("empty-bottles", 3), ("full-square", 2)])
+                                    ("empty-bottles", 3), ("full-square", 2), ("sierpinski-triangle", 5),
+                                    ("sierpinski-triangle", 11), ("full-square", 7)])
 def test_bb_engine_vs_oracle(name, r):
     """The expanded bounding-box engine equals the oracle's O5 definition on the embedding."""
     o = BUILTINS[name]
@@ -275,6 +276,26 @@ def test_bb_engine_vs_oracle(name, r):
         assert np.array_equal(np.where(mask, grid, 0), st) and (grid[~mask] == 2).all()
         p.bb_to_compact(g1, comp)
         assert np.array_equal(host(p, comp), A.transport(o, r, st))
+        g0, g1 = g1, g0
+
+
+@pytest.mark.parametrize("rule", [(1 << 2, 0), ((1 << 3) | (1 << 6), (1 << 2) | (1 << 3)), (0b110110110, 0b001001001)])
+def test_bb_bitsliced_rules_vs_oracle(rule):
+    """The bit-sliced BB kernel (n % 32 == 0: row strips, band walk, carry-save count) with other
+    rules, at a size with several 1024-cell segments and 64-row bands (r=11, n=2048)."""
+    o = BUILTINS["sierpinski-triangle"]
+    r = 11
+    p = mk("sierpinski-triangle", r, rule=rule)
+    st, mask = A.seed_expanded(o, r, 7, 0.5)
+    g0, g1 = p.new_bb(), p.new_bb()
+    p.bb_seed(g0, 7, 0.5)
+    n = 2 ** r
+    for t in range(3):
+        p.bb_step(g0, g1)
+        st = A.expanded_step(st, mask, rule)
+        torch.cuda.synchronize()
+        grid = g1[:n * n].cpu().numpy().reshape(n, n)
+        assert np.array_equal(np.where(mask, grid, 0), st) and (grid[~mask] == 2).all(), t
         g0, g1 = g1, g0
 
 
