@@ -435,30 +435,51 @@ def main():
                                  "ms_per_step_stderr": (statistics.stdev(reps) / len(reps) ** 0.5) if len(reps) > 1
                                  else None, "ms_per_step": reps}
         del bufs
-        # --- end to end through the public API from (pinned) host memory
+        # --- end to end through the public API from (pinned) host memory.  Headline: the state
+        # crosses PCIe at 1 bit per cell (squeeze_run_host_bits: H2D of the packed state, device
+        # unpack, K byte steps, device pack, D2H); beside it the byte-for-byte transfer.
         if not args.no_e2e:
-            try:
-                h = torch.empty(g.state_bytes, dtype=torch.uint8, pin_memory=True)
-                pinned = True
-            except RuntimeError:
-                h = torch.empty(g.state_bytes, dtype=torch.uint8)
-                pinned = False
+            def pinned_empty(n, dtype):
+                try:
+                    return torch.empty(n, dtype=dtype, pin_memory=True), True
+                except RuntimeError:
+                    return torch.empty(n, dtype=dtype), False
+
             init = sq.new_state()
             sq.seed(init, args.seed, args.density)
-            h.copy_(init)
-            del init
+            dp = sq.new_packed()
+            sq.pack(init, dp)
+            hb, pinned = pinned_empty(g.packed_bytes // 4, torch.int32)
+            hb.copy_(dp[:g.packed_bytes // 4])
             torch.cuda.synchronize()
-            ea, eb = a, b
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            sq.run_host(h, ea, eb, K)
+            sq.run_host_bits(hb, a, b, dp, K)
             e1.record(stream)
             torch.cuda.synchronize()
             e_ms = e0.elapsed_time(e1)
             extras["e2e"] = {"value": cells_per_s(g.cells_total, K, e_ms), "unit": "cells/s",
-                             "h2d_bytes_per_step": g.state_bytes / K, "d2h_bytes_per_step": g.state_bytes / K,
-                             "mode": f"squeeze_run_host: H2D of the state, {K} steps, D2H of the state, "
-                                     f"{'pinned' if pinned else 'pageable'} host buffer", "ms": e_ms}
+                             "h2d_bytes_per_step": g.packed_bytes / K, "d2h_bytes_per_step": g.packed_bytes / K,
+                             "mode": f"squeeze_run_host_bits: H2D of the state at 1 bit per cell (packed layout, "
+                                     f"{g.packed_bytes / 1e9:.2f} GB), device unpack, {K} byte-state steps, device "
+                                     f"pack, D2H; {'pinned' if pinned else 'pageable'} host buffer", "ms": e_ms,
+                             "value_over_device_value": cells_per_s(g.cells_total, K, e_ms) / value}
+            del hb, dp
+            h, pinned = pinned_empty(g.state_bytes, torch.uint8)
+            h.copy_(init)
+            del init
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sq.run_host(h, a, b, K)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            eb_ms = e0.elapsed_time(e1)
+            extras["e2e"]["byte_transfer"] = {
+                "value": cells_per_s(g.cells_total, K, eb_ms), "unit": "cells/s", "ms": eb_ms,
+                "h2d_bytes_per_step": g.state_bytes / K, "d2h_bytes_per_step": g.state_bytes / K,
+                "mode": f"squeeze_run_host: H2D of the byte state ({g.state_bytes / 1e9:.1f} GB), {K} steps, D2H; "
+                        "PCIe-bound"}
             launches_e2e = K
             del h
         # --- literal per-cell engine (the paper's per-thread formulation) at the same level
@@ -602,42 +623,62 @@ def main():
         torch.cuda.empty_cache()
         # --- BASELINE configs[3]: other NBB fractals through the generic H-table
         fr_rows = {}
+
+        def time_steps(fn, fa, fb):
+            for i in range(3):
+                fn(fa if i % 2 == 0 else fb, fb if i % 2 == 0 else fa)
+            torch.cuda.synchronize()
+            reps_ms = []  # 100 steps x 5 repetitions
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for i in range(100):
+                    fn(fa if i % 2 == 0 else fb, fb if i % 2 == 0 else fa)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                reps_ms.append(e0.elapsed_time(e1) / 100)
+            return statistics.fmean(reps_ms), statistics.stdev(reps_ms) / 5 ** 0.5
+
         for fname, lvl in (("sierpinski-carpet", 10), ("empty-bottles", 11)):
             pf = pkg.Squeeze(pkg.builtin_fractal(fname), lvl, device=local)
             gf = pf.geometry
-            row = {"level": lvl, "cells": gf.cells_total, "tile_level": gf.tile_level, "remote_links": gf.remote_links}
-            for mode in ("bytes", "packed"):
-                if mode == "bytes":
-                    fa, fb = pf.new_state(), pf.new_state()
-                    pf.seed(fa, args.seed, args.density)
-                    fn, nbytes = pf.step, 2 * gf.cells_total
-                else:
-                    fa, fb = pf.new_packed(), pf.new_packed()
-                    pf.seed_packed(fa, args.seed, args.density)
-                    fn, nbytes = pf.step_packed, 2 * gf.packed_bytes
-                for i in range(3):
-                    fn(fa if i % 2 == 0 else fb, fb if i % 2 == 0 else fa)
-                torch.cuda.synchronize()
-                reps_ms = []  # 100 steps x 5 repetitions
-                for _ in range(5):
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    e0.record(stream)
-                    for i in range(100):
-                        fn(fa if i % 2 == 0 else fb, fb if i % 2 == 0 else fa)
-                    e1.record(stream)
-                    torch.cuda.synchronize()
-                    reps_ms.append(e0.elapsed_time(e1) / 100)
-                fms = statistics.fmean(reps_ms)
-                row[mode] = {"ms_per_step": fms, "ms_per_step_stderr": statistics.stdev(reps_ms) / 5 ** 0.5,
-                             "cells_per_s": cells_per_s(gf.cells_total, 1, fms),
-                             "hbm_frac": nbytes / (fms / 1e3) / 1e9 / peak, "steps": 100, "repetitions": 5}
+            row = {"level": lvl, "cells": gf.cells_total}
+            fa, fb = pf.new_state(), pf.new_state()
+            pf.seed(fa, args.seed, args.density)
+            fms, ferr = time_steps(pf.step, fa, fb)
+            row["bytes"] = {"ms_per_step": fms, "ms_per_step_stderr": ferr, "cells_per_s": cells_per_s(gf.cells_total, 1, fms),
+                            "hbm_frac": 2 * gf.cells_total / (fms / 1e3) / 1e9 / peak, "steps": 100, "repetitions": 5,
+                            "tile_level": gf.tile_level, "tile_cells": gf.tile_cells, "remote_links": gf.remote_links,
+                            "kernel": "sqz::k_step_stream" if gf.byte_kernel else "sqz::k_step_tile"}
+            del fa, fb
+            # the packed step at the auto level and the level below; the faster one is the row
+            packed = {}
+            for g in (gf.tile_level, gf.tile_level - 1):
+                pg = pf if g == gf.tile_level else pkg.Squeeze(pkg.builtin_fractal(fname), lvl, device=local, tile_level=g)
+                gg = pg.geometry
+                if not gg.packed_ok:
+                    continue
+                fa, fb = pg.new_packed(), pg.new_packed()
+                pg.seed_packed(fa, args.seed, args.density)
+                pms, perr = time_steps(pg.step_packed, fa, fb)
+                packed[g] = {"ms_per_step": pms, "ms_per_step_stderr": perr,
+                             "cells_per_s": cells_per_s(gg.cells_total, 1, pms),
+                             "hbm_frac": 2 * gg.packed_bytes / (pms / 1e3) / 1e9 / peak, "steps": 100, "repetitions": 5,
+                             "tile_level": g, "remote_links": gg.remote_links}
                 del fa, fb
+                if pg is not pf:
+                    pg.close()
+            best = min(packed, key=lambda k: packed[k]["ms_per_step"])
+            row["packed"] = dict(packed[best], levels_timed={str(k): v["ms_per_step"] for k, v in packed.items()})
             pf.close()
+            torch.cuda.empty_cache()
             fr_rows[fname] = row
         extras["fractal_configs"] = {"note": "BASELINE configs[3]: carpet (D11 row-major minus centre) and empty "
                                              "bottles (D11 assumed silhouette), 100 steps x 5 repetitions each (SURVEY §8d C4), "
                                              "B3/S23; hbm_frac on the algorithmic bytes (2 B/cell bytes, "
-                                             "2 x packed_bytes packed)",
+                                             "2 x packed_bytes packed); bytes at the library's tile level "
+                                             "(level 4: the streaming large-tile step), packed at the faster of "
+                                             "that level and the one below",
                                      "rows": fr_rows}
         torch.cuda.empty_cache()
         # --- NEXT-3 ablation: batched ν map, LUT kernel vs integer tensor-core product

@@ -185,6 +185,25 @@ def test_run_graph_and_host():
     assert np.array_equal(p.to_cells(h).numpy(), want[5])
 
 
+@pytest.mark.parametrize("name,r,steps", [("sierpinski-triangle", 10, 7), ("sierpinski-triangle", 12, 6),
+                                          ("sierpinski-carpet", 5, 5), ("empty-bottles", 6, 4)])
+def test_run_host_bits(name, r, steps):
+    """End to end with the state crossing PCIe at 1 bit per cell (packed layout): the host buffer
+    after the run decodes to the oracle's state (packed layout decoded on the host)."""
+    want = oracle_run(name, r, 11, 0.5, steps)
+    p = mk(name, r)
+    g = p.geometry
+    a, b, dp = p.new_state(), p.new_state(), p.new_packed()
+    p.seed(a, 11, 0.5)
+    p.pack(a, dp)
+    h = dp[:g.packed_bytes // 4].cpu().pin_memory()
+    a.fill_(3)
+    p.run_host_bits(h, a, b, dp, steps)
+    dev = p.new_packed()
+    dev[:g.packed_bytes // 4] = h.cuda()
+    assert np.array_equal(p.packed_to_cells(dev), want[steps])
+
+
 def test_count_alive():
     for r in (0, 3, 8, 11):
         p = mk("sierpinski-triangle", r)
