@@ -653,18 +653,19 @@ def main():
             del fa, fb
             # the packed step at the auto level and the level below; the faster one is the row
             packed = {}
-            for g in (gf.tile_level, gf.tile_level - 1):
-                pg = pf if g == gf.tile_level else pkg.Squeeze(pkg.builtin_fractal(fname), lvl, device=local, tile_level=g)
+            for tl in (gf.tile_level, gf.tile_level - 1):
+                pg = pf if tl == gf.tile_level else pkg.Squeeze(pkg.builtin_fractal(fname), lvl, device=local,
+                                                                tile_level=tl)
                 gg = pg.geometry
                 if not gg.packed_ok:
                     continue
                 fa, fb = pg.new_packed(), pg.new_packed()
                 pg.seed_packed(fa, args.seed, args.density)
                 pms, perr = time_steps(pg.step_packed, fa, fb)
-                packed[g] = {"ms_per_step": pms, "ms_per_step_stderr": perr,
+                packed[tl] = {"ms_per_step": pms, "ms_per_step_stderr": perr,
                              "cells_per_s": cells_per_s(gg.cells_total, 1, pms),
                              "hbm_frac": 2 * gg.packed_bytes / (pms / 1e3) / 1e9 / peak, "steps": 100, "repetitions": 5,
-                             "tile_level": g, "remote_links": gg.remote_links}
+                             "tile_level": tl, "remote_links": gg.remote_links}
                 del fa, fb
                 if pg is not pf:
                     pg.close()
