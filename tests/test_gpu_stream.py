@@ -148,3 +148,68 @@ def test_stream_config3_sampled(name, r):
     want = A.compact_step_sampled(f, r, om, lambda q: fetch(b, q))
     assert np.array_equal(fetch(a, om), want)
     assert p.device_error() == 0
+
+
+def run_peer_in_process(name, r, nranks, steps, g=0):
+    """The fused peer-memory halo (PEER kernel variants) with every shard in THIS process: each
+    step kernel stores its send cells straight into the other shards' receive buffers (plain device
+    pointers here, CUDA IPC mappings across processes), receive buffers alternate by step parity."""
+    f = sq.builtin_fractal(name)
+    parts = [sq.Squeeze(f, r, rank=i, nranks=nranks, device=0, tile_level=g) for i in range(nranks)]
+    ranges = [p.shard_range(i) for i, p in enumerate(parts)]
+    needs = [p.halo_needs().astype(np.int64) for p in parts]
+    recv = [[sq.ipc_alloc(max(1, nd.size), 0) for _ in range(2)] for nd in needs]
+    send_bufs = []  # (bound, unused by the peer transport)
+    for i, p in enumerate(parts):  # sends of shard i: what the others need from its range, by destination
+        lo, hi = ranges[i]
+        sends, peer, pos = [], [], []
+        for d, nd in enumerate(needs):
+            if d == i:
+                continue
+            sel = np.nonzero((nd >= lo) & (nd < hi))[0]
+            sends.append(nd[sel])
+            peer.append(np.full(sel.size, d, np.uint32))
+            pos.append(sel.astype(np.uint64))
+        p.halo_set_sends(np.concatenate(sends).astype(np.uint64))
+        send_bufs.append(torch.zeros(max(1, sum(x.size for x in sends)), dtype=torch.uint8, device="cuda"))
+        p.halo_peer_plan(np.concatenate(peer), np.concatenate(pos))
+        for par in range(2):
+            p.halo_peer_bind(par, [0 if d == i else recv[d][par] for d in range(nranks)])
+    bufs = []
+    for p in parts:
+        a, b = p.new_state(), p.new_state()
+        p.seed(a, 42, 0.5)
+        bufs.append([a, b])
+    for p, bf in zip(parts, bufs):
+        p.halo_peer_push(bf[0], 0)
+    torch.cuda.synchronize()
+    for t in range(steps):
+        par = t % 2
+        for i, (p, bf) in enumerate(zip(parts, bufs)):
+            p.halo_bind(send_bufs[i], recv[i][par])  # reads parity par ...
+            p.halo_peer_select(1 - par)       # ... and its kernel writes the next halo into 1 - par
+            p.step(bf[0], bf[1])
+            p.halo_peer_select(-1)
+        torch.cuda.synchronize()  # (across processes: the ordering barrier between steps)
+        for bf in bufs:
+            bf.reverse()
+    for p in parts:
+        assert p.device_error() == 0
+    out = np.concatenate([host(pp, bf[0]) for pp, bf in zip(parts, bufs)])
+    kinds = {p.geometry.byte_kernel for p in parts}
+    for p in parts:
+        p.close()
+    for rr in recv:
+        for ptr in rr:
+            sq.ipc_free(ptr)
+    return out, kinds
+
+
+@pytest.mark.parametrize("name,r,nranks,g,kind", [("sierpinski-carpet", 6, 3, 4, 1), ("empty-bottles", 7, 2, 4, 1),
+                                                  ("sierpinski-triangle", 12, 4, 7, 1),
+                                                  ("sierpinski-triangle", 12, 3, 5, 0)])
+def test_peer_halo_in_process_vs_oracle(name, r, nranks, g, kind):
+    got, kinds = run_peer_in_process(name, r, nranks, 5, g)
+    assert kinds == {kind}
+    want = A.compact_run(BUILTINS[name], r, A.seed_compact(BUILTINS[name], r, 42, 0.5), 5)
+    assert np.array_equal(got, want)

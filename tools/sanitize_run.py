@@ -1,6 +1,8 @@
 """Small multi-chunk runs of every step kernel, for compute-sanitizer (memcheck/racecheck/synccheck):
-byte tile step (+ literal step), packed step at small and level-7 tiles, packed/byte conversions,
-heat step, sharded packed step with a halo, tensor-core ν map."""
+byte tile step (+ literal step), the streaming large-tile byte step, packed step at small and
+level-7 tiles, packed/byte conversions, heat step, BB steps (bit-sliced and per-cell), the 1-bit
+end-to-end run, sharded steps with a halo, the fused peer-memory halo (PEER variants of both byte
+kernels + squeeze_halo_peer_push), tensor-core ν map."""
 import os
 import sys
 
@@ -10,9 +12,11 @@ import torch  # noqa: E402
 
 import paper_2201_00613_b200 as pkg  # noqa: E402
 
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 for name, r, g in [("sierpinski-triangle", 11, 3), ("sierpinski-triangle", 12, 7), ("sierpinski-carpet", 5, 2),
-                   ("empty-bottles", 6, 2)]:
+                   ("empty-bottles", 6, 2), ("sierpinski-carpet", 6, 4), ("empty-bottles", 7, 4)]:
     p = pkg.Squeeze(pkg.builtin_fractal(name), r, device=0, tile_level=g, ctas_per_sm=1)
+    print(name, r, "g", p.geometry.tile_level, "byte kernel", p.geometry.byte_kernel, flush=True)
     a, b = p.new_state(), p.new_state()
     p.seed(a, 42, 0.5)
     p.run(a, b, 3)
@@ -22,9 +26,14 @@ for name, r, g in [("sierpinski-triangle", 11, 3), ("sierpinski-triangle", 12, 7
     p.run_packed(pa, pb, 3)
     p.unpack(pb, a)
     p.count_alive(a)
-    ha, hb = p.new_heat(), p.new_heat()
-    p.heat_seed(ha, 3)
-    p.heat_run(ha, hb, 3)
+    if p.geometry.heat_ok:
+        ha, hb = p.new_heat(), p.new_heat()
+        p.heat_seed(ha, 3)
+        p.heat_run(ha, hb, 3)
+    dp = p.new_packed()
+    p.pack(a, dp)
+    h = dp[:p.geometry.packed_bytes // 4].cpu().pin_memory()
+    p.run_host_bits(h, a, b, dp, 3)
     x, y = p.map_lambda(torch.arange(min(4096, p.geometry.cells_total), device="cuda"))
     p.map_nu_mma(x, y)
     torch.cuda.synchronize()
@@ -46,3 +55,20 @@ for p in parts:
     p.step(s, st)
 torch.cuda.synchronize()
 print("ok sharded", flush=True)
+
+# BB engine: bit-sliced (n % 32 == 0) and per-cell (s = 3)
+for name, r in [("sierpinski-triangle", 7), ("sierpinski-triangle", 11), ("sierpinski-carpet", 3)]:
+    p = pkg.Squeeze(pkg.builtin_fractal(name), r, device=0)
+    g0, g1 = p.new_bb(), p.new_bb()
+    p.bb_seed(g0, 42, 0.5)
+    p.bb_step(g0, g1)
+    p.bb_step(g1, g0)
+torch.cuda.synchronize()
+print("ok bb", flush=True)
+
+# fused peer-memory halo, every shard in this process (PEER variants + squeeze_halo_peer_push)
+from test_gpu_stream import run_peer_in_process  # noqa: E402
+
+for name, r, nr, g in [("sierpinski-triangle", 10, 2, 4), ("sierpinski-carpet", 6, 2, 4)]:
+    _, kinds = run_peer_in_process(name, r, nr, 3, g)
+    print("ok peer", name, r, "byte kernels", kinds, flush=True)
