@@ -523,7 +523,6 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
         c->packed_grid = sms * std::max(1, pocc);
       else
         c->packed_grid = 0;
-      cudaGetLastError();  // (clears a refused shared-memory attribute)
       // ν tensor-core ablation: H_ν as int16 and the per-level weight bytes of k^(μ-1)
       if (c->f.s * c->f.s <= kMmaMaxS2 && c->f.k <= 256 && r <= 32) {
         std::vector<int16_t> hh(c->f.hnu.begin(), c->f.hnu.end());
@@ -571,8 +570,10 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
         }  // (at least 2 stages: a unit's successor is filled while the unit is computed)
         h.stages = c->heat_stages;
         int hocc = 0;
-        c->heat_grid = heat_prepare(h, q, &hocc) == cudaSuccess ? sms * std::max(1, hocc) : 0;
-        cudaGetLastError();
+        // a heat unit that does not fit shared memory leaves the heat step unavailable at this tile
+        // level (its calls return SQZ_E_INVALID_LEVEL); no attribute call is made for it
+        c->heat_grid = heat_smem_bytes(h, q) <= 227 * 1024 && heat_prepare(h, q, &hocc) == cudaSuccess
+                           ? sms * std::max(1, hocc) : 0;
       }
       // tile adjacency: the coarse λ and one coarse ν per link direction of every local tile,
       // evaluated once here instead of every step

@@ -130,6 +130,7 @@ __device__ __forceinline__ void link_prefetch(const TileParams& p, const StreamS
 
 template <int DMAX, bool CONWAY, int RB, int MINB, int NOUT, bool PEER>
 __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, const uint8_t* __restrict__ cur,
+                                                              uint8_t* __restrict__ next,
                                                               const __grid_constant__ CUtensorMap tm_in,
                                                               const __grid_constant__ CUtensorMap tm_out) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -331,7 +332,8 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
         const uint32_t m = 0x01010101u;
         sts128(o + box_off(cw * 32), xb & m, (xb >> 1) & m, (xb >> 2) & m, (xb >> 3) & m);
         sts128(o + box_off(cw * 32 + 16), (xb >> 4) & m, (xb >> 5) & m, (xb >> 6) & m, (xb >> 7) & m);
-        if (jb + 1 == nblk && Kp > KP32) sts128(o + box_off(cw * 32 + 32), 0u, 0u, 0u, 0u);  // 16 zero padding bytes
+        if (jb + 1 == nblk && Kp > KP32 && (uint32_t)lane < c.nt)  // the tile's 16 zero padding bytes (the
+          *reinterpret_cast<uint4*>(next + (c.t0 - p.tile_lo + lane) * Kp + KP32) = make_uint4(0u, 0u, 0u, 0u);  // maps stop at KP32
       }
       fence_proxy_async();
       __syncwarp();
@@ -358,7 +360,7 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
   if (PEER && peer_sent) __threadfence_system();
 }
 
-using StreamFn = void (*)(TileParams, const uint8_t*, const CUtensorMap, const CUtensorMap);
+using StreamFn = void (*)(TileParams, const uint8_t*, uint8_t*, const CUtensorMap, const CUtensorMap);
 
 template <bool PEER, int RB, int MINB>
 static StreamFn pick_stream_r(const TileParams& p) {
@@ -416,8 +418,10 @@ cudaError_t stream_prepare(const TileParams& p, size_t smem, int minb, int* occu
   return blocks > 0 ? cudaSuccess : cudaErrorInvalidConfiguration;
 }
 
-// 2D tensor map of a tile-padded state buffer: dim 0 = the Kp bytes of a tile, dim 1 = the shard's
-// tiles (row pitch Kp, a multiple of 16); boxes of [32 tiles x 240 B]; out-of-range reads are zero.
+// 2D tensor map of a tile-padded state buffer: dim 0 = the first round_up(K, 32) bytes of a tile (the
+// last 16 padding bytes, if Kp has them, are written by the consumer that owns the tile's last
+// block), dim 1 = the shard's tiles (row pitch Kp, a multiple of 16); boxes of [32 tiles x 240 B];
+// out-of-range reads are zero, out-of-range box parts are not stored.
 static cudaError_t state_tensor_map(CUtensorMap* tm, const TileParams& p, const void* base) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
@@ -428,7 +432,7 @@ static cudaError_t state_tensor_map(CUtensorMap* tm, const TileParams& p, const 
       return cudaErrorNotSupported;
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  const cuuint64_t dims[2] = {p.Kp, p.tile_hi - p.tile_lo};
+  const cuuint64_t dims[2] = {(p.K + 31) & ~31ull, p.tile_hi - p.tile_lo};  // cells + zero bytes to 32
   const cuuint64_t strides[1] = {p.Kp};
   const cuuint32_t box[2] = {kStreamBox, kChunkTiles};
   const cuuint32_t estr[2] = {1, 1};
@@ -446,7 +450,7 @@ cudaError_t launch_step_stream(const TileParams& p, const uint8_t* cur, uint8_t*
   if (e == cudaSuccess) e = state_tensor_map(&tout, p, next);
   if (e != cudaSuccess) return e;
   StreamFn fn = p.peer_recv ? pick_stream_t<true>(p, minb) : pick_stream_t<false>(p, minb);
-  fn<<<grid, kStreamThreads, smem, st>>>(p, cur, tin, tout);
+  fn<<<grid, kStreamThreads, smem, st>>>(p, cur, next, tin, tout);
   return cudaGetLastError();
 }
 
