@@ -261,9 +261,12 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_tile(TileParams p, const ui
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.bar[2 + buf]);
+    if (PEER) {  // the chunk's output complete for the halo epilogue: a named barrier the last warp waits on
+      if (warp == lw) asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
+      else asm volatile("bar.arrive 1, %0;" ::"r"(blockDim.x) : "memory");
+    }
     if (PEER && warp == lw && pe1 > pe0) {
       // fused halo: the last warp stores this chunk's send cells straight into the peers' buffers
-      mbar_wait(&S.bar[2 + buf], (it >> 1) & 1);
       for (uint32_t e = pe0 + (uint32_t)lane; e < pe1; e += 32) {
         const uint32_t cell = p.peer_cell[e];
         p.peer_recv[p.peer_of[e]][p.peer_pos[e]] = inb[(cell >> 16) * St + (cell & 0xFFFFu)];
