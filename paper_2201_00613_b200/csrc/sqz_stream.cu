@@ -101,29 +101,39 @@ __device__ __forceinline__ void adj_prefetch(const TileParams& p, uint32_t* ntl,
   cp_async_commit();
 }
 
-// For every link e (spread over the consumer warps) whose neighbour tile lies outside chunk c: the
-// word holding the neighbour byte, by a 4-byte cp.async (or from the halo for another shard's tile).
+// 4-byte cp.async issued only where `pred` is set (a predicated instruction, no branch)
+__device__ __forceinline__ void cp_async4_if(uint32_t dst, const void* src, uint32_t pred) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p cp.async.ca.shared.global [%0], [%1], 4;\n\t}" ::"r"(dst),
+      "l"(src), "r"(pred)
+      : "memory");
+}
+
+// For every link e of warp cw's contiguous range [E cw / NW, E (cw+1) / NW) (links are sorted by
+// direction: the neighbour tile is looked up once per direction) whose neighbour tile lies outside
+// chunk c: the word holding the neighbour byte, by a predicated 4-byte cp.async (or, for another
+// shard's tile, from the halo).  Tile indices fit 32 bits (checked on the host).
 __device__ __forceinline__ void link_prefetch(const TileParams& p, const StreamSmem& S, const uint32_t* ntl,
                                               const ChunkInfo& c, const uint8_t* __restrict__ cur, int cw, int lane) {
-  // warp cw: the contiguous link range [E cw / NW, E (cw+1) / NW) (links are sorted by direction, so
-  // the neighbour tile is looked up once per direction)
   const uint32_t e1 = p.E * (uint32_t)(cw + 1) / kStreamNW;
-  uint32_t dprev = ~0u;
-  int64_t tn = -1;
-  bool out = false;
+  const uint32_t t0 = (uint32_t)c.t0, tlo = (uint32_t)p.tile_lo, nloc = (uint32_t)(p.tile_hi - p.tile_lo);
+  const uint32_t r_s = smem_u32(S.R) + 4u * (uint32_t)lane;
+  uint32_t dprev = ~0u, out = 0, a1 = 0;
+  const uint8_t* rowp = cur;
+  bool far = false;  // outside this shard: the halo
   for (uint32_t e = p.E * (uint32_t)cw / kStreamNW; e < e1; ++e) {
     const uint32_t le = S.lj2[e], j2 = le & 0xFFFFu, d = le >> 16;
     if (d != dprev) {
       dprev = d;
-      tn = (int64_t)ntl[d * kChunkTiles + lane] - 1;
-      out = tn >= 0 && ((uint64_t)tn < c.t0 || (uint64_t)tn >= c.t0 + c.nt);
+      a1 = ntl[d * kChunkTiles + lane];  // neighbour tile + 1 (0 = none)
+      const uint32_t tl = a1 - 1u - tlo;
+      out = (a1 != 0u && a1 - 1u - t0 >= c.nt) ? 1u : 0u;
+      far = out && tl >= nloc;
+      rowp = cur + (uint64_t)(far ? 0u : tl) * p.Kp;
     }
-    if (!out) continue;
-    uint32_t* dst = &S.R[e * kChunkTiles + lane];
-    if ((uint64_t)tn >= p.tile_lo && (uint64_t)tn < p.tile_hi)
-      cp_async4(dst, cur + ((((uint64_t)tn - p.tile_lo) * p.Kp + j2) & ~3ull));
-    else
-      *dst = fetch_cell(cur, (uint64_t)tn * p.K + j2, p.halo) << (8 * (j2 & 3u));  // halo: rare, synchronous
+    cp_async4_if(r_s + e * (kChunkTiles * 4), rowp + (j2 & ~3u), out && !far);
+    if (far)  // another shard's tile (sharded contexts): rare, synchronous
+      S.R[e * kChunkTiles + lane] = fetch_cell(cur, (uint64_t)(a1 - 1u) * p.K + j2, p.halo) << (8 * (j2 & 3u));
   }
   cp_async_commit();
 }
@@ -255,26 +265,31 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
     cp_async_wait_all();  // this chunk's link gathers and the next chunk's adjacency (own copies)
     consumers_sync();     // Z, R and both adjacency buffers visible to every consumer warp
 
-    // Phase B: link words, links spread over the warps (contiguous ranges)
+    // Phase B: link words, links spread over the warps (contiguous ranges, branch-free per link:
+    // the word from the chunk's Z or the prefetched one, selected per lane); a lane keeps the ballot
+    // of one link and the warp stores up to 32 link words at once
     {
-    const uint32_t e1 = E * (uint32_t)(cw + 1) / kStreamNW;  // this warp's contiguous link range
-    uint32_t dprev = ~0u, rel = 0;
-    bool inside = false, present = false;
-    for (uint32_t e = E * (uint32_t)cw / kStreamNW; e < e1; ++e) {
-      const uint32_t le = S.lj2[e], j2 = le & 0xFFFFu, d = le >> 16;
-      if (d != dprev) {  // the neighbour tile of this lane's tile in direction d
-        dprev = d;
-        const int64_t tn = (int64_t)ntl[d * kChunkTiles + lane] - 1;
-        present = tn >= 0;
-        rel = (uint32_t)(tn - (int64_t)c.t0);
-        inside = present && (uint64_t)(tn - (int64_t)c.t0) < c.nt;
+      const uint32_t e0 = E * (uint32_t)cw / kStreamNW, e1 = E * (uint32_t)(cw + 1) / kStreamNW;
+      const uint32_t t0 = (uint32_t)c.t0, r_s = smem_u32(S.R) + 4u * (uint32_t)lane;
+      uint32_t dprev = ~0u, rel = 0, present = 0, inside = 0, mine = 0;
+      for (uint32_t e = e0; e < e1; ++e) {
+        const uint32_t le = S.lj2[e], j2 = le & 0xFFFFu, d = le >> 16;
+        if (d != dprev) {  // the neighbour tile of this lane's tile in direction d
+          dprev = d;
+          const uint32_t a1 = ntl[d * kChunkTiles + lane];
+          present = a1 != 0u ? 1u : 0u;
+          rel = a1 - 1u - t0;
+          inside = present && rel < c.nt;
+        }
+        const uint32_t zv = lds32(z_s + 4 * j2), rv = lds32(r_s + e * (kChunkTiles * 4));
+        const uint32_t v = (inside ? zv >> (rel & 31u) : rv >> (8 * (j2 & 3u))) & present;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v & 1u);
+        const uint32_t k = (e - e0) & 31u;
+        if ((uint32_t)lane == k) mine = bal;
+        if (k == 31u || e + 1 == e1) {
+          if ((uint32_t)lane <= k) sts32(z_s + 4 * (K + e - k + (uint32_t)lane), mine);
+        }
       }
-      uint32_t v = 0;
-      if (inside) v = (lds32(z_s + 4 * j2) >> rel) & 1u;
-      else if (present) v = (S.R[e * kChunkTiles + lane] >> (8 * (j2 & 3u))) & 0xFFu;
-      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
-      if (lane == 0) S.Z[K + e] = bal;
-    }
     }
     consumers_sync();  // link words published; R and this chunk's adjacency buffer are free
     if (chunk + 2 * G < p.nchunks) adj_prefetch(p, ntl, chunk_info(p, chunk + 2 * G), cw, lane);
