@@ -44,6 +44,7 @@ struct StreamSmem {
   uint32_t* ntl;    // [2][ndirs][32] neighbour tile + 1 of each lane's tile, by chunk parity
   uint32_t* R;      // [E][32] words holding the out-of-chunk neighbour byte of each link (this chunk)
   uint32_t* lj2;    // [E] link e: its cell in the neighbour tile | direction << 16
+  uint32_t* ds;     // [ndirs + 1] first link of each direction (links are sorted by direction)
   uint64_t* bar;    // infull[nin], inempty[nin], outfull[nout], outempty[nout]
 };
 
@@ -64,6 +65,8 @@ __host__ __device__ inline size_t stream_layout(const TileParams& p, bool peer, 
   off += (size_t)(p.E ? p.E : 1) * kChunkTiles * 4;
   if (s) s->lj2 = (uint32_t*)(base + off);
   off += align16((size_t)(p.E ? p.E : 1) * 4);
+  if (s) s->ds = (uint32_t*)(base + off);
+  off += align16((size_t)(p.ndirs + 1) * 4);
   if (s) s->bar = (uint64_t*)(base + off);
   off += (size_t)2 * (p.sin + p.sout) * 8;
   return align16(off);
@@ -118,22 +121,24 @@ __device__ __forceinline__ void link_prefetch(const TileParams& p, const StreamS
   const uint32_t e1 = p.E * (uint32_t)(cw + 1) / kStreamNW;
   const uint32_t t0 = (uint32_t)c.t0, tlo = (uint32_t)p.tile_lo, nloc = (uint32_t)(p.tile_hi - p.tile_lo);
   const uint32_t r_s = smem_u32(S.R) + 4u * (uint32_t)lane;
-  uint32_t dprev = ~0u, out = 0, a1 = 0;
-  const uint8_t* rowp = cur;
-  bool far = false;  // outside this shard: the halo
-  for (uint32_t e = p.E * (uint32_t)cw / kStreamNW; e < e1; ++e) {
-    const uint32_t le = S.lj2[e], j2 = le & 0xFFFFu, d = le >> 16;
-    if (d != dprev) {
-      dprev = d;
-      a1 = ntl[d * kChunkTiles + lane];  // neighbour tile + 1 (0 = none)
-      const uint32_t tl = a1 - 1u - tlo;
-      out = (a1 != 0u && a1 - 1u - t0 >= c.nt) ? 1u : 0u;
-      far = out && tl >= nloc;
-      rowp = cur + (uint64_t)(far ? 0u : tl) * p.Kp;
+  for (uint32_t e = p.E * (uint32_t)cw / kStreamNW; e < e1;) {
+    const uint32_t d = S.lj2[e] >> 16, eend = min(e1, S.ds[d + 1]);
+    const uint32_t a1 = ntl[d * kChunkTiles + lane];  // neighbour tile + 1 (0 = none)
+    const uint32_t tl = a1 - 1u - tlo;
+    const bool out = a1 != 0u && a1 - 1u - t0 >= c.nt;
+    const bool far = out && tl >= nloc;  // outside this shard: the halo
+    const uint8_t* rowp = cur + (uint64_t)(far ? 0u : tl) * p.Kp;
+    const uint32_t go = out && !far ? 1u : 0u;
+    if (!far) {
+#pragma unroll 4
+      for (; e < eend; ++e) cp_async4_if(r_s + e * (kChunkTiles * 4), rowp + ((S.lj2[e] & 0xFFFFu) & ~3u), go);
+    } else {
+      for (; e < eend; ++e) {  // another shard's tile (sharded contexts): rare, synchronous
+        const uint32_t j2 = S.lj2[e] & 0xFFFFu;
+        S.R[e * kChunkTiles + lane] = fetch_cell(cur, (uint64_t)(a1 - 1u) * p.K + j2, p.halo) << (8 * (j2 & 3u));
+      }
     }
-    cp_async4_if(r_s + e * (kChunkTiles * 4), rowp + (j2 & ~3u), out && !far);
-    if (far)  // another shard's tile (sharded contexts): rare, synchronous
-      S.R[e * kChunkTiles + lane] = fetch_cell(cur, (uint64_t)(a1 - 1u) * p.K + j2, p.halo) << (8 * (j2 & 3u));
+    e = eend;
   }
   cp_async_commit();
 }
@@ -156,6 +161,7 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
   uint64_t* outempty = S.bar + 2 * NIN + NOUT;
 
   for (uint32_t e = tid; e < E; e += blockDim.x) S.lj2[e] = p.link_j2[e] | ((uint32_t)p.link_dir[e] << 16);
+  for (uint32_t d = tid; d <= p.ndirs; d += blockDim.x) S.ds[d] = p.dir_start[d];
   if (tid == 0) {
     S.Z[p.zslot] = 0;
     for (uint32_t i = 0; i < NIN; ++i) {
@@ -271,25 +277,26 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
     {
       const uint32_t e0 = E * (uint32_t)cw / kStreamNW, e1 = E * (uint32_t)(cw + 1) / kStreamNW;
       const uint32_t t0 = (uint32_t)c.t0, r_s = smem_u32(S.R) + 4u * (uint32_t)lane;
-      uint32_t dprev = ~0u, rel = 0, present = 0, inside = 0, mine = 0;
-      for (uint32_t e = e0; e < e1; ++e) {
-        const uint32_t le = S.lj2[e], j2 = le & 0xFFFFu, d = le >> 16;
-        if (d != dprev) {  // the neighbour tile of this lane's tile in direction d
-          dprev = d;
-          const uint32_t a1 = ntl[d * kChunkTiles + lane];
-          present = a1 != 0u ? 1u : 0u;
-          rel = a1 - 1u - t0;
-          inside = present && rel < c.nt;
-        }
-        const uint32_t zv = lds32(z_s + 4 * j2), rv = lds32(r_s + e * (kChunkTiles * 4));
-        const uint32_t v = (inside ? zv >> (rel & 31u) : rv >> (8 * (j2 & 3u))) & present;
-        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v & 1u);
-        const uint32_t k = (e - e0) & 31u;
-        if ((uint32_t)lane == k) mine = bal;
-        if (k == 31u || e + 1 == e1) {
-          if ((uint32_t)lane <= k) sts32(z_s + 4 * (K + e - k + (uint32_t)lane), mine);
+      uint32_t mine = 0;
+      for (uint32_t e = e0; e < e1;) {
+        const uint32_t d = S.lj2[e] >> 16, eend = min(e1, S.ds[d + 1]);
+        const uint32_t a1 = ntl[d * kChunkTiles + lane];  // the neighbour tile of this lane's tile in direction d
+        const uint32_t present = a1 != 0u ? 1u : 0u, rel = a1 - 1u - t0;
+        const bool inside = present && rel < c.nt;
+        const uint32_t zsh = rel & 31u;
+#pragma unroll 2
+        for (; e < eend; ++e) {
+          const uint32_t j2 = S.lj2[e] & 0xFFFFu;
+          const uint32_t zv = lds32(z_s + 4 * j2), rv = lds32(r_s + e * (kChunkTiles * 4));
+          const uint32_t v = (inside ? zv >> zsh : rv >> (8 * (j2 & 3u))) & present;
+          const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v & 1u);
+          const uint32_t k = (e - e0) & 31u;
+          if ((uint32_t)lane == k) mine = bal;
+          if (k == 31u) sts32(z_s + 4 * (K + e - 31u + (uint32_t)lane), mine);
         }
       }
+      const uint32_t k = (e1 - e0) & 31u;  // the last partial group of link words
+      if (e1 > e0 && k != 0u && (uint32_t)lane < k) sts32(z_s + 4 * (K + e1 - k + (uint32_t)lane), mine);
     }
     consumers_sync();  // link words published; R and this chunk's adjacency buffer are free
     if (chunk + 2 * G < p.nchunks) adj_prefetch(p, ntl, chunk_info(p, chunk + 2 * G), cw, lane);
