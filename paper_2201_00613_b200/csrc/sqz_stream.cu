@@ -143,7 +143,7 @@ __device__ __forceinline__ void link_prefetch(const TileParams& p, const StreamS
   cp_async_commit();
 }
 
-template <int DMAX, bool CONWAY, int RB, int MINB, int NOUT, bool PEER>
+template <int DMAX, bool CONWAY, int RB, int MINB, int NIN, int NOUT, bool PEER>
 __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, const uint8_t* __restrict__ cur,
                                                               uint8_t* __restrict__ next,
                                                               const __grid_constant__ CUtensorMap tm_in,
@@ -152,7 +152,7 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
   StreamSmem S;
   stream_layout(p, PEER, smem_raw, &S);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t K = (uint32_t)p.K, Kp = p.Kp, E = p.E, NIN = p.sin;
+  const uint32_t K = (uint32_t)p.K, Kp = p.Kp, E = p.E;
   const uint32_t KP32 = (K + 31) & ~31u, nblk = KP32 / 32;
   const uint32_t nsl = (KP32 + kStreamSW - 1) / kStreamSW;
   uint64_t* infull = S.bar;
@@ -384,45 +384,36 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
 
 using StreamFn = void (*)(TileParams, const uint8_t*, uint8_t*, const CUtensorMap, const CUtensorMap);
 
-template <bool PEER, int RB, int MINB>
+template <bool PEER, int RB, int MINB, int NIN, int NOUT>
 static StreamFn pick_stream_r(const TileParams& p) {
   const bool conway = (p.birth == (1u << 3)) && (p.survive == ((1u << 2) | (1u << 3)));
-  if (p.sout >= 3) {
-    if (p.dmax <= 5) return conway ? k_step_stream<5, true, RB, MINB, 3, PEER> : k_step_stream<5, false, RB, MINB, 3, PEER>;
-    return conway ? k_step_stream<8, true, RB, MINB, 3, PEER> : k_step_stream<8, false, RB, MINB, 3, PEER>;
-  }
-  if (p.dmax <= 5) return conway ? k_step_stream<5, true, RB, MINB, 2, PEER> : k_step_stream<5, false, RB, MINB, 2, PEER>;
-  return conway ? k_step_stream<8, true, RB, MINB, 2, PEER> : k_step_stream<8, false, RB, MINB, 2, PEER>;
+  if (p.dmax <= 5)
+    return conway ? k_step_stream<5, true, RB, MINB, NIN, NOUT, PEER> : k_step_stream<5, false, RB, MINB, NIN, NOUT, PEER>;
+  return conway ? k_step_stream<8, true, RB, MINB, NIN, NOUT, PEER> : k_step_stream<8, false, RB, MINB, NIN, NOUT, PEER>;
 }
 
 // RB = slices whose neighbour rows stay in registers: 8 at one CTA per SM (carpet level 4: 8 of
 // its 9 slices), 2 at two CTAs per SM (64 registers).
 template <bool PEER>
 static StreamFn pick_stream_t(const TileParams& p, int minb) {
-  return minb >= 2 ? pick_stream_r<PEER, 2, 2>(p) : pick_stream_r<PEER, 8, 1>(p);
+  return minb >= 2 ? pick_stream_r<PEER, 2, 2, 4, 2>(p) : pick_stream_r<PEER, 8, 1, 4, 4>(p);
 }
 
-// The ring depths (p.sin, p.sout) and CTAs per SM for these tables: two CTAs per SM when both fit
-// with at least three input slots, else one CTA with the deepest input ring that fits.
+// The ring depths (p.sin, p.sout: powers of two, slot indices are masks) and CTAs per SM: two CTAs
+// per SM with 4 input and 2 output slots when that fits twice, else one CTA with 4 + 4.
 bool stream_plan(TileParams& p, bool peer, int* minb) {
   if (p.E > kStreamMaxLinks) return false;
   const size_t cap = 227 * 1024;
   const char* force = getenv("SQZ_STREAM_CTAS");  // tuning knob: 1 or 2 CTAs per SM
-  if (!force || atoi(force) >= 2) {
-    for (uint32_t out = 3; out >= 2; --out) {
-      p.sout = out;
-      p.sin = out + 1;
-      if (2 * stream_smem_bytes(p, peer) <= cap) {
-        *minb = 2;
-        return true;
-      }
-    }
+  p.sin = 4;
+  p.sout = 2;
+  if ((!force || atoi(force) >= 2) && 2 * stream_smem_bytes(p, peer) <= cap) {
+    *minb = 2;
+    return true;
   }
   *minb = 1;
-  p.sout = 3;
-  for (p.sin = 8; p.sin >= 2; --p.sin)
-    if (stream_smem_bytes(p, peer) <= cap) return true;
-  return false;
+  p.sout = 4;
+  return stream_smem_bytes(p, peer) <= cap;
 }
 
 int stream_threads() { return kStreamThreads; }
