@@ -430,6 +430,18 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
     // the tile kernel are bank-conflict-free (measured: 15.7 vs 16.1 ms at r=22 despite +2.2% bytes)
     c->Kp = (uint32_t)((c->tt.K + 31) & ~31ull);
     if ((c->Kp / 16) % 2 == 0) c->Kp += 16;
+    {  // two double-buffered 32-tile chunks per SM, else the streaming step (sqz_stream.cu), whose
+       // tiles are rows of round_up(K, 32) bytes (whole 32-cell blocks, 256-bit aligned stores)
+      TileParams q{};
+      q.K = c->tt.K;
+      q.Kp = c->Kp;
+      q.St = c->Kp;
+      q.E = c->tt.E;
+      q.ndirs = c->tt.ndirs;
+      q.dmax = c->tt.max_degree;
+      c->stream = 2 * tile_smem_bytes(q) > 227 * 1024;
+      if (c->stream) c->Kp = (uint32_t)((c->tt.K + 31) & ~31ull);
+    }
     c->state_bytes = (c->sr.tile_hi - c->sr.tile_lo) * c->Kp;
     c->Kw = (uint32_t)((c->tt.K + 3) & ~3ull);
     c->packed_bytes = ((c->sr.tile_hi - c->sr.tile_lo + kPackTiles - 1) / kPackTiles) * c->Kw * 16;
@@ -485,9 +497,8 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
       // two double-buffered 32-tile chunks per SM, else the streaming step (sqz_stream.cu)
-      c->stream = 2 * c->tile_smem > 227 * 1024 || tile_prepare(p, c->tile_smem, c->tile_threads, &occ) != cudaSuccess;
+      if (!c->stream && tile_prepare(p, c->tile_smem, c->tile_threads, &occ) != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
       if (c->stream) {
-        cudaGetLastError();  // a refused attribute of the chunk-staged kernel is not an error of the context
         if (c->tt.K > 0xFFFFu || !stream_plan(p, c->nranks > 1, &c->stream_minb)) return fail(SQZ_E_INVALID_LEVEL);
         c->stream_sin = p.sin;
         c->stream_sout = p.sout;
@@ -495,8 +506,8 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
         c->tile_threads = stream_threads();
         const cudaError_t se = stream_prepare(p, c->tile_smem, c->stream_minb, &occ);
         if (getenv("SQZ_DEBUG"))
-          fprintf(stderr, "sqz: streaming step K=%llu E=%u rings %u/%u smem %zu minb %d occupancy %d (%s)\n",
-                  (unsigned long long)c->tt.K, c->tt.E, p.sin, p.sout, c->tile_smem, c->stream_minb, occ,
+          fprintf(stderr, "sqz: streaming step K=%llu E=%u input ring %u smem %zu minb %d occupancy %d (%s)\n",
+                  (unsigned long long)c->tt.K, c->tt.E, p.sin, c->tile_smem, c->stream_minb, occ,
                   cudaGetErrorString(se));
         if (se != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
         c->stream_grid = sms * std::max(1, occ);

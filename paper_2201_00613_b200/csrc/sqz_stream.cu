@@ -35,17 +35,19 @@ constexpr uint32_t kStreamSlot = 2 * kChunkTiles * kStreamBox;  // bytes per rin
 constexpr int kStreamNW = 15;         // consumer warps: one j-block of each slice apiece
 constexpr int kStreamThreads = 32 * (kStreamNW + 1);
 constexpr uint32_t kStreamMaxLinks = 1024;
+constexpr uint32_t kStreamMaxItems = 64;  // link groups: ceil(links of d / 32) per direction d
 
 struct StreamSmem {
-  uint8_t* in0;     // nin slots of two [32][240] boxes
-  uint8_t* out0;    // nout slots of two [32][240] boxes
+  uint8_t* in0;     // p.sin slots of two [32][240] boxes
   uint32_t* Z;      // [K state words | E link words | zero word]
   uint32_t* Wn;     // PEER: the chunk's new state words (bit i = tile i), K words
   uint32_t* ntl;    // [2][ndirs][32] neighbour tile + 1 of each lane's tile, by chunk parity
-  uint32_t* R;      // [E][32] words holding the out-of-chunk neighbour byte of each link (this chunk)
+  uint32_t* G;      // [32][E] word holding the neighbour byte of link e for tile i, where tile i's
+                    // neighbour tile lies outside the chunk (this chunk's gathers)
   uint32_t* lj2;    // [E] link e: its cell in the neighbour tile | direction << 16
-  uint32_t* ds;     // [ndirs + 1] first link of each direction (links are sorted by direction)
-  uint64_t* bar;    // infull[nin], inempty[nin], outfull[nout], outempty[nout]
+  uint32_t* items;  // [kStreamMaxItems] link groups: first link | count - 1 << 11 | direction << 16
+  uint32_t* nitems;
+  uint64_t* bar;    // infull[sin], inempty[sin]
 };
 
 __host__ __device__ inline size_t stream_layout(const TileParams& p, bool peer, uint8_t* base, StreamSmem* s) {
@@ -53,22 +55,22 @@ __host__ __device__ inline size_t stream_layout(const TileParams& p, bool peer, 
   size_t off = 0;
   if (s) s->in0 = base + off;
   off += p.sin * slot;
-  if (s) s->out0 = base + off;
-  off += p.sout * slot;
   if (s) s->Z = (uint32_t*)(base + off);
   off += align16((size_t)(p.K + p.E + 1) * 4);
   if (s) s->Wn = (uint32_t*)(base + off);
   off += peer ? align16((size_t)p.K * 4) : 0;
   if (s) s->ntl = (uint32_t*)(base + off);
   off += (size_t)2 * (p.ndirs ? p.ndirs : 1) * kChunkTiles * 4;
-  if (s) s->R = (uint32_t*)(base + off);
+  if (s) s->G = (uint32_t*)(base + off);
   off += (size_t)(p.E ? p.E : 1) * kChunkTiles * 4;
   if (s) s->lj2 = (uint32_t*)(base + off);
   off += align16((size_t)(p.E ? p.E : 1) * 4);
-  if (s) s->ds = (uint32_t*)(base + off);
-  off += align16((size_t)(p.ndirs + 1) * 4);
+  if (s) s->items = (uint32_t*)(base + off);
+  off += (size_t)kStreamMaxItems * 4;
+  if (s) s->nitems = (uint32_t*)(base + off);
+  off += 16;
   if (s) s->bar = (uint64_t*)(base + off);
-  off += (size_t)2 * (p.sin + p.sout) * 8;
+  off += (size_t)2 * p.sin * 8;
   return align16(off);
 }
 
@@ -112,42 +114,100 @@ __device__ __forceinline__ void cp_async4_if(uint32_t dst, const void* src, uint
       : "memory");
 }
 
-// For every link e of warp cw's contiguous range [E cw / NW, E (cw+1) / NW) (links are sorted by
-// direction: the neighbour tile is looked up once per direction) whose neighbour tile lies outside
-// chunk c: the word holding the neighbour byte, by a predicated 4-byte cp.async (or, for another
-// shard's tile, from the halo).  Tile indices fit 32 bits (checked on the host).
+// Link groups: the links of one direction d (sorted by direction), 32 at a time; lane = link.
+// Tiles of a chunk are lanes of the bit-sliced words, and a direction's neighbour tiles are the same
+// for all its links, so per (group, tile) the work is uniform across the warp: the in-chunk part of
+// a link word is a few masked rotations of the neighbour cell's Z word (one per distinct lane
+// offset rel - i), the out-of-chunk part one gathered word per outside tile.
+struct LinkGroup {
+  uint32_t e;      // this lane's link (valid lanes: lane < n)
+  uint32_t j2;     // its cell in the neighbour tile
+  uint32_t d;      // direction
+  bool valid;
+};
+
+__device__ __forceinline__ LinkGroup link_group(const StreamSmem& S, uint32_t item, int lane) {
+  LinkGroup g;
+  const uint32_t e0 = item & 0x7FFu, n = ((item >> 11) & 31u) + 1u;
+  g.d = item >> 16;
+  g.valid = (uint32_t)lane < n;
+  g.e = e0 + (g.valid ? (uint32_t)lane : 0u);
+  g.j2 = S.lj2[g.e] & 0xFFFFu;
+  return g;
+}
+
+// Item k = warp cw, cw + NW, ...: for every tile i of chunk c whose neighbour tile in the group's
+// direction lies outside the chunk, the 4-byte word holding the neighbour cell of each of the
+// group's links (lane = link), by cp.async (or, for another shard's tile, from the halo).  The
+// same warp consumes them in Phase B of chunk c.  Tile indices fit 32 bits (checked on the host).
 __device__ __forceinline__ void link_prefetch(const TileParams& p, const StreamSmem& S, const uint32_t* ntl,
                                               const ChunkInfo& c, const uint8_t* __restrict__ cur, int cw, int lane) {
-  const uint32_t e1 = p.E * (uint32_t)(cw + 1) / kStreamNW;
   const uint32_t t0 = (uint32_t)c.t0, tlo = (uint32_t)p.tile_lo, nloc = (uint32_t)(p.tile_hi - p.tile_lo);
-  const uint32_t r_s = smem_u32(S.R) + 4u * (uint32_t)lane;
-  for (uint32_t e = p.E * (uint32_t)cw / kStreamNW; e < e1;) {
-    const uint32_t d = S.lj2[e] >> 16, eend = min(e1, S.ds[d + 1]);
-    const uint32_t a1 = ntl[d * kChunkTiles + lane];  // neighbour tile + 1 (0 = none)
+  const uint32_t ni = *S.nitems, E = p.E;
+  for (uint32_t k = (uint32_t)cw; k < ni; k += kStreamNW) {
+    const LinkGroup g = link_group(S, S.items[k], lane);
+    const uint32_t a1 = ntl[g.d * kChunkTiles + lane];  // lane = tile here: neighbour tile + 1 (0 = none)
     const uint32_t tl = a1 - 1u - tlo;
     const bool out = a1 != 0u && a1 - 1u - t0 >= c.nt;
-    const bool far = out && tl >= nloc;  // outside this shard: the halo
-    const uint8_t* rowp = cur + (uint64_t)(far ? 0u : tl) * p.Kp;
-    const uint32_t go = out && !far ? 1u : 0u;
-    if (!far) {
-#pragma unroll 4
-      for (; e < eend; ++e) cp_async4_if(r_s + e * (kChunkTiles * 4), rowp + ((S.lj2[e] & 0xFFFFu) & ~3u), go);
-    } else {
-      for (; e < eend; ++e) {  // another shard's tile (sharded contexts): rare, synchronous
-        const uint32_t j2 = S.lj2[e] & 0xFFFFu;
-        S.R[e * kChunkTiles + lane] = fetch_cell(cur, (uint64_t)(a1 - 1u) * p.K + j2, p.halo) << (8 * (j2 & 3u));
+    uint32_t om = __ballot_sync(0xFFFFFFFFu, out);
+    const uint32_t farm = __ballot_sync(0xFFFFFFFFu, out && tl >= nloc);  // outside this shard: the halo
+    const uint32_t gs = smem_u32(S.G) + 4u * g.e, jo = g.j2 & ~3u, pv = g.valid ? 1u : 0u;
+    while (om) {
+      const uint32_t i = __ffs(om) - 1u;
+      om &= om - 1u;
+      const uint32_t tli = __shfl_sync(0xFFFFFFFFu, tl, i);
+      if (!((farm >> i) & 1u)) {
+        cp_async4_if(gs + i * (E * 4u), cur + (uint64_t)tli * p.Kp + jo, pv);
+      } else if (g.valid) {  // another shard's tile (sharded contexts): rare, synchronous
+        S.G[i * E + g.e] = fetch_cell(cur, (uint64_t)(tli + tlo) * p.K + g.j2, p.halo) << (8 * (g.j2 & 3u));
       }
     }
-    e = eend;
   }
   cp_async_commit();
 }
 
-template <int DMAX, bool CONWAY, int RB, int MINB, int NIN, int NOUT, bool PEER>
+// Phase B for item k of chunk c: link word e (bit i = neighbour cell of tile i) -> Z[K + e].
+__device__ __forceinline__ void link_words(const TileParams& p, const StreamSmem& S, const uint32_t* ntl,
+                                           const ChunkInfo& c, int cw, int lane) {
+  const uint32_t t0 = (uint32_t)c.t0, ni = *S.nitems, E = p.E, K = (uint32_t)p.K;
+  for (uint32_t k = (uint32_t)cw; k < ni; k += kStreamNW) {
+    const LinkGroup g = link_group(S, S.items[k], lane);
+    const uint32_t a1 = ntl[g.d * kChunkTiles + lane];  // lane = tile
+    const uint32_t rel = a1 - 1u - t0;
+    const bool present = a1 != 0u, inside = present && rel < c.nt;
+    const uint32_t dl = (rel - (uint32_t)lane) & 31u;  // tile i's neighbour is tile i + dl (mod 32)
+    uint32_t im = __ballot_sync(0xFFFFFFFFu, inside);
+    uint32_t om = __ballot_sync(0xFFFFFFFFu, present && !inside);
+    const uint32_t z = S.Z[g.j2];  // lane = link from here on
+    uint32_t w = 0;
+    while (im) {  // tiles with the same offset: one masked rotation
+      const uint32_t dd = __shfl_sync(0xFFFFFFFFu, dl, __ffs(im) - 1u);
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, inside && dl == dd);
+      im &= ~m;
+      w |= __funnelshift_r(z, z, dd) & m;
+    }
+    const uint32_t gs = smem_u32(S.G) + 4u * g.e, sh = 8u * (g.j2 & 3u);
+    while (om) {  // tiles whose neighbour tile is outside the chunk: the gathered words
+      const uint32_t i = __ffs(om) - 1u;
+      om &= om - 1u;
+      w |= ((lds32(gs + i * (E * 4u)) >> sh) & 1u) << i;
+    }
+    if (g.valid) S.Z[K + g.e] = w;
+  }
+}
+
+// 32 bytes to global memory with one 256-bit store (32-byte aligned).
+__device__ __forceinline__ void stg256(void* dst, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t a4,
+                                       uint32_t a5, uint32_t a6, uint32_t a7) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(a0), "r"(a1), "r"(a2),
+               "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7)
+               : "memory");
+}
+
+template <int DMAX, bool CONWAY, int RB, int MINB, int NIN, bool PEER>
 __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, const uint8_t* __restrict__ cur,
                                                               uint8_t* __restrict__ next,
-                                                              const __grid_constant__ CUtensorMap tm_in,
-                                                              const __grid_constant__ CUtensorMap tm_out) {
+                                                              const __grid_constant__ CUtensorMap tm_in) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   StreamSmem S;
   stream_layout(p, PEER, smem_raw, &S);
@@ -157,34 +217,32 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
   const uint32_t nsl = (KP32 + kStreamSW - 1) / kStreamSW;
   uint64_t* infull = S.bar;
   uint64_t* inempty = S.bar + NIN;
-  uint64_t* outfull = S.bar + 2 * NIN;
-  uint64_t* outempty = S.bar + 2 * NIN + NOUT;
 
   for (uint32_t e = tid; e < E; e += blockDim.x) S.lj2[e] = p.link_j2[e] | ((uint32_t)p.link_dir[e] << 16);
-  for (uint32_t d = tid; d <= p.ndirs; d += blockDim.x) S.ds[d] = p.dir_start[d];
   if (tid == 0) {
+    uint32_t n = 0;  // link groups: each direction's links, 32 at a time
+    for (uint32_t d = 0; d < p.ndirs; ++d)
+      for (uint32_t e = p.dir_start[d]; e < p.dir_start[d + 1]; e += 32)
+        S.items[n++] = e | ((min(32u, p.dir_start[d + 1] - e) - 1u) << 11) | (d << 16);
+    *S.nitems = n;
     S.Z[p.zslot] = 0;
     for (uint32_t i = 0; i < NIN; ++i) {
       mbar_init(&infull[i], 1);
       mbar_init(&inempty[i], kStreamNW);
-    }
-    for (uint32_t i = 0; i < NOUT; ++i) {
-      mbar_init(&outfull[i], kStreamNW);
-      mbar_init(&outempty[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if ((uint64_t)blockIdx.x >= p.nchunks) return;
   const uint64_t G = gridDim.x;
-  const uint32_t in_base = smem_u32(S.in0), out_base = smem_u32(S.out0);
+  const uint32_t in_base = smem_u32(S.in0);
   const uint32_t slot_bytes = kStreamSlot;
 
-  if (warp == 0) {  // ------------------------------------------- the copy warp (one thread): slices in and out
+  if (warp == 0) {  // ------------------------------------------- the copy warp (one thread): slices in
     if (lane == 0) {
       const uint32_t total = (uint32_t)((p.nchunks - blockIdx.x + G - 1) / G) * nsl;
       auto load = [&](uint32_t s) {  // slice s of this CTA: two 2D boxes [32 tiles x 240 B] (rows past the
-        const uint32_t slot = s % NIN, q = s % nsl;  // shard and columns past Kp read as zero)
+        const uint32_t slot = s % NIN, q = s % nsl;  // shard and columns past round_up(K, 32) read as zero)
         const uint64_t chunk = blockIdx.x + (uint64_t)(s / nsl) * G;
         const uint32_t bar = smem_u32(&infull[slot]);
         const int32_t row = (int32_t)(chunk * kChunkTiles), x0 = (int32_t)(q * kStreamSW);
@@ -198,28 +256,11 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
       };
       uint32_t ld = 0;
       for (; ld < NIN && ld < total; ++ld) load(ld);
-      // the consumers' order: Phase A frees the chunk's input slots one slice at a time (each freed
-      // slot takes the slice NIN ahead), then C+D fills its output slices in order
-      for (uint32_t s0 = 0; s0 < total; s0 += nsl) {
-        for (uint32_t s = s0; s < s0 + nsl && ld < total; ++s, ++ld) {
-          mbar_wait(&inempty[s % NIN], (s / NIN) & 1);
-          load(ld);
-        }
-        for (uint32_t s = s0; s < s0 + nsl; ++s) {
-          const uint32_t oslot = s % NOUT, q = s % nsl;
-          mbar_wait(&outfull[oslot], (s / NOUT) & 1);
-          const int32_t row = (int32_t)((blockIdx.x + (uint64_t)(s / nsl) * G) * kChunkTiles);
-          for (int h = 0; h < 2; ++h)  // rows past the shard and columns past Kp are not written
-            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&tm_out),
-                         "r"((int32_t)(q * kStreamSW) + h * (int32_t)kStreamBox), "r"(row),
-                         "r"(out_base + oslot * slot_bytes + h * (kStreamSlot / 2))
-                         : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          bulk_wait_read<NOUT - 1>();  // slice s + 1 - NOUT has been read out: its slot may be refilled
-          if (s + 1 >= NOUT) mbar_arrive(&outempty[(s + 1) % NOUT]);
-        }
+      // Phase A frees the input slots one slice at a time; each freed slot takes the slice NIN ahead
+      for (; ld < total; ++ld) {
+        mbar_wait(&inempty[ld % NIN], ((ld - NIN) / NIN) & 1);
+        load(ld);
       }
-      bulk_wait_all();
     }
     return;
   }
@@ -271,42 +312,16 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
     cp_async_wait_all();  // this chunk's link gathers and the next chunk's adjacency (own copies)
     consumers_sync();     // Z, R and both adjacency buffers visible to every consumer warp
 
-    // Phase B: link words, links spread over the warps (contiguous ranges, branch-free per link:
-    // the word from the chunk's Z or the prefetched one, selected per lane); a lane keeps the ballot
-    // of one link and the warp stores up to 32 link words at once
-    {
-      const uint32_t e0 = E * (uint32_t)cw / kStreamNW, e1 = E * (uint32_t)(cw + 1) / kStreamNW;
-      const uint32_t t0 = (uint32_t)c.t0, r_s = smem_u32(S.R) + 4u * (uint32_t)lane;
-      uint32_t mine = 0;
-      for (uint32_t e = e0; e < e1;) {
-        const uint32_t d = S.lj2[e] >> 16, eend = min(e1, S.ds[d + 1]);
-        const uint32_t a1 = ntl[d * kChunkTiles + lane];  // the neighbour tile of this lane's tile in direction d
-        const uint32_t present = a1 != 0u ? 1u : 0u, rel = a1 - 1u - t0;
-        const bool inside = present && rel < c.nt;
-        const uint32_t zsh = rel & 31u;
-#pragma unroll 2
-        for (; e < eend; ++e) {
-          const uint32_t j2 = S.lj2[e] & 0xFFFFu;
-          const uint32_t zv = lds32(z_s + 4 * j2), rv = lds32(r_s + e * (kChunkTiles * 4));
-          const uint32_t v = (inside ? zv >> zsh : rv >> (8 * (j2 & 3u))) & present;
-          const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v & 1u);
-          const uint32_t k = (e - e0) & 31u;
-          if ((uint32_t)lane == k) mine = bal;
-          if (k == 31u) sts32(z_s + 4 * (K + e - 31u + (uint32_t)lane), mine);
-        }
-      }
-      const uint32_t k = (e1 - e0) & 31u;  // the last partial group of link words
-      if (e1 > e0 && k != 0u && (uint32_t)lane < k) sts32(z_s + 4 * (K + e1 - k + (uint32_t)lane), mine);
-    }
-    consumers_sync();  // link words published; R and this chunk's adjacency buffer are free
+    // Phase B: link words, by link groups (lane = link)
+    link_words(p, S, ntl, c, cw, lane);
+    consumers_sync();  // link words published; G and this chunk's adjacency buffer are free
     if (chunk + 2 * G < p.nchunks) adj_prefetch(p, ntl, chunk_info(p, chunk + 2 * G), cw, lane);
     if (chunk + G < p.nchunks) link_prefetch(p, S, S.ntl + ((it + 1) & 1) * ntl_words, chunk_info(p, chunk + G), cur, cw, lane);
 
-    // Phase C+D: slice q -> out-ring slot (the copy warp stores it)
+    // Phase C+D: j-block q * NW + cw -> HBM (lane = tile: one 256-bit store of its 32 cells)
     const uint32_t live_lanes = c.nt >= 32 ? 0xFFFFFFFFu : ((1u << c.nt) - 1u);
+    uint8_t* tile_out = next + (uint64_t)((uint32_t)(c.t0 - p.tile_lo) + (uint32_t)lane) * Kp;
     auto slice_out = [&](uint32_t q, const uint4& row) {
-      const uint32_t s = seq + q, oslot = s % NOUT, u = s / NOUT;
-      if (u > 0) mbar_wait(&outempty[oslot], (u - 1) & 1);
       const uint32_t jb = q * kStreamNW + (uint32_t)cw;
       if (jb < nblk) {
         const uint32_t j = jb * 32 + my_jj;
@@ -350,16 +365,11 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
           if (PEER) S.Wn[j] = nw;
         }
         const uint32_t xb = tr(nw);  // bit 8p+m = cell jb*32 + 4m + p of this lane's tile (0 past K)
-        const uint32_t o = out_base + oslot * slot_bytes + (uint32_t)lane * kStreamBox;
         const uint32_t m = 0x01010101u;
-        sts128(o + box_off(cw * 32), xb & m, (xb >> 1) & m, (xb >> 2) & m, (xb >> 3) & m);
-        sts128(o + box_off(cw * 32 + 16), (xb >> 4) & m, (xb >> 5) & m, (xb >> 6) & m, (xb >> 7) & m);
-        if (jb + 1 == nblk && Kp > KP32 && (uint32_t)lane < c.nt)  // the tile's 16 zero padding bytes (the
-          *reinterpret_cast<uint4*>(next + (c.t0 - p.tile_lo + lane) * Kp + KP32) = make_uint4(0u, 0u, 0u, 0u);  // maps stop at KP32
+        if ((uint32_t)lane < c.nt)  // Kp = round_up(K, 32): the block's 32 bytes are one aligned sector
+          stg256(tile_out + jb * 32, xb & m, (xb >> 1) & m, (xb >> 2) & m, (xb >> 3) & m, (xb >> 4) & m,
+                 (xb >> 5) & m, (xb >> 6) & m, (xb >> 7) & m);
       }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&outfull[oslot]);
     };
 #pragma unroll
     for (int i = 0; i < RB; ++i)
@@ -382,37 +392,41 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
   if (PEER && peer_sent) __threadfence_system();
 }
 
-using StreamFn = void (*)(TileParams, const uint8_t*, uint8_t*, const CUtensorMap, const CUtensorMap);
+using StreamFn = void (*)(TileParams, const uint8_t*, uint8_t*, const CUtensorMap);
 
-template <bool PEER, int RB, int MINB, int NIN, int NOUT>
+template <bool PEER, int RB, int MINB, int NIN>
 static StreamFn pick_stream_r(const TileParams& p) {
   const bool conway = (p.birth == (1u << 3)) && (p.survive == ((1u << 2) | (1u << 3)));
   if (p.dmax <= 5)
-    return conway ? k_step_stream<5, true, RB, MINB, NIN, NOUT, PEER> : k_step_stream<5, false, RB, MINB, NIN, NOUT, PEER>;
-  return conway ? k_step_stream<8, true, RB, MINB, NIN, NOUT, PEER> : k_step_stream<8, false, RB, MINB, NIN, NOUT, PEER>;
+    return conway ? k_step_stream<5, true, RB, MINB, NIN, PEER> : k_step_stream<5, false, RB, MINB, NIN, PEER>;
+  return conway ? k_step_stream<8, true, RB, MINB, NIN, PEER> : k_step_stream<8, false, RB, MINB, NIN, PEER>;
 }
 
 // RB = slices whose neighbour rows stay in registers: 8 at one CTA per SM (carpet level 4: 8 of
 // its 9 slices), 2 at two CTAs per SM (64 registers).
 template <bool PEER>
 static StreamFn pick_stream_t(const TileParams& p, int minb) {
-  return minb >= 2 ? pick_stream_r<PEER, 2, 2, 4, 2>(p) : pick_stream_r<PEER, 8, 1, 4, 4>(p);
+  if (minb >= 2) return pick_stream_r<PEER, 2, 2, 4>(p);
+  return p.sin >= 8 ? pick_stream_r<PEER, 8, 1, 8>(p) : pick_stream_r<PEER, 8, 1, 4>(p);
 }
 
-// The ring depths (p.sin, p.sout: powers of two, slot indices are masks) and CTAs per SM: two CTAs
-// per SM with 4 input and 2 output slots when that fits twice, else one CTA with 4 + 4.
+// The input ring depth p.sin (a power of two: slot indices are masks) and CTAs per SM: two CTAs
+// per SM with 4 slots each when that fits twice, else one CTA with 8 slots (the whole next chunk of
+// a level-4 carpet but one slice in flight while the current one is computed), else 4.
 bool stream_plan(TileParams& p, bool peer, int* minb) {
   if (p.E > kStreamMaxLinks) return false;
   const size_t cap = 227 * 1024;
   const char* force = getenv("SQZ_STREAM_CTAS");  // tuning knob: 1 or 2 CTAs per SM
   p.sin = 4;
-  p.sout = 2;
+  p.sout = 0;
   if ((!force || atoi(force) >= 2) && 2 * stream_smem_bytes(p, peer) <= cap) {
     *minb = 2;
     return true;
   }
   *minb = 1;
-  p.sout = 4;
+  p.sin = 8;
+  if (stream_smem_bytes(p, peer) <= cap) return true;
+  p.sin = 4;
   return stream_smem_bytes(p, peer) <= cap;
 }
 
@@ -431,10 +445,9 @@ cudaError_t stream_prepare(const TileParams& p, size_t smem, int minb, int* occu
   return blocks > 0 ? cudaSuccess : cudaErrorInvalidConfiguration;
 }
 
-// 2D tensor map of a tile-padded state buffer: dim 0 = the first round_up(K, 32) bytes of a tile (the
-// last 16 padding bytes, if Kp has them, are written by the consumer that owns the tile's last
-// block), dim 1 = the shard's tiles (row pitch Kp, a multiple of 16); boxes of [32 tiles x 240 B];
-// out-of-range reads are zero, out-of-range box parts are not stored.
+// 2D tensor map of a tile-padded state buffer (streaming contexts: Kp = round_up(K, 32)): dim 0 = the
+// Kp bytes of a tile, dim 1 = the shard's tiles; boxes of [32 tiles x 240 B]; out-of-range reads
+// are zero.
 static cudaError_t state_tensor_map(CUtensorMap* tm, const TileParams& p, const void* base) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
@@ -445,7 +458,7 @@ static cudaError_t state_tensor_map(CUtensorMap* tm, const TileParams& p, const 
       return cudaErrorNotSupported;
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  const cuuint64_t dims[2] = {(p.K + 31) & ~31ull, p.tile_hi - p.tile_lo};  // cells + zero bytes to 32
+  const cuuint64_t dims[2] = {p.Kp, p.tile_hi - p.tile_lo};
   const cuuint64_t strides[1] = {p.Kp};
   const cuuint32_t box[2] = {kStreamBox, kChunkTiles};
   const cuuint32_t estr[2] = {1, 1};
@@ -458,12 +471,13 @@ static cudaError_t state_tensor_map(CUtensorMap* tm, const TileParams& p, const 
 cudaError_t launch_step_stream(const TileParams& p, const uint8_t* cur, uint8_t* next, int grid, int minb,
                                size_t smem, cudaStream_t st) {
   if (p.nchunks == 0) return cudaSuccess;
-  alignas(64) CUtensorMap tin, tout;
+  // 256-bit stores of whole 32-cell blocks: rows of Kp = round_up(K, 32) bytes, 32-byte aligned buffers
+  if (p.Kp != ((p.K + 31) & ~31ull) || ((uintptr_t)cur & 31u) || ((uintptr_t)next & 31u)) return cudaErrorInvalidValue;
+  alignas(64) CUtensorMap tin;
   cudaError_t e = state_tensor_map(&tin, p, cur);
-  if (e == cudaSuccess) e = state_tensor_map(&tout, p, next);
   if (e != cudaSuccess) return e;
   StreamFn fn = p.peer_recv ? pick_stream_t<true>(p, minb) : pick_stream_t<false>(p, minb);
-  fn<<<grid, kStreamThreads, smem, st>>>(p, cur, next, tin, tout);
+  fn<<<grid, kStreamThreads, smem, st>>>(p, cur, next, tin);
   return cudaGetLastError();
 }
 
