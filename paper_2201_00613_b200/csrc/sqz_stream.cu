@@ -39,14 +39,16 @@ constexpr uint32_t kStreamMaxItems = 64;  // link groups: ceil(links of d / 32) 
 
 struct StreamSmem {
   uint8_t* in0;     // p.sin slots of two [32][240] boxes
-  uint32_t* Z;      // [K state words | E link words | zero word]
+  uint32_t* Z0;     // 2 x [K state words | E link words | zero word], by chunk parity
+  uint32_t zn;      // words per Z buffer
   uint32_t* Wn;     // PEER: the chunk's new state words (bit i = tile i), K words
   uint32_t* ntl;    // [2][ndirs][32] neighbour tile + 1 of each lane's tile, by chunk parity
   uint32_t* G;      // [32][E] word holding the neighbour byte of link e for tile i, where tile i's
                     // neighbour tile lies outside the chunk (this chunk's gathers)
   uint32_t* lj2;    // [E] link e: its cell in the neighbour tile | direction << 16
-  uint32_t* items;  // [kStreamMaxItems] link groups: first link | count - 1 << 11 | direction << 16
+  uint32_t* items;  // [kStreamMaxItems] link work items (see link_items)
   uint32_t* nitems;
+  uint32_t* slinks; // [E] the links of the short directions, handled by ballots
   uint64_t* bar;    // infull[sin], inempty[sin]
 };
 
@@ -55,8 +57,12 @@ __host__ __device__ inline size_t stream_layout(const TileParams& p, bool peer, 
   size_t off = 0;
   if (s) s->in0 = base + off;
   off += p.sin * slot;
-  if (s) s->Z = (uint32_t*)(base + off);
-  off += align16((size_t)(p.K + p.E + 1) * 4);
+  const size_t zn = align16((size_t)(p.K + p.E + 1) * 4) / 4;
+  if (s) {
+    s->Z0 = (uint32_t*)(base + off);
+    s->zn = (uint32_t)zn;
+  }
+  off += 2 * zn * 4;
   if (s) s->Wn = (uint32_t*)(base + off);
   off += peer ? align16((size_t)p.K * 4) : 0;
   if (s) s->ntl = (uint32_t*)(base + off);
@@ -69,12 +75,19 @@ __host__ __device__ inline size_t stream_layout(const TileParams& p, bool peer, 
   off += (size_t)kStreamMaxItems * 4;
   if (s) s->nitems = (uint32_t*)(base + off);
   off += 16;
+  if (s) s->slinks = (uint32_t*)(base + off);
+  off += align16((size_t)(p.E ? p.E : 1) * 4);
   if (s) s->bar = (uint64_t*)(base + off);
   off += (size_t)2 * p.sin * 8;
   return align16(off);
 }
 
 size_t stream_smem_bytes(const TileParams& p, bool peer) { return stream_layout(p, peer, nullptr, nullptr); }
+
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(v));
+  return v;
+}
 
 __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;" ::"r"(kStreamNW * 32) : "memory");
@@ -114,11 +127,45 @@ __device__ __forceinline__ void cp_async4_if(uint32_t dst, const void* src, uint
       : "memory");
 }
 
-// Link groups: the links of one direction d (sorted by direction), 32 at a time; lane = link.
+// Link work items.  A GROUP item (bit 31 clear: first link | count - 1 << 11 | direction << 16)
+// holds up to 32 links of one long direction d (links are sorted by direction); lane = link.
 // Tiles of a chunk are lanes of the bit-sliced words, and a direction's neighbour tiles are the same
 // for all its links, so per (group, tile) the work is uniform across the warp: the in-chunk part of
 // a link word is a few masked rotations of the neighbour cell's Z word (one per distinct lane
-// offset rel - i), the out-of-chunk part one gathered word per outside tile.
+// offset rel - i), the out-of-chunk part one gathered word per outside tile.  A BALLOT item (bit 31
+// set: first index into slinks | count - 1 << 11) holds the links of the short directions (a
+// corner's single link), lane = tile, one ballot per link.  Items are built so that their number
+// stays at most one per warp where possible (link_items).
+constexpr uint32_t kBallotItem = 1u << 31;
+constexpr uint32_t kLongDirection = 8;  // links per direction from which a direction gets group items
+
+__device__ void link_items(const TileParams& p, const StreamSmem& S) {  // one thread, at launch
+  uint32_t n = 0, ns = 0;
+  for (uint32_t d = 0; d < p.ndirs; ++d) {
+    const uint32_t e0 = p.dir_start[d], e1 = p.dir_start[d + 1], nd = e1 - e0;
+    if (nd == 0) continue;
+    if (nd < kLongDirection) {
+      for (uint32_t e = e0; e < e1; ++e) S.slinks[ns++] = e;
+      continue;
+    }
+    const uint32_t ng = (nd + 31) / 32;  // groups of balanced sizes
+    for (uint32_t k = 0, e = e0; k < ng; ++k) {
+      const uint32_t m = (nd - (e - e0) + (ng - k) - 1) / (ng - k);
+      S.items[n++] = e | ((m - 1u) << 11) | (d << 16);
+      e += m;
+    }
+  }
+  // the short directions' links in ballot items: as many as the warps left over allow (at least one)
+  const uint32_t free_w = n < (uint32_t)kStreamNW ? (uint32_t)kStreamNW - n : 1u;
+  const uint32_t nb = ns == 0 ? 0u : min(ns, free_w);
+  for (uint32_t k = 0, i = 0; k < nb; ++k) {
+    const uint32_t m = (ns - i + (nb - k) - 1) / (nb - k);
+    S.items[n++] = kBallotItem | i | ((m - 1u) << 11);
+    i += m;
+  }
+  *S.nitems = n;
+}
+
 struct LinkGroup {
   uint32_t e;      // this lane's link (valid lanes: lane < n)
   uint32_t j2;     // its cell in the neighbour tile
@@ -129,23 +176,37 @@ struct LinkGroup {
 __device__ __forceinline__ LinkGroup link_group(const StreamSmem& S, uint32_t item, int lane) {
   LinkGroup g;
   const uint32_t e0 = item & 0x7FFu, n = ((item >> 11) & 31u) + 1u;
-  g.d = item >> 16;
+  g.d = (item >> 16) & 0xFFu;
   g.valid = (uint32_t)lane < n;
   g.e = e0 + (g.valid ? (uint32_t)lane : 0u);
   g.j2 = S.lj2[g.e] & 0xFFFFu;
   return g;
 }
 
-// Item k = warp cw, cw + NW, ...: for every tile i of chunk c whose neighbour tile in the group's
+// Item k = warp cw, cw + NW, ...: for every tile i of chunk c whose neighbour tile in the item's
 // direction lies outside the chunk, the 4-byte word holding the neighbour cell of each of the
-// group's links (lane = link), by cp.async (or, for another shard's tile, from the halo).  The
+// item's links, into G[i][e], by cp.async (or, for another shard's tile, from the halo).  The
 // same warp consumes them in Phase B of chunk c.  Tile indices fit 32 bits (checked on the host).
 __device__ __forceinline__ void link_prefetch(const TileParams& p, const StreamSmem& S, const uint32_t* ntl,
                                               const ChunkInfo& c, const uint8_t* __restrict__ cur, int cw, int lane) {
   const uint32_t t0 = (uint32_t)c.t0, tlo = (uint32_t)p.tile_lo, nloc = (uint32_t)(p.tile_hi - p.tile_lo);
   const uint32_t ni = *S.nitems, E = p.E;
   for (uint32_t k = (uint32_t)cw; k < ni; k += kStreamNW) {
-    const LinkGroup g = link_group(S, S.items[k], lane);
+    const uint32_t item = S.items[k];
+    if (item & kBallotItem) {  // lane = tile, link by link
+      const uint32_t i0 = item & 0x7FFu, n = ((item >> 11) & 31u) + 1u;
+      const uint32_t gs = smem_u32(S.G) + 4u * (uint32_t)lane * E;
+      for (uint32_t i = i0; i < i0 + n; ++i) {
+        const uint32_t e = S.slinks[i], le = S.lj2[e], j2 = le & 0xFFFFu;
+        const uint32_t a1 = ntl[(le >> 16) * kChunkTiles + lane];
+        const uint32_t tl = a1 - 1u - tlo;
+        const bool out = a1 != 0u && a1 - 1u - t0 >= c.nt;
+        if (out && tl >= nloc) S.G[lane * E + e] = fetch_cell(cur, (uint64_t)(a1 - 1u) * p.K + j2, p.halo) << (8 * (j2 & 3u));
+        else cp_async4_if(gs + 4u * e, cur + (uint64_t)(out ? tl : 0u) * p.Kp + (j2 & ~3u), out ? 1u : 0u);
+      }
+      continue;
+    }
+    const LinkGroup g = link_group(S, item, lane);
     const uint32_t a1 = ntl[g.d * kChunkTiles + lane];  // lane = tile here: neighbour tile + 1 (0 = none)
     const uint32_t tl = a1 - 1u - tlo;
     const bool out = a1 != 0u && a1 - 1u - t0 >= c.nt;
@@ -167,18 +228,32 @@ __device__ __forceinline__ void link_prefetch(const TileParams& p, const StreamS
 }
 
 // Phase B for item k of chunk c: link word e (bit i = neighbour cell of tile i) -> Z[K + e].
-__device__ __forceinline__ void link_words(const TileParams& p, const StreamSmem& S, const uint32_t* ntl,
-                                           const ChunkInfo& c, int cw, int lane) {
+__device__ __forceinline__ void link_words(const TileParams& p, const StreamSmem& S, uint32_t* Z,
+                                           const uint32_t* ntl, const ChunkInfo& c, int cw, int lane) {
   const uint32_t t0 = (uint32_t)c.t0, ni = *S.nitems, E = p.E, K = (uint32_t)p.K;
   for (uint32_t k = (uint32_t)cw; k < ni; k += kStreamNW) {
-    const LinkGroup g = link_group(S, S.items[k], lane);
+    const uint32_t item = S.items[k];
+    if (item & kBallotItem) {  // lane = tile, one ballot per link
+      const uint32_t i0 = item & 0x7FFu, n = ((item >> 11) & 31u) + 1u;
+      for (uint32_t i = i0; i < i0 + n; ++i) {
+        const uint32_t e = S.slinks[i], le = S.lj2[e], j2 = le & 0xFFFFu;
+        const uint32_t a1 = ntl[(le >> 16) * kChunkTiles + lane];
+        const uint32_t rel = a1 - 1u - t0;
+        const bool inside = a1 != 0u && rel < c.nt;
+        const uint32_t v = inside ? Z[j2] >> (rel & 31u) : a1 != 0u ? S.G[lane * E + e] >> (8u * (j2 & 3u)) : 0u;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v & 1u);
+        if (lane == 0) Z[K + e] = bal;
+      }
+      continue;
+    }
+    const LinkGroup g = link_group(S, item, lane);
     const uint32_t a1 = ntl[g.d * kChunkTiles + lane];  // lane = tile
     const uint32_t rel = a1 - 1u - t0;
     const bool present = a1 != 0u, inside = present && rel < c.nt;
     const uint32_t dl = (rel - (uint32_t)lane) & 31u;  // tile i's neighbour is tile i + dl (mod 32)
     uint32_t im = __ballot_sync(0xFFFFFFFFu, inside);
     uint32_t om = __ballot_sync(0xFFFFFFFFu, present && !inside);
-    const uint32_t z = S.Z[g.j2];  // lane = link from here on
+    const uint32_t z = Z[g.j2];  // lane = link from here on
     uint32_t w = 0;
     while (im) {  // tiles with the same offset: one masked rotation
       const uint32_t dd = __shfl_sync(0xFFFFFFFFu, dl, __ffs(im) - 1u);
@@ -187,12 +262,15 @@ __device__ __forceinline__ void link_words(const TileParams& p, const StreamSmem
       w |= __funnelshift_r(z, z, dd) & m;
     }
     const uint32_t gs = smem_u32(S.G) + 4u * g.e, sh = 8u * (g.j2 & 3u);
-    while (om) {  // tiles whose neighbour tile is outside the chunk: the gathered words
+    while (om) {  // tiles whose neighbour tile is outside the chunk: the gathered words, two at a time
       const uint32_t i = __ffs(om) - 1u;
       om &= om - 1u;
-      w |= ((lds32(gs + i * (E * 4u)) >> sh) & 1u) << i;
+      const uint32_t i2 = om ? __ffs(om) - 1u : i;
+      om &= om - 1u;
+      const uint32_t g1 = lds32(gs + i * (E * 4u)), g2 = lds32(gs + i2 * (E * 4u));
+      w |= (((g1 >> sh) & 1u) << i) | (((g2 >> sh) & 1u) << i2);
     }
-    if (g.valid) S.Z[K + g.e] = w;
+    if (g.valid) Z[K + g.e] = w;
   }
 }
 
@@ -220,12 +298,9 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
 
   for (uint32_t e = tid; e < E; e += blockDim.x) S.lj2[e] = p.link_j2[e] | ((uint32_t)p.link_dir[e] << 16);
   if (tid == 0) {
-    uint32_t n = 0;  // link groups: each direction's links, 32 at a time
-    for (uint32_t d = 0; d < p.ndirs; ++d)
-      for (uint32_t e = p.dir_start[d]; e < p.dir_start[d + 1]; e += 32)
-        S.items[n++] = e | ((min(32u, p.dir_start[d + 1] - e) - 1u) << 11) | (d << 16);
-    *S.nitems = n;
-    S.Z[p.zslot] = 0;
+    link_items(p, S);
+    S.Z0[p.zslot] = 0;
+    S.Z0[S.zn + p.zslot] = 0;
     for (uint32_t i = 0; i < NIN; ++i) {
       mbar_init(&infull[i], 1);
       mbar_init(&inempty[i], kStreamNW);
@@ -254,12 +329,22 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
               "l"(&tm_in), "r"(x0 + h * (int32_t)kStreamBox), "r"(row), "r"(bar)
               : "memory");
       };
+      auto prefetch = [&](uint32_t s) {  // slice s into L2 (the slice after the one just issued: the next
+        const uint32_t q = s % nsl;      // chunk's last slice otherwise waits for its slot at full latency)
+        const int32_t row = (int32_t)((blockIdx.x + (uint64_t)(s / nsl) * G) * kChunkTiles), x0 = (int32_t)(q * kStreamSW);
+        for (int h = 0; h < 2; ++h)
+          asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(&tm_in),
+                       "r"(x0 + h * (int32_t)kStreamBox), "r"(row)
+                       : "memory");
+      };
       uint32_t ld = 0;
       for (; ld < NIN && ld < total; ++ld) load(ld);
+      if (ld < total) prefetch(ld);
       // Phase A frees the input slots one slice at a time; each freed slot takes the slice NIN ahead
       for (; ld < total; ++ld) {
         mbar_wait(&inempty[ld % NIN], ((ld - NIN) / NIN) & 1);
         load(ld);
+        if (ld + 1 < total) prefetch(ld + 1);
       }
     }
     return;
@@ -275,9 +360,28 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
     const uint32_t j = ((uint32_t)i * kStreamNW + (uint32_t)cw) * 32 + my_jj;
     rows[i] = j < K ? __ldg(reinterpret_cast<const uint4*>(p.nbr) + j) : make_uint4(0, 0, 0, 0);
   }
-  const uint32_t z_s = smem_u32(S.Z);
+  // slices q < RB whose block reads a link word (a neighbour slot in [K, K + E)): done after the
+  // link words are published; link-free blocks first, so early warps overlap the link phase
+  uint32_t lmask = 0;
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    const uint32_t lo = 4u * K, hi = 4u * (K + E);
+    const uint4 r = rows[i];
+    const uint32_t v[8] = {r.x & 0xFFFFu, r.x >> 16, r.y & 0xFFFFu, r.y >> 16,
+                           r.z & 0xFFFFu, r.z >> 16, r.w & 0xFFFFu, r.w >> 16};
+    bool dep = false;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dep |= v[k] >= lo && v[k] < hi;
+    if (__any_sync(0xFFFFFFFFu, dep)) lmask |= 1u << i;
+  }
   const uint32_t ntl_words = (p.ndirs ? p.ndirs : 1) * kChunkTiles;
   bool peer_sent = false;
+  // Phase A per-lane constants (opaque, so ptxas keeps them instead of re-deriving them per slice):
+  // the lane's two 16-byte units of its warp's j-block in slot 0, and its cell within a slice
+  const uint32_t ja = (uint32_t)cw * 32, jl = ja + my_jj, za = opaque_u32(4 * jl);
+  const uint32_t na = opaque_u32(KP32 > ja ? KP32 - ja : 0u), nl = opaque_u32(K > jl ? K - jl : 0u);
+  const uint32_t pa0 = opaque_u32(in_base + (uint32_t)lane * kStreamBox + box_off(ja));
+  const uint32_t pa1 = opaque_u32(in_base + (uint32_t)lane * kStreamBox + box_off(ja + 16));
   {  // prologue: adjacency of the first two chunks, the first chunk's link gathers
     adj_prefetch(p, S.ntl, chunk_info(p, blockIdx.x), cw, lane);
     if (blockIdx.x + G < p.nchunks) adj_prefetch(p, S.ntl + ntl_words, chunk_info(p, blockIdx.x + G), cw, lane);
@@ -290,21 +394,20 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
   for (uint64_t chunk = blockIdx.x; chunk < p.nchunks; chunk += G, seq += nsl, ++it) {
     const ChunkInfo c = chunk_info(p, chunk);
     uint32_t* ntl = S.ntl + (it & 1) * ntl_words;
+    uint32_t* Zb = S.Z0 + (it & 1) * S.zn;  // double-buffered: no barrier between C+D and the next Phase A
+    const uint32_t z_s = smem_u32(Zb);
     uint32_t pe0 = 0, pe1 = 0;
     if (PEER && cw == kStreamNW - 1) {
       pe0 = p.peer_chunk_start[chunk];
       pe1 = p.peer_chunk_start[chunk + 1];
     }
     // Phase A: slice q, j-block q * NW + cw -> Z
-    for (uint32_t q = 0; q < nsl; ++q) {
+    for (uint32_t q = 0, qc = 0, zq = z_s + za; q < nsl; ++q, qc += kStreamSW, zq += 4 * kStreamSW) {
       const uint32_t s = seq + q, slot = s % NIN;
       mbar_wait(&infull[slot], (s / NIN) & 1);
-      const uint32_t jb = q * kStreamNW + (uint32_t)cw;
-      if (jb < nblk) {
-        const uint32_t a = in_base + slot * slot_bytes + (uint32_t)lane * kStreamBox;
-        const uint32_t x = tr(pack01(lds128(a + box_off(cw * 32)), lds128(a + box_off(cw * 32 + 16))));
-        const uint32_t j = jb * 32 + my_jj;
-        if (j < K) sts32(z_s + 4 * j, x);
+      if (qc < na) {  // this warp's j-block exists in slice q
+        const uint32_t x = tr(pack01(lds128(pa0 + slot * slot_bytes), lds128(pa1 + slot * slot_bytes)));
+        if (qc < nl) sts32(zq, x);  // cell j < K
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&inempty[slot]);
@@ -313,20 +416,17 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
     consumers_sync();     // Z, R and both adjacency buffers visible to every consumer warp
 
     // Phase B: link words, by link groups (lane = link)
-    link_words(p, S, ntl, c, cw, lane);
-    consumers_sync();  // link words published; G and this chunk's adjacency buffer are free
-    if (chunk + 2 * G < p.nchunks) adj_prefetch(p, ntl, chunk_info(p, chunk + 2 * G), cw, lane);
-    if (chunk + G < p.nchunks) link_prefetch(p, S, S.ntl + ((it + 1) & 1) * ntl_words, chunk_info(p, chunk + G), cur, cw, lane);
+    link_words(p, S, Zb, ntl, c, cw, lane);
 
     // Phase C+D: j-block q * NW + cw -> HBM (lane = tile: one 256-bit store of its 32 cells)
     const uint32_t live_lanes = c.nt >= 32 ? 0xFFFFFFFFu : ((1u << c.nt) - 1u);
     uint8_t* tile_out = next + (uint64_t)((uint32_t)(c.t0 - p.tile_lo) + (uint32_t)lane) * Kp;
-    auto slice_out = [&](uint32_t q, const uint4& row) {
-      const uint32_t jb = q * kStreamNW + (uint32_t)cw;
-      if (jb < nblk) {
-        const uint32_t j = jb * 32 + my_jj;
+    const uint32_t zA = z_s + za;  // Z word of this lane's cell in slice 0
+    uint8_t* const outA = tile_out + ja;
+    auto slice_out = [&](uint32_t qc, const uint4& row) {  // qc: the block's cell offset from this warp's
+      if (qc < na) {                                       // block of slice 0 (q * NW * 32 unless rotated)  // this warp's j-block exists in slice q
         uint32_t nw = 0;
-        if (j < K) {
+        if (qc < nl) {  // cell j < K
           uint32_t x[8];
           x[0] = lds32(z_s + (row.x & 0xFFFFu));
           x[1] = lds32(z_s + (row.x >> 16));
@@ -358,27 +458,37 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
             c2 = ke ^ kf;
             c3 = ke & kf;
           }
-          const uint32_t alive = lds32(z_s + 4 * j);
+          const uint32_t alive = lds32(zA + 4 * qc);
           if (CONWAY) nw = c1 & ~c2 & ~c3 & (c0 | alive);  // B3/S23
           else nw = (alive & rule_bits(p.survive, c0, c1, c2, c3)) | (~alive & rule_bits(p.birth, c0, c1, c2, c3));
           nw &= live_lanes;
-          if (PEER) S.Wn[j] = nw;
+          if (PEER) S.Wn[jl + qc] = nw;
         }
         const uint32_t xb = tr(nw);  // bit 8p+m = cell jb*32 + 4m + p of this lane's tile (0 past K)
         const uint32_t m = 0x01010101u;
         if ((uint32_t)lane < c.nt)  // Kp = round_up(K, 32): the block's 32 bytes are one aligned sector
-          stg256(tile_out + jb * 32, xb & m, (xb >> 1) & m, (xb >> 2) & m, (xb >> 3) & m, (xb >> 4) & m,
+          stg256(outA + qc, xb & m, (xb >> 1) & m, (xb >> 2) & m, (xb >> 3) & m, (xb >> 4) & m,
                  (xb >> 5) & m, (xb >> 6) & m, (xb >> 7) & m);
       }
     };
 #pragma unroll
-    for (int i = 0; i < RB; ++i)
-      if ((uint32_t)i < nsl) slice_out((uint32_t)i, rows[i]);
+    for (int i = 0; i < RB; ++i)  // link-free blocks
+      if ((uint32_t)i < nsl && !((lmask >> i) & 1u)) slice_out((uint32_t)i * kStreamSW, rows[i]);
+    consumers_sync();  // link words published; G and this chunk's adjacency buffer are free
+    if (chunk + 2 * G < p.nchunks) adj_prefetch(p, ntl, chunk_info(p, chunk + 2 * G), cw, lane);
+    if (chunk + G < p.nchunks) link_prefetch(p, S, S.ntl + ((it + 1) & 1) * ntl_words, chunk_info(p, chunk + G), cur, cw, lane);
+#pragma unroll
+    for (int i = 0; i < RB; ++i)  // blocks reading link words
+      if ((uint32_t)i < nsl && ((lmask >> i) & 1u)) slice_out((uint32_t)i * kStreamSW, rows[i]);
     for (uint32_t q = RB; q < nsl; ++q) {
-      const uint32_t j = (q * kStreamNW + (uint32_t)cw) * 32 + my_jj;
-      slice_out(q, j < K ? __ldg(reinterpret_cast<const uint4*>(p.nbr) + j) : make_uint4(0, 0, 0, 0));
+      // a partial last slice (r < NW blocks) goes to the LAST r warps here (Phase A gave it to the
+      // first r), so every warp carries the same number of blocks per chunk
+      const uint32_t r = nblk - q * kStreamNW, sh = q + 1 == nsl && r < kStreamNW ? kStreamNW - r : 0u;
+      if ((uint32_t)cw < sh) continue;
+      const uint32_t qc = q * kStreamSW - sh * 32, j = jl + qc;
+      slice_out(qc, j < K ? __ldg(reinterpret_cast<const uint4*>(p.nbr) + j) : make_uint4(0, 0, 0, 0));
     }
-    consumers_sync();  // Z (and Wn) no longer read: the next chunk may overwrite them
+    if (PEER) consumers_sync();  // the chunk's new state words Wn complete for the halo epilogue
     if (PEER && cw == kStreamNW - 1 && pe1 > pe0) {
       // fused halo: the chunk's send cells, from the new state words, straight into the peers' buffers
       for (uint32_t e = pe0 + (uint32_t)lane; e < pe1; e += 32) {
