@@ -513,10 +513,11 @@ static StreamFn pick_stream_r(const TileParams& p) {
 }
 
 // RB = slices whose neighbour rows stay in registers: 8 at one CTA per SM (carpet level 4: 8 of
-// its 9 slices), 2 at two CTAs per SM (64 registers).
+// its 9 slices), 1 at two CTAs per SM (64 registers; empty bottles level 4: 0.82 ms against 0.90
+// with 2, which spills).
 template <bool PEER>
 static StreamFn pick_stream_t(const TileParams& p, int minb) {
-  if (minb >= 2) return pick_stream_r<PEER, 2, 2, 4>(p);
+  if (minb >= 2) return pick_stream_r<PEER, 1, 2, 4>(p);
   return p.sin >= 8 ? pick_stream_r<PEER, 8, 1, 8>(p) : pick_stream_r<PEER, 8, 1, 4>(p);
 }
 
