@@ -24,6 +24,10 @@ namespace sqz {
 // Results go straight from registers to HBM (coalesced 512-byte warp stores): no output staging
 // and one CTA barrier per chunk.
 constexpr uint32_t kAdjSlots = 4;
+constexpr uint32_t kPackMaxItems = 64;
+constexpr uint32_t kPackBallotItem = 1u << 31;
+constexpr uint32_t kPackLongDirection = 8;
+constexpr uint32_t kSlotBatch = 4;  // link slots per pass in the slot split (Sierpinski: 32 slots, 8 warps)
 
 __host__ __device__ inline uint32_t pack_zw(const TileParams& p) { return (p.Kw + p.E + 1) * 4; }
 
@@ -35,6 +39,8 @@ struct PackSmem {
   uint32_t* sl;   // [4E] link slot u = 4e + q: j2 << 10 | (direction * 128 + 32 q)
   uint32_t* dp;   // [4 ndirs] direction pair v = 4d + q: first link << 16 | one past the last
   uint64_t* bar;  // [pstages] state copies landed, then [kAdjSlots] adjacency copies landed
+  uint32_t* items;   // [kPackMaxItems] link work items (BYDIR, see pack_link_items), then the count
+  uint32_t* slinks;  // [E] the links of the short directions (ballot items)
   uint32_t ndirs, ns;
   __device__ __forceinline__ uint32_t* Z(uint32_t s) const { return Z0 + s * zw; }
   __device__ __forceinline__ const uint32_t* ntl(uint32_t a) const { return A0 + a * ndirs * kPackTiles; }
@@ -62,6 +68,10 @@ __host__ __device__ inline size_t packed_layout(const TileParams& p, uint8_t* ba
   off += align16((size_t)(p.ndirs ? 4 * p.ndirs : 1) * 4);
   if (s) s->bar = (uint64_t*)(base + off);
   off += (ns + kAdjSlots) * 8;
+  if (s) s->items = (uint32_t*)(base + off);
+  off += (kPackMaxItems + 4) * 4;
+  if (s) s->slinks = (uint32_t*)(base + off);
+  off += align16((size_t)(p.E ? p.E : 1) * 4);
   return align16(off);
 }
 
@@ -127,6 +137,7 @@ __device__ __forceinline__ void chunk_prefetch_slots(const TileParams& p, const 
                                                const uint32_t* ntl, const uint32_t* __restrict__ cur32, int warp,
                                                int nwarps, int lane) {
   const uint32_t E = prefetch_links(p);
+#pragma unroll 4
   for (uint32_t u = (uint32_t)warp; u < 4 * E; u += (uint32_t)nwarps) {
     const uint32_t sl = S.sl[u];
     const uint32_t a1 = ntl[(sl & 1023u) + lane];
@@ -139,6 +150,136 @@ __device__ __forceinline__ void chunk_prefetch_slots(const TileParams& p, const 
     }
   }
   cp_async_commit();
+}
+
+// BYDIR link work items (link-heavy fractals, prefetched links).  A GROUP item (bit 31 clear: first
+// link | count - 1 << 11 | direction << 16) holds up to 32 links of one long direction; lane = link.
+// A direction's neighbour tiles are the same for all its links, so per (group, lane group q, tile)
+// the work is warp-uniform: the in-chunk part of a link word is a few masked rotations of the
+// neighbour cell's state word (one per distinct (source lane group, offset) of the tiles of q),
+// the out-of-chunk part one gathered word per outside tile.  A BALLOT item (bit 31 set: first index
+// into slinks | count - 1 << 11) holds links of the short directions (a corner's single link),
+// lane = tile, one ballot per (link, q).  R holds the gathers as [tile t of the chunk][link e].
+__device__ void pack_link_items(const TileParams& p, const PackSmem& S, uint32_t nwarps) {  // one thread
+  uint32_t n = 0, ns = 0;
+  for (uint32_t d = 0; d < p.ndirs; ++d) {
+    const uint32_t e0 = p.dir_start[d], e1 = p.dir_start[d + 1], nd = e1 - e0;
+    if (nd == 0) continue;
+    if (nd < kPackLongDirection) {
+      for (uint32_t e = e0; e < e1; ++e) S.slinks[ns++] = e;
+      continue;
+    }
+    const uint32_t ng = (nd + 31) / 32;  // groups of balanced sizes
+    for (uint32_t k = 0, e = e0; k < ng; ++k) {
+      const uint32_t m = (nd - (e - e0) + (ng - k) - 1) / (ng - k);
+      S.items[n++] = e | ((m - 1u) << 11) | (d << 16);
+      e += m;
+    }
+  }
+  const uint32_t free_w = n < nwarps ? nwarps - n : 1u;  // short links: one ballot item per idle warp
+  const uint32_t nb = ns == 0 ? 0u : min(ns, free_w);
+  for (uint32_t k = 0, i = 0; k < nb; ++k) {
+    const uint32_t m = (ns - i + (nb - k) - 1) / (nb - k);
+    S.items[n++] = kPackBallotItem | i | ((m - 1u) << 11);
+    i += m;
+  }
+  S.items[kPackMaxItems] = n;
+}
+
+template <bool SHARDED>
+__device__ __forceinline__ void chunk_prefetch_items(const TileParams& p, const PackSmem& S, const PackChunk& pc,
+                                                     const uint32_t* ntl, const uint32_t* __restrict__ cur32,
+                                                     int warp, int nwarps, int lane) {
+  const uint32_t E = p.E, ni = S.items[kPackMaxItems], tlo = (uint32_t)p.tile_lo, Kw = p.Kw;
+  const uint32_t nloc = (uint32_t)(p.tile_hi - p.tile_lo), gs0 = smem_u32(S.R);
+  for (uint32_t k = (uint32_t)warp; k < ni; k += (uint32_t)nwarps) {
+    const uint32_t item = S.items[k], i0 = item & 0x7FFu, n = ((item >> 11) & 31u) + 1u;
+    if (item & kPackBallotItem) {  // lane = tile, link by link
+      for (uint32_t i = i0; i < i0 + n; ++i) {
+        const uint32_t e = S.slinks[i], d = p.link_dir[e], j2 = p.link_j2[e];
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) {
+          const uint32_t a1 = ntl[d * kPackTiles + q * 32 + lane], tl = a1 - 1u - tlo, t = q * 32 + lane;
+          const bool out = a1 != 0 && a1 - 1u - pc.t0 >= pc.nt;
+          if (SHARDED && out && tl >= nloc) S.R[t * E + e] = halo_fetch(p.halo, (uint64_t)(a1 - 1u) * p.K + j2) << (tl & 31u);
+          else cp_async4_if(gs0 + 4u * (t * E + e), cur32 + ((uint64_t)((out ? tl : 0u) >> 7) * Kw + j2) * 4 + ((tl >> 5) & 3u),
+                            out ? 1u : 0u);
+        }
+      }
+      continue;
+    }
+    const uint32_t d = item >> 16, valid = (uint32_t)lane < n ? 1u : 0u;
+    const uint32_t e = i0 + (valid ? (uint32_t)lane : 0u), j2 = p.link_j2[e];
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+      const uint32_t a1 = ntl[d * kPackTiles + q * 32 + lane], tl = a1 - 1u - tlo;  // lane = tile here
+      const bool out = a1 != 0 && a1 - 1u - pc.t0 >= pc.nt;
+      uint32_t om = __ballot_sync(0xFFFFFFFFu, out);
+      const uint32_t farm = SHARDED ? __ballot_sync(0xFFFFFFFFu, out && tl >= nloc) : 0u;
+      while (om) {  // lane = link from here on
+        const uint32_t i = __ffs(om) - 1u;
+        om &= om - 1u;
+        const uint32_t tli = __shfl_sync(0xFFFFFFFFu, tl, i), t = q * 32 + i;
+        if (!SHARDED || !((farm >> i) & 1u))
+          cp_async4_if(gs0 + 4u * (t * E + e), cur32 + ((uint64_t)(tli >> 7) * Kw + j2) * 4 + ((tli >> 5) & 3u), valid);
+        else if (valid)  // another shard's tile (sharded contexts): the bit from the halo, placed where it is read
+          S.R[t * E + e] = halo_fetch(p.halo, (uint64_t)(tli + tlo) * p.K + j2) << (tli & 31u);
+      }
+    }
+  }
+  cp_async_commit();
+}
+
+// Link words of chunk pc (BYDIR items): bit i of u32 lane q of word Kw + e = cell j2 of the
+// neighbour tile (link e) of tile 32q + i.
+__device__ __forceinline__ void chunk_link_items(const TileParams& p, const PackSmem& S, const PackChunk& pc,
+                                                 const uint32_t* ntl, uint32_t* Z, int warp, int nwarps, int lane) {
+  const uint32_t E = p.E, ni = S.items[kPackMaxItems], tlo = (uint32_t)p.tile_lo, Kw = p.Kw;
+  for (uint32_t k = (uint32_t)warp; k < ni; k += (uint32_t)nwarps) {
+    const uint32_t item = S.items[k], i0 = item & 0x7FFu, n = ((item >> 11) & 31u) + 1u;
+    if (item & kPackBallotItem) {  // lane = tile, one ballot per (link, q)
+      for (uint32_t i = i0; i < i0 + n; ++i) {
+        const uint32_t e = S.slinks[i], d = p.link_dir[e], j2 = p.link_j2[e];
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) {
+          const uint32_t a1 = ntl[d * kPackTiles + q * 32 + lane], rel = a1 - 1u - pc.t0, tl = a1 - 1u - tlo;
+          const bool in = rel < pc.nt;
+          const uint32_t v = a1 == 0 ? 0u : in ? Z[j2 * 4 + (rel >> 5)] >> (rel & 31u) : S.R[(q * 32 + lane) * E + e] >> (tl & 31u);
+          const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v & 1u);
+          if (lane == 0) Z[(Kw + e) * 4 + q] = bal;
+        }
+      }
+      continue;
+    }
+    const uint32_t d = item >> 16, valid = (uint32_t)lane < n ? 1u : 0u;
+    const uint32_t e = i0 + (valid ? (uint32_t)lane : 0u), j2 = p.link_j2[e];
+    const uint4 z = *reinterpret_cast<const uint4*>(Z + j2 * 4);  // the neighbour cell's word, all 128 tiles
+    uint32_t w4[4];
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+      const uint32_t a1 = ntl[d * kPackTiles + q * 32 + lane], rel = a1 - 1u - pc.t0, tl = a1 - 1u - tlo;  // lane = tile
+      const bool present = a1 != 0, inside = present && rel < pc.nt;
+      const uint32_t key = (rel & ~31u) | ((rel - (uint32_t)lane) & 31u);  // source lane group, offset
+      uint32_t im = __ballot_sync(0xFFFFFFFFu, inside);
+      uint32_t om = __ballot_sync(0xFFFFFFFFu, present && !inside);
+      uint32_t w = 0;
+      while (im) {  // tiles with the same (source group, offset): one masked rotation
+        const uint32_t kk = __shfl_sync(0xFFFFFFFFu, key, __ffs(im) - 1u);
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, inside && key == kk);
+        im &= ~m;
+        const uint32_t g = kk >> 5, src = g == 0 ? z.x : g == 1 ? z.y : g == 2 ? z.z : z.w;
+        w |= __funnelshift_r(src, src, kk & 31u) & m;
+      }
+      while (om) {  // tiles whose neighbour tile is outside the chunk: the gathered words
+        const uint32_t i = __ffs(om) - 1u;
+        om &= om - 1u;
+        const uint32_t sh = __shfl_sync(0xFFFFFFFFu, tl, i) & 31u;
+        w |= ((S.R[(q * 32 + i) * E + e] >> sh) & 1u) << i;
+      }
+      w4[q] = w;
+    }
+    if (valid) *reinterpret_cast<uint4*>(Z + (Kw + e) * 4) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+  }
 }
 
 template <bool SHARDED>
@@ -168,7 +309,8 @@ template <bool SHARDED, bool BYDIR>
 __device__ __forceinline__ void chunk_prefetch(const TileParams& p, const PackSmem& S, const PackChunk& pc,
                                                const uint32_t* ntl, const uint32_t* __restrict__ cur32, int warp,
                                                int nwarps, int lane) {
-  if (BYDIR) chunk_prefetch_pairs<SHARDED>(p, S, pc, ntl, cur32, warp, nwarps, lane);
+  if (BYDIR && prefetch_links(p)) chunk_prefetch_items<SHARDED>(p, S, pc, ntl, cur32, warp, nwarps, lane);
+  else if (BYDIR) chunk_prefetch_pairs<SHARDED>(p, S, pc, ntl, cur32, warp, nwarps, lane);
   else chunk_prefetch_slots<SHARDED>(p, S, pc, ntl, cur32, warp, nwarps, lane);
 }
 
@@ -233,6 +375,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
   for (uint32_t v = tid; v < 4 * p.ndirs; v += blockDim.x)
     S.dp[v] = ((uint32_t)p.dir_start[v >> 2] << 16) | p.dir_start[(v >> 2) + 1];
   if (tid == 0) {
+    if (BYDIR) pack_link_items(p, S, (uint32_t)nwarps);
     for (uint32_t s = 0; s < NS + kAdjSlots; ++s) mbar_init(&S.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -260,7 +403,13 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
 
     // link words: bit i of u32 lane q of word Kw + e = cell j2 of the neighbour tile (link e)
     // of tile 32q + i
-    if (BYDIR) {
+    if (BYDIR && Epf) {
+      if ((uint32_t)warp < S.items[kPackMaxItems]) {
+        mbar_wait(S.abar(a), (it / kAdjSlots) & 1);  // (already complete when the prefetch ran)
+        cp_async_wait_all();
+        chunk_link_items(p, S, pc, ntl, Z, warp, nwarps, lane);
+      }
+    } else if (BYDIR) {
     if ((uint32_t)warp < 4 * p.ndirs) {
       mbar_wait(S.abar(a), (it / kAdjSlots) & 1);  // (already complete when the prefetch ran)
       cp_async_wait_all();
@@ -297,23 +446,35 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
       cp_async_wait_all();
       const uint32_t rs = smem_u32(S.R) + lane * 4;
       const uint32_t ntl_s = smem_u32(ntl) + lane * 4;
-      for (uint32_t u = (uint32_t)warp; u < 4 * E; u += (uint32_t)nwarps) {
-        const uint32_t sl = S.sl[u], j2 = sl >> 10;
-        const uint32_t a1 = lds32(ntl_s + (sl & 1023u) * 4);
-        const uint32_t rel = a1 - 1u - pc.t0, tl = a1 - 1u - (uint32_t)p.tile_lo;
-        uint32_t v;
-        if (Epf) {  // branch-free: the word from this chunk's stage, or the prefetched one
-          const bool in = rel < pc.nt;
-          v = lds32(in ? zs + (j2 * 4 + (rel >> 5)) * 4 : rs + u * 128) >> ((in ? rel : tl) & 31u);
-          v &= a1 != 0 ? 1u : 0u;
-        } else {  // more links than the prefetch holds: synchronous gathers
-          v = rel < pc.nt         ? lds32(zs + (j2 * 4 + (rel >> 5)) * 4) >> (rel & 31u)
-              : a1 == 0             ? 0u
-              : !SHARDED || tl < nloc ? __ldg(cur32 + ((uint64_t)(tl >> 7) * Kw + j2) * 4 + ((tl >> 5) & 3u)) >> (tl & 31u)
-                                    : halo_fetch(p.halo, (uint64_t)(a1 - 1u) * K + j2);  // another shard's tile
+      // kSlotBatch slots per pass, their loads issued together (independent chains: the link phase
+      // sits in front of the chunk barrier, so its latency, not its instruction count, matters)
+      for (uint32_t u0 = (uint32_t)warp; u0 < 4 * E; u0 += kSlotBatch * (uint32_t)nwarps) {
+        uint32_t v[kSlotBatch];
+#pragma unroll
+        for (uint32_t k = 0; k < kSlotBatch; ++k) {
+          const uint32_t u = u0 + k * (uint32_t)nwarps;
+          v[k] = 0;
+          if (u >= 4 * E) continue;
+          const uint32_t sl = S.sl[u], j2 = sl >> 10;
+          const uint32_t a1 = lds32(ntl_s + (sl & 1023u) * 4);
+          const uint32_t rel = a1 - 1u - pc.t0, tl = a1 - 1u - (uint32_t)p.tile_lo;
+          if (Epf) {  // branch-free: the word from this chunk's stage, or the prefetched one
+            const bool in = rel < pc.nt;
+            v[k] = lds32(in ? zs + (j2 * 4 + (rel >> 5)) * 4 : rs + u * 128) >> ((in ? rel : tl) & 31u);
+            v[k] &= a1 != 0 ? 1u : 0u;
+          } else {  // more links than the prefetch holds: synchronous gathers
+            v[k] = rel < pc.nt         ? lds32(zs + (j2 * 4 + (rel >> 5)) * 4) >> (rel & 31u)
+                   : a1 == 0             ? 0u
+                   : !SHARDED || tl < nloc ? __ldg(cur32 + ((uint64_t)(tl >> 7) * Kw + j2) * 4 + ((tl >> 5) & 3u)) >> (tl & 31u)
+                                         : halo_fetch(p.halo, (uint64_t)(a1 - 1u) * K + j2);  // another shard's tile
+          }
         }
-        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v & 1u);
-        if (lane == 0) Z[(Kw + (u >> 2)) * 4 + (u & 3u)] = bal;
+#pragma unroll
+        for (uint32_t k = 0; k < kSlotBatch; ++k) {
+          const uint32_t u = u0 + k * (uint32_t)nwarps;
+          const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v[k] & 1u);
+          if (lane == 0 && u < 4 * E) Z[(Kw + (u >> 2)) * 4 + (u & 3u)] = bal;
+        }
       }
     }
     }
@@ -328,7 +489,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
     }
     if (c + G < nch) {  // out-of-chunk link gathers of the next chunk (its adjacency was issued long ago)
       const uint32_t a1 = (it + 1) & (kAdjSlots - 1);
-      if ((uint32_t)warp < (BYDIR ? 4 * p.ndirs : 4 * Epf) && Epf) mbar_wait(S.abar(a1), ((it + 1) / kAdjSlots) & 1);
+      if ((uint32_t)warp < (BYDIR ? S.items[kPackMaxItems] : 4 * Epf) && Epf) mbar_wait(S.abar(a1), ((it + 1) / kAdjSlots) & 1);
       chunk_prefetch<SHARDED, BYDIR>(p, S, pack_chunk(p, c + G), S.ntl(a1), cur32, warp, nwarps, lane);
     }
 

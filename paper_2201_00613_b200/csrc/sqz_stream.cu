@@ -119,13 +119,6 @@ __device__ __forceinline__ void adj_prefetch(const TileParams& p, uint32_t* ntl,
   cp_async_commit();
 }
 
-// 4-byte cp.async issued only where `pred` is set (a predicated instruction, no branch)
-__device__ __forceinline__ void cp_async4_if(uint32_t dst, const void* src, uint32_t pred) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p cp.async.ca.shared.global [%0], [%1], 4;\n\t}" ::"r"(dst),
-      "l"(src), "r"(pred)
-      : "memory");
-}
 
 // Link work items.  A GROUP item (bit 31 clear: first link | count - 1 << 11 | direction << 16)
 // holds up to 32 links of one long direction d (links are sorted by direction); lane = link.
