@@ -369,6 +369,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
     for (int k = 0; k < DMAX; ++k) off[i][k] = ((w[k >> 1] >> (16 * (k & 1))) & 0xFFFFu) * 16;
   }
 
+  uint32_t fullmask = 0;  // blocks i < RB whose 32 words are all cells
+#pragma unroll
+  for (int i = 0; i < RB; ++i)
+    if (((uint32_t)warp + (uint32_t)(i * nwarps) + 1) * 32 <= K) fullmask |= 1u << i;
   for (uint32_t i = tid; i < NS * 4; i += blockDim.x) S.Z(i >> 2)[(Kw + E) * 4 + (i & 3)] = 0;  // zero slot
   for (uint32_t u = tid; u < 4 * E; u += blockDim.x)
     S.sl[u] = (p.link_j2[u >> 2] << 10) | (p.link_dir[u >> 2] * kPackTiles + 32 * (u & 3u));
@@ -395,7 +399,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
   for (; c < nch; c += G, ++it, s = (s + 1 == NS) ? 0 : s + 1) {
     const PackChunk pc = pack_chunk(p, c);
     uint32_t* Z = S.Z(s);
-    const uint32_t zs = smem_u32(Z);
+    const uint32_t zs = __reduce_or_sync(0xFFFFFFFFu, smem_u32(Z));  // warp-uniform: a uniform register, folded into the LDS addresses
     const uint32_t a = it & (kAdjSlots - 1);
     const uint32_t* ntl = S.ntl(a);
     mbar_wait(&S.bar[s], (sphase >> s) & 1);
@@ -521,7 +525,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
         nw.y = cell_rule<DMAX, CONWAY>(x1, al.y, p.birth, p.survive);
         nw.z = cell_rule<DMAX, CONWAY>(x2, al.z, p.birth, p.survive);
         nw.w = cell_rule<DMAX, CONWAY>(x3, al.w, p.birth, p.survive);
-        if (pc.nt < kPackTiles) {  // the shard's last chunk only
+        // the shard's last chunk: bits of tiles past its end stay 0.  Under B3/S23 they do so anyway
+        // (their state bits and link bits are 0, so their count is 0: no birth)
+        if (!CONWAY && pc.nt < kPackTiles) {
           nw.x &= lm.x;
           nw.y &= lm.y;
           nw.z &= lm.z;
@@ -530,8 +536,36 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
       }
       outc[j] = nw;  // padding words K..Kw-1 are written 0
     };
+    auto word_full = [&](uint32_t j, const uint32_t* o) {  // a block whose 32 words are all cells (j < K)
+      uint32_t x0[DMAX], x1[DMAX], x2[DMAX], x3[DMAX];
 #pragma unroll
-    for (int i = 0; i < RB; ++i) word(((uint32_t)warp + (uint32_t)(i * nwarps)) * 32 + lane, off[i]);
+      for (int k = 0; k < DMAX; ++k) {
+        const uint4 v = lds128(zs + o[k]);
+        x0[k] = v.x;
+        x1[k] = v.y;
+        x2[k] = v.z;
+        x3[k] = v.w;
+      }
+      const uint4 al = lds128(zs + j * 16);
+      uint4 nw;
+      nw.x = cell_rule<DMAX, CONWAY>(x0, al.x, p.birth, p.survive);
+      nw.y = cell_rule<DMAX, CONWAY>(x1, al.y, p.birth, p.survive);
+      nw.z = cell_rule<DMAX, CONWAY>(x2, al.z, p.birth, p.survive);
+      nw.w = cell_rule<DMAX, CONWAY>(x3, al.w, p.birth, p.survive);
+      if (!CONWAY && pc.nt < kPackTiles) {
+        nw.x &= lm.x;
+        nw.y &= lm.y;
+        nw.z &= lm.z;
+        nw.w &= lm.w;
+      }
+      outc[j] = nw;
+    };
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      const uint32_t j = ((uint32_t)warp + (uint32_t)(i * nwarps)) * 32 + lane;
+      if ((fullmask >> i) & 1u) word_full(j, off[i]);
+      else word(j, off[i]);
+    }
     for (uint32_t jb = (uint32_t)warp + (uint32_t)(RB * nwarps); jb * 32 < Kw; jb += (uint32_t)nwarps) {
       const uint32_t j = jb * 32 + lane;
       const uint4 row = j < K ? __ldg(reinterpret_cast<const uint4*>(p.nbr) + j) : make_uint4(0, 0, 0, 0);
