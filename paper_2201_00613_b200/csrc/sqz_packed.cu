@@ -451,33 +451,27 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
       const uint32_t rs = smem_u32(S.R) + lane * 4;
       const uint32_t ntl_s = smem_u32(ntl) + lane * 4;
       // kSlotBatch slots per pass, their loads issued together (independent chains: the link phase
-      // sits in front of the chunk barrier, so its latency, not its instruction count, matters)
+      // sits in front of the chunk barrier, so its latency, not its instruction count, matters).
+      // The slot split only runs with every link prefetched (E < 3 ndirs <= 24 <= kMaxPrefetchLinks).
+      const uint32_t zl = zs + 16u * Kw, m1t0 = ~pc.t0, m1tlo = ~(uint32_t)p.tile_lo, nt = pc.nt;
       for (uint32_t u0 = (uint32_t)warp; u0 < 4 * E; u0 += kSlotBatch * (uint32_t)nwarps) {
         uint32_t v[kSlotBatch];
 #pragma unroll
         for (uint32_t k = 0; k < kSlotBatch; ++k) {
-          const uint32_t u = u0 + k * (uint32_t)nwarps;
-          v[k] = 0;
-          if (u >= 4 * E) continue;
-          const uint32_t sl = S.sl[u], j2 = sl >> 10;
+          const uint32_t u0k = u0 + k * (uint32_t)nwarps, u = u0k < 4 * E ? u0k : 0u;  // branch-free: straight-line
+          const uint32_t sl = S.sl[u];                                                   // code interleaves the slots' loads
           const uint32_t a1 = lds32(ntl_s + (sl & 1023u) * 4);
-          const uint32_t rel = a1 - 1u - pc.t0, tl = a1 - 1u - (uint32_t)p.tile_lo;
-          if (Epf) {  // branch-free: the word from this chunk's stage, or the prefetched one
-            const bool in = rel < pc.nt;
-            v[k] = lds32(in ? zs + (j2 * 4 + (rel >> 5)) * 4 : rs + u * 128) >> ((in ? rel : tl) & 31u);
-            v[k] &= a1 != 0 ? 1u : 0u;
-          } else {  // more links than the prefetch holds: synchronous gathers
-            v[k] = rel < pc.nt         ? lds32(zs + (j2 * 4 + (rel >> 5)) * 4) >> (rel & 31u)
-                   : a1 == 0             ? 0u
-                   : !SHARDED || tl < nloc ? __ldg(cur32 + ((uint64_t)(tl >> 7) * Kw + j2) * 4 + ((tl >> 5) & 3u)) >> (tl & 31u)
-                                         : halo_fetch(p.halo, (uint64_t)(a1 - 1u) * K + j2);  // another shard's tile
-          }
+          const uint32_t rel = a1 + m1t0;  // neighbour tile - t0 (a1 = tile + 1)
+          const bool in = rel < nt;
+          const uint32_t w = lds32(in ? zs + (sl >> 10) * 16 + ((rel >> 3) & ~3u) : rs + u * 128);
+          const uint32_t sh = in ? rel : a1 + m1tlo;
+          v[k] = a1 != 0 && u0k < 4 * E ? (w >> (sh & 31u)) & 1u : 0u;
         }
 #pragma unroll
         for (uint32_t k = 0; k < kSlotBatch; ++k) {
           const uint32_t u = u0 + k * (uint32_t)nwarps;
-          const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v[k] & 1u);
-          if (lane == 0 && u < 4 * E) Z[(Kw + (u >> 2)) * 4 + (u & 3u)] = bal;
+          const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v[k] != 0);
+          if (lane == 0 && u < 4 * E) sts32(zl + 4 * u, bal);
         }
       }
     }
