@@ -39,7 +39,10 @@ CASES = [("sierpinski-triangle", 0, 0), ("sierpinski-triangle", 1, 1), ("sierpin
          ("sierpinski-triangle", 5, 2), ("sierpinski-triangle", 8, 0), ("sierpinski-triangle", 10, 6),
          ("sierpinski-triangle", 11, 7), ("sierpinski-triangle", 12, 5), ("sierpinski-carpet", 4, 3),
          ("sierpinski-carpet", 5, 2), ("vicsek", 5, 4), ("empty-bottles", 5, 3), ("full-square", 7, 3),
-         ("sierpinski-triangle", 14, 3), ("sierpinski-carpet", 6, 2)]
+         ("sierpinski-triangle", 14, 3), ("sierpinski-carpet", 6, 2),
+         # link items (lane = link) over many chunks: carpet level 3 (27 links per side, the
+         # configs[3] level), empty bottles level 3/4, Vicsek level 5 (two link groups per side)
+         ("sierpinski-carpet", 7, 3), ("empty-bottles", 7, 3), ("empty-bottles", 8, 4), ("vicsek", 9, 5)]
 
 
 @pytest.mark.parametrize("name,r,g", CASES)
@@ -305,3 +308,34 @@ def test_run_host_packed_round_trip():
     dev = p.new_packed()
     dev[:g.packed_bytes // 4] = h.cuda()
     assert np.array_equal(cells(p, dev), want)
+
+
+@pytest.mark.parametrize("name,r,g", [("sierpinski-carpet", 10, 3), ("empty-bottles", 11, 4)])
+def test_packed_config3_full_size(name, r, g):
+    """BASELINE configs[3] on the packed state at the bench's tile levels (1.07e9 / 1.98e9 cells):
+    step 1 from the seed equals the byte path's step 1 (itself checked against the oracle in
+    test_gpu_stream), and step 2 is checked against the oracle at 2e5 sampled cells, the oracle
+    reading the packed step-1 values it needs."""
+    f = BUILTINS[name]
+    p = mk(name, r, tile_level=g)
+    geo = p.geometry
+    assert geo.packed_ok
+    a, b = p.new_packed(), p.new_packed()
+    p.seed_packed(a, 42, 0.5)
+    p.step_packed(a, b)
+    pb = mk(name, r)  # the byte path at the library's tile level
+    x, y = pb.new_state(), pb.new_state()
+    pb.seed(x, 42, 0.5)
+    pb.step(x, y)
+    torch.cuda.synchronize()
+    one = cells(p, b)
+    assert np.array_equal(one, pb.to_cells(y).cpu().numpy())
+    del x, y
+    pb.close()
+    p.step_packed(b, a)
+    two = cells(p, a)
+    om = np.unique(sqz_inputs.random_indices(200_000, f.k ** r, seed=r).astype(np.int64))
+    om = np.concatenate([om, [0, f.k ** r - 1]]).astype(np.int64)
+    want = A.compact_step_sampled(f, r, om, lambda q: one[q])
+    assert np.array_equal(two[om], want)
+    assert p.device_error() == 0
