@@ -395,7 +395,25 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
       pe1 = p.peer_chunk_start[chunk + 1];
     }
     // Phase A: slice q, j-block q * NW + cw -> Z
-    for (uint32_t q = 0, qc = 0, zq = z_s + za; q < nsl; ++q, qc += kStreamSW, zq += 4 * kStreamSW) {
+    // Slices in pairs: two independent transpose chains per warp interleave (the shuffle chain's
+    // latency, not its instruction count, bounds this phase at 16 warps per SM)
+    uint32_t q = 0, qc = 0, zq = z_s + za;
+    for (; MINB == 1 && q + 1 < nsl; q += 2, qc += 2 * kStreamSW, zq += 8 * kStreamSW) {  // (64 registers: singles)
+      const uint32_t s0 = seq + q, s1 = s0 + 1, slot0 = s0 % NIN, slot1 = s1 % NIN;
+      mbar_wait(&infull[slot0], (s0 / NIN) & 1);
+      mbar_wait(&infull[slot1], (s1 / NIN) & 1);
+      const uint4 l0 = lds128(pa0 + slot0 * slot_bytes), h0 = lds128(pa1 + slot0 * slot_bytes);
+      const uint4 l1 = lds128(pa0 + slot1 * slot_bytes), h1 = lds128(pa1 + slot1 * slot_bytes);
+      const uint32_t x0 = tr(pack01(l0, h0)), x1 = tr(pack01(l1, h1));  // (past K: not stored)
+      if (qc < nl) sts32(zq, x0);  // cell j < K
+      if (qc + kStreamSW < nl) sts32(zq + 4 * kStreamSW, x1);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&inempty[slot0]);
+        mbar_arrive(&inempty[slot1]);
+      }
+    }
+    for (; q < nsl; ++q, qc += kStreamSW, zq += 4 * kStreamSW) {  // an odd last slice
       const uint32_t s = seq + q, slot = s % NIN;
       mbar_wait(&infull[slot], (s / NIN) & 1);
       if (qc < na) {  // this warp's j-block exists in slice q
