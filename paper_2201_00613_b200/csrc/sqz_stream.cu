@@ -434,62 +434,88 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
     uint8_t* tile_out = next + (uint64_t)((uint32_t)(c.t0 - p.tile_lo) + (uint32_t)lane) * Kp;
     const uint32_t zA = z_s + za;  // Z word of this lane's cell in slice 0
     uint8_t* const outA = tile_out + ja;
-    auto slice_out = [&](uint32_t qc, const uint4& row) {  // qc: the block's cell offset from this warp's
-      if (qc < na) {                                       // block of slice 0 (q * NW * 32 unless rotated)  // this warp's j-block exists in slice q
-        uint32_t nw = 0;
-        if (qc < nl) {  // cell j < K
-          uint32_t x[8];
-          x[0] = lds32(z_s + (row.x & 0xFFFFu));
-          x[1] = lds32(z_s + (row.x >> 16));
-          x[2] = lds32(z_s + (row.y & 0xFFFFu));
-          x[3] = lds32(z_s + (row.y >> 16));
-          x[4] = lds32(z_s + (row.z & 0xFFFFu));
-          if (DMAX > 5) {
-            x[5] = lds32(z_s + (row.z >> 16));
-            x[6] = lds32(z_s + (row.w & 0xFFFFu));
-            x[7] = lds32(z_s + (row.w >> 16));
-          }
-          uint32_t c0, c1, c2, c3;
-          if (DMAX <= 5) {
-            const uint32_t s1 = x[0] ^ x[1] ^ x[2], k1 = maj3(x[0], x[1], x[2]);
-            const uint32_t s2 = s1 ^ x[3] ^ x[4], k2 = maj3(s1, x[3], x[4]);
-            c0 = s2;
-            c1 = k1 ^ k2;
-            c2 = k1 & k2;
-            c3 = 0;
-          } else {
-            const uint32_t sa = x[0] ^ x[1] ^ x[2], ka = maj3(x[0], x[1], x[2]);
-            const uint32_t sb = x[3] ^ x[4] ^ x[5], kb = maj3(x[3], x[4], x[5]);
-            const uint32_t sc = sa ^ sb ^ x[6], kc = maj3(sa, sb, x[6]);
-            c0 = sc ^ x[7];
-            const uint32_t kd = sc & x[7];
-            const uint32_t se = ka ^ kb ^ kc, ke = maj3(ka, kb, kc);
-            c1 = se ^ kd;
-            const uint32_t kf = se & kd;
-            c2 = ke ^ kf;
-            c3 = ke & kf;
-          }
-          const uint32_t alive = lds32(zA + 4 * qc);
-          if (CONWAY) nw = c1 & ~c2 & ~c3 & (c0 | alive);  // B3/S23
-          else nw = (alive & rule_bits(p.survive, c0, c1, c2, c3)) | (~alive & rule_bits(p.birth, c0, c1, c2, c3));
-          nw &= live_lanes;
-          if (PEER) S.Wn[jl + qc] = nw;
+    // the new state word of this lane's cell in the block at offset qc (0 for cells past K)
+    auto block_nw = [&](uint32_t qc, const uint4& row) -> uint32_t {
+      uint32_t nw = 0;
+      if (qc < nl) {  // cell j < K
+        uint32_t x[8];
+        x[0] = lds32(z_s + (row.x & 0xFFFFu));
+        x[1] = lds32(z_s + (row.x >> 16));
+        x[2] = lds32(z_s + (row.y & 0xFFFFu));
+        x[3] = lds32(z_s + (row.y >> 16));
+        x[4] = lds32(z_s + (row.z & 0xFFFFu));
+        if (DMAX > 5) {
+          x[5] = lds32(z_s + (row.z >> 16));
+          x[6] = lds32(z_s + (row.w & 0xFFFFu));
+          x[7] = lds32(z_s + (row.w >> 16));
         }
-        const uint32_t xb = tr(nw);  // bit 8p+m = cell jb*32 + 4m + p of this lane's tile (0 past K)
-        const uint32_t m = 0x01010101u;
-        if ((uint32_t)lane < c.nt)  // Kp = round_up(K, 32): the block's 32 bytes are one aligned sector
-          stg256(outA + qc, xb & m, (xb >> 1) & m, (xb >> 2) & m, (xb >> 3) & m, (xb >> 4) & m,
-                 (xb >> 5) & m, (xb >> 6) & m, (xb >> 7) & m);
+        uint32_t c0, c1, c2, c3;
+        if (DMAX <= 5) {
+          const uint32_t s1 = x[0] ^ x[1] ^ x[2], k1 = maj3(x[0], x[1], x[2]);
+          const uint32_t s2 = s1 ^ x[3] ^ x[4], k2 = maj3(s1, x[3], x[4]);
+          c0 = s2;
+          c1 = k1 ^ k2;
+          c2 = k1 & k2;
+          c3 = 0;
+        } else {
+          const uint32_t sa = x[0] ^ x[1] ^ x[2], ka = maj3(x[0], x[1], x[2]);
+          const uint32_t sb = x[3] ^ x[4] ^ x[5], kb = maj3(x[3], x[4], x[5]);
+          const uint32_t sc = sa ^ sb ^ x[6], kc = maj3(sa, sb, x[6]);
+          c0 = sc ^ x[7];
+          const uint32_t kd = sc & x[7];
+          const uint32_t se = ka ^ kb ^ kc, ke = maj3(ka, kb, kc);
+          c1 = se ^ kd;
+          const uint32_t kf = se & kd;
+          c2 = ke ^ kf;
+          c3 = ke & kf;
+        }
+        const uint32_t alive = lds32(zA + 4 * qc);
+        if (CONWAY) nw = c1 & ~c2 & ~c3 & (c0 | alive);  // B3/S23
+        else nw = (alive & rule_bits(p.survive, c0, c1, c2, c3)) | (~alive & rule_bits(p.birth, c0, c1, c2, c3));
+        nw &= live_lanes;
+        if (PEER) S.Wn[jl + qc] = nw;
       }
+      return nw;
     };
+    // xb: the transposed block, bit 8p+m = cell 4m+p of the block in this lane's tile (0 past K)
+    auto block_out = [&](uint32_t qc, uint32_t xb) {
+      const uint32_t m = 0x01010101u;
+      if (qc < na && (uint32_t)lane < c.nt)  // Kp = round_up(K, 32): the block's 32 bytes are one sector
+        stg256(outA + qc, xb & m, (xb >> 1) & m, (xb >> 2) & m, (xb >> 3) & m, (xb >> 4) & m, (xb >> 5) & m,
+               (xb >> 6) & m, (xb >> 7) & m);
+    };
+    // qc: the block's cell offset from this warp's block of slice 0 (q * NW * 32 unless rotated)
+    auto slice_out = [&](uint32_t qc, const uint4& row) {
+      if (qc < na) block_out(qc, tr(block_nw(qc, row)));  // this warp's j-block exists in slice q
+    };
+    auto pair_out = [&](uint32_t qa, const uint4& ra, uint32_t qb, const uint4& rb) {  // two chains interleave
+      const uint32_t wa = block_nw(qa, ra), wb = block_nw(qb, rb);
+      const uint32_t xa = tr(wa), xb = tr(wb);
+      block_out(qa, xa);
+      block_out(qb, xb);
+    };
+    constexpr int RP = MINB == 1 ? RB / 2 : 0;  // block pairs at one CTA per SM (128 registers)
 #pragma unroll
-    for (int i = 0; i < RB; ++i)  // link-free blocks
+    for (int i = 0; i < RP; ++i)  // link-free pairs
+      if ((uint32_t)(2 * i + 1) < nsl && !((lmask >> (2 * i)) & 3u))
+        pair_out((uint32_t)(2 * i) * kStreamSW, rows[2 * i], (uint32_t)(2 * i + 1) * kStreamSW, rows[2 * i + 1]);
+#pragma unroll
+    for (int i = 2 * RP; i < RB; ++i)  // link-free single blocks
       if ((uint32_t)i < nsl && !((lmask >> i) & 1u)) slice_out((uint32_t)i * kStreamSW, rows[i]);
     consumers_sync();  // link words published; G and this chunk's adjacency buffer are free
     if (chunk + 2 * G < p.nchunks) adj_prefetch(p, ntl, chunk_info(p, chunk + 2 * G), cw, lane);
     if (chunk + G < p.nchunks) link_prefetch(p, S, S.ntl + ((it + 1) & 1) * ntl_words, chunk_info(p, chunk + G), cur, cw, lane);
 #pragma unroll
-    for (int i = 0; i < RB; ++i)  // blocks reading link words
+    for (int i = 0; i < RP; ++i) {  // pairs reading link words (or a pair past the chunk's slices)
+      if ((uint32_t)(2 * i + 1) < nsl) {
+        if ((lmask >> (2 * i)) & 3u)
+          pair_out((uint32_t)(2 * i) * kStreamSW, rows[2 * i], (uint32_t)(2 * i + 1) * kStreamSW, rows[2 * i + 1]);
+      } else if ((uint32_t)(2 * i) < nsl) {
+        slice_out((uint32_t)(2 * i) * kStreamSW, rows[2 * i]);
+      }
+    }
+#pragma unroll
+    for (int i = 2 * RP; i < RB; ++i)  // single blocks reading link words
       if ((uint32_t)i < nsl && ((lmask >> i) & 1u)) slice_out((uint32_t)i * kStreamSW, rows[i]);
     for (uint32_t q = RB; q < nsl; ++q) {
       // a partial last slice (r < NW blocks) goes to the LAST r warps here (Phase A gave it to the
