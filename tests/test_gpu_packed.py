@@ -81,10 +81,10 @@ RULES = [(1 << 3 | 1 << 6, 1 << 2 | 1 << 3), (1 << 1, 0x1FF), (0x1FF, 0), (1 << 
 
 
 @pytest.mark.parametrize("rule", RULES)
-def test_packed_rules(rule):
-    r = 9
-    p = mk("sierpinski-triangle", r, rule=rule)
-    want = oracle_run("sierpinski-triangle", r, 3, 0.5, 3, rule)
+@pytest.mark.parametrize("name,r,g", [("sierpinski-triangle", 9, 0), ("sierpinski-carpet", 5, 3), ("empty-bottles", 6, 3)])
+def test_packed_rules(rule, name, r, g):  # ragged chunks (slot split; link items) under births at count 0
+    p = mk(name, r, rule=rule, tile_level=g)
+    want = oracle_run(name, r, 3, 0.5, 3, rule)
     a, b = p.new_packed(), p.new_packed()
     p.seed_packed(a, 3, 0.5)
     fin = p.run_packed(a, b, 3)

@@ -66,7 +66,9 @@ def test_auto_levels_for_link_heavy_fractals():
 
 
 @pytest.mark.parametrize("rule", [(1 << 3, (1 << 2) | (1 << 3)), (1 << 2, 0), ((1 << 3) | (1 << 6), (1 << 2) | (1 << 3)),
-                                  (0b110110110, 0b001001001)])
+                                  (0b110110110, 0b001001001),
+                                  ((1 << 0) | (1 << 3), (1 << 2) | (1 << 3))])  # B03/S23: births at count 0
+                                  # exercise the masks of tiles past the shard's end and cells past K
 @pytest.mark.parametrize("name,r,g", [("sierpinski-carpet", 5, 4), ("sierpinski-triangle", 10, 7)])
 def test_stream_rules(rule, name, r, g):
     f = BUILTINS[name]
