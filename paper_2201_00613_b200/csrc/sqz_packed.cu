@@ -153,7 +153,9 @@ __device__ __forceinline__ void chunk_prefetch_slots(const TileParams& p, const 
 }
 
 // BYDIR link work items (link-heavy fractals, prefetched links).  A GROUP item (bit 31 clear: first
-// link | count - 1 << 11 | direction << 16) holds up to 32 links of one long direction; lane = link.
+// link | count - 1 << 11 | direction << 16 | lane group q << 24) holds up to 32 links of one long
+// direction for the 32 tiles of lane group q (four items per link group: finer work units balance
+// the warps in front of the chunk barrier); lane = link.
 // A direction's neighbour tiles are the same for all its links, so per (group, lane group q, tile)
 // the work is warp-uniform: the in-chunk part of a link word is a few masked rotations of the
 // neighbour cell's state word (one per distinct (source lane group, offset) of the tiles of q),
@@ -172,11 +174,11 @@ __device__ void pack_link_items(const TileParams& p, const PackSmem& S, uint32_t
     const uint32_t ng = (nd + 31) / 32;  // groups of balanced sizes
     for (uint32_t k = 0, e = e0; k < ng; ++k) {
       const uint32_t m = (nd - (e - e0) + (ng - k) - 1) / (ng - k);
-      S.items[n++] = e | ((m - 1u) << 11) | (d << 16);
+      for (uint32_t q = 0; q < 4; ++q) S.items[n++] = e | ((m - 1u) << 11) | (d << 16) | (q << 24);
       e += m;
     }
   }
-  const uint32_t free_w = n < nwarps ? nwarps - n : 1u;  // short links: one ballot item per idle warp
+  const uint32_t free_w = nwarps - n % nwarps;  // short links: ballot items on the warps of the last round
   const uint32_t nb = ns == 0 ? 0u : min(ns, free_w);
   for (uint32_t k = 0, i = 0; k < nb; ++k) {
     const uint32_t m = (ns - i + (nb - k) - 1) / (nb - k);
@@ -208,10 +210,9 @@ __device__ __forceinline__ void chunk_prefetch_items(const TileParams& p, const 
       }
       continue;
     }
-    const uint32_t d = item >> 16, valid = (uint32_t)lane < n ? 1u : 0u;
+    const uint32_t d = (item >> 16) & 0xFFu, q = (item >> 24) & 3u, valid = (uint32_t)lane < n ? 1u : 0u;
     const uint32_t e = i0 + (valid ? (uint32_t)lane : 0u), j2 = p.link_j2[e];
-#pragma unroll
-    for (uint32_t q = 0; q < 4; ++q) {
+    {
       const uint32_t a1 = ntl[d * kPackTiles + q * 32 + lane], tl = a1 - 1u - tlo;  // lane = tile here
       const bool out = a1 != 0 && a1 - 1u - pc.t0 >= pc.nt;
       uint32_t om = __ballot_sync(0xFFFFFFFFu, out);
@@ -251,12 +252,10 @@ __device__ __forceinline__ void chunk_link_items(const TileParams& p, const Pack
       }
       continue;
     }
-    const uint32_t d = item >> 16, valid = (uint32_t)lane < n ? 1u : 0u;
+    const uint32_t d = (item >> 16) & 0xFFu, q = (item >> 24) & 3u, valid = (uint32_t)lane < n ? 1u : 0u;
     const uint32_t e = i0 + (valid ? (uint32_t)lane : 0u), j2 = p.link_j2[e];
     const uint4 z = *reinterpret_cast<const uint4*>(Z + j2 * 4);  // the neighbour cell's word, all 128 tiles
-    uint32_t w4[4];
-#pragma unroll
-    for (uint32_t q = 0; q < 4; ++q) {
+    {
       const uint32_t a1 = ntl[d * kPackTiles + q * 32 + lane], rel = a1 - 1u - pc.t0, tl = a1 - 1u - tlo;  // lane = tile
       const bool present = a1 != 0, inside = present && rel < pc.nt;
       const uint32_t key = (rel & ~31u) | ((rel - (uint32_t)lane) & 31u);  // source lane group, offset
@@ -276,9 +275,8 @@ __device__ __forceinline__ void chunk_link_items(const TileParams& p, const Pack
         const uint32_t sh = __shfl_sync(0xFFFFFFFFu, tl, i) & 31u;
         w |= ((S.R[(q * 32 + i) * E + e] >> sh) & 1u) << i;
       }
-      w4[q] = w;
+      if (valid) Z[(Kw + e) * 4 + q] = w;
     }
-    if (valid) *reinterpret_cast<uint4*>(Z + (Kw + e) * 4) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
   }
 }
 
