@@ -269,11 +269,14 @@ __device__ __forceinline__ void chunk_link_items(const TileParams& p, const Pack
         const uint32_t g = kk >> 5, src = g == 0 ? z.x : g == 1 ? z.y : g == 2 ? z.z : z.w;
         w |= __funnelshift_r(src, src, kk & 31u) & m;
       }
-      while (om) {  // tiles whose neighbour tile is outside the chunk: the gathered words
+      while (om) {  // tiles whose neighbour tile is outside the chunk: the gathered words, two at a time
         const uint32_t i = __ffs(om) - 1u;
         om &= om - 1u;
-        const uint32_t sh = __shfl_sync(0xFFFFFFFFu, tl, i) & 31u;
-        w |= ((S.R[(q * 32 + i) * E + e] >> sh) & 1u) << i;
+        const uint32_t i2 = om ? __ffs(om) - 1u : i;
+        om &= om - 1u;
+        const uint32_t sh = __shfl_sync(0xFFFFFFFFu, tl, i) & 31u, sh2 = __shfl_sync(0xFFFFFFFFu, tl, i2) & 31u;
+        const uint32_t g1 = S.R[(q * 32 + i) * E + e], g2 = S.R[(q * 32 + i2) * E + e];
+        w |= (((g1 >> sh) & 1u) << i) | (((g2 >> sh2) & 1u) << i2);
       }
       if (valid) Z[(Kw + e) * 4 + q] = w;
     }
