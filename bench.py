@@ -464,6 +464,23 @@ def main():
                                      f"{g.packed_bytes / 1e9:.2f} GB), device unpack, {K} byte-state steps, device "
                                      f"pack, D2H; {'pinned' if pinned else 'pageable'} host buffer", "ms": e_ms,
                              "value_over_device_value": cells_per_s(g.cells_total, K, e_ms) / value}
+            # the transfer floor: the same pinned buffer over PCIe alone, each direction timed
+            dev_ms = g.cells_total / value * 1e3  # the device-timed step
+            t0, t1, t2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            t0.record(stream)
+            dp[:g.packed_bytes // 4].copy_(hb, non_blocking=True)
+            t1.record(stream)
+            hb.copy_(dp[:g.packed_bytes // 4], non_blocking=True)
+            t2.record(stream)
+            torch.cuda.synchronize()
+            h2d_ms, d2h_ms = t0.elapsed_time(t1), t1.elapsed_time(t2)
+            extras["e2e"]["breakdown"] = {
+                "h2d_ms": h2d_ms, "d2h_ms": d2h_ms, "h2d_gbps": g.packed_bytes / h2d_ms / 1e6,
+                "d2h_gbps": g.packed_bytes / d2h_ms / 1e6, "steps_ms": K * dev_ms,
+                "unpack_pack_and_overhead_ms": e_ms - h2d_ms - d2h_ms - K * dev_ms,
+                "floor_value": cells_per_s(g.cells_total, K, h2d_ms + d2h_ms + K * dev_ms),
+                "note": "the state must cross PCIe both ways (1 bit per cell is its entropy at density 0.5), so at "
+                        "K steps e2e <= cells x K / (h2d + d2h + K x step)"}
             del hb, dp
             h, pinned = pinned_empty(g.state_bytes, torch.uint8)
             h.copy_(init)

@@ -197,8 +197,11 @@ squeeze_status squeeze_run_host(void* ctx, uint8_t* h_state, uint8_t* d_a, uint8
  * convert on the device), d_packed is a caller-owned device buffer of packed_bytes.  H2D of
  * h_packed, unpack into d_a, `steps` byte-state steps (the CUDA-graph ping-pong of squeeze_run),
  * pack of the final state, D2H into h_packed, synchronise.  The state is binary, so this moves 8x
- * fewer bytes over PCIe than squeeze_run_host for the same result.  Unsharded contexts only
- * (SQZ_E_CONFIG before any copy otherwise). */
+ * fewer bytes over PCIe than squeeze_run_host for the same result.  The transfers run on an
+ * internal copy stream in up to 8 segments of whole 128-tile packed chunks, ordered after prior
+ * work on `stream`: each segment's unpack overlaps the next one's H2D, each segment's D2H the next
+ * one's pack; the call returns after everything completed.  Unsharded contexts only (SQZ_E_CONFIG
+ * before any copy otherwise). */
 squeeze_status squeeze_run_host_bits(void* ctx, uint32_t* h_packed, uint8_t* d_a, uint8_t* d_b, uint32_t* d_packed,
                                     uint64_t steps, squeeze_stream_t stream);
 /* *d_out (device uint64) = number of alive cells of this shard. */

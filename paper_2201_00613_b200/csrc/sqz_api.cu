@@ -818,14 +818,57 @@ squeeze_status squeeze_run_host_bits(void* ctx, uint32_t* h_packed, uint8_t* d_a
   if (c->nranks > 1 || d_a == d_b) return SQZ_E_CONFIG;  // before any transfer is enqueued
   DevGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
-  // the state crosses PCIe at 1 bit per cell (the packed layout); the step runs on bytes
-  if (cudaMemcpyAsync(d_packed, h_packed, c->packed_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return SQZ_E_CUDA;
-  if ((st = cu(launch_unpack(tile_params(c), d_packed, d_a, s))) != SQZ_OK) return st;
-  if ((st = squeeze_run(ctx, d_a, d_b, steps, 1, stream)) != SQZ_OK) return st;
+  // The state crosses PCIe at 1 bit per cell (the packed layout); the step runs on bytes.  The
+  // transfers run on a second stream in segments of whole 128-tile packed chunks, so each
+  // segment's unpack overlaps the next segment's H2D and each segment's D2H the next one's pack.
+  const TileParams p = tile_params(c);
+  const uint64_t ntiles = p.tile_hi - p.tile_lo, nch = (ntiles + kPackTiles - 1) / kPackTiles;
+  const uint64_t nseg = std::min<uint64_t>(8, nch ? nch : 1), per = nch ? (nch + nseg - 1) / nseg : 0;
+  cudaStream_t cs = nullptr;
+  std::vector<cudaEvent_t> ev(2 * nseg + 2, nullptr);
+  auto cleanup = [&](squeeze_status r) {
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+    if (cs) cudaStreamDestroy(cs);
+    return r;
+  };
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return cleanup(SQZ_E_CUDA);
+  for (cudaEvent_t& e : ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return cleanup(SQZ_E_CUDA);
+  auto seg = [&](uint64_t i, TileParams& q, uint64_t& poff, uint64_t& boff, uint64_t& pbytes) {
+    const uint64_t c0 = i * per, c1 = std::min(nch, c0 + per);
+    q = p;
+    q.tile_lo = 0;
+    q.tile_hi = std::min(ntiles, c1 * kPackTiles) - c0 * kPackTiles;
+    poff = c0 * (uint64_t)c->Kw * 4;  // u32 words
+    boff = c0 * kPackTiles * (uint64_t)c->Kp;
+    pbytes = (c1 - c0) * (uint64_t)c->Kw * 16;
+  };
+  if (cudaEventRecord(ev[2 * nseg], s) != cudaSuccess || cudaStreamWaitEvent(cs, ev[2 * nseg], 0) != cudaSuccess)
+    return cleanup(SQZ_E_CUDA);
+  for (uint64_t i = 0; i < nseg && nch; ++i) {  // H2D (copy stream) -> unpack (stream), segment by segment
+    TileParams q;
+    uint64_t poff, boff, pbytes;
+    seg(i, q, poff, boff, pbytes);
+    if (cudaMemcpyAsync(d_packed + poff, h_packed + poff, pbytes, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+        cudaEventRecord(ev[i], cs) != cudaSuccess || cudaStreamWaitEvent(s, ev[i], 0) != cudaSuccess)
+      return cleanup(SQZ_E_CUDA);
+    if ((st = cu(launch_unpack(q, d_packed + poff, d_a + boff, s))) != SQZ_OK) return cleanup(st);
+  }
+  if ((st = squeeze_run(ctx, d_a, d_b, steps, 1, stream)) != SQZ_OK) return cleanup(st);
   const uint8_t* fin = (steps & 1) ? d_b : d_a;
-  if ((st = cu(launch_pack(tile_params(c), fin, d_packed, s))) != SQZ_OK) return st;
-  if (cudaMemcpyAsync(h_packed, d_packed, c->packed_bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) return SQZ_E_CUDA;
-  return cu(cudaStreamSynchronize(s));
+  for (uint64_t i = 0; i < nseg && nch; ++i) {  // pack (stream) -> D2H (copy stream), segment by segment
+    TileParams q;
+    uint64_t poff, boff, pbytes;
+    seg(i, q, poff, boff, pbytes);
+    if ((st = cu(launch_pack(q, fin + boff, d_packed + poff, s))) != SQZ_OK) return cleanup(st);
+    if (cudaEventRecord(ev[nseg + i], s) != cudaSuccess || cudaStreamWaitEvent(cs, ev[nseg + i], 0) != cudaSuccess ||
+        cudaMemcpyAsync(h_packed + poff, d_packed + poff, pbytes, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+      return cleanup(SQZ_E_CUDA);
+  }
+  if (cudaEventRecord(ev[2 * nseg + 1], cs) != cudaSuccess || cudaStreamWaitEvent(s, ev[2 * nseg + 1], 0) != cudaSuccess)
+    return cleanup(SQZ_E_CUDA);
+  return cleanup(cu(cudaStreamSynchronize(s)));
 }
 
 squeeze_status squeeze_run_host_packed(void* ctx, uint32_t* h_packed, uint32_t* d_a, uint32_t* d_b, uint64_t steps,

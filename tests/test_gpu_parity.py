@@ -186,7 +186,8 @@ def test_run_graph_and_host():
 
 
 @pytest.mark.parametrize("name,r,steps", [("sierpinski-triangle", 10, 7), ("sierpinski-triangle", 12, 6),
-                                          ("sierpinski-carpet", 5, 5), ("empty-bottles", 6, 4)])
+                                          ("sierpinski-carpet", 5, 5), ("empty-bottles", 6, 4),
+                                          ("sierpinski-triangle", 14, 3), ("sierpinski-carpet", 7, 2)])  # 8 segments
 def test_run_host_bits(name, r, steps):
     """End to end with the state crossing PCIe at 1 bit per cell (packed layout): the host buffer
     after the run decodes to the oracle's state (packed layout decoded on the host)."""
