@@ -823,7 +823,7 @@ squeeze_status squeeze_run_host_bits(void* ctx, uint32_t* h_packed, uint8_t* d_a
   // segment's unpack overlaps the next segment's H2D and each segment's D2H the next one's pack.
   const TileParams p = tile_params(c);
   const uint64_t ntiles = p.tile_hi - p.tile_lo, nch = (ntiles + kPackTiles - 1) / kPackTiles;
-  const uint64_t nseg = std::min<uint64_t>(8, nch ? nch : 1), per = nch ? (nch + nseg - 1) / nseg : 0;
+  const uint64_t per = nch ? (nch + 7) / 8 : 0, nseg = nch ? (nch + per - 1) / per : 1;  // no empty segments
   cudaStream_t cs = nullptr;
   std::vector<cudaEvent_t> ev(2 * nseg + 2, nullptr);
   auto cleanup = [&](squeeze_status r) {

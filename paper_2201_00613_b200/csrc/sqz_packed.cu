@@ -275,7 +275,7 @@ __device__ __forceinline__ void chunk_link_items(const TileParams& p, const Pack
         const uint32_t i2 = om ? __ffs(om) - 1u : i;
         om &= om - 1u;
         const uint32_t sh = __shfl_sync(0xFFFFFFFFu, tl, i) & 31u, sh2 = __shfl_sync(0xFFFFFFFFu, tl, i2) & 31u;
-        const uint32_t g1 = S.R[(q * 32 + i) * E + e], g2 = S.R[(q * 32 + i2) * E + e];
+        const uint32_t g1 = valid ? S.R[(q * 32 + i) * E + e] : 0u, g2 = valid ? S.R[(q * 32 + i2) * E + e] : 0u;
         w |= (((g1 >> sh) & 1u) << i) | (((g2 >> sh2) & 1u) << i2);
       }
       if (valid) Z[(Kw + e) * 4 + q] = w;

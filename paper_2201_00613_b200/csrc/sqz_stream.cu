@@ -260,7 +260,7 @@ __device__ __forceinline__ void link_words(const TileParams& p, const StreamSmem
       om &= om - 1u;
       const uint32_t i2 = om ? __ffs(om) - 1u : i;
       om &= om - 1u;
-      const uint32_t g1 = lds32(gs + i * (E * 4u)), g2 = lds32(gs + i2 * (E * 4u));
+      const uint32_t g1 = g.valid ? lds32(gs + i * (E * 4u)) : 0u, g2 = g.valid ? lds32(gs + i2 * (E * 4u)) : 0u;
       w |= (((g1 >> sh) & 1u) << i) | (((g2 >> sh) & 1u) << i2);
     }
     if (g.valid) Z[K + g.e] = w;

@@ -185,14 +185,15 @@ def test_run_graph_and_host():
     assert np.array_equal(p.to_cells(h).numpy(), want[5])
 
 
-@pytest.mark.parametrize("name,r,steps", [("sierpinski-triangle", 10, 7), ("sierpinski-triangle", 12, 6),
-                                          ("sierpinski-carpet", 5, 5), ("empty-bottles", 6, 4),
-                                          ("sierpinski-triangle", 14, 3), ("sierpinski-carpet", 7, 2)])  # 8 segments
-def test_run_host_bits(name, r, steps):
+@pytest.mark.parametrize("name,r,steps,g", [("sierpinski-triangle", 10, 7, 0), ("sierpinski-triangle", 12, 6, 0),
+                                            ("sierpinski-carpet", 5, 5, 0), ("empty-bottles", 6, 4, 0),
+                                            ("sierpinski-triangle", 14, 3, 0), ("sierpinski-carpet", 7, 2, 0),
+                                            ("empty-bottles", 6, 3, 2)])  # 8 segments; 19 chunks in 7 segments
+def test_run_host_bits(name, r, steps, g):
     """End to end with the state crossing PCIe at 1 bit per cell (packed layout): the host buffer
     after the run decodes to the oracle's state (packed layout decoded on the host)."""
     want = oracle_run(name, r, 11, 0.5, steps)
-    p = mk(name, r)
+    p = mk(name, r, tile_level=g)
     g = p.geometry
     a, b, dp = p.new_state(), p.new_state(), p.new_packed()
     p.seed(a, 11, 0.5)
