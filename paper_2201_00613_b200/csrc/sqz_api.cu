@@ -96,7 +96,7 @@ struct Ctx {
   // large tiles (a 32-tile chunk does not fit shared memory twice): the streaming byte step
   bool stream = false;
   int stream_minb = 1, stream_grid = 0;
-  uint32_t stream_sin = 0, stream_sout = 0;
+  uint32_t stream_sin = 0;
   std::map<uint32_t, BlockLevel> blocks;  // by m = log_s rho
   // CUDA graph of the two-step ping-pong
   cudaGraphExec_t graph = nullptr;
@@ -245,7 +245,6 @@ TileParams tile_params(const Ctx* c) {
   p.adj_stride = adj_stride(c);
   p.pstages = c->packed_stages;
   p.sin = c->stream_sin;
-  p.sout = c->stream_sout;
   if (c->peer_parity >= 0 && c->d_peer_chunk_start) {
     p.peer_recv = c->d_peer_recv[c->peer_parity];
     p.peer_chunk_start = c->d_peer_chunk_start;
@@ -501,7 +500,6 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       if (c->stream) {
         if (c->tt.K > 0xFFFFu || !stream_plan(p, c->nranks > 1, &c->stream_minb)) return fail(SQZ_E_INVALID_LEVEL);
         c->stream_sin = p.sin;
-        c->stream_sout = p.sout;
         c->tile_smem = stream_smem_bytes(p, c->nranks > 1);
         c->tile_threads = stream_threads();
         const cudaError_t se = stream_prepare(p, c->tile_smem, c->stream_minb, &occ);

@@ -58,7 +58,7 @@ struct TileParams {
   const uint32_t* adj;
   uint64_t adj_stride;  // a multiple of kPackTiles
   uint32_t pstages;     // pipeline stages of the packed step
-  uint32_t sin, sout;   // slice-ring depths of the large-tile byte step (sqz_stream.cu)
+  uint32_t sin;        // input slice-ring depth of the large-tile byte step (sqz_stream.cu)
 };
 
 // ν as an integer tensor-core product (sqz_mma.cu, SURVEY NEXT-3 ablation).

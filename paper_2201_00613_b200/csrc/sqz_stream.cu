@@ -3,20 +3,21 @@
 // Link-heavy fractals (the carpet's full tile edges: 112 outside cells per 512-cell tile
 // at tile level 3) need larger tiles: at level 4 the carpet's links fall to 328 per 4096 cells
 // (SURVEY §7 hard part 3).  A 32-tile chunk of such tiles (131 KB) no longer fits shared memory
-// twice, so this kernel keeps the chunk only in its bit-sliced form Z (4 B per cell position, bit
-// i = tile i, the same form k_step_tile builds) and STREAMS the bytes through two small rings:
+// twice, so this kernel keeps only the chunk's bit-sliced form Z (4 B per cell position, bit i =
+// tile i, the form k_step_tile builds; double-buffered by chunk parity) and STREAMS the bytes:
 //
-//   producer warp:   slice q of the chunk (cells [480q, 480q+480) of its 32 tiles) -> in-ring slot
-//                    (32 one-dimensional bulk copies, one per tile, on the slot's mbarrier)
-//   consumer warps:  Phase A  slice -> Z (lane = tile: pack 32 bytes, 32x32 warp transpose)
-//                    Phase B  boundary-link words from Z (neighbour tile in the chunk) or from the
-//                             4-byte gathers issued one chunk ahead (outside the chunk)
-//                    Phase C+D count + rule per j-block, transpose back -> out-ring slot; consumer
-//                             warp 0 bulk-stores each finished slice (32 copies, one per tile)
+//   copy thread:  slice q of the chunk (cells [480q, 480q+480) of its 32 tiles) -> input-ring slot
+//                 (one 2D TMA box pair on the slot's mbarrier, an L2 prefetch of the slice after)
+//   Phase A       slice -> Z (lane = tile: pack 32 bytes, 32x32 warp transpose; slices in pairs)
+//   Phase B       boundary-link words by link items: lane = link for the long directions (masked
+//                 rotations of the neighbour cell's Z word per in-chunk offset, one gathered word
+//                 per outside tile), ballots for the short ones (see link_items)
+//   Phase C+D     count + rule per j-block, transpose back, one 256-bit store per lane straight to
+//                 HBM; blocks that read no link word before the links barrier
 //
 // Consumer warp w owns j-block w of every slice (15 warps x 32 cells = 480), so its neighbour
-// table rows stay in registers; three named barriers per chunk (Z complete, links complete, Z
-// free).  The neighbour structure is the one of k_step_tile (P:57, P:189 at tile level).
+// table rows stay in registers; two named barriers per chunk (Z and gathers complete, link words
+// published).  The neighbour structure is the one of k_step_tile (P:57, P:189 at tile level).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -91,11 +92,6 @@ __device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
 
 __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;" ::"r"(kStreamNW * 32) : "memory");
-}
-
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 
 // Shared-memory offset of byte x (a multiple of 16, < 480) of a tile's slice row, relative to the
@@ -566,7 +562,6 @@ bool stream_plan(TileParams& p, bool peer, int* minb) {
   const size_t cap = 227 * 1024;
   const char* force = getenv("SQZ_STREAM_CTAS");  // tuning knob: 1 or 2 CTAs per SM
   p.sin = 4;
-  p.sout = 0;
   if ((!force || atoi(force) >= 2) && 2 * stream_smem_bytes(p, peer) <= cap) {
     *minb = 2;
     return true;
