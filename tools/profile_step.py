@@ -19,6 +19,7 @@ ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--naive", action="store_true")
 ap.add_argument("--bb", action="store_true")
 ap.add_argument("--packed", action="store_true")
+ap.add_argument("--heat", action="store_true")
 ap.add_argument("--tile-level", type=int, default=0)
 ap.add_argument("--block-threads", type=int, default=0)
 ap.add_argument("--ctas-per-sm", type=int, default=0)
@@ -30,6 +31,12 @@ if a.packed:
     p.seed_packed(x, 42, 0.5)
     for i in range(a.steps):
         p.step_packed(x, y)
+        x, y = y, x
+elif a.heat:
+    x, y = p.new_heat(), p.new_heat()
+    p.heat_seed(x, 42)
+    for i in range(a.steps):
+        p.heat_step(x, y)
         x, y = y, x
 elif a.bb:
     x, y = p.new_bb(), p.new_bb()
