@@ -59,6 +59,7 @@ struct Ctx {
   uint32_t* d_adj = nullptr;         // tile adjacency [ndirs][local tiles], built once at init
   int packed_threads = 256;
   uint32_t packed_stages = 3;
+  uint32_t packed_rcap = 0;  // compacted link-gather buffer of the packed step (words; 0 = none)
   uint32_t Kw = 4;                    // packed words per chunk
   uint64_t packed_bytes = 0;
   int packed_grid = 0;
@@ -244,6 +245,7 @@ TileParams tile_params(const Ctx* c) {
   p.adj = c->d_adj;
   p.adj_stride = adj_stride(c);
   p.pstages = c->packed_stages;
+  p.rcap = c->packed_rcap;
   p.sin = c->stream_sin;
   if (c->peer_parity >= 0 && c->d_peer_chunk_start) {
     p.peer_recv = c->d_peer_recv[c->peer_parity];
@@ -523,6 +525,20 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       if (p.pstages == 3 && 2 * packed_smem_bytes(p) > 220 * 1024) p.pstages = 2;
       if (const char* e = getenv("SQZ_PACKED_STAGES")) p.pstages = (uint32_t)atoi(e);
       if (p.pstages < 2 || p.pstages > 4) return fail(SQZ_E_CONFIG);
+      // more links than the [tile][link] gather buffer holds (the carpet at level 4): a compacted
+      // buffer of the outside (tile, link) pairs, as large as the CTAs per SM allow (at most every
+      // pair of the chunk); pairs past it are read synchronously (sqz_packed.cu)
+      p.rcap = 0;
+      if (packed_compact_gathers(p)) {
+        const size_t base = packed_smem_bytes(p), budget = 2 * base <= 200 * 1024 ? 110 * 1024 : 226 * 1024;
+        if (base < budget) p.rcap = (uint32_t)std::min<size_t>((size_t)kPackTiles * p.E, (budget - base) / 4) & ~31u;
+        if (const char* e = getenv("SQZ_PACKED_RCAP")) p.rcap = std::min<uint32_t>(p.rcap, (uint32_t)atoi(e));  // tests: overflow
+      }
+      c->packed_rcap = p.rcap;
+      // a compacted-gather chunk leaves one CTA per SM: 16 warps instead of 8 (8 neighbour slots only)
+      if (p.rcap && p.dmax > 5 && 2 * packed_smem_bytes(p) > 228 * 1024) c->packed_threads = 512;
+      if (const char* e = getenv("SQZ_PACKED_THREADS"))  // A/B timing
+        if (p.dmax > 5 && (atoi(e) == 256 || atoi(e) == 512)) c->packed_threads = atoi(e);
       c->packed_stages = p.pstages;
       c->packed_smem = packed_smem_bytes(p);
       int pocc = 0;
@@ -532,6 +548,8 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
         c->packed_grid = sms * std::max(1, pocc);
       else
         c->packed_grid = 0;
+      if (const char* e = getenv("SQZ_PACKED_GRID"))  // tests: several chunks per CTA at small sizes
+        if (atoi(e) > 0 && c->packed_grid) c->packed_grid = std::min(c->packed_grid, atoi(e));
       // ν tensor-core ablation: H_ν as int16 and the per-level weight bytes of k^(μ-1)
       if (c->f.s * c->f.s <= kMmaMaxS2 && c->f.k <= 256 && r <= 32) {
         std::vector<int16_t> hh(c->f.hnu.begin(), c->f.hnu.end());

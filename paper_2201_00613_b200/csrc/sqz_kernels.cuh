@@ -59,6 +59,8 @@ struct TileParams {
   uint64_t adj_stride;  // a multiple of kPackTiles
   uint32_t pstages;     // pipeline stages of the packed step
   uint32_t sin;        // input slice-ring depth of the large-tile byte step (sqz_stream.cu)
+  uint32_t rcap;       // packed step, link items with E > kMaxPrefetchLinks: words of the compacted
+                       // gather buffer (0 otherwise; sqz_packed.cu)
 };
 
 // ν as an integer tensor-core product (sqz_mma.cu, SURVEY NEXT-3 ablation).
@@ -94,6 +96,8 @@ cudaError_t stream_prepare(const TileParams& p, size_t smem, int minb, int* occu
 cudaError_t launch_step_stream(const TileParams& p, const uint8_t* cur, uint8_t* next, int grid, int minb,
                                size_t smem, cudaStream_t st);
 size_t packed_smem_bytes(const TileParams& p);
+// true when the packed step gathers out-of-chunk links through a compacted buffer of p.rcap words
+bool packed_compact_gathers(const TileParams& p);
 cudaError_t packed_prepare(const TileParams& p, size_t smem, int threads, int* occupancy);
 cudaError_t launch_step_packed(const TileParams& p, const uint32_t* cur, uint32_t* next, int grid, int threads,
                                size_t smem, cudaStream_t st);

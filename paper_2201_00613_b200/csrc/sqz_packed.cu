@@ -35,9 +35,12 @@ struct PackSmem {
   uint32_t* Z0;   // pstages x zw u32 (state/link/zero words)
   uint32_t zw;
   uint32_t* A0;   // kAdjSlots x ndirs x 128 adjacency words
-  uint32_t* R;    // [4E][32] prefetched words holding out-of-chunk neighbour bits (next chunk)
+  uint32_t* R;    // prefetched words holding out-of-chunk neighbour bits (next chunk): [4E][32]
+                  // (slots), [128 tiles][E] (link items), or compacted (p.rcap words, below)
+  uint32_t* rctr; // compacted R: [2] words allocated per chunk parity
+  uint32_t* rb;   // compacted R: [2][kPackMaxItems] first word of each group item's gathers
+  uint32_t* rbb;  // compacted R: [2][4E] first word of each (short link, lane group)'s gathers
   uint32_t* sl;   // [4E] link slot u = 4e + q: j2 << 10 | (direction * 128 + 32 q)
-  uint32_t* dp;   // [4 ndirs] direction pair v = 4d + q: first link << 16 | one past the last
   uint64_t* bar;  // [pstages] state copies landed, then [kAdjSlots] adjacency copies landed
   uint32_t* items;   // [kPackMaxItems] link work items (BYDIR, see pack_link_items), then the count
   uint32_t* slinks;  // [E] the links of the short directions (ballot items)
@@ -61,11 +64,15 @@ __host__ __device__ inline size_t packed_layout(const TileParams& p, uint8_t* ba
   if (s) s->A0 = (uint32_t*)(base + off);
   off += (size_t)kAdjSlots * p.ndirs * kPackTiles * 4;
   if (s) s->R = (uint32_t*)(base + off);
-  off += (size_t)4 * (prefetch_links(p) ? prefetch_links(p) : 1) * 32 * 4;
+  off += prefetch_links(p) ? (size_t)4 * prefetch_links(p) * 32 * 4 : align16((size_t)(p.rcap ? p.rcap : 1) * 4);
+  if (s) s->rctr = (uint32_t*)(base + off);
+  off += 16;
+  if (s) s->rb = (uint32_t*)(base + off);
+  off += prefetch_links(p) ? 0 : (size_t)2 * kPackMaxItems * 4;
+  if (s) s->rbb = (uint32_t*)(base + off);
+  off += prefetch_links(p) ? 0 : align16((size_t)2 * 4 * (p.E ? p.E : 1) * 4);
   if (s) s->sl = (uint32_t*)(base + off);
   off += align16((size_t)(p.E ? 4 * p.E : 1) * 4);
-  if (s) s->dp = (uint32_t*)(base + off);
-  off += align16((size_t)(p.ndirs ? 4 * p.ndirs : 1) * 4);
   if (s) s->bar = (uint64_t*)(base + off);
   off += (ns + kAdjSlots) * 8;
   if (s) s->items = (uint32_t*)(base + off);
@@ -76,6 +83,7 @@ __host__ __device__ inline size_t packed_layout(const TileParams& p, uint8_t* ba
 }
 
 size_t packed_smem_bytes(const TileParams& p) { return packed_layout(p, nullptr, nullptr); }
+bool packed_compact_gathers(const TileParams& p) { return prefetch_links(p) == 0; }
 
 __host__ __device__ inline uint64_t pack_chunks(const TileParams& p) {
   return (p.tile_hi - p.tile_lo + kPackTiles - 1) / kPackTiles;
@@ -125,10 +133,8 @@ __device__ __forceinline__ void adj_load(const TileParams& p, const PackSmem& S,
 
 // Link slot u = 4e + q: link e for the 32 tiles of lane group q (tiles 32q..32q+31 of the chunk).
 // Two work splits.  SLOTS: slot u belongs to warp u mod W (few links per direction, e.g. the
-// Sierpinski triangle's 8 links).  PAIRS (BYDIR): the links of one direction d share each tile's
-// neighbour tile, so the work is split by pair v = 4d + q: the neighbour tile is read once per
-// pair, then each link of d costs one load, one ballot and one store (link-heavy fractals: the
-// carpet's 112 links per tile).  Either way a slot/pair belongs to the same warp here and in the
+// Sierpinski triangle's 8 links).  BYDIR: link work items (below; link-heavy fractals such as the
+// carpet's 112 links per tile).  Either way a slot/item belongs to the same warp here and in the
 // link phase of the next iteration (same thread: program order suffices).  For a link whose neighbour tile is outside the chunk: a 4-byte
 // cp.async of the packed word holding the neighbour bit.  `ntl` = the chunk's adjacency words
 // (neighbour tile + 1, from the coarse λ + ν at init: P:189 at tile level).  Commits one group.
@@ -152,7 +158,7 @@ __device__ __forceinline__ void chunk_prefetch_slots(const TileParams& p, const 
   cp_async_commit();
 }
 
-// BYDIR link work items (link-heavy fractals, prefetched links).  A GROUP item (bit 31 clear: first
+// BYDIR link work items (link-heavy fractals).  A GROUP item (bit 31 clear: first
 // link | count - 1 << 11 | direction << 16 | lane group q << 24) holds up to 32 links of one long
 // direction for the 32 tiles of lane group q (four items per link group: finer work units balance
 // the warps in front of the chunk barrier); lane = link.
@@ -161,7 +167,8 @@ __device__ __forceinline__ void chunk_prefetch_slots(const TileParams& p, const 
 // neighbour cell's state word (one per distinct (source lane group, offset) of the tiles of q),
 // the out-of-chunk part one gathered word per outside tile.  A BALLOT item (bit 31 set: first index
 // into slinks | count - 1 << 11) holds links of the short directions (a corner's single link),
-// lane = tile, one ballot per (link, q).  R holds the gathers as [tile t of the chunk][link e].
+// lane = tile, one ballot per (link, q).  R holds the gathers as [tile t of the chunk][link e], or
+// compacted (chunk_prefetch_items).
 __device__ void pack_link_items(const TileParams& p, const PackSmem& S, uint32_t nwarps) {  // one thread
   uint32_t n = 0, ns = 0;
   for (uint32_t d = 0; d < p.ndirs; ++d) {
@@ -188,12 +195,31 @@ __device__ void pack_link_items(const TileParams& p, const PackSmem& S, uint32_t
   S.items[kPackMaxItems] = n;
 }
 
+// The packed word holding the neighbour bit (tile tl of the shard, cell j2), read synchronously: a
+// compacted gather buffer's overflow.  Another shard's tile (sharded contexts): the bit from the
+// halo, placed where the link reads it (bit tl mod 32).
+template <bool SHARDED>
+__device__ __forceinline__ uint32_t link_gather(const TileParams& p, const uint32_t* __restrict__ cur32, uint32_t tl,
+                                                uint32_t j2, uint32_t nloc) {
+  if (SHARDED && tl >= nloc) return halo_fetch(p.halo, (uint64_t)(tl + (uint32_t)p.tile_lo) * p.K + j2) << (tl & 31u);
+  return __ldg(cur32 + ((uint64_t)(tl >> 7) * p.Kw + j2) * 4 + ((tl >> 5) & 3u));
+}
+
+// Gathers of chunk pc's out-of-chunk links (issued one chunk ahead).  With E <= kMaxPrefetchLinks
+// R is [tile t of the chunk][link e].  Above that (the carpet at level 4: 328 links, a [128][E]
+// buffer would be 168 KB) R is COMPACTED: only the (outside tile, link) pairs the chunk has get a
+// word.  Each item takes its words with one shared atomicAdd on the chunk parity's counter and
+// records where they start (rb / rbb); the words of its r-th outside tile (in ballot order) are
+// base + r n + link.  Pairs past p.rcap are not prefetched: the link item reads them synchronously
+// (link_gather).  Producer and consumer of a word are the same lane (same item-to-warp split).
 template <bool SHARDED>
 __device__ __forceinline__ void chunk_prefetch_items(const TileParams& p, const PackSmem& S, const PackChunk& pc,
                                                      const uint32_t* ntl, const uint32_t* __restrict__ cur32,
-                                                     int warp, int nwarps, int lane) {
+                                                     int warp, int nwarps, int lane, uint32_t par) {
   const uint32_t E = p.E, ni = S.items[kPackMaxItems], tlo = (uint32_t)p.tile_lo, Kw = p.Kw;
   const uint32_t nloc = (uint32_t)(p.tile_hi - p.tile_lo), gs0 = smem_u32(S.R);
+  const bool compact = prefetch_links(p) == 0;
+  const uint32_t rcap = p.rcap, lt = (1u << lane) - 1u;
   for (uint32_t k = (uint32_t)warp; k < ni; k += (uint32_t)nwarps) {
     const uint32_t item = S.items[k], i0 = item & 0x7FFu, n = ((item >> 11) & 31u) + 1u;
     if (item & kPackBallotItem) {  // lane = tile, link by link
@@ -203,9 +229,20 @@ __device__ __forceinline__ void chunk_prefetch_items(const TileParams& p, const 
         for (uint32_t q = 0; q < 4; ++q) {
           const uint32_t a1 = ntl[d * kPackTiles + q * 32 + lane], tl = a1 - 1u - tlo, t = q * 32 + lane;
           const bool out = a1 != 0 && a1 - 1u - pc.t0 >= pc.nt;
-          if (SHARDED && out && tl >= nloc) S.R[t * E + e] = halo_fetch(p.halo, (uint64_t)(a1 - 1u) * p.K + j2) << (tl & 31u);
-          else cp_async4_if(gs0 + 4u * (t * E + e), cur32 + ((uint64_t)((out ? tl : 0u) >> 7) * Kw + j2) * 4 + ((tl >> 5) & 3u),
-                            out ? 1u : 0u);
+          uint32_t slot = t * E + e;
+          bool fits = true;
+          if (compact) {
+            const uint32_t om = __ballot_sync(0xFFFFFFFFu, out);
+            uint32_t base = 0;
+            if (lane == 0 && om) base = atomicAdd(&S.rctr[par], (uint32_t)__popc(om));
+            base = __shfl_sync(0xFFFFFFFFu, base, 0);
+            if (lane == 0) S.rbb[par * 4 * E + i * 4 + q] = base;
+            slot = base + (uint32_t)__popc(om & lt);
+            fits = slot < rcap;
+          }
+          if (SHARDED && out && fits && tl >= nloc) S.R[slot] = halo_fetch(p.halo, (uint64_t)(a1 - 1u) * p.K + j2) << (tl & 31u);
+          else cp_async4_if(gs0 + 4u * (fits ? slot : 0u), cur32 + ((uint64_t)((out ? tl : 0u) >> 7) * Kw + j2) * 4 + ((tl >> 5) & 3u),
+                            out && fits ? 1u : 0u);
         }
       }
       continue;
@@ -217,14 +254,24 @@ __device__ __forceinline__ void chunk_prefetch_items(const TileParams& p, const 
       const bool out = a1 != 0 && a1 - 1u - pc.t0 >= pc.nt;
       uint32_t om = __ballot_sync(0xFFFFFFFFu, out);
       const uint32_t farm = SHARDED ? __ballot_sync(0xFFFFFFFFu, out && tl >= nloc) : 0u;
+      uint32_t br = 0;  // compacted: first word of the current outside tile's n links
+      if (compact) {
+        const uint32_t cnt = (uint32_t)__popc(om) * n;
+        if (lane == 0 && cnt) br = atomicAdd(&S.rctr[par], cnt);
+        br = __shfl_sync(0xFFFFFFFFu, br, 0);
+        if (lane == 0) S.rb[par * kPackMaxItems + k] = br;
+      }
       while (om) {  // lane = link from here on
         const uint32_t i = __ffs(om) - 1u;
         om &= om - 1u;
         const uint32_t tli = __shfl_sync(0xFFFFFFFFu, tl, i), t = q * 32 + i;
+        const uint32_t slot = compact ? br + (uint32_t)lane : t * E + e;
+        const uint32_t ok = compact ? (br + n <= rcap ? valid : 0u) : valid;
+        br += n;
         if (!SHARDED || !((farm >> i) & 1u))
-          cp_async4_if(gs0 + 4u * (t * E + e), cur32 + ((uint64_t)(tli >> 7) * Kw + j2) * 4 + ((tli >> 5) & 3u), valid);
-        else if (valid)  // another shard's tile (sharded contexts): the bit from the halo, placed where it is read
-          S.R[t * E + e] = halo_fetch(p.halo, (uint64_t)(tli + tlo) * p.K + j2) << (tli & 31u);
+          cp_async4_if(gs0 + 4u * (ok ? slot : 0u), cur32 + ((uint64_t)(tli >> 7) * Kw + j2) * 4 + ((tli >> 5) & 3u), ok);
+        else if (ok)  // another shard's tile (sharded contexts): the bit from the halo, placed where it is read
+          S.R[slot] = halo_fetch(p.halo, (uint64_t)(tli + tlo) * p.K + j2) << (tli & 31u);
       }
     }
   }
@@ -233,9 +280,13 @@ __device__ __forceinline__ void chunk_prefetch_items(const TileParams& p, const 
 
 // Link words of chunk pc (BYDIR items): bit i of u32 lane q of word Kw + e = cell j2 of the
 // neighbour tile (link e) of tile 32q + i.
+template <bool SHARDED>
 __device__ __forceinline__ void chunk_link_items(const TileParams& p, const PackSmem& S, const PackChunk& pc,
-                                                 const uint32_t* ntl, uint32_t* Z, int warp, int nwarps, int lane) {
+                                                 const uint32_t* ntl, uint32_t* Z, const uint32_t* __restrict__ cur32,
+                                                 int warp, int nwarps, int lane, uint32_t par) {
   const uint32_t E = p.E, ni = S.items[kPackMaxItems], tlo = (uint32_t)p.tile_lo, Kw = p.Kw;
+  const bool compact = prefetch_links(p) == 0;
+  const uint32_t rcap = p.rcap, lt = (1u << lane) - 1u, nloc = (uint32_t)(p.tile_hi - p.tile_lo);
   for (uint32_t k = (uint32_t)warp; k < ni; k += (uint32_t)nwarps) {
     const uint32_t item = S.items[k], i0 = item & 0x7FFu, n = ((item >> 11) & 31u) + 1u;
     if (item & kPackBallotItem) {  // lane = tile, one ballot per (link, q)
@@ -245,7 +296,15 @@ __device__ __forceinline__ void chunk_link_items(const TileParams& p, const Pack
         for (uint32_t q = 0; q < 4; ++q) {
           const uint32_t a1 = ntl[d * kPackTiles + q * 32 + lane], rel = a1 - 1u - pc.t0, tl = a1 - 1u - tlo;
           const bool in = rel < pc.nt;
-          const uint32_t v = a1 == 0 ? 0u : in ? Z[j2 * 4 + (rel >> 5)] >> (rel & 31u) : S.R[(q * 32 + lane) * E + e] >> (tl & 31u);
+          uint32_t g;
+          if (compact) {
+            const uint32_t om = __ballot_sync(0xFFFFFFFFu, a1 != 0 && !in);
+            const uint32_t slot = S.rbb[par * 4 * E + i * 4 + q] + (uint32_t)__popc(om & lt);
+            g = a1 == 0 || in ? 0u : slot < rcap ? S.R[slot] : link_gather<SHARDED>(p, cur32, tl, j2, nloc);
+          } else {
+            g = a1 == 0 || in ? 0u : S.R[(q * 32 + lane) * E + e];
+          }
+          const uint32_t v = a1 == 0 ? 0u : in ? Z[j2 * 4 + (rel >> 5)] >> (rel & 31u) : g >> (tl & 31u);
           const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v & 1u);
           if (lane == 0) Z[(Kw + e) * 4 + q] = bal;
         }
@@ -269,6 +328,17 @@ __device__ __forceinline__ void chunk_link_items(const TileParams& p, const Pack
         const uint32_t g = kk >> 5, src = g == 0 ? z.x : g == 1 ? z.y : g == 2 ? z.z : z.w;
         w |= __funnelshift_r(src, src, kk & 31u) & m;
       }
+      if (compact) {  // the gathered words of the outside tiles, in the prefetch's order
+        uint32_t br = S.rb[par * kPackMaxItems + k];
+        while (om) {
+          const uint32_t i = __ffs(om) - 1u;
+          om &= om - 1u;
+          const uint32_t tli = __shfl_sync(0xFFFFFFFFu, tl, i);
+          const uint32_t g = !valid ? 0u : br + n <= rcap ? S.R[br + lane] : link_gather<SHARDED>(p, cur32, tli, j2, nloc);
+          br += n;
+          w |= ((g >> (tli & 31u)) & 1u) << i;
+        }
+      }
       while (om) {  // tiles whose neighbour tile is outside the chunk: the gathered words, two at a time
         const uint32_t i = __ffs(om) - 1u;
         om &= om - 1u;
@@ -283,35 +353,11 @@ __device__ __forceinline__ void chunk_link_items(const TileParams& p, const Pack
   }
 }
 
-template <bool SHARDED>
-__device__ __forceinline__ void chunk_prefetch_pairs(const TileParams& p, const PackSmem& S, const PackChunk& pc,
-                                               const uint32_t* ntl, const uint32_t* __restrict__ cur32, int warp,
-                                               int nwarps, int lane) {
-  if (prefetch_links(p)) {
-    for (uint32_t v = (uint32_t)warp; v < 4 * p.ndirs; v += (uint32_t)nwarps) {  // (direction, lane group)
-      const uint32_t q = v & 3u, d = v >> 2, span = S.dp[v];
-      const uint32_t a1 = ntl[d * kPackTiles + q * 32 + lane];
-      const uint32_t tl = a1 - 1u - (uint32_t)p.tile_lo;
-      if (a1 == 0 || a1 - 1u - pc.t0 < pc.nt) continue;
-      const bool local = !SHARDED || tl < (uint32_t)(p.tile_hi - p.tile_lo);
-      for (uint32_t e = span >> 16; e < (span & 0xFFFFu); ++e) {
-        const uint32_t j2 = S.sl[4 * e] >> 10, u = 4 * e + q;
-        if (local)
-          cp_async4(&S.R[u * 32 + lane], cur32 + ((uint64_t)(tl >> 7) * p.Kw + j2) * 4 + ((tl >> 5) & 3u));
-        else  // another shard's tile (sharded contexts): the bit from the halo, placed where the link reads it
-          S.R[u * 32 + lane] = halo_fetch(p.halo, (uint64_t)(a1 - 1u) * p.K + j2) << (tl & 31u);
-      }
-    }
-  }
-  cp_async_commit();
-}
-
 template <bool SHARDED, bool BYDIR>
 __device__ __forceinline__ void chunk_prefetch(const TileParams& p, const PackSmem& S, const PackChunk& pc,
                                                const uint32_t* ntl, const uint32_t* __restrict__ cur32, int warp,
-                                               int nwarps, int lane) {
-  if (BYDIR && prefetch_links(p)) chunk_prefetch_items<SHARDED>(p, S, pc, ntl, cur32, warp, nwarps, lane);
-  else if (BYDIR) chunk_prefetch_pairs<SHARDED>(p, S, pc, ntl, cur32, warp, nwarps, lane);
+                                               int nwarps, int lane, uint32_t par) {
+  if (BYDIR) chunk_prefetch_items<SHARDED>(p, S, pc, ntl, cur32, warp, nwarps, lane, par);
   else chunk_prefetch_slots<SHARDED>(p, S, pc, ntl, cur32, warp, nwarps, lane);
 }
 
@@ -377,9 +423,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
   for (uint32_t i = tid; i < NS * 4; i += blockDim.x) S.Z(i >> 2)[(Kw + E) * 4 + (i & 3)] = 0;  // zero slot
   for (uint32_t u = tid; u < 4 * E; u += blockDim.x)
     S.sl[u] = (p.link_j2[u >> 2] << 10) | (p.link_dir[u >> 2] * kPackTiles + 32 * (u & 3u));
-  for (uint32_t v = tid; v < 4 * p.ndirs; v += blockDim.x)
-    S.dp[v] = ((uint32_t)p.dir_start[v >> 2] << 16) | p.dir_start[(v >> 2) + 1];
   if (tid == 0) {
+    S.rctr[0] = S.rctr[1] = 0;
     if (BYDIR) pack_link_items(p, S, (uint32_t)nwarps);
     for (uint32_t s = 0; s < NS + kAdjSlots; ++s) mbar_init(&S.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -394,7 +439,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
     for (uint32_t a = 0; a + 1 < kAdjSlots && c + a * G < nch; ++a) adj_load(p, S, pack_chunk(p, c + a * G), a);
   }
   mbar_wait(S.abar(0), 0);
-  chunk_prefetch<SHARDED, BYDIR>(p, S, pack_chunk(p, c), S.ntl(0), cur32, warp, nwarps, lane);
+  chunk_prefetch<SHARDED, BYDIR>(p, S, pack_chunk(p, c), S.ntl(0), cur32, warp, nwarps, lane, 0u);
 
   uint32_t it = 0, s = 0, sphase = 0;  // sphase bit s: parity of state stage s's next completion
   for (; c < nch; c += G, ++it, s = (s + 1 == NS) ? 0 : s + 1) {
@@ -408,43 +453,13 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
 
     // link words: bit i of u32 lane q of word Kw + e = cell j2 of the neighbour tile (link e)
     // of tile 32q + i
-    if (BYDIR && Epf) {
+    if (tid == 0) S.rctr[(it + 1) & 1u] = 0;  // compacted R: the counter chunk it+1's prefetch allocates from
+    if (BYDIR) {
       if ((uint32_t)warp < S.items[kPackMaxItems]) {
         mbar_wait(S.abar(a), (it / kAdjSlots) & 1);  // (already complete when the prefetch ran)
         cp_async_wait_all();
-        chunk_link_items(p, S, pc, ntl, Z, warp, nwarps, lane);
+        chunk_link_items<SHARDED>(p, S, pc, ntl, Z, cur32, warp, nwarps, lane, it & 1u);
       }
-    } else if (BYDIR) {
-    if ((uint32_t)warp < 4 * p.ndirs) {
-      mbar_wait(S.abar(a), (it / kAdjSlots) & 1);  // (already complete when the prefetch ran)
-      cp_async_wait_all();
-      const uint32_t rs = smem_u32(S.R) + lane * 4;
-      const uint32_t ntl_s = smem_u32(ntl) + lane * 4;
-      for (uint32_t v = (uint32_t)warp; v < 4 * p.ndirs; v += (uint32_t)nwarps) {  // (direction, lane group)
-        const uint32_t q = v & 3u, d = v >> 2, span = S.dp[v];
-        const uint32_t a1 = lds32(ntl_s + (d * kPackTiles + q * 32) * 4);
-        const uint32_t rel = a1 - 1u - pc.t0, tl = a1 - 1u - (uint32_t)p.tile_lo;
-        const bool in = rel < pc.nt;
-        const uint32_t present = a1 != 0 ? 1u : 0u;
-        const uint32_t sh = (in ? rel : tl) & 31u;
-        const uint32_t zrow = zs + (rel >> 5) * 4;
-        for (uint32_t e = span >> 16; e < (span & 0xFFFFu); ++e) {
-          const uint32_t j2 = S.sl[4 * e] >> 10, u = 4 * e + q;
-          uint32_t bit;
-          if (Epf) {  // branch-free: the word from this chunk's stage, or the prefetched one
-            bit = (lds32(in ? zrow + j2 * 16 : rs + u * 128) >> sh) & present;
-          } else {  // more links than the prefetch holds: synchronous gathers
-            bit = in           ? lds32(zrow + j2 * 16) >> sh
-                  : a1 == 0    ? 0u
-                  : !SHARDED || tl < nloc
-                      ? __ldg(cur32 + ((uint64_t)(tl >> 7) * Kw + j2) * 4 + ((tl >> 5) & 3u)) >> sh
-                      : halo_fetch(p.halo, (uint64_t)(a1 - 1u) * K + j2);  // another shard's tile
-          }
-          const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit & 1u);
-          if (lane == 0) Z[(Kw + e) * 4 + q] = bal;
-        }
-      }
-    }
     } else {
     if ((uint32_t)warp < 4 * E) {
       mbar_wait(S.abar(a), (it / kAdjSlots) & 1);  // (already complete when the prefetch ran)
@@ -488,8 +503,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
     }
     if (c + G < nch) {  // out-of-chunk link gathers of the next chunk (its adjacency was issued long ago)
       const uint32_t a1 = (it + 1) & (kAdjSlots - 1);
-      if ((uint32_t)warp < (BYDIR ? S.items[kPackMaxItems] : 4 * Epf) && Epf) mbar_wait(S.abar(a1), ((it + 1) / kAdjSlots) & 1);
-      chunk_prefetch<SHARDED, BYDIR>(p, S, pack_chunk(p, c + G), S.ntl(a1), cur32, warp, nwarps, lane);
+      if (BYDIR ? (uint32_t)warp < S.items[kPackMaxItems] : ((uint32_t)warp < 4 * Epf && Epf))
+        mbar_wait(S.abar(a1), ((it + 1) / kAdjSlots) & 1);
+      chunk_prefetch<SHARDED, BYDIR>(p, S, pack_chunk(p, c + G), S.ntl(a1), cur32, warp, nwarps, lane, (it + 1) & 1u);
     }
 
     // count + rule: lane = word j (128 cells), straight to HBM
@@ -703,6 +719,8 @@ static PackedFn pick_packed_t(const TileParams& p, int threads) {
     if (rb <= 3) return conway ? k_step_packed<5, true, 3, 256, 3, SH, BD> : k_step_packed<5, false, 3, 256, 3, SH, BD>;
     return conway ? k_step_packed<5, true, 9, 256, 2, SH, BD> : k_step_packed<5, false, 9, 256, 2, SH, BD>;
   }
+  // one CTA per SM (the compacted-gather chunks of level-4 carpet tiles): 16 warps
+  if (threads == 512) return conway ? k_step_packed<8, true, 6, 512, 1, SH, BD> : k_step_packed<8, false, 6, 512, 1, SH, BD>;
   if (rb <= 2) return conway ? k_step_packed<8, true, 2, 256, 3, SH, BD> : k_step_packed<8, false, 2, 256, 3, SH, BD>;
   return conway ? k_step_packed<8, true, 6, 256, 2, SH, BD> : k_step_packed<8, false, 6, 256, 2, SH, BD>;
 }

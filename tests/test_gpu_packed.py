@@ -3,6 +3,8 @@
 Every expected value comes from ``oracle/`` or a closed form; the packed buffers are decoded
 on the host (``Squeeze.packed_to_cells``) and compared bit-exactly.
 """
+import functools
+
 import numpy as np
 import pytest
 import torch
@@ -19,6 +21,7 @@ def mk(name, r, **kw):
     return sq.Squeeze(sq.builtin_fractal(name), r, device=0, **kw)
 
 
+@functools.lru_cache(maxsize=8)
 def oracle_run(name, r, seed, density, steps, rule=A.B3S23):
     o = BUILTINS[name]
     cur = A.seed_compact(o, r, seed, density)
@@ -78,6 +81,42 @@ def test_packed_step_vs_oracle(name, r, g):
 
 
 RULES = [(1 << 3 | 1 << 6, 1 << 2 | 1 << 3), (1 << 1, 0x1FF), (0x1FF, 0), (1 << 0 | 1 << 4, 1 << 5 | 1 << 8)]
+
+
+# Link-heavy tiles past the [tile][link] gather buffer (E > 160: the carpet at level 4 has 328 links,
+# the full square at level 6 260): the out-of-chunk gathers go through the COMPACTED buffer.  The
+# grid is capped so each CTA walks several chunks (both counter parities, the adjacency ring), and
+# rcap is capped so the buffer overflows and the rest is read synchronously.
+@pytest.mark.parametrize("rcap", [None, 64, 4096])
+@pytest.mark.parametrize("name,r,g,grid", [("sierpinski-carpet", 7, 4, 2), ("sierpinski-carpet", 7, 4, 0),
+                                           ("full-square", 10, 6, 1), ("sierpinski-carpet", 7, 4, 1)])
+def test_packed_compacted_gathers(monkeypatch, rcap, name, r, g, grid):
+    if rcap is not None:
+        monkeypatch.setenv("SQZ_PACKED_RCAP", str(rcap))
+    if grid:
+        monkeypatch.setenv("SQZ_PACKED_GRID", str(grid))
+    p = mk(name, r, tile_level=g)
+    assert p.geometry.remote_links > 160 and p.geometry.packed_ok
+    steps = 3
+    want = oracle_run(name, r, 5, 0.45, steps)
+    a, b = p.new_packed(), p.new_packed()
+    p.seed_packed(a, 5, 0.45)
+    for t in range(steps):
+        p.step_packed(a, b)
+        assert np.array_equal(cells(p, b), want[t + 1]), f"step {t + 1}"
+        a, b = b, a
+
+
+@pytest.mark.parametrize("rule", RULES[:2])
+def test_packed_compacted_gathers_rules_ragged(monkeypatch, rule):  # a ragged last chunk, births at count 0
+    monkeypatch.setenv("SQZ_PACKED_GRID", "3")
+    name, r = "sierpinski-carpet", 6  # 64 tiles of level 4: one ragged chunk
+    p = mk(name, r, rule=rule, tile_level=4)
+    want = oracle_run(name, r, 3, 0.5, 3, rule)
+    a, b = p.new_packed(), p.new_packed()
+    p.seed_packed(a, 3, 0.5)
+    fin = p.run_packed(a, b, 3)
+    assert np.array_equal(cells(p, fin), want[3])
 
 
 @pytest.mark.parametrize("rule", RULES)
@@ -198,8 +237,13 @@ def run_sharded_packed_local(name, r, nranks, steps, g=0):
 @pytest.mark.parametrize("name,r,nranks,g", [("sierpinski-triangle", 10, 2, 3), ("sierpinski-triangle", 12, 3, 4),
                                              ("sierpinski-triangle", 13, 8, 5), ("sierpinski-carpet", 5, 4, 2),
                                              ("empty-bottles", 6, 5, 2), ("sierpinski-triangle", 14, 2, 7),
-                                             ("sierpinski-triangle", 4, 4, 1)])  # the last: 3 empty shards
-def test_sharded_packed_equals_oracle(name, r, nranks, g):
+                                             ("sierpinski-triangle", 4, 4, 1),  # 3 empty shards
+                                             ("sierpinski-carpet", 7, 3, 4), ("sierpinski-carpet", 7, 2, 4)])
+def test_sharded_packed_equals_oracle(monkeypatch, name, r, nranks, g):
+    if name == "sierpinski-carpet" and g == 4:  # compacted gathers, halo bits among them; overflow at P=2
+        monkeypatch.setenv("SQZ_PACKED_GRID", "1")
+        if nranks == 2:
+            monkeypatch.setenv("SQZ_PACKED_RCAP", "512")
     got = run_sharded_packed_local(name, r, nranks, 5, g)
     assert np.array_equal(got, oracle_run(name, r, 42, 0.5, 5)[5])
 
@@ -310,7 +354,7 @@ def test_run_host_packed_round_trip():
     assert np.array_equal(cells(p, dev), want)
 
 
-@pytest.mark.parametrize("name,r,g", [("sierpinski-carpet", 10, 3), ("empty-bottles", 11, 4)])
+@pytest.mark.parametrize("name,r,g", [("sierpinski-carpet", 10, 3), ("sierpinski-carpet", 10, 4), ("empty-bottles", 11, 4)])
 def test_packed_config3_full_size(name, r, g):
     """BASELINE configs[3] on the packed state at the bench's tile levels (1.07e9 / 1.98e9 cells):
     step 1 from the seed equals the byte path's step 1 (itself checked against the oracle in
