@@ -2,7 +2,7 @@
 byte tile step (+ literal step), the streaming large-tile byte step, packed step at small and
 level-7 tiles, packed/byte conversions, heat step, BB steps (bit-sliced and per-cell), the 1-bit
 end-to-end run, sharded steps with a halo, the fused peer-memory halo (PEER variants of both byte
-kernels + squeeze_halo_peer_push), tensor-core ν map."""
+kernels + squeeze_halo_peer_push), tensor-core ν map, the packed step's compacted link gathers."""
 import os
 import sys
 
@@ -55,6 +55,28 @@ for p in parts:
     p.step(s, st)
 torch.cuda.synchronize()
 print("ok sharded", flush=True)
+
+# packed step with the compacted link-gather buffer (carpet level 4, E = 328): several chunks per
+# CTA, the buffer overflowing (synchronous reads), then sharded with a halo
+os.environ["SQZ_PACKED_GRID"], os.environ["SQZ_PACKED_RCAP"] = "1", "256"
+p = pkg.Squeeze(pkg.builtin_fractal("sierpinski-carpet"), 7, device=0, tile_level=4)
+pa, pb = p.new_packed(), p.new_packed()
+p.seed_packed(pa, 42, 0.5)
+p.run_packed(pa, pb, 3)
+del os.environ["SQZ_PACKED_RCAP"]
+f = pkg.builtin_fractal("sierpinski-carpet")
+parts = [pkg.Squeeze(f, 7, rank=i, nranks=2, device=0, tile_level=4) for i in range(2)]
+for p in parts:
+    nd = p.halo_needs()
+    rv = torch.zeros(max(1, len(nd)), dtype=torch.uint8, device="cuda")
+    p.halo_set_sends(np.zeros(0, np.uint64))
+    p.halo_bind(None, rv)
+    a, b = p.new_packed(), p.new_packed()
+    p.seed_packed(a, 42, 0.5)
+    p.run_packed(a, b, 2)
+del os.environ["SQZ_PACKED_GRID"]
+torch.cuda.synchronize()
+print("ok packed compacted gathers", flush=True)
 
 # BB engine: bit-sliced (n % 32 == 0) and per-cell (s = 3)
 for name, r in [("sierpinski-triangle", 7), ("sierpinski-triangle", 11), ("sierpinski-carpet", 3)]:
