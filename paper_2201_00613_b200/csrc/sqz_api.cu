@@ -98,6 +98,7 @@ struct Ctx {
   bool stream = false;
   int stream_minb = 1, stream_grid = 0;
   uint32_t stream_sin = 0;
+  uint32_t stream_srcap = 0;  // compacted gather buffer of the streaming step (words; 0 = [32][E])
   std::map<uint32_t, BlockLevel> blocks;  // by m = log_s rho
   // CUDA graph of the two-step ping-pong
   cudaGraphExec_t graph = nullptr;
@@ -247,6 +248,7 @@ TileParams tile_params(const Ctx* c) {
   p.pstages = c->packed_stages;
   p.rcap = c->packed_rcap;
   p.sin = c->stream_sin;
+  p.srcap = c->stream_srcap;
   if (c->peer_parity >= 0 && c->d_peer_chunk_start) {
     p.peer_recv = c->d_peer_recv[c->peer_parity];
     p.peer_chunk_start = c->d_peer_chunk_start;
@@ -502,6 +504,7 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       if (c->stream) {
         if (c->tt.K > 0xFFFFu || !stream_plan(p, c->nranks > 1, &c->stream_minb)) return fail(SQZ_E_INVALID_LEVEL);
         c->stream_sin = p.sin;
+        c->stream_srcap = p.srcap;
         c->tile_smem = stream_smem_bytes(p, c->nranks > 1);
         c->tile_threads = stream_threads();
         const cudaError_t se = stream_prepare(p, c->tile_smem, c->stream_minb, &occ);
@@ -511,6 +514,8 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
                   cudaGetErrorString(se));
         if (se != cudaSuccess) return fail(SQZ_E_INVALID_LEVEL);
         c->stream_grid = sms * std::max(1, occ);
+        if (const char* e = getenv("SQZ_STREAM_GRID"))  // tests: several chunks per CTA at small sizes
+          if (atoi(e) > 0) c->stream_grid = std::min(c->stream_grid, atoi(e));
       }
       if (c->opts.ctas_per_sm) occ = std::min<int>(occ, (int)c->opts.ctas_per_sm);
       c->tile_grid = sms * std::max(1, occ);

@@ -61,6 +61,7 @@ struct TileParams {
   uint32_t sin;        // input slice-ring depth of the large-tile byte step (sqz_stream.cu)
   uint32_t rcap;       // packed step, link items with E > kMaxPrefetchLinks: words of the compacted
                        // gather buffer (0 otherwise; sqz_packed.cu)
+  uint32_t srcap;      // large-tile byte step: words of its compacted gather buffer (0: [32][E]; sqz_stream.cu)
 };
 
 // ν as an integer tensor-core product (sqz_mma.cu, SURVEY NEXT-3 ablation).

@@ -24,6 +24,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "sqz_bits.cuh"
 
 namespace sqz {
@@ -45,7 +47,11 @@ struct StreamSmem {
   uint32_t* Wn;     // PEER: the chunk's new state words (bit i = tile i), K words
   uint32_t* ntl;    // [2][ndirs][32] neighbour tile + 1 of each lane's tile, by chunk parity
   uint32_t* G;      // [32][E] word holding the neighbour byte of link e for tile i, where tile i's
-                    // neighbour tile lies outside the chunk (this chunk's gathers)
+                    // neighbour tile lies outside the chunk (this chunk's gathers); or COMPACTED
+                    // (p.srcap words: only the chunk's outside (tile, link) pairs, see link_prefetch)
+  uint32_t* gctr;   // compacted G: [2] words allocated per chunk parity
+  uint32_t* grb;    // compacted G: [2][kStreamMaxItems] first word of each group item's gathers
+  uint32_t* grbb;   // compacted G: [2][E] first word of each short link's gathers (ballot items)
   uint32_t* lj2;    // [E] link e: its cell in the neighbour tile | direction << 16
   uint32_t* items;  // [kStreamMaxItems] link work items (see link_items)
   uint32_t* nitems;
@@ -69,7 +75,13 @@ __host__ __device__ inline size_t stream_layout(const TileParams& p, bool peer, 
   if (s) s->ntl = (uint32_t*)(base + off);
   off += (size_t)2 * (p.ndirs ? p.ndirs : 1) * kChunkTiles * 4;
   if (s) s->G = (uint32_t*)(base + off);
-  off += (size_t)(p.E ? p.E : 1) * kChunkTiles * 4;
+  off += p.srcap ? align16((size_t)p.srcap * 4) : (size_t)(p.E ? p.E : 1) * kChunkTiles * 4;
+  if (s) s->gctr = (uint32_t*)(base + off);
+  off += 16;
+  if (s) s->grb = (uint32_t*)(base + off);
+  off += p.srcap ? (size_t)2 * kStreamMaxItems * 4 : 0;
+  if (s) s->grbb = (uint32_t*)(base + off);
+  off += p.srcap ? align16((size_t)2 * (p.E ? p.E : 1) * 4) : 0;
   if (s) s->lj2 = (uint32_t*)(base + off);
   off += align16((size_t)(p.E ? p.E : 1) * 4);
   if (s) s->items = (uint32_t*)(base + off);
@@ -172,26 +184,51 @@ __device__ __forceinline__ LinkGroup link_group(const StreamSmem& S, uint32_t it
   return g;
 }
 
+// The word holding byte j2 of local tile tl (its 4-byte group), or for another shard's tile the
+// cell from the halo placed at its byte: a compacted G's overflow, read synchronously.
+__device__ __forceinline__ uint32_t stream_gather(const TileParams& p, const uint8_t* __restrict__ cur, uint32_t tl,
+                                                  uint32_t j2, uint32_t nloc) {
+  if (tl >= nloc) return fetch_cell(cur, (uint64_t)(tl + (uint32_t)p.tile_lo) * p.K + j2, p.halo) << (8 * (j2 & 3u));
+  return __ldg(reinterpret_cast<const uint32_t*>(cur + (uint64_t)tl * p.Kp + (j2 & ~3u)));
+}
+
 // Item k = warp cw, cw + NW, ...: for every tile i of chunk c whose neighbour tile in the item's
 // direction lies outside the chunk, the 4-byte word holding the neighbour cell of each of the
 // item's links, into G[i][e], by cp.async (or, for another shard's tile, from the halo).  The
 // same warp consumes them in Phase B of chunk c.  Tile indices fit 32 bits (checked on the host).
+// COMPACTED G (p.srcap != 0, link-heavy tiles at two CTAs per SM): only the chunk's (outside tile,
+// link) pairs get a word; each item takes its words with one shared atomicAdd on the chunk parity's
+// counter and records where they start (grb / grbb), the words of its r-th outside tile (ballot
+// order) being base + r n + link (group items) or base + rank of the tile (ballot items); pairs past
+// srcap are read synchronously by link_words (stream_gather).
 __device__ __forceinline__ void link_prefetch(const TileParams& p, const StreamSmem& S, const uint32_t* ntl,
-                                              const ChunkInfo& c, const uint8_t* __restrict__ cur, int cw, int lane) {
+                                              const ChunkInfo& c, const uint8_t* __restrict__ cur, int cw, int lane,
+                                              uint32_t par) {
   const uint32_t t0 = (uint32_t)c.t0, tlo = (uint32_t)p.tile_lo, nloc = (uint32_t)(p.tile_hi - p.tile_lo);
-  const uint32_t ni = *S.nitems, E = p.E;
+  const uint32_t ni = *S.nitems, E = p.E, cap = p.srcap, lt = (1u << lane) - 1u;
   for (uint32_t k = (uint32_t)cw; k < ni; k += kStreamNW) {
     const uint32_t item = S.items[k];
     if (item & kBallotItem) {  // lane = tile, link by link
       const uint32_t i0 = item & 0x7FFu, n = ((item >> 11) & 31u) + 1u;
-      const uint32_t gs = smem_u32(S.G) + 4u * (uint32_t)lane * E;
       for (uint32_t i = i0; i < i0 + n; ++i) {
         const uint32_t e = S.slinks[i], le = S.lj2[e], j2 = le & 0xFFFFu;
         const uint32_t a1 = ntl[(le >> 16) * kChunkTiles + lane];
         const uint32_t tl = a1 - 1u - tlo;
         const bool out = a1 != 0u && a1 - 1u - t0 >= c.nt;
-        if (out && tl >= nloc) S.G[lane * E + e] = fetch_cell(cur, (uint64_t)(a1 - 1u) * p.K + j2, p.halo) << (8 * (j2 & 3u));
-        else cp_async4_if(gs + 4u * e, cur + (uint64_t)(out ? tl : 0u) * p.Kp + (j2 & ~3u), out ? 1u : 0u);
+        uint32_t slot = (uint32_t)lane * E + e;
+        bool fits = true;
+        if (cap) {
+          const uint32_t om = __ballot_sync(0xFFFFFFFFu, out);
+          uint32_t base = 0;
+          if (lane == 0 && om) base = atomicAdd(&S.gctr[par], (uint32_t)__popc(om));
+          base = __shfl_sync(0xFFFFFFFFu, base, 0);
+          if (lane == 0) S.grbb[par * E + i] = base;
+          slot = base + (uint32_t)__popc(om & lt);
+          fits = slot < cap;
+        }
+        if (out && fits && tl >= nloc) S.G[slot] = fetch_cell(cur, (uint64_t)(a1 - 1u) * p.K + j2, p.halo) << (8 * (j2 & 3u));
+        else cp_async4_if(smem_u32(S.G) + 4u * (fits ? slot : 0u), cur + (uint64_t)(out ? tl : 0u) * p.Kp + (j2 & ~3u),
+                          out && fits ? 1u : 0u);
       }
       continue;
     }
@@ -201,15 +238,26 @@ __device__ __forceinline__ void link_prefetch(const TileParams& p, const StreamS
     const bool out = a1 != 0u && a1 - 1u - t0 >= c.nt;
     uint32_t om = __ballot_sync(0xFFFFFFFFu, out);
     const uint32_t farm = __ballot_sync(0xFFFFFFFFu, out && tl >= nloc);  // outside this shard: the halo
-    const uint32_t gs = smem_u32(S.G) + 4u * g.e, jo = g.j2 & ~3u, pv = g.valid ? 1u : 0u;
+    const uint32_t n = ((item >> 11) & 31u) + 1u, jo = g.j2 & ~3u, pv = g.valid ? 1u : 0u;
+    uint32_t br = 0;  // compacted: first word of the current outside tile's n links
+    if (cap) {
+      const uint32_t cnt = (uint32_t)__popc(om) * n;
+      if (lane == 0 && cnt) br = atomicAdd(&S.gctr[par], cnt);
+      br = __shfl_sync(0xFFFFFFFFu, br, 0);
+      if (lane == 0) S.grb[par * kStreamMaxItems + k] = br;
+    }
+    const uint32_t gs = smem_u32(S.G) + 4u * g.e;
     while (om) {
       const uint32_t i = __ffs(om) - 1u;
       om &= om - 1u;
       const uint32_t tli = __shfl_sync(0xFFFFFFFFu, tl, i);
+      const uint32_t dst = cap ? smem_u32(S.G) + 4u * (br + (uint32_t)lane) : gs + i * (E * 4u);
+      const uint32_t ok = cap ? (br + n <= cap ? pv : 0u) : pv;
+      br += n;
       if (!((farm >> i) & 1u)) {
-        cp_async4_if(gs + i * (E * 4u), cur + (uint64_t)tli * p.Kp + jo, pv);
-      } else if (g.valid) {  // another shard's tile (sharded contexts): rare, synchronous
-        S.G[i * E + g.e] = fetch_cell(cur, (uint64_t)(tli + tlo) * p.K + g.j2, p.halo) << (8 * (g.j2 & 3u));
+        cp_async4_if(ok ? dst : smem_u32(S.G), cur + (uint64_t)tli * p.Kp + jo, ok);
+      } else if (ok) {  // another shard's tile (sharded contexts): rare, synchronous
+        sts32(dst, fetch_cell(cur, (uint64_t)(tli + tlo) * p.K + g.j2, p.halo) << (8 * (g.j2 & 3u)));
       }
     }
   }
@@ -218,8 +266,10 @@ __device__ __forceinline__ void link_prefetch(const TileParams& p, const StreamS
 
 // Phase B for item k of chunk c: link word e (bit i = neighbour cell of tile i) -> Z[K + e].
 __device__ __forceinline__ void link_words(const TileParams& p, const StreamSmem& S, uint32_t* Z,
-                                           const uint32_t* ntl, const ChunkInfo& c, int cw, int lane) {
-  const uint32_t t0 = (uint32_t)c.t0, ni = *S.nitems, E = p.E, K = (uint32_t)p.K;
+                                           const uint32_t* ntl, const ChunkInfo& c, const uint8_t* __restrict__ cur,
+                                           int cw, int lane, uint32_t par) {
+  const uint32_t t0 = (uint32_t)c.t0, ni = *S.nitems, E = p.E, K = (uint32_t)p.K, cap = p.srcap;
+  const uint32_t tlo = (uint32_t)p.tile_lo, nloc = (uint32_t)(p.tile_hi - p.tile_lo), lt = (1u << lane) - 1u;
   for (uint32_t k = (uint32_t)cw; k < ni; k += kStreamNW) {
     const uint32_t item = S.items[k];
     if (item & kBallotItem) {  // lane = tile, one ballot per link
@@ -229,7 +279,15 @@ __device__ __forceinline__ void link_words(const TileParams& p, const StreamSmem
         const uint32_t a1 = ntl[(le >> 16) * kChunkTiles + lane];
         const uint32_t rel = a1 - 1u - t0;
         const bool inside = a1 != 0u && rel < c.nt;
-        const uint32_t v = inside ? Z[j2] >> (rel & 31u) : a1 != 0u ? S.G[lane * E + e] >> (8u * (j2 & 3u)) : 0u;
+        uint32_t gw = 0;
+        if (cap) {
+          const uint32_t om = __ballot_sync(0xFFFFFFFFu, a1 != 0u && !inside);
+          const uint32_t slot = S.grbb[par * E + i] + (uint32_t)__popc(om & lt);
+          if (a1 != 0u && !inside) gw = slot < cap ? S.G[slot] : stream_gather(p, cur, a1 - 1u - tlo, j2, nloc);
+        } else if (a1 != 0u && !inside) {
+          gw = S.G[lane * E + e];
+        }
+        const uint32_t v = inside ? Z[j2] >> (rel & 31u) : gw >> (8u * (j2 & 3u));
         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v & 1u);
         if (lane == 0) Z[K + e] = bal;
       }
@@ -250,7 +308,20 @@ __device__ __forceinline__ void link_words(const TileParams& p, const StreamSmem
       im &= ~m;
       w |= __funnelshift_r(z, z, dd) & m;
     }
-    const uint32_t gs = smem_u32(S.G) + 4u * g.e, sh = 8u * (g.j2 & 3u);
+    const uint32_t sh = 8u * (g.j2 & 3u);
+    if (cap) {  // compacted: the gathered words in the prefetch's order
+      const uint32_t n = ((item >> 11) & 31u) + 1u, tl = a1 - 1u - tlo;
+      uint32_t br = S.grb[par * kStreamMaxItems + k];
+      while (om) {
+        const uint32_t i = __ffs(om) - 1u;
+        om &= om - 1u;
+        const uint32_t tli = __shfl_sync(0xFFFFFFFFu, tl, i);
+        const uint32_t gv = !g.valid ? 0u : br + n <= cap ? S.G[br + lane] : stream_gather(p, cur, tli, g.j2, nloc);
+        br += n;
+        w |= ((gv >> sh) & 1u) << i;
+      }
+    }
+    const uint32_t gs = smem_u32(S.G) + 4u * g.e;
     while (om) {  // tiles whose neighbour tile is outside the chunk: the gathered words, two at a time
       const uint32_t i = __ffs(om) - 1u;
       om &= om - 1u;
@@ -287,6 +358,7 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
 
   for (uint32_t e = tid; e < E; e += blockDim.x) S.lj2[e] = p.link_j2[e] | ((uint32_t)p.link_dir[e] << 16);
   if (tid == 0) {
+    S.gctr[0] = S.gctr[1] = 0;
     link_items(p, S);
     S.Z0[p.zslot] = 0;
     S.Z0[S.zn + p.zslot] = 0;
@@ -376,12 +448,13 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
     if (blockIdx.x + G < p.nchunks) adj_prefetch(p, S.ntl + ntl_words, chunk_info(p, blockIdx.x + G), cw, lane);
     cp_async_wait_all();
     consumers_sync();
-    link_prefetch(p, S, S.ntl, chunk_info(p, blockIdx.x), cur, cw, lane);
+    link_prefetch(p, S, S.ntl, chunk_info(p, blockIdx.x), cur, cw, lane, 0u);
   }
 
   uint32_t seq = 0, it = 0;
   for (uint64_t chunk = blockIdx.x; chunk < p.nchunks; chunk += G, seq += nsl, ++it) {
     const ChunkInfo c = chunk_info(p, chunk);
+    if (cw == 0 && lane == 0) S.gctr[(it + 1) & 1u] = 0;  // compacted G: chunk it+1's prefetch allocates from it
     uint32_t* ntl = S.ntl + (it & 1) * ntl_words;
     uint32_t* Zb = S.Z0 + (it & 1) * S.zn;  // double-buffered: no barrier between C+D and the next Phase A
     const uint32_t z_s = smem_u32(Zb);
@@ -423,7 +496,7 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
     consumers_sync();     // Z, R and both adjacency buffers visible to every consumer warp
 
     // Phase B: link words, by link groups (lane = link)
-    link_words(p, S, Zb, ntl, c, cw, lane);
+    link_words(p, S, Zb, ntl, c, cur, cw, lane, it & 1u);
 
     // Phase C+D: j-block q * NW + cw -> HBM (lane = tile: one 256-bit store of its 32 cells)
     const uint32_t live_lanes = c.nt >= 32 ? 0xFFFFFFFFu : ((1u << c.nt) - 1u);
@@ -500,7 +573,8 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
       if ((uint32_t)i < nsl && !((lmask >> i) & 1u)) slice_out((uint32_t)i * kStreamSW, rows[i]);
     consumers_sync();  // link words published; G and this chunk's adjacency buffer are free
     if (chunk + 2 * G < p.nchunks) adj_prefetch(p, ntl, chunk_info(p, chunk + 2 * G), cw, lane);
-    if (chunk + G < p.nchunks) link_prefetch(p, S, S.ntl + ((it + 1) & 1) * ntl_words, chunk_info(p, chunk + G), cur, cw, lane);
+    if (chunk + G < p.nchunks)
+      link_prefetch(p, S, S.ntl + ((it + 1) & 1) * ntl_words, chunk_info(p, chunk + G), cur, cw, lane, (it + 1) & 1u);
 #pragma unroll
     for (int i = 0; i < RP; ++i) {  // pairs reading link words (or a pair past the chunk's slices)
       if ((uint32_t)(2 * i + 1) < nsl) {
@@ -559,12 +633,33 @@ static StreamFn pick_stream_t(const TileParams& p, int minb) {
 // a level-4 carpet but one slice in flight while the current one is computed), else 4.
 bool stream_plan(TileParams& p, bool peer, int* minb) {
   if (p.E > kStreamMaxLinks) return false;
-  const size_t cap = 227 * 1024;
+  // one CTA per SM: 227 KB; two: 113 KB each (228 KB per SM, 1 KB of it reserved per CTA)
+  const size_t cap = 227 * 1024, cap2 = 113 * 1024;
   const char* force = getenv("SQZ_STREAM_CTAS");  // tuning knob: 1 or 2 CTAs per SM
   p.sin = 4;
-  if ((!force || atoi(force) >= 2) && 2 * stream_smem_bytes(p, peer) <= cap) {
+  p.srcap = 0;
+  if ((!force || atoi(force) >= 2) && stream_smem_bytes(p, peer) <= cap2) {
     *minb = 2;
     return true;
+  }
+  // link-heavy tiles (the carpet at level 4: [32][328] gather words = 42 KB): two CTAs per SM with
+  // the COMPACTED gather buffer (the chunk's outside (tile, link) pairs, at most ~2K words for the
+  // carpet), if it leaves room for the outside pairs of 4 tiles per link
+  const char* compact = getenv("SQZ_STREAM_COMPACT");  // tuning knob: 0 = never
+  if ((!force || atoi(force) >= 2) && (!compact || atoi(compact) != 0)) {
+    p.srcap = 32;
+    const size_t base = stream_smem_bytes(p, peer) - 32 * 4;
+    if (base < cap2) {
+      p.srcap = (uint32_t)((cap2 - base) / 4) & ~31u;
+      const char* rc = getenv("SQZ_STREAM_RCAP");  // tests: a smaller buffer (overflow read synchronously)
+      const uint32_t want = rc ? (uint32_t)atoi(rc) : 0u;
+      if (p.srcap >= 4 * p.E && stream_smem_bytes(p, peer) <= cap2) {
+        if (want) p.srcap = std::min(p.srcap, std::max(32u, want & ~31u));
+        *minb = 2;
+        return true;
+      }
+    }
+    p.srcap = 0;
   }
   *minb = 1;
   p.sin = 8;

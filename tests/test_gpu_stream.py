@@ -55,6 +55,33 @@ def test_stream_step_vs_oracle(name, r, g, steps):
         a, b = b, a
 
 
+# Link-heavy tiles at two CTAs per SM go through the COMPACTED gather buffer (the carpet at level 4:
+# [32][328] words would not fit twice; the full square at level 6 likewise).  The grid is capped so
+# each CTA walks several chunks (both counter parities) and the buffer so it overflows (read
+# synchronously); rcap None = the planned capacity.
+@pytest.mark.parametrize("rcap", [None, 32, 1024])
+@pytest.mark.parametrize("name,r,g,grid", [("sierpinski-carpet", 7, 4, 3), ("full-square", 9, 6, 1),
+                                           ("sierpinski-carpet", 6, 4, 0)])
+def test_stream_compacted_gathers(monkeypatch, rcap, name, r, g, grid):
+    if rcap is not None:
+        monkeypatch.setenv("SQZ_STREAM_RCAP", str(rcap))
+    if grid:
+        monkeypatch.setenv("SQZ_STREAM_GRID", str(grid))
+    f = BUILTINS[name]
+    p = mk(name, r, tile_level=g)
+    assert p.geometry.byte_kernel == 1 and p.geometry.remote_links > 160
+    a, b = p.new_state(), p.new_state()
+    b.fill_(7)
+    p.seed(a, 5, 0.45)
+    cur = A.seed_compact(f, r, 5, 0.45)
+    for t in range(3):
+        p.step(a, b)
+        cur = A.compact_step(f, r, cur)
+        assert np.array_equal(host(p, b), cur), (t + 1)
+        assert padding_is_zero(p, b)
+        a, b = b, a
+
+
 def test_auto_levels_for_link_heavy_fractals():
     """The library takes the next tile level for link-heavy fractals (E/K > 2%) and the streaming
     step when a 32-tile chunk does not fit shared memory twice; Sierpinski keeps level 6 and the
