@@ -224,7 +224,7 @@ __device__ __forceinline__ void chunk_prefetch_items(const TileParams& p, const 
     const uint32_t item = S.items[k], i0 = item & 0x7FFu, n = ((item >> 11) & 31u) + 1u;
     if (item & kPackBallotItem) {  // lane = tile, link by link
       for (uint32_t i = i0; i < i0 + n; ++i) {
-        const uint32_t e = S.slinks[i], d = p.link_dir[e], j2 = p.link_j2[e];
+        const uint32_t e = S.slinks[i], sl = S.sl[4 * e], d = (sl & 1023u) >> 7, j2 = sl >> 10;  // (lane group 0's slot)
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q) {
           const uint32_t a1 = ntl[d * kPackTiles + q * 32 + lane], tl = a1 - 1u - tlo, t = q * 32 + lane;
@@ -248,7 +248,7 @@ __device__ __forceinline__ void chunk_prefetch_items(const TileParams& p, const 
       continue;
     }
     const uint32_t d = (item >> 16) & 0xFFu, q = (item >> 24) & 3u, valid = (uint32_t)lane < n ? 1u : 0u;
-    const uint32_t e = i0 + (valid ? (uint32_t)lane : 0u), j2 = p.link_j2[e];
+    const uint32_t e = i0 + (valid ? (uint32_t)lane : 0u), j2 = S.sl[4 * e] >> 10;
     {
       const uint32_t a1 = ntl[d * kPackTiles + q * 32 + lane], tl = a1 - 1u - tlo;  // lane = tile here
       const bool out = a1 != 0 && a1 - 1u - pc.t0 >= pc.nt;
@@ -291,7 +291,7 @@ __device__ __forceinline__ void chunk_link_items(const TileParams& p, const Pack
     const uint32_t item = S.items[k], i0 = item & 0x7FFu, n = ((item >> 11) & 31u) + 1u;
     if (item & kPackBallotItem) {  // lane = tile, one ballot per (link, q)
       for (uint32_t i = i0; i < i0 + n; ++i) {
-        const uint32_t e = S.slinks[i], d = p.link_dir[e], j2 = p.link_j2[e];
+        const uint32_t e = S.slinks[i], sl = S.sl[4 * e], d = (sl & 1023u) >> 7, j2 = sl >> 10;  // (lane group 0's slot)
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q) {
           const uint32_t a1 = ntl[d * kPackTiles + q * 32 + lane], rel = a1 - 1u - pc.t0, tl = a1 - 1u - tlo;
@@ -312,7 +312,7 @@ __device__ __forceinline__ void chunk_link_items(const TileParams& p, const Pack
       continue;
     }
     const uint32_t d = (item >> 16) & 0xFFu, q = (item >> 24) & 3u, valid = (uint32_t)lane < n ? 1u : 0u;
-    const uint32_t e = i0 + (valid ? (uint32_t)lane : 0u), j2 = p.link_j2[e];
+    const uint32_t e = i0 + (valid ? (uint32_t)lane : 0u), j2 = S.sl[4 * e] >> 10;
     const uint4 z = *reinterpret_cast<const uint4*>(Z + j2 * 4);  // the neighbour cell's word, all 128 tiles
     {
       const uint32_t a1 = ntl[d * kPackTiles + q * 32 + lane], rel = a1 - 1u - pc.t0, tl = a1 - 1u - tlo;  // lane = tile
@@ -325,7 +325,8 @@ __device__ __forceinline__ void chunk_link_items(const TileParams& p, const Pack
         const uint32_t kk = __shfl_sync(0xFFFFFFFFu, key, __ffs(im) - 1u);
         const uint32_t m = __ballot_sync(0xFFFFFFFFu, inside && key == kk);
         im &= ~m;
-        const uint32_t g = kk >> 5, src = g == 0 ? z.x : g == 1 ? z.y : g == 2 ? z.z : z.w;
+        const uint32_t lo = (kk & 32u) ? z.y : z.x, hi = (kk & 32u) ? z.w : z.z;  // source group kk >> 5, by selects
+        const uint32_t src = (kk & 64u) ? hi : lo;
         w |= __funnelshift_r(src, src, kk & 31u) & m;
       }
       if (compact) {  // the gathered words of the outside tiles, in the prefetch's order
@@ -571,15 +572,21 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
       }
       outc[j] = nw;
     };
+    // blocks past the register-resident ones read their neighbour-table rows through L1, one block
+    // ahead (the first one issued before the register blocks), so the load latency is hidden
+    const uint4* nbr4 = reinterpret_cast<const uint4*>(p.nbr);
+    uint32_t jb = (uint32_t)warp + (uint32_t)(RB * nwarps);
+    uint4 rown = jb * 32 + lane < K ? __ldg(nbr4 + jb * 32 + lane) : make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int i = 0; i < RB; ++i) {
       const uint32_t j = ((uint32_t)warp + (uint32_t)(i * nwarps)) * 32 + lane;
       if ((fullmask >> i) & 1u) word_full(j, off[i]);
       else word(j, off[i]);
     }
-    for (uint32_t jb = (uint32_t)warp + (uint32_t)(RB * nwarps); jb * 32 < Kw; jb += (uint32_t)nwarps) {
-      const uint32_t j = jb * 32 + lane;
-      const uint4 row = j < K ? __ldg(reinterpret_cast<const uint4*>(p.nbr) + j) : make_uint4(0, 0, 0, 0);
+    for (; jb * 32 < Kw; jb += (uint32_t)nwarps) {
+      const uint32_t j = jb * 32 + lane, jn = j + 32 * (uint32_t)nwarps;
+      const uint4 row = rown;
+      rown = jn < K ? __ldg(nbr4 + jn) : make_uint4(0, 0, 0, 0);
       const uint32_t w[4] = {row.x, row.y, row.z, row.w};
       uint32_t o[DMAX];
 #pragma unroll
