@@ -574,9 +574,13 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
     };
     // blocks past the register-resident ones read their neighbour-table rows through L1, one block
     // ahead (the first one issued before the register blocks), so the load latency is hidden
+    // (large-tile variants only: the small-tile ones, three CTAs per SM, hold every block's slots in
+    // registers, and the extra live row cost them 3% at the carpet's level 3)
+    constexpr bool kRowAhead = MINB < 3;
     const uint4* nbr4 = reinterpret_cast<const uint4*>(p.nbr);
     uint32_t jb = (uint32_t)warp + (uint32_t)(RB * nwarps);
-    uint4 rown = jb * 32 + lane < K ? __ldg(nbr4 + jb * 32 + lane) : make_uint4(0, 0, 0, 0);
+    uint4 rown = make_uint4(0, 0, 0, 0);
+    if (kRowAhead && jb * 32 + lane < K) rown = __ldg(nbr4 + jb * 32 + lane);
 #pragma unroll
     for (int i = 0; i < RB; ++i) {
       const uint32_t j = ((uint32_t)warp + (uint32_t)(i * nwarps)) * 32 + lane;
@@ -585,8 +589,13 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
     }
     for (; jb * 32 < Kw; jb += (uint32_t)nwarps) {
       const uint32_t j = jb * 32 + lane, jn = j + 32 * (uint32_t)nwarps;
-      const uint4 row = rown;
-      rown = jn < K ? __ldg(nbr4 + jn) : make_uint4(0, 0, 0, 0);
+      uint4 row;
+      if (kRowAhead) {
+        row = rown;
+        rown = jn < K ? __ldg(nbr4 + jn) : make_uint4(0, 0, 0, 0);
+      } else {
+        row = j < K ? __ldg(nbr4 + j) : make_uint4(0, 0, 0, 0);
+      }
       const uint32_t w[4] = {row.x, row.y, row.z, row.w};
       uint32_t o[DMAX];
 #pragma unroll

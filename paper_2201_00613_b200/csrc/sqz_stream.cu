@@ -572,6 +572,22 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
     for (int i = 2 * RP; i < RB; ++i)  // link-free single blocks
       if ((uint32_t)i < nsl && !((lmask >> i) & 1u)) slice_out((uint32_t)i * kStreamSW, rows[i]);
     consumers_sync();  // link words published; G and this chunk's adjacency buffer are free
+    // slices q >= RB read their neighbour-table rows through L1, one slice ahead (the first one now)
+    // so the load latency is hidden.  A partial last slice (r < NW blocks) goes to the LAST r warps
+    // here (Phase A gave it to the first r), so every warp carries the same number of blocks per chunk.
+    auto tail_block = [&](uint32_t q, uint32_t& qc) -> bool {  // false: no block of this warp in slice q
+      const uint32_t r = nblk - q * kStreamNW, sh = q + 1 == nsl && r < kStreamNW ? kStreamNW - r : 0u;
+      qc = q * kStreamSW - sh * 32;
+      return (uint32_t)cw >= sh;
+    };
+    // (one CTA per SM only: at two, 64 registers, the live row spills: bottles 0.85 -> 0.90 ms)
+    auto tail_row = [&](uint32_t q) -> uint4 {
+      uint32_t qc;
+      if (q >= nsl || !tail_block(q, qc) || jl + qc >= K) return make_uint4(0, 0, 0, 0);
+      return __ldg(reinterpret_cast<const uint4*>(p.nbr) + jl + qc);
+    };
+    uint4 rown = make_uint4(0, 0, 0, 0);
+    if (MINB == 1) rown = tail_row(RB);
     if (chunk + 2 * G < p.nchunks) adj_prefetch(p, ntl, chunk_info(p, chunk + 2 * G), cw, lane);
     if (chunk + G < p.nchunks)
       link_prefetch(p, S, S.ntl + ((it + 1) & 1) * ntl_words, chunk_info(p, chunk + G), cur, cw, lane, (it + 1) & 1u);
@@ -588,12 +604,15 @@ __global__ void __maxnreg__(StreamRegs<MINB>::n) k_step_stream(TileParams p, con
     for (int i = 2 * RP; i < RB; ++i)  // single blocks reading link words
       if ((uint32_t)i < nsl && ((lmask >> i) & 1u)) slice_out((uint32_t)i * kStreamSW, rows[i]);
     for (uint32_t q = RB; q < nsl; ++q) {
-      // a partial last slice (r < NW blocks) goes to the LAST r warps here (Phase A gave it to the
-      // first r), so every warp carries the same number of blocks per chunk
-      const uint32_t r = nblk - q * kStreamNW, sh = q + 1 == nsl && r < kStreamNW ? kStreamNW - r : 0u;
-      if ((uint32_t)cw < sh) continue;
-      const uint32_t qc = q * kStreamSW - sh * 32, j = jl + qc;
-      slice_out(qc, j < K ? __ldg(reinterpret_cast<const uint4*>(p.nbr) + j) : make_uint4(0, 0, 0, 0));
+      uint32_t qc;
+      const bool mine = tail_block(q, qc);
+      if (MINB == 1) {
+        const uint4 row = rown;
+        rown = tail_row(q + 1);
+        if (mine) slice_out(qc, row);
+      } else if (mine) {
+        slice_out(qc, tail_row(q));
+      }
     }
     if (PEER) consumers_sync();  // the chunk's new state words Wn complete for the halo epilogue
     if (PEER && cw == kStreamNW - 1 && pe1 > pe0) {
@@ -642,11 +661,13 @@ bool stream_plan(TileParams& p, bool peer, int* minb) {
     *minb = 2;
     return true;
   }
-  // link-heavy tiles (the carpet at level 4: [32][328] gather words = 42 KB): two CTAs per SM with
-  // the COMPACTED gather buffer (the chunk's outside (tile, link) pairs, at most ~2K words for the
-  // carpet), if it leaves room for the outside pairs of 4 tiles per link
-  const char* compact = getenv("SQZ_STREAM_COMPACT");  // tuning knob: 0 = never
-  if ((!force || atoi(force) >= 2) && (!compact || atoi(compact) != 0)) {
+  // link-heavy tiles (the carpet at level 4: [32][328] gather words = 42 KB) can run two CTAs per
+  // SM with the COMPACTED gather buffer (the chunk's outside (tile, link) pairs, at most ~2K words
+  // for the carpet), if it leaves room for the outside pairs of 4 tiles per link.  Opt-in: the
+  // carpet runs faster at one CTA per SM with 128 registers (0.515 against 0.523 ms; the full
+  // square at level 6 the other way round, 0.0474 against 0.0436 ms; profiles/ab/round2_stream_*)
+  const char* compact = getenv("SQZ_STREAM_COMPACT");  // tuning knob: 1 = two CTAs with compacted gathers
+  if ((!force || atoi(force) >= 2) && compact && atoi(compact) != 0) {
     p.srcap = 32;
     const size_t base = stream_smem_bytes(p, peer) - 32 * 4;
     if (base < cap2) {

@@ -55,14 +55,15 @@ def test_stream_step_vs_oracle(name, r, g, steps):
         a, b = b, a
 
 
-# Link-heavy tiles at two CTAs per SM go through the COMPACTED gather buffer (the carpet at level 4:
-# [32][328] words would not fit twice; the full square at level 6 likewise).  The grid is capped so
+# Link-heavy tiles at two CTAs per SM (SQZ_STREAM_COMPACT=1) go through the COMPACTED gather buffer
+# (the carpet at level 4: [32][328] words would not fit twice; the full square at level 6 likewise).  The grid is capped so
 # each CTA walks several chunks (both counter parities) and the buffer so it overflows (read
 # synchronously); rcap None = the planned capacity.
 @pytest.mark.parametrize("rcap", [None, 32, 1024])
 @pytest.mark.parametrize("name,r,g,grid", [("sierpinski-carpet", 7, 4, 3), ("full-square", 9, 6, 1),
                                            ("sierpinski-carpet", 6, 4, 0)])
 def test_stream_compacted_gathers(monkeypatch, rcap, name, r, g, grid):
+    monkeypatch.setenv("SQZ_STREAM_COMPACT", "1")
     if rcap is not None:
         monkeypatch.setenv("SQZ_STREAM_RCAP", str(rcap))
     if grid:
