@@ -60,6 +60,7 @@ struct Ctx {
   int packed_threads = 256;
   uint32_t packed_stages = 3;
   uint32_t packed_rcap = 0;  // compacted link-gather buffer of the packed step (words; 0 = none)
+  uint32_t packed_flags = 0;  // packed step options (sqz_packed.cu kPack*; A/B knobs)
   uint32_t Kw = 4;                    // packed words per chunk
   uint64_t packed_bytes = 0;
   int packed_grid = 0;
@@ -247,6 +248,7 @@ TileParams tile_params(const Ctx* c) {
   p.adj_stride = adj_stride(c);
   p.pstages = c->packed_stages;
   p.rcap = c->packed_rcap;
+  p.pflags = c->packed_flags;
   p.sin = c->stream_sin;
   p.srcap = c->stream_srcap;
   if (c->peer_parity >= 0 && c->d_peer_chunk_start) {
@@ -540,6 +542,9 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
         if (const char* e = getenv("SQZ_PACKED_RCAP")) p.rcap = std::min<uint32_t>(p.rcap, (uint32_t)atoi(e));  // tests: overflow
       }
       c->packed_rcap = p.rcap;
+      // A/B: the compacted gathers with the static link-item split (2) instead of the dynamic one
+      if (const char* e = getenv("SQZ_PACKED_STATIC_ITEMS")) c->packed_flags = atoi(e) ? 2u : 0u;
+      p.pflags = c->packed_flags;
       // a compacted-gather chunk leaves one CTA per SM: 16 warps instead of 8 (8 neighbour slots only)
       if (p.rcap && p.dmax > 5 && 2 * packed_smem_bytes(p) > 228 * 1024) c->packed_threads = 512;
       if (const char* e = getenv("SQZ_PACKED_THREADS"))  // A/B timing
@@ -549,7 +554,9 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       int pocc = 0;
       // a chunk of 128 tiles that does not fit shared memory leaves the packed step unavailable at
       // this tile level (its entry points return SQZ_E_INVALID_LEVEL), not the context
-      if (c->packed_smem <= 227 * 1024 && packed_prepare(p, c->packed_smem, c->packed_threads, &pocc) == cudaSuccess)
+      if (c->packed_smem <= 227 * 1024 &&
+          packed_items_fit(c->tt.dir_start.data(), c->tt.ndirs, c->tt.E, (uint32_t)c->packed_threads / 32) &&
+          packed_prepare(p, c->packed_smem, c->packed_threads, &pocc) == cudaSuccess)
         c->packed_grid = sms * std::max(1, pocc);
       else
         c->packed_grid = 0;

@@ -62,6 +62,7 @@ struct TileParams {
   uint32_t rcap;       // packed step, link items with E > kMaxPrefetchLinks: words of the compacted
                        // gather buffer (0 otherwise; sqz_packed.cu)
   uint32_t srcap;      // large-tile byte step: words of its compacted gather buffer (0: [32][E]; sqz_stream.cu)
+  uint32_t pflags;     // packed step options (sqz_packed.cu kPack* flags; tuning A/B only)
 };
 
 // ν as an integer tensor-core product (sqz_mma.cu, SURVEY NEXT-3 ablation).
@@ -99,6 +100,8 @@ cudaError_t launch_step_stream(const TileParams& p, const uint8_t* cur, uint8_t*
 size_t packed_smem_bytes(const TileParams& p);
 // true when the packed step gathers out-of-chunk links through a compacted buffer of p.rcap words
 bool packed_compact_gathers(const TileParams& p);
+// false when the packed step's link work items would overflow (sqz_packed.cu); dir_start on the host
+bool packed_items_fit(const uint16_t* dir_start, uint32_t ndirs, uint32_t E, uint32_t nwarps);
 cudaError_t packed_prepare(const TileParams& p, size_t smem, int threads, int* occupancy);
 cudaError_t launch_step_packed(const TileParams& p, const uint32_t* cur, uint32_t* next, int grid, int threads,
                                size_t smem, cudaStream_t st);

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "sqz_bits.cuh"
 
 namespace sqz {
@@ -28,6 +30,7 @@ constexpr uint32_t kPackMaxItems = 64;
 constexpr uint32_t kPackBallotItem = 1u << 31;
 constexpr uint32_t kPackLongDirection = 8;
 constexpr uint32_t kSlotBatch = 4;  // link slots per pass in the slot split (Sierpinski: 32 slots, 8 warps)
+constexpr uint32_t kPackStaticItems = 2;  // TileParams::pflags: compacted gathers with the static item split (A/B)
 
 __host__ __device__ inline uint32_t pack_zw(const TileParams& p) { return (p.Kw + p.E + 1) * 4; }
 
@@ -84,6 +87,23 @@ __host__ __device__ inline size_t packed_layout(const TileParams& p, uint8_t* ba
 
 size_t packed_smem_bytes(const TileParams& p) { return packed_layout(p, nullptr, nullptr); }
 bool packed_compact_gathers(const TileParams& p) { return prefetch_links(p) == 0; }
+
+// Host check of the link work items pack_link_items builds (BYDIR variants, E >= 3 ndirs): at most
+// kPackMaxItems of them, link indices below 2^11 (their 11-bit fields).  Contexts that fail it (a
+// line-like fractal whose tile is nearly all boundary) leave the packed step unavailable.
+bool packed_items_fit(const uint16_t* dir_start, uint32_t ndirs, uint32_t E, uint32_t nwarps) {
+  if (E < 3 * ndirs) return true;  // slot split: no items
+  if (E >= 2048 || nwarps == 0) return false;
+  uint32_t n = 0, ns = 0;
+  for (uint32_t d = 0; d < ndirs; ++d) {
+    const uint32_t nd = (uint32_t)dir_start[d + 1] - dir_start[d];
+    if (nd == 0) continue;
+    if (nd < kPackLongDirection) ns += nd;
+    else n += 4 * ((nd + 31) / 32);
+  }
+  const uint32_t free_w = nwarps - n % nwarps;
+  return n + (ns == 0 ? 0u : std::min(ns, free_w)) <= kPackMaxItems;
+}
 
 __host__ __device__ inline uint64_t pack_chunks(const TileParams& p) {
   return (p.tile_hi - p.tile_lo + kPackTiles - 1) / kPackTiles;
@@ -215,11 +235,13 @@ __device__ __forceinline__ uint32_t link_gather(const TileParams& p, const uint3
 template <bool SHARDED>
 __device__ __forceinline__ void chunk_prefetch_items(const TileParams& p, const PackSmem& S, const PackChunk& pc,
                                                      const uint32_t* ntl, const uint32_t* __restrict__ cur32,
-                                                     int warp, int nwarps, int lane, uint32_t par) {
+                                                     int warp, int nwarps, int lane, uint32_t par, uint32_t ro,
+                                                     uint32_t rcap) {
+  // compacted: words [ro, ro + rcap) of R (ro = 0, rcap = p.rcap; or one parity's half, DYN)
   const uint32_t E = p.E, ni = S.items[kPackMaxItems], tlo = (uint32_t)p.tile_lo, Kw = p.Kw;
   const uint32_t nloc = (uint32_t)(p.tile_hi - p.tile_lo), gs0 = smem_u32(S.R);
   const bool compact = prefetch_links(p) == 0;
-  const uint32_t rcap = p.rcap, lt = (1u << lane) - 1u;
+  const uint32_t lt = (1u << lane) - 1u;
   for (uint32_t k = (uint32_t)warp; k < ni; k += (uint32_t)nwarps) {
     const uint32_t item = S.items[k], i0 = item & 0x7FFu, n = ((item >> 11) & 31u) + 1u;
     if (item & kPackBallotItem) {  // lane = tile, link by link
@@ -239,6 +261,7 @@ __device__ __forceinline__ void chunk_prefetch_items(const TileParams& p, const 
             if (lane == 0) S.rbb[par * 4 * E + i * 4 + q] = base;
             slot = base + (uint32_t)__popc(om & lt);
             fits = slot < rcap;
+            slot += ro;
           }
           if (SHARDED && out && fits && tl >= nloc) S.R[slot] = halo_fetch(p.halo, (uint64_t)(a1 - 1u) * p.K + j2) << (tl & 31u);
           else cp_async4_if(gs0 + 4u * (fits ? slot : 0u), cur32 + ((uint64_t)((out ? tl : 0u) >> 7) * Kw + j2) * 4 + ((tl >> 5) & 3u),
@@ -261,15 +284,19 @@ __device__ __forceinline__ void chunk_prefetch_items(const TileParams& p, const 
         br = __shfl_sync(0xFFFFFFFFu, br, 0);
         if (lane == 0) S.rb[par * kPackMaxItems + k] = br;
       }
+      // the source word of tile tli: this link's word of chunk tli / 128, u32 lane (tli / 32) mod 4
+      const uint64_t gb = reinterpret_cast<uint64_t>(cur32) + (uint64_t)j2 * 16u;
+      const uint32_t kw16 = Kw * 16u;
       while (om) {  // lane = link from here on
         const uint32_t i = __ffs(om) - 1u;
         om &= om - 1u;
         const uint32_t tli = __shfl_sync(0xFFFFFFFFu, tl, i), t = q * 32 + i;
-        const uint32_t slot = compact ? br + (uint32_t)lane : t * E + e;
+        const uint32_t slot = compact ? ro + br + (uint32_t)lane : t * E + e;
         const uint32_t ok = compact ? (br + n <= rcap ? valid : 0u) : valid;
         br += n;
         if (!SHARDED || !((farm >> i) & 1u))
-          cp_async4_if(gs0 + 4u * (ok ? slot : 0u), cur32 + ((uint64_t)(tli >> 7) * Kw + j2) * 4 + ((tli >> 5) & 3u), ok);
+          cp_async4_if(gs0 + 4u * (ok ? slot : 0u),
+                       reinterpret_cast<const void*>(gb + (uint64_t)(tli >> 7) * kw16 + ((tli >> 3) & 12u)), ok);
         else if (ok)  // another shard's tile (sharded contexts): the bit from the halo, placed where it is read
           S.R[slot] = halo_fetch(p.halo, (uint64_t)(tli + tlo) * p.K + j2) << (tli & 31u);
       }
@@ -281,13 +308,21 @@ __device__ __forceinline__ void chunk_prefetch_items(const TileParams& p, const 
 // Link words of chunk pc (BYDIR items): bit i of u32 lane q of word Kw + e = cell j2 of the
 // neighbour tile (link e) of tile 32q + i.
 template <bool SHARDED>
+// dctr != nullptr (DYN): items are taken dynamically from that shared counter (their gathers were
+// completed before a CTA barrier, so any warp may read them); else item k belongs to warp k mod W.
 __device__ __forceinline__ void chunk_link_items(const TileParams& p, const PackSmem& S, const PackChunk& pc,
                                                  const uint32_t* ntl, uint32_t* Z, const uint32_t* __restrict__ cur32,
-                                                 int warp, int nwarps, int lane, uint32_t par) {
+                                                 int warp, int nwarps, int lane, uint32_t par, uint32_t ro,
+                                                 uint32_t rcap, uint32_t* dctr) {
   const uint32_t E = p.E, ni = S.items[kPackMaxItems], tlo = (uint32_t)p.tile_lo, Kw = p.Kw;
   const bool compact = prefetch_links(p) == 0;
-  const uint32_t rcap = p.rcap, lt = (1u << lane) - 1u, nloc = (uint32_t)(p.tile_hi - p.tile_lo);
-  for (uint32_t k = (uint32_t)warp; k < ni; k += (uint32_t)nwarps) {
+  const uint32_t lt = (1u << lane) - 1u, nloc = (uint32_t)(p.tile_hi - p.tile_lo);
+  auto grab = [&]() -> uint32_t {
+    uint32_t v = 0;
+    if (lane == 0) v = atomicAdd(dctr, 1u);
+    return __shfl_sync(0xFFFFFFFFu, v, 0);
+  };
+  for (uint32_t k = dctr ? grab() : (uint32_t)warp; k < ni; k = dctr ? grab() : k + (uint32_t)nwarps) {
     const uint32_t item = S.items[k], i0 = item & 0x7FFu, n = ((item >> 11) & 31u) + 1u;
     if (item & kPackBallotItem) {  // lane = tile, one ballot per (link, q)
       for (uint32_t i = i0; i < i0 + n; ++i) {
@@ -300,7 +335,7 @@ __device__ __forceinline__ void chunk_link_items(const TileParams& p, const Pack
           if (compact) {
             const uint32_t om = __ballot_sync(0xFFFFFFFFu, a1 != 0 && !in);
             const uint32_t slot = S.rbb[par * 4 * E + i * 4 + q] + (uint32_t)__popc(om & lt);
-            g = a1 == 0 || in ? 0u : slot < rcap ? S.R[slot] : link_gather<SHARDED>(p, cur32, tl, j2, nloc);
+            g = a1 == 0 || in ? 0u : slot < rcap ? S.R[ro + slot] : link_gather<SHARDED>(p, cur32, tl, j2, nloc);
           } else {
             g = a1 == 0 || in ? 0u : S.R[(q * 32 + lane) * E + e];
           }
@@ -331,13 +366,18 @@ __device__ __forceinline__ void chunk_link_items(const TileParams& p, const Pack
       }
       if (compact) {  // the gathered words of the outside tiles, in the prefetch's order
         uint32_t br = S.rb[par * kPackMaxItems + k];
-        while (om) {
+        while (om) {  // two outside tiles at a time (independent loads)
           const uint32_t i = __ffs(om) - 1u;
           om &= om - 1u;
-          const uint32_t tli = __shfl_sync(0xFFFFFFFFu, tl, i);
-          const uint32_t g = !valid ? 0u : br + n <= rcap ? S.R[br + lane] : link_gather<SHARDED>(p, cur32, tli, j2, nloc);
-          br += n;
-          w |= ((g >> (tli & 31u)) & 1u) << i;
+          const bool two = om != 0u;
+          const uint32_t i2 = two ? __ffs(om) - 1u : i;
+          om &= om - 1u;
+          const uint32_t t1 = __shfl_sync(0xFFFFFFFFu, tl, i), t2 = __shfl_sync(0xFFFFFFFFu, tl, i2);
+          const uint32_t b1 = br, b2 = two ? br + n : br;
+          br = b2 + n;
+          const uint32_t g1 = !valid ? 0u : b1 + n <= rcap ? S.R[ro + b1 + lane] : link_gather<SHARDED>(p, cur32, t1, j2, nloc);
+          const uint32_t g2 = !valid ? 0u : b2 + n <= rcap ? S.R[ro + b2 + lane] : link_gather<SHARDED>(p, cur32, t2, j2, nloc);
+          w |= (((g1 >> (t1 & 31u)) & 1u) << i) | (((g2 >> (t2 & 31u)) & 1u) << i2);
         }
       }
       while (om) {  // tiles whose neighbour tile is outside the chunk: the gathered words, two at a time
@@ -357,8 +397,8 @@ __device__ __forceinline__ void chunk_link_items(const TileParams& p, const Pack
 template <bool SHARDED, bool BYDIR>
 __device__ __forceinline__ void chunk_prefetch(const TileParams& p, const PackSmem& S, const PackChunk& pc,
                                                const uint32_t* ntl, const uint32_t* __restrict__ cur32, int warp,
-                                               int nwarps, int lane, uint32_t par) {
-  if (BYDIR) chunk_prefetch_items<SHARDED>(p, S, pc, ntl, cur32, warp, nwarps, lane, par);
+                                               int nwarps, int lane, uint32_t par, uint32_t ro, uint32_t rcap) {
+  if (BYDIR) chunk_prefetch_items<SHARDED>(p, S, pc, ntl, cur32, warp, nwarps, lane, par, ro, rcap);
   else chunk_prefetch_slots<SHARDED>(p, S, pc, ntl, cur32, warp, nwarps, lane);
 }
 
@@ -393,7 +433,11 @@ __device__ __forceinline__ uint32_t cell_rule(const uint32_t* x, uint32_t alive,
 // DMAX: neighbour slots per cell (5 for the Sierpinski triangle, else 8).  RB: j-blocks per warp
 // whose neighbour slots stay in registers for the whole launch (block jb = warp + i * W); later
 // blocks read their slots through L1.
-template <int DMAX, bool CONWAY, int RB, int MAXT, int MINB, bool SHARDED, bool BYDIR>
+// DYN (link items with compacted gathers, one CTA per SM): the out-of-chunk gathers run TWO chunks
+// ahead into R halves by chunk parity and complete before the chunk barrier in between, so the link
+// items of a chunk can be taken dynamically by whichever warp is free (the static split left 21% of
+// the carpet's stall samples at the chunk barrier, waiting for the warps with the costliest items).
+template <int DMAX, bool CONWAY, int RB, int MAXT, int MINB, bool SHARDED, bool BYDIR, bool DYN>
 __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const uint4* __restrict__ cur,
                                                         uint4* __restrict__ next) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -425,7 +469,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
   for (uint32_t u = tid; u < 4 * E; u += blockDim.x)
     S.sl[u] = (p.link_j2[u >> 2] << 10) | (p.link_dir[u >> 2] * kPackTiles + 32 * (u & 3u));
   if (tid == 0) {
-    S.rctr[0] = S.rctr[1] = 0;
+    S.rctr[0] = S.rctr[1] = S.rctr[2] = S.rctr[3] = 0;  // allocation counters, DYN item counters
     if (BYDIR) pack_link_items(p, S, (uint32_t)nwarps);
     for (uint32_t s = 0; s < NS + kAdjSlots; ++s) mbar_init(&S.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -439,8 +483,18 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
     for (uint32_t s = 0; s + 1 < NS && c + s * G < nch; ++s) state_load(p, S, pack_chunk(p, c + s * G), s, cur);
     for (uint32_t a = 0; a + 1 < kAdjSlots && c + a * G < nch; ++a) adj_load(p, S, pack_chunk(p, c + a * G), a);
   }
+  const uint32_t rh = DYN ? (p.rcap / 2) & ~31u : p.rcap;  // DYN: R in two halves by chunk parity
+  auto ro_of = [&](uint32_t par) -> uint32_t { return DYN ? par * rh : 0u; };
   mbar_wait(S.abar(0), 0);
-  chunk_prefetch<SHARDED, BYDIR>(p, S, pack_chunk(p, c), S.ntl(0), cur32, warp, nwarps, lane, 0u);
+  chunk_prefetch<SHARDED, BYDIR>(p, S, pack_chunk(p, c), S.ntl(0), cur32, warp, nwarps, lane, 0u, 0u, rh);
+  if (DYN) {  // the second chunk's gathers too; both complete before the first chunk's link items
+    if (c + G < nch) {
+      mbar_wait(S.abar(1), 0);
+      chunk_prefetch<SHARDED, BYDIR>(p, S, pack_chunk(p, c + G), S.ntl(1), cur32, warp, nwarps, lane, 1u, ro_of(1), rh);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+  }
 
   uint32_t it = 0, s = 0, sphase = 0;  // sphase bit s: parity of state stage s's next completion
   for (; c < nch; c += G, ++it, s = (s + 1 == NS) ? 0 : s + 1) {
@@ -454,12 +508,14 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
 
     // link words: bit i of u32 lane q of word Kw + e = cell j2 of the neighbour tile (link e)
     // of tile 32q + i
-    if (tid == 0) S.rctr[(it + 1) & 1u] = 0;  // compacted R: the counter chunk it+1's prefetch allocates from
+    // compacted R: the counter chunk it+1's (DYN: it+2's) prefetch allocates from
+    if (tid == 0) S.rctr[DYN ? (it & 1u) : ((it + 1) & 1u)] = 0;
     if (BYDIR) {
-      if ((uint32_t)warp < S.items[kPackMaxItems]) {
+      if (DYN || (uint32_t)warp < S.items[kPackMaxItems]) {
         mbar_wait(S.abar(a), (it / kAdjSlots) & 1);  // (already complete when the prefetch ran)
-        cp_async_wait_all();
-        chunk_link_items<SHARDED>(p, S, pc, ntl, Z, cur32, warp, nwarps, lane, it & 1u);
+        if (!DYN) cp_async_wait_all();
+        chunk_link_items<SHARDED>(p, S, pc, ntl, Z, cur32, warp, nwarps, lane, it & 1u, ro_of(it & 1u), rh,
+                                  DYN ? &S.rctr[2 + (it & 1u)] : nullptr);
       }
     } else {
     if ((uint32_t)warp < 4 * E) {
@@ -493,7 +549,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
       }
     }
     }
+    if (DYN) cp_async_wait_all();  // this warp's gathers of chunk it+1 (issued an iteration ago)
     __syncthreads();  // the one CTA barrier per chunk: state + link words in place, chunk it-1 done
+    if (DYN && tid == 0) S.rctr[2 + (it & 1u)] = 0;  // the item counter, for chunk it+2
     if (issuer) {
       if (c + (NS - 1) * G < nch) {
         fence_proxy_async();
@@ -502,11 +560,13 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
       if (c + (kAdjSlots - 1) * G < nch)
         adj_load(p, S, pack_chunk(p, c + (kAdjSlots - 1) * G), (it + kAdjSlots - 1) & (kAdjSlots - 1));
     }
-    if (c + G < nch) {  // out-of-chunk link gathers of the next chunk (its adjacency was issued long ago)
-      const uint32_t a1 = (it + 1) & (kAdjSlots - 1);
-      if (BYDIR ? (uint32_t)warp < S.items[kPackMaxItems] : ((uint32_t)warp < 4 * Epf && Epf))
-        mbar_wait(S.abar(a1), ((it + 1) / kAdjSlots) & 1);
-      chunk_prefetch<SHARDED, BYDIR>(p, S, pack_chunk(p, c + G), S.ntl(a1), cur32, warp, nwarps, lane, (it + 1) & 1u);
+    // out-of-chunk link gathers of the next chunk (DYN: the one after; its adjacency was issued long ago)
+    if (c + (DYN ? 2 : 1) * G < nch) {
+      const uint32_t itn = it + (DYN ? 2u : 1u), a1 = itn & (kAdjSlots - 1);
+      if (DYN || (BYDIR ? (uint32_t)warp < S.items[kPackMaxItems] : ((uint32_t)warp < 4 * Epf && Epf)))
+        mbar_wait(S.abar(a1), (itn / kAdjSlots) & 1);
+      chunk_prefetch<SHARDED, BYDIR>(p, S, pack_chunk(p, c + (DYN ? 2 : 1) * G), S.ntl(a1), cur32, warp, nwarps,
+                                     lane, itn & 1u, ro_of(itn & 1u), rh);
     }
 
     // count + rule: lane = word j (128 cells), straight to HBM
@@ -732,13 +792,15 @@ static PackedFn pick_packed_t(const TileParams& p, int threads) {
   // small tiles: 3 blocks per warp, 3 CTAs per SM; large tiles (level 7 Sierpinski: 69 blocks):
   // all 9 blocks' slots in registers (108 registers), 2 CTAs per SM (tools/packed_timing.py)
   if (p.dmax <= 5) {
-    if (rb <= 3) return conway ? k_step_packed<5, true, 3, 256, 3, SH, BD> : k_step_packed<5, false, 3, 256, 3, SH, BD>;
-    return conway ? k_step_packed<5, true, 9, 256, 2, SH, BD> : k_step_packed<5, false, 9, 256, 2, SH, BD>;
+    if (rb <= 3) return conway ? k_step_packed<5, true, 3, 256, 3, SH, BD, false> : k_step_packed<5, false, 3, 256, 3, SH, BD, false>;
+    return conway ? k_step_packed<5, true, 9, 256, 2, SH, BD, false> : k_step_packed<5, false, 9, 256, 2, SH, BD, false>;
   }
   // one CTA per SM (the compacted-gather chunks of level-4 carpet tiles): 16 warps
-  if (threads == 512) return conway ? k_step_packed<8, true, 6, 512, 1, SH, BD> : k_step_packed<8, false, 6, 512, 1, SH, BD>;
-  if (rb <= 2) return conway ? k_step_packed<8, true, 2, 256, 3, SH, BD> : k_step_packed<8, false, 2, 256, 3, SH, BD>;
-  return conway ? k_step_packed<8, true, 6, 256, 2, SH, BD> : k_step_packed<8, false, 6, 256, 2, SH, BD>;
+  if (threads == 512 && BD && packed_compact_gathers(p) && !(p.pflags & kPackStaticItems))
+    return conway ? k_step_packed<8, true, 6, 512, 1, SH, BD, BD> : k_step_packed<8, false, 6, 512, 1, SH, BD, BD>;
+  if (threads == 512) return conway ? k_step_packed<8, true, 6, 512, 1, SH, BD, false> : k_step_packed<8, false, 6, 512, 1, SH, BD, false>;
+  if (rb <= 2) return conway ? k_step_packed<8, true, 2, 256, 3, SH, BD, false> : k_step_packed<8, false, 2, 256, 3, SH, BD, false>;
+  return conway ? k_step_packed<8, true, 6, 256, 2, SH, BD, false> : k_step_packed<8, false, 6, 256, 2, SH, BD, false>;
 }
 
 // link work by (direction, lane group) pairs when directions carry several links each

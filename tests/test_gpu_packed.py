@@ -107,6 +107,24 @@ def test_packed_compacted_gathers(monkeypatch, rcap, name, r, g, grid):
         a, b = b, a
 
 
+@pytest.mark.parametrize("knob", ["SQZ_PACKED_STATIC_ITEMS", "SQZ_PACKED_THREADS"])
+def test_packed_compacted_gathers_static_split(monkeypatch, knob):
+    """The compacted gathers under the static link-item split (one chunk ahead, item k on warp k
+    mod W) instead of the default dynamic one: forced by the A/B knob, or by 8 warps per CTA."""
+    monkeypatch.setenv(knob, "1" if knob == "SQZ_PACKED_STATIC_ITEMS" else "256")
+    monkeypatch.setenv("SQZ_PACKED_GRID", "2")
+    monkeypatch.setenv("SQZ_PACKED_RCAP", "1024")
+    name, r = "sierpinski-carpet", 7
+    p = mk(name, r, tile_level=4)
+    want = oracle_run(name, r, 5, 0.45, 3)
+    a, b = p.new_packed(), p.new_packed()
+    p.seed_packed(a, 5, 0.45)
+    for t in range(3):
+        p.step_packed(a, b)
+        assert np.array_equal(cells(p, b), want[t + 1]), f"step {t + 1}"
+        a, b = b, a
+
+
 @pytest.mark.parametrize("rule", RULES[:2])
 def test_packed_compacted_gathers_rules_ragged(monkeypatch, rule):  # a ragged last chunk, births at count 0
     monkeypatch.setenv("SQZ_PACKED_GRID", "3")
@@ -383,3 +401,35 @@ def test_packed_config3_full_size(name, r, g):
     want = A.compact_step_sampled(f, r, om, lambda q: one[q])
     assert np.array_equal(two[om], want)
     assert p.device_error() == 0
+
+
+def test_packed_link_items_guard():
+    """A hollow square (s=12, the 44 border cells: k=44) has 144-cell tile edges at level 2:
+    4 x 5 group items per edge = 80 link items, more than the packed step's 64 slots.  The context
+    must report the packed step unavailable there (and refuse it), while level 1 (16 items +
+    corners) runs and matches the oracle; the byte step (streaming kernel at level 2) runs at both."""
+    from oracle.fractals import Fractal
+    s_ = 12
+    tau = tuple((x, y) for y in range(s_) for x in range(s_) if x in (0, s_ - 1) or y in (0, s_ - 1))
+    of = Fractal("hollow-12", len(tau), s_, tau)
+    of.validate()
+    f = sq.Fractal("hollow-12", len(tau), s_, tau)
+    r = 3
+    want = [A.seed_compact(of, r, 9, 0.5)]
+    for _ in range(2):
+        want.append(A.compact_step(of, r, want[-1]))
+    p2 = sq.Squeeze(f, r, device=0, tile_level=2)
+    assert p2.geometry.remote_links == 580 and not p2.geometry.packed_ok
+    with pytest.raises(sq.SqueezeError):
+        p2.step_packed(p2.new_packed(), p2.new_packed())
+    a, b = p2.new_state(), p2.new_state()
+    p2.seed(a, 9, 0.5)
+    fin = p2.run(a, b, 2)
+    torch.cuda.synchronize()
+    assert np.array_equal(p2.to_cells(fin).cpu().numpy(), want[2])
+    p1 = sq.Squeeze(f, r, device=0, tile_level=1)
+    assert p1.geometry.packed_ok
+    a, b = p1.new_packed(), p1.new_packed()
+    p1.seed_packed(a, 9, 0.5)
+    fin = p1.run_packed(a, b, 2)
+    assert np.array_equal(cells(p1, fin), want[2])
