@@ -527,6 +527,10 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       // two do, else 2
       c->packed_threads = 256;
       // stages: 4 if three CTAs still fit an SM, else 3 if two do, else 2
+      // A/B: the compacted link gathers (dynamic link items) for every link-item context (flag 4)
+      if (const char* e = getenv("SQZ_PACKED_COMPACT"))
+        if (atoi(e) && c->tt.E >= 3 * c->tt.ndirs) c->packed_flags |= 4u;
+      p.pflags = c->packed_flags;
       p.pstages = 4;
       if (3 * packed_smem_bytes(p) > 220 * 1024) p.pstages = 3;
       if (p.pstages == 3 && 2 * packed_smem_bytes(p) > 220 * 1024) p.pstages = 2;
@@ -543,7 +547,8 @@ squeeze_status squeeze_init(void** out_ctx, const squeeze_fractal* f, uint32_t r
       }
       c->packed_rcap = p.rcap;
       // A/B: the compacted gathers with the static link-item split (2) instead of the dynamic one
-      if (const char* e = getenv("SQZ_PACKED_STATIC_ITEMS")) c->packed_flags = atoi(e) ? 2u : 0u;
+      if (const char* e = getenv("SQZ_PACKED_STATIC_ITEMS"))
+        c->packed_flags = (c->packed_flags & ~2u) | (atoi(e) ? 2u : 0u);
       p.pflags = c->packed_flags;
       // a compacted-gather chunk leaves one CTA per SM: 16 warps instead of 8 (8 neighbour slots only)
       if (p.rcap && p.dmax > 5 && 2 * packed_smem_bytes(p) > 228 * 1024) c->packed_threads = 512;

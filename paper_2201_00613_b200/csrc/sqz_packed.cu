@@ -31,6 +31,12 @@ constexpr uint32_t kPackBallotItem = 1u << 31;
 constexpr uint32_t kPackLongDirection = 8;
 constexpr uint32_t kSlotBatch = 4;  // link slots per pass in the slot split (Sierpinski: 32 slots, 8 warps)
 constexpr uint32_t kPackStaticItems = 2;  // TileParams::pflags: compacted gathers with the static item split (A/B)
+constexpr uint32_t kPackCompact = 4;      // TileParams::pflags: compacted gathers for any link-item context
+
+// Links whose out-of-chunk gathers go to a [tile][link] (or [slot][32]) buffer; 0 = compacted buffer.
+__host__ __device__ inline uint32_t pack_prefetch_links(const TileParams& p) {
+  return (p.pflags & kPackCompact) ? 0u : prefetch_links(p);
+}
 
 __host__ __device__ inline uint32_t pack_zw(const TileParams& p) { return (p.Kw + p.E + 1) * 4; }
 
@@ -67,13 +73,13 @@ __host__ __device__ inline size_t packed_layout(const TileParams& p, uint8_t* ba
   if (s) s->A0 = (uint32_t*)(base + off);
   off += (size_t)kAdjSlots * p.ndirs * kPackTiles * 4;
   if (s) s->R = (uint32_t*)(base + off);
-  off += prefetch_links(p) ? (size_t)4 * prefetch_links(p) * 32 * 4 : align16((size_t)(p.rcap ? p.rcap : 1) * 4);
+  off += pack_prefetch_links(p) ? (size_t)4 * pack_prefetch_links(p) * 32 * 4 : align16((size_t)(p.rcap ? p.rcap : 1) * 4);
   if (s) s->rctr = (uint32_t*)(base + off);
   off += 16;
   if (s) s->rb = (uint32_t*)(base + off);
-  off += prefetch_links(p) ? 0 : (size_t)2 * kPackMaxItems * 4;
+  off += pack_prefetch_links(p) ? 0 : (size_t)2 * kPackMaxItems * 4;
   if (s) s->rbb = (uint32_t*)(base + off);
-  off += prefetch_links(p) ? 0 : align16((size_t)2 * 4 * (p.E ? p.E : 1) * 4);
+  off += pack_prefetch_links(p) ? 0 : align16((size_t)2 * 4 * (p.E ? p.E : 1) * 4);
   if (s) s->sl = (uint32_t*)(base + off);
   off += align16((size_t)(p.E ? 4 * p.E : 1) * 4);
   if (s) s->bar = (uint64_t*)(base + off);
@@ -86,7 +92,7 @@ __host__ __device__ inline size_t packed_layout(const TileParams& p, uint8_t* ba
 }
 
 size_t packed_smem_bytes(const TileParams& p) { return packed_layout(p, nullptr, nullptr); }
-bool packed_compact_gathers(const TileParams& p) { return prefetch_links(p) == 0; }
+bool packed_compact_gathers(const TileParams& p) { return pack_prefetch_links(p) == 0; }
 
 // Host check of the link work items pack_link_items builds (BYDIR variants, E >= 3 ndirs): at most
 // kPackMaxItems of them, link indices below 2^11 (their 11-bit fields).  Contexts that fail it (a
@@ -162,7 +168,7 @@ template <bool SHARDED>
 __device__ __forceinline__ void chunk_prefetch_slots(const TileParams& p, const PackSmem& S, const PackChunk& pc,
                                                const uint32_t* ntl, const uint32_t* __restrict__ cur32, int warp,
                                                int nwarps, int lane) {
-  const uint32_t E = prefetch_links(p);
+  const uint32_t E = pack_prefetch_links(p);
 #pragma unroll 4
   for (uint32_t u = (uint32_t)warp; u < 4 * E; u += (uint32_t)nwarps) {
     const uint32_t sl = S.sl[u];
@@ -240,7 +246,7 @@ __device__ __forceinline__ void chunk_prefetch_items(const TileParams& p, const 
   // compacted: words [ro, ro + rcap) of R (ro = 0, rcap = p.rcap; or one parity's half, DYN)
   const uint32_t E = p.E, ni = S.items[kPackMaxItems], tlo = (uint32_t)p.tile_lo, Kw = p.Kw;
   const uint32_t nloc = (uint32_t)(p.tile_hi - p.tile_lo), gs0 = smem_u32(S.R);
-  const bool compact = prefetch_links(p) == 0;
+  const bool compact = pack_prefetch_links(p) == 0;
   const uint32_t lt = (1u << lane) - 1u;
   for (uint32_t k = (uint32_t)warp; k < ni; k += (uint32_t)nwarps) {
     const uint32_t item = S.items[k], i0 = item & 0x7FFu, n = ((item >> 11) & 31u) + 1u;
@@ -315,7 +321,7 @@ __device__ __forceinline__ void chunk_link_items(const TileParams& p, const Pack
                                                  int warp, int nwarps, int lane, uint32_t par, uint32_t ro,
                                                  uint32_t rcap, uint32_t* dctr) {
   const uint32_t E = p.E, ni = S.items[kPackMaxItems], tlo = (uint32_t)p.tile_lo, Kw = p.Kw;
-  const bool compact = prefetch_links(p) == 0;
+  const bool compact = pack_prefetch_links(p) == 0;
   const uint32_t lt = (1u << lane) - 1u, nloc = (uint32_t)(p.tile_hi - p.tile_lo);
   auto grab = [&]() -> uint32_t {
     uint32_t v = 0;
@@ -445,7 +451,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_step_packed(TileParams p, const 
   packed_layout(p, smem_raw, &S);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const uint32_t K = (uint32_t)p.K, Kw = p.Kw, E = p.E, NS = p.pstages;
-  const uint32_t Epf = prefetch_links(p);
+  const uint32_t Epf = pack_prefetch_links(p);
   const uint64_t nch = pack_chunks(p);
   const bool issuer = warp == nwarps - 1 && lane == 0;
   const uint32_t* cur32 = reinterpret_cast<const uint32_t*>(cur);
@@ -799,7 +805,12 @@ static PackedFn pick_packed_t(const TileParams& p, int threads) {
   if (threads == 512 && BD && packed_compact_gathers(p) && !(p.pflags & kPackStaticItems))
     return conway ? k_step_packed<8, true, 6, 512, 1, SH, BD, BD> : k_step_packed<8, false, 6, 512, 1, SH, BD, BD>;
   if (threads == 512) return conway ? k_step_packed<8, true, 6, 512, 1, SH, BD, false> : k_step_packed<8, false, 6, 512, 1, SH, BD, false>;
-  if (rb <= 2) return conway ? k_step_packed<8, true, 2, 256, 3, SH, BD, false> : k_step_packed<8, false, 2, 256, 3, SH, BD, false>;
+  const bool dyn = BD && packed_compact_gathers(p) && !(p.pflags & kPackStaticItems);
+  if (rb <= 2) {
+    if (dyn) return conway ? k_step_packed<8, true, 2, 256, 3, SH, BD, BD> : k_step_packed<8, false, 2, 256, 3, SH, BD, BD>;
+    return conway ? k_step_packed<8, true, 2, 256, 3, SH, BD, false> : k_step_packed<8, false, 2, 256, 3, SH, BD, false>;
+  }
+  if (dyn) return conway ? k_step_packed<8, true, 6, 256, 2, SH, BD, BD> : k_step_packed<8, false, 6, 256, 2, SH, BD, BD>;
   return conway ? k_step_packed<8, true, 6, 256, 2, SH, BD, false> : k_step_packed<8, false, 6, 256, 2, SH, BD, false>;
 }
 

@@ -125,6 +125,22 @@ def test_packed_compacted_gathers_static_split(monkeypatch, knob):
         a, b = b, a
 
 
+@pytest.mark.parametrize("name,r,g", [("empty-bottles", 7, 4), ("sierpinski-carpet", 6, 3), ("vicsek", 7, 5)])
+def test_packed_forced_compaction(monkeypatch, name, r, g):
+    """SQZ_PACKED_COMPACT=1 (an A/B knob): the compacted gathers and dynamic link items on contexts
+    that default to the [tile][link] buffer (two and three CTAs per SM), several chunks per CTA."""
+    monkeypatch.setenv("SQZ_PACKED_COMPACT", "1")
+    monkeypatch.setenv("SQZ_PACKED_GRID", "2")
+    p = mk(name, r, tile_level=g)
+    want = oracle_run(name, r, 5, 0.45, 3)
+    a, b = p.new_packed(), p.new_packed()
+    p.seed_packed(a, 5, 0.45)
+    for t in range(3):
+        p.step_packed(a, b)
+        assert np.array_equal(cells(p, b), want[t + 1]), f"step {t + 1}"
+        a, b = b, a
+
+
 @pytest.mark.parametrize("rule", RULES[:2])
 def test_packed_compacted_gathers_rules_ragged(monkeypatch, rule):  # a ragged last chunk, births at count 0
     monkeypatch.setenv("SQZ_PACKED_GRID", "3")
