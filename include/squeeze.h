@@ -116,7 +116,9 @@ typedef struct {
                           * large-tile step (k_step_stream, when a 32-tile chunk does not fit shared
                           * memory twice); both compute the same step on the same layout */
   uint32_t packed_ok;    /* 1 if the packed step fits at this tile level (else its calls return
-                          * SQZ_E_INVALID_LEVEL) */
+                          * SQZ_E_INVALID_LEVEL): the 128-tile chunk fits shared memory twice and its
+                          * boundary links need at most 64 link work items (a tile with very long
+                          * edges, e.g. a hollow square with s=12 at tile level 2, does not) */
   uint32_t heat_ok;      /* 1 if the heat step fits at this tile level (likewise) */
 } squeeze_geometry_t;
 
